@@ -1,0 +1,159 @@
+/*
+ * sv.h — C ABI of the B200 cache-blocked state-vector library (libsv.so).
+ *
+ * The operation: apply a circuit of 1-/2-qubit unitaries, diagonal gates and swaps to an
+ * n-qubit state vector of 2^n complex amplitudes (§II-A), with the state
+ * split into chunks and the top log2(G) qubits indexing GPUs, using the
+ * cache-blocking transpiler of §IV-A (Listing 3) so every gate runs inside one
+ * chunk-sized tile and data crosses GPUs only at chunk_swaps.
+ *
+ * Conventions
+ *   - Qubit k <-> bit k of the amplitude index, zero-based, little-endian.
+ *   - Amplitudes are complex interleaved (re, im): 16 B (SV_FP64) or 8 B (SV_FP32) each.
+ *   - Gate matrices are always fp64, complex interleaved, ROW-major, and are rounded to
+ *     nearest to fp32 on upload for SV_FP32.  U2 sub-index s = bit(q0) + 2*bit(q1), so
+ *     CNOT(control c, target t) = U2(q0 = t, q1 = c, Eq. 2 matrix).
+ *   - Diagonality is declared by kind (SV_D1 / SV_D2), never detected.
+ *   - Every getter speaks LOGICAL qubits / indices; the library tracks the permutation the
+ *     blocking pass leaves behind (order is restored only on request).
+ *
+ * Ownership: the caller owns every input array and host output buffer (sizes given by the
+ * caller).  The library copies gates before returning and never retains caller pointers,
+ * except ext_dev_buf in sv_create_dist, which must outlive the handle.  Arrays the library
+ * returns (sv_block_circuit, sv_plan_circuit) are freed with sv_free.
+ *
+ * Errors: every int-returning call returns SV_OK (0) or a negative SV_E* code; the message is
+ * available from sv_last_error(handle) (thread-local when handle == NULL).  No C++ exception
+ * crosses the ABI.  Handles are not thread-safe.  With world > 1 every call on a handle is
+ * collective: all ranks call it in the same order with the same arguments.
+ *
+ * Preconditions: 1 <= chunk_bits <= n - log2(world); world is a power of two; n <= 40.
+ */
+#ifndef SV_H
+#define SV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sv_state* sv_handle;
+
+typedef enum { SV_FP32 = 0, SV_FP64 = 1 } sv_precision;
+
+/* Gate / token kinds.  1-5 are input gates; 6-9 appear only in library output
+ * (sv_block_circuit: 6-8; sv_plan_circuit: 6-9). */
+enum {
+  SV_U1 = 1,         /* 2x2 unitary on q0 (m[0..7]) — u3 of Eq. 1 arrives as this */
+  SV_U2 = 2,         /* 4x4 unitary on (q0, q1) (m[0..31]) — CNOT of Eq. 2        */
+  SV_D1 = 3,         /* diag(d0, d1) on q0 (m[0..3]) — u1                             */
+  SV_D2 = 4,         /* diag(d0..d3) on (q0, q1) (m[0..7]) — controlled phase         */
+  SV_SWAP = 5,       /* swap of q0 and q1, no payload                                        */
+  SV_CHUNK_SWAP = 6, /* chunk_swap(sq0 = q0 < sq1 = q1) inserted by the pass  */
+  SV_BEGIN = 7,      /* begin_blocking                                               */
+  SV_END = 8,        /* end_blocking                                                 */
+  SV_EXCHANGE = 9    /* plan only: physically swap local memory bit q0 with rank bit q1      */
+};
+
+typedef struct {
+  int32_t kind, q0, q1, pad; /* pad: ignored on input; sv_block_circuit writes the input index */
+  double m[32];
+} sv_gate;
+
+/* Flags for sv_apply_circuit / sv_block_circuit / sv_plan_circuit. */
+#define SV_UNBLOCKED     (1u << 0) /* per-gate baseline: one HBM pass per gate, no pass  */
+#define SV_RESTORE_ORDER (1u << 1) /* append swaps returning the paper-physical order to logical */
+#define SV_EXCHANGE_NCCL (1u << 2) /* cross-GPU exchange by NCCL send/recv through a staging ring */
+                                   /* instead of the peer-memory swap kernel                    */
+
+/* Error codes. */
+#define SV_OK           0
+#define SV_EINVAL      -1 /* bad qubit, duplicate qubit, bad chunk_bits / world / argument  */
+#define SV_ECAPACITY   -2 /* state does not fit device (or host) memory                      */
+#define SV_EINFEASIBLE -3 /* non-diagonal 2-qubit gate with chunk_bits < 2; or a    */
+                          /* per-gate (unblocked) non-diagonal gate on a global qubit          */
+#define SV_EMALFORMED  -4 /* malformed record / marker sequence                               */
+#define SV_ECUDA       -5 /* CUDA runtime failure                                              */
+#define SV_ENCCL       -6 /* NCCL failure or NCCL library not loadable                         */
+
+typedef struct sv_stats {
+  uint64_t circuits;          /* sv_apply_circuit calls                                       */
+  uint64_t gates;             /* input gates applied                                          */
+  uint64_t sections;          /* blocked sections executed (one HBM pass each)         */
+  uint64_t chunk_swaps;       /* chunk_swap tokens from the pass (all virtual relabels)       */
+  uint64_t exchanges;         /* physical cross-GPU bit exchanges (local bit <-> rank bit)    */
+  uint64_t exchange_batches;  /* exchange steps (each one grouped all-to-all in a subcube)    */
+  uint64_t bytes_sent;        /* amplitude bytes this rank moved to peers                     */
+  uint64_t kernel_launches;   /* library kernels launched                                     */
+  double pass_ms;             /* host time in the blocking pass + planning (last call)        */
+  double apply_ms;            /* host wall time of the last sv_apply_circuit                   */
+} sv_stats;
+
+/* ---- lifetime ------------------------------------------------------------------------- */
+/* One GPU (the caller's current CUDA device), state |0..0>, memory allocated by the library. */
+int sv_create(int n_qubits, int chunk_bits, sv_precision prec, sv_handle* out);
+/* One rank of a world of `world` GPUs (one process per GPU, current device).  nccl_unique_id:
+ * 128 bytes from sv_nccl_unique_id on rank 0, broadcast by the caller (required if world>1).
+ * ext_dev_buf (nullable): device buffer of >= ext_bytes = 2^(n-log2 world) * amp bytes that
+ * holds this rank's shard; cuda_stream (nullable): stream all work is issued on (default: a
+ * library-created stream).  Rank r holds the amplitudes whose top log2(world) memory bits = r
+ * (contiguous placement). */
+int sv_create_dist(int n_qubits, int chunk_bits, sv_precision prec, int rank, int world,
+                   const void* nccl_unique_id, void* ext_dev_buf, size_t ext_bytes,
+                   void* cuda_stream, sv_handle* out);
+int sv_destroy(sv_handle h);
+/* Write ncclGetUniqueId() into out (128 bytes). */
+int sv_nccl_unique_id(void* out128);
+
+/* ---- evolution ------------------------------------------------------------------------ */
+/* |k> for LOGICAL basis index k; resets the tracked permutations to identity. */
+int sv_reset(sv_handle h, uint64_t basis_index);
+/* Apply n_gates input records (kinds SV_U1..SV_SWAP, logical qubits) in order.  Default:
+ * blocked (Listing 3 pass, then one section kernel per section and exchanges only for
+ * global qubits).  Returns after all work is enqueued on the handle's stream. */
+int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t flags);
+/* Block until the handle's stream is idle. */
+int sv_synchronize(sv_handle h);
+
+/* ---- readout (all collective; results on every rank) --------------------------------- */
+/* host_out[i] = amplitude of LOGICAL index logical_idx[i] (cnt complex values, amp dtype). */
+int sv_get_amplitudes(sv_handle h, const uint64_t* logical_idx, size_t cnt, void* host_out);
+/* Full state in LOGICAL order into host_out (2^n complex, amp dtype); written on rank 0 only. */
+int sv_get_state(sv_handle h, void* host_out);
+/* sum |a|^2 */
+int sv_norm(sv_handle h, double* out);
+/* Marginal probabilities over LOGICAL qubits Q (qubits[0] -> bit 0 of the output index),
+ * host_out has 2^nq doubles, nq <= 24.  p[y] = sum_{x : x|Q = y} |a_x|^2 (DESIGN R17). */
+int sv_probabilities(sv_handle h, const int32_t* qubits, int nq, double* host_out);
+/* shots samples of LOGICAL basis indices from |a|^2 into host_out; u_s = (splitmix64(seed ^ s)
+ * >> 11) * 2^-53 is inverted through the CDF in memory order (DESIGN R16). */
+int sv_sample(sv_handle h, size_t shots, uint64_t seed, uint64_t* host_out);
+/* logical_to_physical[q] = paper-physical position of logical qubit q (the pass's pi). */
+int sv_get_permutation(sv_handle h, int32_t* logical_to_physical);
+int sv_stats_get(sv_handle h, sv_stats* out);
+const char* sv_last_error(sv_handle h);
+
+/* ---- host-only (no GPU needed; used for parity of the pass and the plan) -------------- */
+/* The cache-blocking pass (Listing 3, DESIGN R2-R6) on logical gates.  *out receives the
+ * token stream (SV_CHUNK_SWAP / SV_BEGIN / SV_END and gates on physical qubits, pad = input
+ * index); pi_final[q] = physical position of logical q.  pi0 nullable (= identity). */
+int sv_block_circuit(const sv_gate* gates, size_t n_gates, int n, int chunk_bits,
+                     const int32_t* pi0, uint32_t flags, sv_gate** out, size_t* n_out,
+                     int32_t* pi_final);
+/* The executor's plan for a world of 2^world_log2 GPUs: SV_EXCHANGE records (q0 = local
+ * memory bit, q1 = rank memory bit >= n - world_log2), and BEGIN ... END sections whose gates
+ * act on MEMORY bits.  pi0/sigma0 nullable (= identity); pi_final / sigma_final receive the
+ * logical->physical and physical->memory maps after the circuit. */
+int sv_plan_circuit(const sv_gate* gates, size_t n_gates, int n, int chunk_bits, int world_log2,
+                    const int32_t* pi0, const int32_t* sigma0, uint32_t flags, sv_gate** out,
+                    size_t* n_out, int32_t* pi_final, int32_t* sigma_final);
+void sv_free(void* p);
+/* ABI version (for the binding's check). */
+int sv_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SV_H */

@@ -1,0 +1,848 @@
+// api.cpp — the C ABI (include/sv.h): handle, sharded state store, executor, readout.
+//
+// Layers: L1 this file (validation, errors, handle) -> L2 host planner (blocking.cpp,
+// plan.cpp, compile.cpp) -> L3 sharded store + scheduler (this file: pi/sigma maps, stream,
+// program upload, step execution) -> L4 kernels (kernels.cu) and L5 comm (comm.cpp, NCCL +
+// CUDA IPC peer memory).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "comm.h"
+#include "common.h"
+#include "compile.h"
+#include "kernels.cuh"
+
+using namespace sv;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+double now_ms() {
+  using namespace std::chrono;
+  return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+struct PinBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+// Bit-permutation evaluated with byte tables: f(x) = OR_j T_j[byte_j(x)].
+struct BitPerm {
+  std::vector<uint64_t> t;  // nbytes * 256
+  int nbytes = 0;
+  void build(const std::vector<int>& dst_of_src_bit) {  // bit i of x goes to bit dst[i]
+    const int n = (int)dst_of_src_bit.size();
+    nbytes = (n + 7) / 8;
+    t.assign((size_t)nbytes * 256, 0);
+    for (int j = 0; j < nbytes; j++)
+      for (int v = 0; v < 256; v++) {
+        uint64_t o = 0;
+        for (int b = 0; b < 8; b++)
+          if (((v >> b) & 1) && 8 * j + b < n) o |= 1ull << dst_of_src_bit[8 * j + b];
+        t[(size_t)j * 256 + v] = o;
+      }
+  }
+  uint64_t operator()(uint64_t x) const {
+    uint64_t o = 0;
+    for (int j = 0; j < nbytes; j++) o |= t[(size_t)j * 256 + ((x >> (8 * j)) & 255)];
+    return o;
+  }
+};
+
+}  // namespace
+
+struct sv_state {
+  int n = 0, c = 0, nL = 0, g = 0, rank = 0, world = 1, device = 0;
+  bool dbl = true;
+  size_t amp = 16;
+  void* sv = nullptr;
+  bool own_sv = false;
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  std::vector<int> pi, sigma;
+
+  DevBuf d_prog, d_coef, d_scratch, d_small, d_tmp, d_tmp2, d_stage;
+  PinBuf h_stage, h_stage2;
+  cudaEvent_t ev_upload = nullptr;
+  bool upload_pending = false;
+
+  Nccl* nc = nullptr;
+  Nccl::Comm comm = nullptr;
+  std::vector<void*> peers;       // peer shard pointers mapped in this process (self = sv)
+  std::vector<void*> ipc_opened;  // to close
+  bool p2p = false;
+
+  Program prog;
+  sv_stats stats{};
+  std::string err;
+};
+
+namespace {
+
+int fail(sv_state* h, int code, const std::string& msg) {
+  if (h) h->err = msg;
+  g_last_error = msg;
+  return code;
+}
+int fail(sv_state* h, const Status& s) { return fail(h, s.code, s.msg); }
+
+#define CUDA_TRY(h, expr)                                                                        \
+  do {                                                                                           \
+    cudaError_t _e = (expr);                                                                     \
+    if (_e != cudaSuccess)                                                                       \
+      return fail(h, SV_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));              \
+  } while (0)
+
+#define NCCL_TRY(h, expr)                                                                        \
+  do {                                                                                           \
+    int _r = (expr);                                                                             \
+    if (_r != 0)                                                                                 \
+      return fail(h, SV_ENCCL, std::string(#expr) + ": " + (h)->nc->GetErrorString(_r));        \
+  } while (0)
+
+int ensure_dev(sv_state* h, DevBuf& b, size_t bytes) {
+  if (b.cap >= bytes) return SV_OK;
+  if (b.p) {
+    CUDA_TRY(h, cudaStreamSynchronize(h->st));
+    CUDA_TRY(h, cudaFree(b.p));
+    b.p = nullptr;
+    b.cap = 0;
+  }
+  size_t cap = std::max<size_t>(bytes, 4096);
+  cap = (cap + 4095) & ~size_t(4095);
+  cudaError_t e = cudaMalloc(&b.p, cap);
+  if (e != cudaSuccess) return fail(h, SV_ECAPACITY, std::string("device scratch allocation failed: ") + cudaGetErrorString(e));
+  b.cap = cap;
+  return SV_OK;
+}
+
+int ensure_pin(sv_state* h, PinBuf& b, size_t bytes) {
+  if (b.cap >= bytes) return SV_OK;
+  if (b.p) {
+    CUDA_TRY(h, cudaStreamSynchronize(h->st));
+    CUDA_TRY(h, cudaFreeHost(b.p));
+    b.p = nullptr;
+    b.cap = 0;
+  }
+  size_t cap = std::max<size_t>(bytes, 1 << 16);
+  CUDA_TRY(h, cudaMallocHost(&b.p, cap));
+  b.cap = cap;
+  return SV_OK;
+}
+
+// memory index of logical index x: bit q of x -> bit sigma[pi[q]]
+BitPerm mu_of(const sv_state* h) {
+  std::vector<int> dst(h->n);
+  for (int q = 0; q < h->n; q++) dst[q] = h->sigma[h->pi[q]];
+  BitPerm p;
+  p.build(dst);
+  return p;
+}
+BitPerm mu_inv_of(const sv_state* h) {
+  std::vector<int> dst(h->n);
+  for (int q = 0; q < h->n; q++) dst[h->sigma[h->pi[q]]] = q;
+  BitPerm p;
+  p.build(dst);
+  return p;
+}
+
+int barrier(sv_state* h) {
+  if (h->world == 1) return SV_OK;
+  NCCL_TRY(h, h->nc->AllReduce(h->d_small.p, h->d_small.p, 1, Nccl::F32, 0, h->comm, h->st));
+  return SV_OK;
+}
+
+// Cross-GPU exchange of local memory bits with rank bits (one grouped step, §8(e)).
+int do_exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags) {
+  std::sort(pairs.begin(), pairs.end(), [](const ExPair& a, const ExPair& b) { return a.m < b.m; });
+  ExchangeArgs a{};
+  a.k = (int)pairs.size();
+  if (a.k > 8) return fail(h, SV_EINVAL, "internal: exchange of more than 8 bits");
+  uint64_t mmask = 0;
+  for (int i = 0; i < a.k; i++) {
+    a.m[i] = pairs[i].m;
+    a.bsel[i] = pairs[i].b - h->nL;
+    mmask |= 1ull << pairs[i].m;
+  }
+  a.h = h->nL - 1;
+  while (a.h >= 0 && ((mmask >> a.h) & 1)) a.h--;
+  if (a.h < 0) return fail(h, SV_EINVAL, "internal: no split bit for the exchange");
+  const uint64_t block = 1ull << (h->nL - a.k);
+  h->stats.bytes_sent += (uint64_t)((1ull << a.k) - 1) * block * h->amp;
+  h->stats.exchanges += a.k;
+  h->stats.exchange_batches++;
+
+  if (h->p2p && !(flags & SV_EXCHANGE_NCCL)) {
+    if (int rc = barrier(h)) return rc;
+    int launches = 0;
+    CUDA_TRY(h, launch_exchange_peer(h->dbl, h->sv, h->peers.data(), h->rank, h->nL, a, h->st, &launches));
+    h->stats.kernel_launches += launches;
+    return barrier(h);
+  }
+
+  // NCCL path: my block mu (local m-bits = mu) goes to the partner whose rank bits are mu; its
+  // block `mine` comes back into the same place, through a staging buffer, run by run.
+  int mine = 0;
+  for (int i = 0; i < a.k; i++) mine |= ((h->rank >> a.bsel[i]) & 1) << i;
+  const int mlow = a.m[0];
+  const uint64_t run = 1ull << mlow;  // contiguous amplitudes per run
+  const uint64_t runs = 1ull << (h->nL - mlow - a.k);
+  const size_t piece_amps = std::min<uint64_t>(run, (64ull << 20) / h->amp);
+  if (int rc = ensure_dev(h, h->d_stage, piece_amps * h->amp)) return rc;
+  std::vector<std::pair<int, int>> partners;  // (partner rank, mu)
+  for (int mu = 0; mu < (1 << a.k); mu++) {
+    if (mu == mine) continue;
+    int p = h->rank;
+    for (int i = 0; i < a.k; i++) p = (p & ~(1 << a.bsel[i])) | (((mu >> i) & 1) << a.bsel[i]);
+    partners.push_back({p, mu});
+  }
+  std::sort(partners.begin(), partners.end());
+  // insert the m-bits (value mu) into a run index: positions above mlow that are not m-bits
+  auto run_start = [&](uint64_t rix, int mu) {
+    uint64_t x = rix << mlow;  // compact index of the run's first element (bits >= mlow)
+    for (int i = 0; i < a.k; i++) {
+      const int p = a.m[i];
+      const uint64_t lo = x & ((1ull << p) - 1);
+      x = ((x - lo) << 1) | ((uint64_t)((mu >> i) & 1) << p) | lo;
+    }
+    return x;
+  };
+  char* base = (char*)h->sv;
+  for (auto& pm : partners) {
+    for (uint64_t rix = 0; rix < runs; rix++) {
+      const uint64_t start = run_start(rix, pm.second);
+      for (uint64_t off = 0; off < run; off += piece_amps) {
+        const size_t cnt = (size_t)std::min<uint64_t>(piece_amps, run - off);
+        char* p = base + (start + off) * h->amp;
+        NCCL_TRY(h, h->nc->GroupStart());
+        NCCL_TRY(h, h->nc->Send(p, cnt * h->amp, Nccl::Uint8, pm.first, h->comm, h->st));
+        NCCL_TRY(h, h->nc->Recv(h->d_stage.p, cnt * h->amp, Nccl::Uint8, pm.first, h->comm, h->st));
+        NCCL_TRY(h, h->nc->GroupEnd());
+        CUDA_TRY(h, cudaMemcpyAsync(p, h->d_stage.p, cnt * h->amp, cudaMemcpyDeviceToDevice, h->st));
+      }
+    }
+  }
+  return SV_OK;
+}
+
+int upload_program(sv_state* h) {
+  const size_t ib = h->prog.ints.size() * sizeof(int);
+  const size_t ncoef = h->prog.coefs.size() / 2;
+  const size_t cb = ncoef * h->amp;
+  if (ib + cb == 0) return SV_OK;
+  if (h->upload_pending) CUDA_TRY(h, cudaEventSynchronize(h->ev_upload));  // staging reuse
+  if (int rc = ensure_pin(h, h->h_stage, ib + cb + 64)) return rc;
+  if (int rc = ensure_dev(h, h->d_prog, ib + 16)) return rc;
+  if (int rc = ensure_dev(h, h->d_coef, cb + 16)) return rc;
+  char* s = (char*)h->h_stage.p;
+  std::memcpy(s, h->prog.ints.data(), ib);
+  char* cs = s + ((ib + 15) & ~size_t(15));
+  if (h->dbl) {
+    std::memcpy(cs, h->prog.coefs.data(), cb);
+  } else {
+    float* f = (float*)cs;
+    for (size_t i = 0; i < 2 * ncoef; i++) f[i] = (float)h->prog.coefs[i];
+  }
+  if (ib) CUDA_TRY(h, cudaMemcpyAsync(h->d_prog.p, s, ib, cudaMemcpyHostToDevice, h->st));
+  if (cb) CUDA_TRY(h, cudaMemcpyAsync(h->d_coef.p, cs, cb, cudaMemcpyHostToDevice, h->st));
+  CUDA_TRY(h, cudaEventRecord(h->ev_upload, h->st));
+  h->upload_pending = true;
+  return SV_OK;
+}
+
+int gate_step(sv_state* h, const sv_gate& gm) {
+  GateArgs a{};
+  a.q0 = gm.q0;
+  a.q1 = gm.q1;
+  auto code = [&](int mb) { return mb >= h->nL ? 200 + ((h->rank >> (mb - h->nL)) & 1) : mb; };
+  switch (gm.kind) {
+    case SV_U1:
+      a.type = SV_OP_U1;
+      std::memcpy(a.m, gm.m, 8 * sizeof(double));
+      break;
+    case SV_U2:
+      a.type = SV_OP_U2;
+      std::memcpy(a.m, gm.m, 32 * sizeof(double));
+      break;
+    case SV_D1:
+    case SV_D2: {
+      a.type = SV_OP_DIAG;
+      a.q0 = code(gm.q0);
+      a.q1 = gm.kind == SV_D2 ? code(gm.q1) : 200;
+      for (int i = 0; i < 8; i++) a.m[i] = (i % 2 == 0) ? 1.0 : 0.0;
+      std::memcpy(a.m, gm.m, (gm.kind == SV_D2 ? 8 : 4) * sizeof(double));
+      break;
+    }
+    case SV_SWAP:
+      a.type = 7;
+      break;
+    default:
+      return fail(h, SV_EMALFORMED, "internal: bad gate step");
+  }
+  CUDA_TRY(h, launch_gate(h->dbl, h->sv, h->nL, a, h->st));
+  h->stats.kernel_launches++;
+  return SV_OK;
+}
+
+int check_handle(sv_state* h) {
+  if (!h) return fail(nullptr, SV_EINVAL, "null handle");
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  return SV_OK;
+}
+
+// Sum `count` values of dtype over all ranks in place (device buffer).
+int allreduce(sv_state* h, void* buf, size_t count, int dtype) {
+  if (h->world == 1) return SV_OK;
+  NCCL_TRY(h, h->nc->AllReduce(buf, buf, count, dtype, 0, h->comm, h->st));
+  return SV_OK;
+}
+
+int setup_p2p(sv_state* h, void* base_alloc, size_t base_off) {
+  // Exchange CUDA IPC handles of every rank's shard allocation (NCCL all-gather).
+  struct Rec {
+    cudaIpcMemHandle_t hd;
+    uint64_t off;
+    int32_t ok;
+    char pad[128 - sizeof(cudaIpcMemHandle_t) - 12];
+  };
+  static_assert(sizeof(Rec) == 128, "rec size");
+  Rec mine{};
+  mine.ok = cudaIpcGetMemHandle(&mine.hd, base_alloc) == cudaSuccess ? 1 : 0;
+  cudaGetLastError();
+  mine.off = base_off;
+  if (int rc = ensure_dev(h, h->d_tmp, sizeof(Rec) * (h->world + 1))) return rc;
+  CUDA_TRY(h, cudaMemcpyAsync((char*)h->d_tmp.p + sizeof(Rec) * h->world, &mine, sizeof(Rec), cudaMemcpyHostToDevice, h->st));
+  NCCL_TRY(h, h->nc->AllGather((char*)h->d_tmp.p + sizeof(Rec) * h->world, h->d_tmp.p, sizeof(Rec), Nccl::Uint8, h->comm, h->st));
+  std::vector<Rec> all(h->world);
+  CUDA_TRY(h, cudaMemcpyAsync(all.data(), h->d_tmp.p, sizeof(Rec) * h->world, cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(h, cudaStreamSynchronize(h->st));
+  int ok = 1;
+  for (auto& r : all) ok &= r.ok;
+  h->peers.assign(h->world, nullptr);
+  h->peers[h->rank] = h->sv;
+  for (int r = 0; ok && r < h->world; r++) {
+    if (r == h->rank) continue;
+    void* p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, all[r].hd, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      ok = 0;
+      break;
+    }
+    h->ipc_opened.push_back(p);
+    h->peers[r] = (char*)p + all[r].off;
+  }
+  // agree across ranks
+  float f = ok ? 0.f : 1.f;
+  CUDA_TRY(h, cudaMemcpyAsync(h->d_small.p, &f, sizeof(float), cudaMemcpyHostToDevice, h->st));
+  if (int rc = allreduce(h, h->d_small.p, 1, Nccl::F32)) return rc;
+  CUDA_TRY(h, cudaMemcpyAsync(&f, h->d_small.p, sizeof(float), cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(h, cudaStreamSynchronize(h->st));
+  h->p2p = (f == 0.f);
+  return SV_OK;
+}
+
+}  // namespace
+
+// ====================================================================== ABI
+extern "C" {
+
+int sv_abi_version(void) { return 1; }
+
+const char* sv_last_error(sv_handle h) { return h ? h->err.c_str() : g_last_error.c_str(); }
+
+void sv_free(void* p) { std::free(p); }
+
+int sv_nccl_unique_id(void* out128) {
+  if (!out128) return fail(nullptr, SV_EINVAL, "null output");
+  std::string e;
+  Nccl* n = nccl(e);
+  if (!n) return fail(nullptr, SV_ENCCL, e);
+  int r = n->GetUniqueId(out128);
+  if (r != 0) return fail(nullptr, SV_ENCCL, n->GetErrorString(r));
+  return SV_OK;
+}
+
+int sv_create(int n_qubits, int chunk_bits, sv_precision prec, sv_handle* out) {
+  return sv_create_dist(n_qubits, chunk_bits, prec, 0, 1, nullptr, nullptr, 0, nullptr, out);
+}
+
+int sv_create_dist(int n_qubits, int chunk_bits, sv_precision prec, int rank, int world, const void* uid,
+                   void* ext_dev_buf, size_t ext_bytes, void* cuda_stream, sv_handle* out) {
+  if (!out) return fail(nullptr, SV_EINVAL, "null output handle");
+  *out = nullptr;
+  if (world < 1 || (world & (world - 1))) return fail(nullptr, SV_EINVAL, "world must be a power of two");
+  if (rank < 0 || rank >= world) return fail(nullptr, SV_EINVAL, "rank out of range");
+  if (prec != SV_FP32 && prec != SV_FP64) return fail(nullptr, SV_EINVAL, "bad precision");
+  const int g = __builtin_ctz((unsigned)world);
+  if (n_qubits < 1 || n_qubits > 40) return fail(nullptr, SV_EINVAL, "n_qubits must be in [1, 40]");
+  if (n_qubits - g < 1) return fail(nullptr, SV_EINVAL, "more GPUs than amplitudes");
+  if (chunk_bits < 1 || chunk_bits > n_qubits - g)
+    return fail(nullptr, SV_EINVAL, "chunk_bits must satisfy 1 <= c <= n - log2(world)");
+  if (world > 1 && !uid) return fail(nullptr, SV_EINVAL, "world > 1 needs an NCCL unique id");
+
+  auto* h = new sv_state();
+  h->n = n_qubits;
+  h->c = chunk_bits;
+  h->g = g;
+  h->nL = n_qubits - g;
+  h->rank = rank;
+  h->world = world;
+  h->dbl = prec == SV_FP64;
+  h->amp = h->dbl ? 16 : 8;
+  h->pi.resize(h->n);
+  h->sigma.resize(h->n);
+  std::iota(h->pi.begin(), h->pi.end(), 0);
+  std::iota(h->sigma.begin(), h->sigma.end(), 0);
+  auto bail = [&](int rc) {
+    sv_destroy(h);
+    return rc;
+  };
+  cudaError_t e = cudaGetDevice(&h->device);
+  if (e != cudaSuccess) return bail(fail(nullptr, SV_ECUDA, std::string("no CUDA device: ") + cudaGetErrorString(e)));
+  const size_t bytes = h->amp << h->nL;
+  if (ext_dev_buf) {
+    if (ext_bytes < bytes) return bail(fail(nullptr, SV_ECAPACITY, "ext_dev_buf smaller than the shard"));
+    h->sv = ext_dev_buf;
+  } else {
+    e = cudaMalloc(&h->sv, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      h->sv = nullptr;
+      return bail(fail(nullptr, SV_ECAPACITY, "shard of " + std::to_string(bytes) + " bytes does not fit: " +
+                                                  cudaGetErrorString(e)));
+    }
+    h->own_sv = true;
+  }
+  if (cuda_stream) {
+    h->st = (cudaStream_t)cuda_stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking) != cudaSuccess)
+      return bail(fail(nullptr, SV_ECUDA, "stream creation failed"));
+    h->own_stream = true;
+  }
+  if (cudaEventCreateWithFlags(&h->ev_upload, cudaEventDisableTiming) != cudaSuccess)
+    return bail(fail(nullptr, SV_ECUDA, "event creation failed"));
+  if (int rc = ensure_dev(h, h->d_small, 4096)) return bail(fail(nullptr, rc, h->err));
+  if (cudaMemsetAsync(h->d_small.p, 0, 4096, h->st) != cudaSuccess) return bail(fail(nullptr, SV_ECUDA, "memset"));
+  if (world > 1) {
+    std::string er;
+    h->nc = nccl(er);
+    if (!h->nc) return bail(fail(nullptr, SV_ENCCL, er));
+    int r = nccl_comm_init(h->nc, &h->comm, world, uid, rank);
+    if (r != 0) return bail(fail(nullptr, SV_ENCCL, std::string("ncclCommInitRank: ") + h->nc->GetErrorString(r)));
+    // allocation base of the shard for CUDA IPC
+    void* base = h->sv;
+    size_t off = 0;
+    if (!h->own_sv) {
+      typedef int (*GetRange)(unsigned long long*, size_t*, unsigned long long);
+      void* lib = dlopen("libcuda.so.1", RTLD_NOW | RTLD_NOLOAD);
+      GetRange fn = lib ? (GetRange)dlsym(lib, "cuMemGetAddressRange_v2") : nullptr;
+      unsigned long long b = 0;
+      size_t sz = 0;
+      if (fn && fn(&b, &sz, (unsigned long long)h->sv) == 0) {
+        base = (void*)b;
+        off = (size_t)((char*)h->sv - (char*)base);
+      }
+    }
+    if (int rc = setup_p2p(h, base, off)) return bail(fail(nullptr, rc, h->err));
+  }
+  if (int rc = sv_reset(h, 0)) return bail(rc);
+  *out = h;
+  return SV_OK;
+}
+
+int sv_destroy(sv_handle h) {
+  if (!h) return SV_OK;
+  cudaSetDevice(h->device);
+  if (h->st) cudaStreamSynchronize(h->st);
+  for (void* p : h->ipc_opened) cudaIpcCloseMemHandle(p);
+  if (h->comm && h->nc) h->nc->CommDestroy(h->comm);
+  for (DevBuf* b : {&h->d_prog, &h->d_coef, &h->d_scratch, &h->d_small, &h->d_tmp, &h->d_tmp2, &h->d_stage})
+    if (b->p) cudaFree(b->p);
+  for (PinBuf* b : {&h->h_stage, &h->h_stage2})
+    if (b->p) cudaFreeHost(b->p);
+  if (h->own_sv && h->sv) cudaFree(h->sv);
+  if (h->ev_upload) cudaEventDestroy(h->ev_upload);
+  if (h->own_stream && h->st) cudaStreamDestroy(h->st);
+  cudaGetLastError();
+  delete h;
+  return SV_OK;
+}
+
+int sv_reset(sv_handle h, uint64_t k) {
+  if (int rc = check_handle(h)) return rc;
+  if (h->n < 64 && (k >> h->n)) return fail(h, SV_EINVAL, "basis index out of range");
+  std::iota(h->pi.begin(), h->pi.end(), 0);
+  std::iota(h->sigma.begin(), h->sigma.end(), 0);
+  const int owner = (int)(k >> h->nL);
+  const int64_t off = owner == h->rank ? (int64_t)(k & ((1ull << h->nL) - 1)) : -1;
+  CUDA_TRY(h, launch_set_basis(h->dbl, h->sv, h->nL, off, h->st));
+  h->stats.kernel_launches += off >= 0 ? 1 : 0;
+  return SV_OK;
+}
+
+int sv_synchronize(sv_handle h) {
+  if (int rc = check_handle(h)) return rc;
+  CUDA_TRY(h, cudaStreamSynchronize(h->st));
+  return SV_OK;
+}
+
+int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t flags) {
+  if (int rc = check_handle(h)) return rc;
+  if (n_gates && !gates) return fail(h, SV_EINVAL, "null gate array");
+  const double t0 = now_ms();
+  std::vector<int> pi = h->pi, sigma = h->sigma;
+  std::vector<Step> steps;
+  PlanCounters ctr;
+  Status s = make_plan(gates, n_gates, h->n, h->c, h->g, pi, sigma, flags, steps, ctr);
+  if (!s.good()) return fail(h, s);
+  h->prog.clear();
+  const int T_default = 12;
+  for (const Step& st : steps) {
+    if (st.type != Step::SECTION) continue;
+    Status cs = compile_section(st.gates, h->nL, h->rank, h->g, T_default, h->dbl ? 3 : 4, h->prog);
+    if (!cs.good()) return fail(h, cs);
+    const Launch& L = h->prog.launches.back();
+    if (L.T > 13)
+      return fail(h, SV_ECAPACITY, "a section needs a tile larger than shared memory (lower chunk_bits)");
+  }
+  h->stats.pass_ms = now_ms() - t0;
+  if (int rc = upload_program(h)) return rc;
+  size_t si = 0;
+  for (const Step& st : steps) {
+    switch (st.type) {
+      case Step::EXCHANGE:
+        if (int rc = do_exchange(h, st.ex, flags)) return rc;
+        break;
+      case Step::SECTION: {
+        const Launch& L = h->prog.launches[si++];
+        CUDA_TRY(h, launch_section(h->dbl, h->sv, (const int*)h->d_prog.p + L.int_off, h->d_coef.p, L.T, L.r, L.n_out, h->st));
+        h->stats.kernel_launches++;
+        h->stats.sections++;
+        break;
+      }
+      case Step::GATE:
+        if (int rc = gate_step(h, st.gates[0])) return rc;
+        break;
+    }
+  }
+  h->pi = pi;
+  h->sigma = sigma;
+  h->stats.circuits++;
+  h->stats.gates += n_gates;
+  h->stats.chunk_swaps += ctr.chunk_swaps;
+  h->stats.apply_ms = now_ms() - t0;
+  return SV_OK;
+}
+
+int sv_get_permutation(sv_handle h, int32_t* out) {
+  if (!h || !out) return fail(h, SV_EINVAL, "null argument");
+  for (int q = 0; q < h->n; q++) out[q] = h->pi[q];
+  return SV_OK;
+}
+
+int sv_stats_get(sv_handle h, sv_stats* out) {
+  if (!h || !out) return fail(h, SV_EINVAL, "null argument");
+  *out = h->stats;
+  return SV_OK;
+}
+
+int sv_norm(sv_handle h, double* out) {
+  if (int rc = check_handle(h)) return rc;
+  if (!out) return fail(h, SV_EINVAL, "null output");
+  if (int rc = ensure_dev(h, h->d_scratch, norm_scratch_doubles() * sizeof(double))) return rc;
+  CUDA_TRY(h, launch_norm(h->dbl, h->sv, h->nL, (double*)h->d_scratch.p, (double*)h->d_small.p + 8, h->st));
+  h->stats.kernel_launches += 2;
+  if (int rc = allreduce(h, (double*)h->d_small.p + 8, 1, Nccl::F64)) return rc;
+  CUDA_TRY(h, cudaMemcpyAsync(out, (double*)h->d_small.p + 8, sizeof(double), cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(h, cudaStreamSynchronize(h->st));
+  return SV_OK;
+}
+
+int sv_probabilities(sv_handle h, const int32_t* qubits, int nq, double* host_out) {
+  if (int rc = check_handle(h)) return rc;
+  if (nq < 0 || nq > 24 || (nq && (!qubits || !host_out))) return fail(h, SV_EINVAL, "bad qubit list (nq <= 24)");
+  uint64_t seen = 0;
+  std::vector<int> loc_bits, loc_pos;
+  int rank_part = 0;
+  for (int i = 0; i < nq; i++) {
+    const int q = qubits[i];
+    if (q < 0 || q >= h->n || ((seen >> q) & 1)) return fail(h, SV_EINVAL, "bad or duplicate qubit");
+    seen |= 1ull << q;
+    const int mb = h->sigma[h->pi[q]];
+    if (mb < h->nL) {
+      loc_bits.push_back(mb);
+      loc_pos.push_back(i);
+    } else {
+      rank_part |= ((h->rank >> (mb - h->nL)) & 1) << i;
+    }
+  }
+  const int nl = (int)loc_bits.size();
+  const size_t bins_l = size_t(1) << nl, bins = size_t(1) << nq;
+  if (int rc = ensure_dev(h, h->d_scratch, std::max(marginal_scratch_doubles(nl), norm_scratch_doubles()) * sizeof(double))) return rc;
+  if (int rc = ensure_dev(h, h->d_tmp, bins * sizeof(double))) return rc;
+  CUDA_TRY(h, launch_marginal(h->dbl, h->sv, h->nL, loc_bits.data(), nl, (double*)h->d_scratch.p, (double*)h->d_tmp.p, h->st));
+  h->stats.kernel_launches += 2;
+  if (h->world == 1) {
+    CUDA_TRY(h, cudaMemcpyAsync(host_out, h->d_tmp.p, bins * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+    CUDA_TRY(h, cudaStreamSynchronize(h->st));
+    return SV_OK;
+  }
+  std::vector<double> loc(bins_l);
+  CUDA_TRY(h, cudaMemcpyAsync(loc.data(), h->d_tmp.p, bins_l * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(h, cudaStreamSynchronize(h->st));
+  std::vector<double> full(bins, 0.0);
+  for (size_t y = 0; y < bins_l; y++) {
+    size_t o = rank_part;
+    for (int j = 0; j < nl; j++) o |= ((y >> j) & 1) << loc_pos[j];
+    full[o] = loc[y];
+  }
+  CUDA_TRY(h, cudaMemcpyAsync(h->d_tmp.p, full.data(), bins * sizeof(double), cudaMemcpyHostToDevice, h->st));
+  if (int rc = allreduce(h, h->d_tmp.p, bins, Nccl::F64)) return rc;
+  CUDA_TRY(h, cudaMemcpyAsync(host_out, h->d_tmp.p, bins * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(h, cudaStreamSynchronize(h->st));
+  return SV_OK;
+}
+
+int sv_get_amplitudes(sv_handle h, const uint64_t* idx, size_t cnt, void* host_out) {
+  if (int rc = check_handle(h)) return rc;
+  if (cnt == 0) return SV_OK;
+  if (!idx || !host_out) return fail(h, SV_EINVAL, "null argument");
+  const BitPerm mu = mu_of(h);
+  const uint64_t lmask = (1ull << h->nL) - 1;
+  const size_t chunk = 1 << 20;
+  if (int rc = ensure_pin(h, h->h_stage2, chunk * sizeof(uint64_t))) return rc;
+  if (int rc = ensure_dev(h, h->d_tmp, chunk * sizeof(uint64_t))) return rc;
+  if (int rc = ensure_dev(h, h->d_tmp2, chunk * h->amp)) return rc;
+  for (size_t b = 0; b < cnt; b += chunk) {
+    const size_t m = std::min(chunk, cnt - b);
+    CUDA_TRY(h, cudaStreamSynchronize(h->st));  // staging reuse
+    uint64_t* offs = (uint64_t*)h->h_stage2.p;
+    for (size_t i = 0; i < m; i++) {
+      const uint64_t x = idx[b + i];
+      if (h->n < 64 && (x >> h->n)) return fail(h, SV_EINVAL, "amplitude index out of range");
+      const uint64_t mem = mu(x);
+      offs[i] = (int)(mem >> h->nL) == h->rank ? (mem & lmask) : ~0ull;
+    }
+    CUDA_TRY(h, cudaMemcpyAsync(h->d_tmp.p, offs, m * sizeof(uint64_t), cudaMemcpyHostToDevice, h->st));
+    CUDA_TRY(h, launch_gather(h->dbl, h->sv, (const uint64_t*)h->d_tmp.p, m, h->d_tmp2.p, h->st));
+    h->stats.kernel_launches++;
+    if (int rc = allreduce(h, h->d_tmp2.p, 2 * m, h->dbl ? Nccl::F64 : Nccl::F32)) return rc;
+    CUDA_TRY(h, cudaMemcpyAsync((char*)host_out + b * h->amp, h->d_tmp2.p, m * h->amp, cudaMemcpyDeviceToHost, h->st));
+  }
+  CUDA_TRY(h, cudaStreamSynchronize(h->st));
+  return SV_OK;
+}
+
+int sv_get_state(sv_handle h, void* host_out) {
+  if (int rc = check_handle(h)) return rc;
+  if (h->rank == 0 && !host_out) return fail(h, SV_EINVAL, "null output");
+  const BitPerm inv = mu_inv_of(h);
+  const size_t piece = std::min<size_t>(size_t(1) << h->nL, (size_t(256) << 20) / h->amp);
+  const size_t shard = size_t(1) << h->nL;
+  if (int rc = ensure_pin(h, h->h_stage2, piece * h->amp)) return rc;
+  if (h->world > 1)
+    if (int rc = ensure_dev(h, h->d_stage, piece * h->amp)) return rc;
+  for (int src = 0; src < h->world; src++) {
+    for (size_t off = 0; off < shard; off += piece) {
+      const size_t cnt = std::min(piece, shard - off);
+      const void* dev = (char*)h->sv + off * h->amp;
+      if (src != 0) {
+        if (h->rank == src) {
+          NCCL_TRY(h, h->nc->Send(dev, cnt * h->amp, Nccl::Uint8, 0, h->comm, h->st));
+        } else if (h->rank == 0) {
+          NCCL_TRY(h, h->nc->Recv(h->d_stage.p, cnt * h->amp, Nccl::Uint8, src, h->comm, h->st));
+          dev = h->d_stage.p;
+        }
+      }
+      if (h->rank != 0) continue;
+      CUDA_TRY(h, cudaMemcpyAsync(h->h_stage2.p, dev, cnt * h->amp, cudaMemcpyDeviceToHost, h->st));
+      CUDA_TRY(h, cudaStreamSynchronize(h->st));
+      const uint64_t mbase = ((uint64_t)src << h->nL) + off;
+      const char* in = (const char*)h->h_stage2.p;
+      char* o = (char*)host_out;
+      for (size_t i = 0; i < cnt; i++) std::memcpy(o + inv(mbase + i) * h->amp, in + i * h->amp, h->amp);
+    }
+  }
+  CUDA_TRY(h, cudaStreamSynchronize(h->st));
+  return SV_OK;
+}
+
+static uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  uint64_t z = x;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+int sv_sample(sv_handle h, size_t shots, uint64_t seed, uint64_t* host_out) {
+  if (int rc = check_handle(h)) return rc;
+  if (shots == 0) return SV_OK;
+  if (!host_out) return fail(h, SV_EINVAL, "null output");
+  const int B = std::min(12, h->nL);
+  const size_t nblk = size_t(1) << (h->nL - B);
+  if (int rc = ensure_dev(h, h->d_tmp, nblk * sizeof(double) + 64)) return rc;
+  CUDA_TRY(h, launch_block_sums(h->dbl, h->sv, h->nL, B, (double*)h->d_tmp.p, h->st));
+  h->stats.kernel_launches++;
+  std::vector<double> bs(nblk);
+  CUDA_TRY(h, cudaMemcpyAsync(bs.data(), h->d_tmp.p, nblk * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(h, cudaStreamSynchronize(h->st));
+  std::vector<double> cum(nblk);
+  double tot = 0.0;
+  for (size_t i = 0; i < nblk; i++) {
+    tot += bs[i];
+    cum[i] = tot;
+  }
+  std::vector<double> totals(h->world, 0.0);
+  totals[h->rank] = tot;
+  if (h->world > 1) {
+    CUDA_TRY(h, cudaMemcpyAsync(h->d_tmp.p, totals.data(), h->world * sizeof(double), cudaMemcpyHostToDevice, h->st));
+    if (int rc = allreduce(h, h->d_tmp.p, h->world, Nccl::F64)) return rc;
+    CUDA_TRY(h, cudaMemcpyAsync(totals.data(), h->d_tmp.p, h->world * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+    CUDA_TRY(h, cudaStreamSynchronize(h->st));
+  }
+  double before = 0.0;
+  for (int r = 0; r < h->rank; r++) before += totals[r];
+  const double mine_end = before + tot;
+  const bool last = h->rank == h->world - 1;
+  // u_s, sorted; shots in [before, mine_end) (the last rank also takes u >= total)
+  std::vector<std::pair<double, size_t>> us(shots);
+  for (size_t s = 0; s < shots; s++) us[s] = {(double)(splitmix64(seed ^ (uint64_t)s) >> 11) * 0x1.0p-53, s};
+  std::sort(us.begin(), us.end());
+  std::vector<int64_t> items;
+  std::vector<double> resid;
+  std::vector<size_t> who;
+  size_t bi = 0;
+  for (auto& pr : us) {
+    const double u = pr.first;
+    if (u < before || (u >= mine_end && !last)) continue;
+    double r = u - before;
+    while (bi + 1 < nblk && cum[bi] <= r) bi++;
+    const double r2 = r - (bi ? cum[bi - 1] : 0.0);
+    if (!items.empty() && items[items.size() - 3] == (int64_t)bi) {
+      items.back()++;
+    } else {
+      items.push_back((int64_t)bi);
+      items.push_back((int64_t)resid.size());
+      items.push_back(1);
+    }
+    resid.push_back(r2);
+    who.push_back(pr.second);
+  }
+  std::vector<uint64_t> res(shots, 0);
+  const size_t nit = items.size() / 3, nsh = resid.size();
+  if (nsh) {
+    if (int rc = ensure_dev(h, h->d_tmp2, items.size() * 8 + nsh * 8 + nsh * 8 + 64)) return rc;
+    char* d = (char*)h->d_tmp2.p;
+    int64_t* d_items = (int64_t*)d;
+    double* d_res = (double*)(d + items.size() * 8);
+    uint64_t* d_off = (uint64_t*)(d + items.size() * 8 + nsh * 8);
+    CUDA_TRY(h, cudaMemcpyAsync(d_items, items.data(), items.size() * 8, cudaMemcpyHostToDevice, h->st));
+    CUDA_TRY(h, cudaMemcpyAsync(d_res, resid.data(), nsh * 8, cudaMemcpyHostToDevice, h->st));
+    CUDA_TRY(h, launch_sample_resolve(h->dbl, h->sv, B, d_items, (int)nit, d_res, d_off, h->st));
+    h->stats.kernel_launches++;
+    std::vector<uint64_t> offs(nsh);
+    CUDA_TRY(h, cudaMemcpyAsync(offs.data(), d_off, nsh * 8, cudaMemcpyDeviceToHost, h->st));
+    CUDA_TRY(h, cudaStreamSynchronize(h->st));
+    const BitPerm inv = mu_inv_of(h);
+    for (size_t i = 0; i < nsh; i++) res[who[i]] = inv(((uint64_t)h->rank << h->nL) | offs[i]);
+  }
+  if (h->world > 1) {
+    if (int rc = ensure_dev(h, h->d_tmp, shots * 8)) return rc;
+    CUDA_TRY(h, cudaMemcpyAsync(h->d_tmp.p, res.data(), shots * 8, cudaMemcpyHostToDevice, h->st));
+    if (int rc = allreduce(h, h->d_tmp.p, shots, Nccl::Uint64)) return rc;
+    CUDA_TRY(h, cudaMemcpyAsync(res.data(), h->d_tmp.p, shots * 8, cudaMemcpyDeviceToHost, h->st));
+    CUDA_TRY(h, cudaStreamSynchronize(h->st));
+  }
+  std::memcpy(host_out, res.data(), shots * 8);
+  return SV_OK;
+}
+
+int sv_block_circuit(const sv_gate* gates, size_t n_gates, int n, int c, const int32_t* pi0, uint32_t flags,
+                     sv_gate** out, size_t* n_out, int32_t* pi_final) {
+  if (!out || !n_out || (n_gates && !gates)) return fail(nullptr, SV_EINVAL, "null argument");
+  std::vector<int> pi(n > 0 ? n : 0);
+  if (n < 1 || n > 63) return fail(nullptr, SV_EINVAL, "n out of range");
+  for (int q = 0; q < n; q++) pi[q] = pi0 ? pi0[q] : q;
+  std::vector<sv_gate> tokens;
+  Status s = block_pass(gates, n_gates, n, c, pi, flags, tokens);
+  if (!s.good()) return fail(nullptr, s);
+  sv_gate* buf = (sv_gate*)std::malloc(sizeof(sv_gate) * std::max<size_t>(tokens.size(), 1));
+  if (!buf) return fail(nullptr, SV_ECAPACITY, "out of host memory");
+  if (!tokens.empty()) std::memcpy(buf, tokens.data(), sizeof(sv_gate) * tokens.size());
+  *out = buf;
+  *n_out = tokens.size();
+  if (pi_final)
+    for (int q = 0; q < n; q++) pi_final[q] = pi[q];
+  return SV_OK;
+}
+
+int sv_plan_circuit(const sv_gate* gates, size_t n_gates, int n, int c, int world_log2, const int32_t* pi0,
+                    const int32_t* sigma0, uint32_t flags, sv_gate** out, size_t* n_out, int32_t* pi_final,
+                    int32_t* sigma_final) {
+  if (!out || !n_out || (n_gates && !gates)) return fail(nullptr, SV_EINVAL, "null argument");
+  if (n < 1 || n > 63) return fail(nullptr, SV_EINVAL, "n out of range");
+  std::vector<int> pi(n), sigma(n);
+  for (int q = 0; q < n; q++) {
+    pi[q] = pi0 ? pi0[q] : q;
+    sigma[q] = sigma0 ? sigma0[q] : q;
+  }
+  std::vector<Step> steps;
+  PlanCounters ctr;
+  Status s = make_plan(gates, n_gates, n, c, world_log2, pi, sigma, flags, steps, ctr);
+  if (!s.good()) return fail(nullptr, s);
+  std::vector<sv_gate> recs;
+  sv_gate mk;
+  std::memset(&mk, 0, sizeof(mk));
+  for (size_t i = 0; i < steps.size(); i++) {
+    const Step& st = steps[i];
+    if (st.type == Step::EXCHANGE) {
+      for (const ExPair& p : st.ex) {
+        sv_gate r = mk;
+        r.kind = SV_EXCHANGE;
+        r.q0 = p.m;
+        r.q1 = p.b;
+        r.pad = (int32_t)i;
+        recs.push_back(r);
+      }
+    } else {
+      sv_gate b = mk;
+      b.kind = SV_BEGIN;
+      b.q0 = b.q1 = -1;
+      b.pad = (int32_t)i;
+      recs.push_back(b);
+      for (const sv_gate& gm : st.gates) recs.push_back(gm);
+      b.kind = SV_END;
+      recs.push_back(b);
+    }
+  }
+  sv_gate* buf = (sv_gate*)std::malloc(sizeof(sv_gate) * std::max<size_t>(recs.size(), 1));
+  if (!buf) return fail(nullptr, SV_ECAPACITY, "out of host memory");
+  if (!recs.empty()) std::memcpy(buf, recs.data(), sizeof(sv_gate) * recs.size());
+  *out = buf;
+  *n_out = recs.size();
+  for (int q = 0; q < n; q++) {
+    if (pi_final) pi_final[q] = pi[q];
+    if (sigma_final) sigma_final[q] = sigma[q];
+  }
+  return SV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,63 @@
+// common.h — internal helpers shared by the host C++ and CUDA sources of libsv.so.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/sv.h"
+
+namespace sv {
+
+inline bool is_diag(int kind) { return kind == SV_D1 || kind == SV_D2; }
+inline bool is_two(int kind) {
+  return kind == SV_U2 || kind == SV_D2 || kind == SV_SWAP || kind == SV_CHUNK_SWAP || kind == SV_EXCHANGE;
+}
+inline bool is_one(int kind) { return kind == SV_U1 || kind == SV_D1; }
+inline uint64_t qmask(const sv_gate& g) {
+  uint64_t m = 0;
+  if (is_one(g.kind)) m = 1ull << g.q0;
+  if (is_two(g.kind)) m = (1ull << g.q0) | (1ull << g.q1);
+  return m;
+}
+
+// Status carried through the host code; converted to an int + message at the ABI.
+struct Status {
+  int code = SV_OK;
+  std::string msg;
+  static Status ok() { return {}; }
+  static Status err(int c, std::string m) {
+    Status s;
+    s.code = c;
+    s.msg = std::move(m);
+    return s;
+  }
+  bool good() const { return code == SV_OK; }
+};
+
+// Validate input gate records (kinds SV_U1..SV_SWAP, qubits in range and distinct).
+Status validate_gates(const sv_gate* g, size_t count, int n);
+
+// ---- blocking pass (blocking.cpp): Listing 3 of the paper, DESIGN readings R2-R6 ----------
+// tokens: SV_CHUNK_SWAP(q0<q1), SV_BEGIN, SV_END, and gates on physical qubits with pad = index.
+Status block_pass(const sv_gate* g, size_t count, int n, int c, std::vector<int>& pi, uint32_t flags,
+                  std::vector<sv_gate>& tokens);
+
+// ---- executor plan (plan.cpp) ---------------------------------------------------------------
+struct ExPair {
+  int m;  // local memory bit
+  int b;  // rank memory bit (>= nL)
+};
+struct Step {
+  enum Type { EXCHANGE = 0, SECTION = 1, GATE = 2 } type;
+  std::vector<ExPair> ex;        // EXCHANGE
+  std::vector<sv_gate> gates;    // SECTION / GATE: memory-frame gates (no SWAP inside SECTION)
+};
+struct PlanCounters {
+  uint64_t sections = 0, chunk_swaps = 0, exchanges = 0, exchange_batches = 0;
+};
+// Runs the pass (unless SV_UNBLOCKED) and maps it onto memory bits: every chunk_swap / SWAP is a
+// relabel of sigma; data moves only where a section needs a rank bit (DESIGN "Executor mapping").
+Status make_plan(const sv_gate* g, size_t count, int n, int c, int world_log2, std::vector<int>& pi,
+                 std::vector<int>& sigma, uint32_t flags, std::vector<Step>& steps, PlanCounters& ctr);
+
+}  // namespace sv

@@ -1,0 +1,834 @@
+// kernels.cu — sm_100a kernels of the cache-blocked state-vector path.
+//
+//   K1 k_section      one HBM read + one HBM write of the shard per blocked section:
+//                     a CTA gathers its 2^T-amplitude tile into shared memory (XOR-fold swizzle),
+//                     runs the section's phases (each thread holds 16 amplitudes in registers and
+//                     applies every gate of the phase there), and writes the tile back once.
+//   K2 k_gate_*       per-gate baseline: one pass per gate with the pair addressing of Listing 2
+//                     (P:242-254), 64-bit indices (the listing's 32-bit int would overflow).
+//   K5 reductions     norm, marginal probabilities, block masses and shot resolution.
+//   K6 k_set_basis    |k>.
+//   K7 k_gather       amplitude gather.
+//   exchange          peer-memory swap of local bit(s) with rank bit(s) over NVLink.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+
+#include "kernels.cuh"
+#include "program.h"
+
+namespace sv {
+namespace {
+
+constexpr int kRedBlocks = 148 * 8;  // fixed grid for deterministic reductions
+constexpr int kRedThreads = 256;
+
+// ------------------------------------------------------------------ complex helpers
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+// acc + m * a
+__device__ __forceinline__ double2 cfma(double2 m, double2 a, double2 acc) {
+  acc.x = fma(m.x, a.x, acc.x);
+  acc.x = fma(-m.y, a.y, acc.x);
+  acc.y = fma(m.x, a.y, acc.y);
+  acc.y = fma(m.y, a.x, acc.y);
+  return acc;
+}
+__device__ __forceinline__ float2 cfma(float2 m, float2 a, float2 acc) {
+  acc.x = fmaf(m.x, a.x, acc.x);
+  acc.x = fmaf(-m.y, a.y, acc.x);
+  acc.y = fmaf(m.x, a.y, acc.y);
+  acc.y = fmaf(m.y, a.x, acc.y);
+  return acc;
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+__device__ __forceinline__ double abs2(double2 a) { return fma(a.x, a.x, a.y * a.y); }
+__device__ __forceinline__ double abs2(float2 a) { return (double)a.x * a.x + (double)a.y * a.y; }
+template <typename V> __device__ __forceinline__ V czero();
+template <> __device__ __forceinline__ double2 czero<double2>() { return make_double2(0.0, 0.0); }
+template <> __device__ __forceinline__ float2 czero<float2>() { return make_float2(0.f, 0.f); }
+template <typename V> __device__ __forceinline__ V cone();
+template <> __device__ __forceinline__ double2 cone<double2>() { return make_double2(1.0, 0.0); }
+template <> __device__ __forceinline__ float2 cone<float2>() { return make_float2(1.f, 0.f); }
+
+__device__ __forceinline__ double2 ldc(const double2* p) { return __ldg(p); }
+__device__ __forceinline__ float2 ldc(const float2* p) { return __ldg(p); }
+// volatile: keeps matrix elements out of long-lived registers (reloaded per use, L1 broadcast)
+__device__ __forceinline__ double2 ldv(const double2* p) {
+  double2 r;
+  asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float2 ldv(const float2* p) {
+  float2 r;
+  asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(r.x), "=f"(r.y) : "l"(p));
+  return r;
+}
+
+template <typename V>
+__device__ __forceinline__ V sel4(int s, V a0, V a1, V a2, V a3) {
+  return s == 0 ? a0 : (s == 1 ? a1 : (s == 2 ? a2 : a3));
+}
+
+// XOR-fold swizzle of a tile element index: the low G bits are XORed with every higher G-bit
+// group.  GF(2)-linear, so swz(a | b) = swz(a) ^ swz(b) for disjoint a, b.
+template <int G>
+__device__ __forceinline__ int swz(int i) {
+  int x = i >> G, f = 0;
+#pragma unroll
+  for (int j = 0; j < 5; j++) {
+    f ^= x;
+    x >>= G;
+  }
+  return i ^ (f & ((1 << G) - 1));
+}
+
+// ------------------------------------------------------------------ register-slot gates
+template <int S0, int S1, typename V>
+__device__ __forceinline__ void u2_slots(V (&v)[16], const V* __restrict__ m) {
+#pragma unroll
+  for (int q = 0; q < 16; q++) {
+    if (((q >> S0) & 1) || ((q >> S1) & 1)) continue;
+    const int i0 = q, i1 = q | (1 << S0), i2 = q | (1 << S1), i3 = q | (1 << S0) | (1 << S1);
+    const V a0 = v[i0], a1 = v[i1], a2 = v[i2], a3 = v[i3];
+#pragma unroll
+    for (int rr = 0; rr < 4; rr++) {
+      V acc = cmul(ldv(m + 4 * rr + 0), a0);
+      acc = cfma(ldv(m + 4 * rr + 1), a1, acc);
+      acc = cfma(ldv(m + 4 * rr + 2), a2, acc);
+      acc = cfma(ldv(m + 4 * rr + 3), a3, acc);
+      v[rr == 0 ? i0 : (rr == 1 ? i1 : (rr == 2 ? i2 : i3))] = acc;
+    }
+  }
+}
+
+template <typename V>
+__device__ __forceinline__ void op_u2(V (&v)[16], int a, int b, const V* __restrict__ m) {
+  switch (a * 4 + b) {
+    case 1: u2_slots<0, 1>(v, m); break;
+    case 2: u2_slots<0, 2>(v, m); break;
+    case 3: u2_slots<0, 3>(v, m); break;
+    case 4: u2_slots<1, 0>(v, m); break;
+    case 6: u2_slots<1, 2>(v, m); break;
+    case 7: u2_slots<1, 3>(v, m); break;
+    case 8: u2_slots<2, 0>(v, m); break;
+    case 9: u2_slots<2, 1>(v, m); break;
+    case 11: u2_slots<2, 3>(v, m); break;
+    case 12: u2_slots<3, 0>(v, m); break;
+    case 13: u2_slots<3, 1>(v, m); break;
+    case 14: u2_slots<3, 2>(v, m); break;
+    default: break;
+  }
+}
+
+template <int S, typename V>
+__device__ __forceinline__ void u1_slot(V (&v)[16], const V* __restrict__ m) {
+  const V m0 = ldc(m), m1 = ldc(m + 1), m2 = ldc(m + 2), m3 = ldc(m + 3);
+#pragma unroll
+  for (int q = 0; q < 16; q++) {
+    if ((q >> S) & 1) continue;
+    const V a0 = v[q], a1 = v[q | (1 << S)];
+    v[q] = cfma(m1, a1, cmul(m0, a0));
+    v[q | (1 << S)] = cfma(m3, a1, cmul(m2, a0));
+  }
+}
+
+template <typename V>
+__device__ __forceinline__ void op_u1(V (&v)[16], int a, const V* __restrict__ m) {
+  switch (a) {
+    case 0: u1_slot<0>(v, m); break;
+    case 1: u1_slot<1>(v, m); break;
+    case 2: u1_slot<2>(v, m); break;
+    case 3: u1_slot<3>(v, m); break;
+    default: break;
+  }
+}
+
+template <int S, typename V, typename R>
+__device__ __forceinline__ void h1_slot(V (&v)[16], R s) {
+#pragma unroll
+  for (int q = 0; q < 16; q++) {
+    if ((q >> S) & 1) continue;
+    const V a0 = v[q], a1 = v[q | (1 << S)];
+    v[q] = cscale(cadd(a0, a1), s);
+    v[q | (1 << S)] = cscale(csub(a0, a1), s);
+  }
+}
+
+template <typename V, typename R>
+__device__ __forceinline__ void op_h1(V (&v)[16], int a, R s) {
+  switch (a) {
+    case 0: h1_slot<0>(v, s); break;
+    case 1: h1_slot<1>(v, s); break;
+    case 2: h1_slot<2>(v, s); break;
+    case 3: h1_slot<3>(v, s); break;
+    default: break;
+  }
+}
+
+template <int S0, int S1, typename V>
+__device__ __forceinline__ void perm_slots(V (&v)[16], int perm) {
+  const int p0 = perm & 3, p1 = (perm >> 2) & 3, p2 = (perm >> 4) & 3, p3 = (perm >> 6) & 3;
+#pragma unroll
+  for (int q = 0; q < 16; q++) {
+    if (((q >> S0) & 1) || ((q >> S1) & 1)) continue;
+    const int i0 = q, i1 = q | (1 << S0), i2 = q | (1 << S1), i3 = q | (1 << S0) | (1 << S1);
+    const V a0 = v[i0], a1 = v[i1], a2 = v[i2], a3 = v[i3];
+    v[i0] = sel4(p0, a0, a1, a2, a3);
+    v[i1] = sel4(p1, a0, a1, a2, a3);
+    v[i2] = sel4(p2, a0, a1, a2, a3);
+    v[i3] = sel4(p3, a0, a1, a2, a3);
+  }
+}
+
+template <typename V>
+__device__ __forceinline__ void op_perm(V (&v)[16], int a, int b, int perm) {
+  switch (a * 4 + b) {
+    case 1: perm_slots<0, 1>(v, perm); break;
+    case 2: perm_slots<0, 2>(v, perm); break;
+    case 3: perm_slots<0, 3>(v, perm); break;
+    case 4: perm_slots<1, 0>(v, perm); break;
+    case 6: perm_slots<1, 2>(v, perm); break;
+    case 7: perm_slots<1, 3>(v, perm); break;
+    case 8: perm_slots<2, 0>(v, perm); break;
+    case 9: perm_slots<2, 1>(v, perm); break;
+    case 11: perm_slots<2, 3>(v, perm); break;
+    case 12: perm_slots<3, 0>(v, perm); break;
+    case 13: perm_slots<3, 1>(v, perm); break;
+    case 14: perm_slots<3, 2>(v, perm); break;
+    default: break;
+  }
+}
+
+__device__ __forceinline__ int code_bit(int code, int idx, uint64_t tile_off) {
+  if (code < 100) return (idx >> code) & 1;
+  if (code < 200) return (int)((tile_off >> (code - 100)) & 1ull);
+  return code - 200;
+}
+
+// ------------------------------------------------------------------ K1: section kernel
+template <typename V, int G, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
+    k_section(V* __restrict__ sv, const int* __restrict__ prog, const V* __restrict__ coef) {
+  using R = decltype(V().x);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* sm = reinterpret_cast<V*>(smem_raw);
+  const SvSecHeader* H = reinterpret_cast<const SvSecHeader*>(prog);
+  const int T = H->T, r = H->r, n_out = H->n_out;
+  const int nt_log = T - r;
+  const int nreg = 1 << r;
+  const int tid = threadIdx.x;
+
+  uint64_t tile_off = 0;
+  {
+    const uint64_t bid = blockIdx.x;
+    for (int j = 0; j < n_out; j++) tile_off |= ((bid >> j) & 1ull) << H->out_bits[j];
+  }
+  uint64_t off_t = 0;
+  for (int j = 0; j < nt_log; j++) off_t |= (uint64_t)((tid >> j) & 1) << H->tile_bits[j];
+  uint64_t hb[SV_R_BITS];
+  int hs[SV_R_BITS];
+#pragma unroll
+  for (int j = 0; j < SV_R_BITS; j++) {
+    hb[j] = j < r ? (1ull << H->tile_bits[nt_log + j]) : 0ull;
+    hs[j] = j < r ? swz<G>(1 << (nt_log + j)) : 0;
+  }
+  const int pt = swz<G>(tid);
+
+  V v[16];
+  const V* src = sv + (tile_off | off_t);
+#pragma unroll
+  for (int k = 0; k < 16; k++) {
+    v[k] = czero<V>();
+    if (k < nreg) {
+      uint64_t o = 0;
+#pragma unroll
+      for (int j = 0; j < SV_R_BITS; j++)
+        if ((k >> j) & 1) o |= hb[j];
+      v[k] = src[o];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 16; k++) {
+    if (k < nreg) {
+      int x = pt;
+#pragma unroll
+      for (int j = 0; j < SV_R_BITS; j++)
+        if ((k >> j) & 1) x ^= hs[j];
+      sm[x] = v[k];
+    }
+  }
+  __syncthreads();
+
+  const SvPhase* P = reinterpret_cast<const SvPhase*>(prog + H->phase_off);
+  const SvOp* O = reinterpret_cast<const SvOp*>(prog + H->op_off);
+  const int nph = H->n_phases;
+  for (int ph = 0; ph < nph; ph++) {
+    const SvPhase* p = P + ph;
+    int base = 0;
+    for (int j = 0; j < nt_log; j++) base |= ((tid >> j) & 1) << p->tpos[j];
+    const int pb = swz<G>(base);
+    int rb[SV_R_BITS], w[SV_R_BITS];
+#pragma unroll
+    for (int s = 0; s < SV_R_BITS; s++) {
+      rb[s] = s < r ? (1 << p->R[s]) : 0;
+      w[s] = swz<G>(rb[s]);
+    }
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+      if (k < nreg) {
+        int x = pb;
+#pragma unroll
+        for (int s = 0; s < SV_R_BITS; s++)
+          if ((k >> s) & 1) x ^= w[s];
+        v[k] = sm[x];
+      }
+    }
+    const int ob = p->op_begin, oc = p->op_count;
+    for (int oi = 0; oi < oc; oi++) {
+      const int4 h = __ldg(reinterpret_cast<const int4*>(O + ob + oi));
+      const int4 h2 = __ldg(reinterpret_cast<const int4*>(O + ob + oi) + 1);
+      const int type = h.x, a = h.y, b = h.z;
+      const V* c = coef + h.w;
+      switch (type) {
+        case SV_OP_U2: op_u2(v, a, b, c); break;
+        case SV_OP_U1: op_u1(v, a, c); break;
+        case SV_OP_H1: op_h1(v, a, (R)ldc(c).x); break;
+        case SV_OP_PERM2: op_perm(v, a, b, h2.x); break;
+        case SV_OP_DIAG: {
+          const V d0 = ldc(c), d1 = ldc(c + 1), d2 = ldc(c + 2), d3 = ldc(c + 3);
+#pragma unroll
+          for (int k = 0; k < 16; k++) {
+            if (k < nreg) {
+              int idx = base;
+#pragma unroll
+              for (int s = 0; s < SV_R_BITS; s++)
+                if ((k >> s) & 1) idx |= rb[s];
+              const int sidx = code_bit(a, idx, tile_off) | (code_bit(b, idx, tile_off) << 1);
+              v[k] = cmul(v[k], sel4(sidx, d0, d1, d2, d3));
+            }
+          }
+          break;
+        }
+        case SV_OP_DIAG_CP: {
+          const V d3 = ldc(c);
+#pragma unroll
+          for (int k = 0; k < 16; k++) {
+            if (k < nreg) {
+              int idx = base;
+#pragma unroll
+              for (int s = 0; s < SV_R_BITS; s++)
+                if ((k >> s) & 1) idx |= rb[s];
+              if (code_bit(a, idx, tile_off) & code_bit(b, idx, tile_off)) v[k] = cmul(v[k], d3);
+            }
+          }
+          break;
+        }
+        default: break;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+      if (k < nreg) {
+        int x = pb;
+#pragma unroll
+        for (int s = 0; s < SV_R_BITS; s++)
+          if ((k >> s) & 1) x ^= w[s];
+        sm[x] = v[k];
+      }
+    }
+    __syncthreads();
+  }
+
+#pragma unroll
+  for (int k = 0; k < 16; k++) {
+    if (k < nreg) {
+      int x = pt;
+#pragma unroll
+      for (int j = 0; j < SV_R_BITS; j++)
+        if ((k >> j) & 1) x ^= hs[j];
+      v[k] = sm[x];
+    }
+  }
+  V* dst = sv + (tile_off | off_t);
+#pragma unroll
+  for (int k = 0; k < 16; k++) {
+    if (k < nreg) {
+      uint64_t o = 0;
+#pragma unroll
+      for (int j = 0; j < SV_R_BITS; j++)
+        if ((k >> j) & 1) o |= hb[j];
+      dst[o] = v[k];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K2: per-gate baseline
+template <typename V>
+struct Mat16 {
+  V m[16];
+};
+
+__device__ __forceinline__ uint64_t insert_zero(uint64_t x, int p) {
+  const uint64_t lo = x & ((1ull << p) - 1);
+  return ((x - lo) << 1) | lo;
+}
+
+template <typename V>
+__global__ void k_gate_u1(V* __restrict__ sv, uint64_t npairs, int q, V m0, V m1, V m2, V m3) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < npairs; i += stride) {
+    const uint64_t i0 = insert_zero(i, q), i1 = i0 | (1ull << q);  // Listing 2
+    const V a0 = sv[i0], a1 = sv[i1];
+    sv[i0] = cfma(m1, a1, cmul(m0, a0));
+    sv[i1] = cfma(m3, a1, cmul(m2, a0));
+  }
+}
+
+template <typename V>
+__global__ void k_gate_u2(V* __restrict__ sv, uint64_t nquads, int q0, int q1, Mat16<V> M) {
+  const int lo = q0 < q1 ? q0 : q1, hi = q0 < q1 ? q1 : q0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nquads; i += stride) {
+    const uint64_t b = insert_zero(insert_zero(i, lo), hi);
+    const uint64_t i0 = b, i1 = b | (1ull << q0), i2 = b | (1ull << q1), i3 = i1 | (1ull << q1);
+    const V a0 = sv[i0], a1 = sv[i1], a2 = sv[i2], a3 = sv[i3];
+    V o[4];
+#pragma unroll
+    for (int rr = 0; rr < 4; rr++)
+      o[rr] = cfma(M.m[4 * rr + 3], a3, cfma(M.m[4 * rr + 2], a2, cfma(M.m[4 * rr + 1], a1, cmul(M.m[4 * rr], a0))));
+    sv[i0] = o[0];
+    sv[i1] = o[1];
+    sv[i2] = o[2];
+    sv[i3] = o[3];
+  }
+}
+
+template <typename V>
+__global__ void k_gate_diag(V* __restrict__ sv, uint64_t N, int c0, int c1, V d0, V d1, V d2, V d3) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < N; x += stride) {
+    const int b0 = c0 < 100 ? (int)((x >> c0) & 1) : c0 - 200;
+    const int b1 = c1 < 100 ? (int)((x >> c1) & 1) : c1 - 200;
+    sv[x] = cmul(sv[x], sel4(b0 | (b1 << 1), d0, d1, d2, d3));
+  }
+}
+
+template <typename V>
+__global__ void k_gate_swap(V* __restrict__ sv, uint64_t nquads, int q0, int q1) {
+  const int lo = q0 < q1 ? q0 : q1, hi = q0 < q1 ? q1 : q0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nquads; i += stride) {
+    const uint64_t b = insert_zero(insert_zero(i, lo), hi);
+    const uint64_t x = b | (1ull << q0), y = b | (1ull << q1);
+    const V t = sv[x];
+    sv[x] = sv[y];
+    sv[y] = t;
+  }
+}
+
+// ------------------------------------------------------------------ K6 / K7
+template <typename V>
+__global__ void k_set_one(V* sv, int64_t off) {
+  sv[off] = cone<V>();
+}
+
+template <typename V>
+__global__ void k_gather(const V* __restrict__ sv, const uint64_t* __restrict__ offs, size_t cnt, V* __restrict__ out) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < cnt; i += (size_t)gridDim.x * blockDim.x) {
+    const uint64_t o = offs[i];
+    out[i] = o == ~0ull ? czero<V>() : sv[o];
+  }
+}
+
+// ------------------------------------------------------------------ K5: reductions
+__device__ __forceinline__ double block_sum(double x, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = x;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < (int)(blockDim.x >> 5); i++) s += red[i];
+  __syncthreads();
+  return s;  // valid in thread 0
+}
+
+template <typename V>
+__global__ void k_norm_partial(const V* __restrict__ sv, uint64_t N, double* __restrict__ partial) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < N; i += stride) acc += abs2(sv[i]);
+  const double s = block_sum(acc, red);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+__global__ void k_sum_partials(const double* __restrict__ partial, int count, double* __restrict__ out) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < count; i += blockDim.x) acc += partial[i];
+  const double s = block_sum(acc, red);
+  if (threadIdx.x == 0) *out = s;
+}
+
+struct QBits {
+  int b[24];
+};
+
+template <typename V>
+__global__ void k_marginal_smem(const V* __restrict__ sv, uint64_t N, QBits q, int nq, double* __restrict__ partial) {
+  extern __shared__ double hist[];
+  const int bins = 1 << nq;
+  for (int i = threadIdx.x; i < bins; i += blockDim.x) hist[i] = 0.0;
+  __syncthreads();
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < N; x += stride) {
+    int y = 0;
+    for (int i = 0; i < nq; i++) y |= (int)((x >> q.b[i]) & 1) << i;
+    atomicAdd(&hist[y], abs2(sv[x]));
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < bins; i += blockDim.x) partial[(size_t)blockIdx.x * bins + i] = hist[i];
+}
+
+__global__ void k_reduce_bins(const double* __restrict__ partial, int blocks, int bins, double* __restrict__ out) {
+  for (int y = blockIdx.x * blockDim.x + threadIdx.x; y < bins; y += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int bk = 0; bk < blocks; bk++) s += partial[(size_t)bk * bins + y];
+    out[y] = s;
+  }
+}
+
+template <typename V>
+__global__ void k_marginal_global(const V* __restrict__ sv, uint64_t N, QBits q, int nq, double* __restrict__ out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < N; x += stride) {
+    uint64_t y = 0;
+    for (int i = 0; i < nq; i++) y |= ((x >> q.b[i]) & 1ull) << i;
+    atomicAdd(&out[y], abs2(sv[x]));
+  }
+}
+
+template <typename V>
+__global__ void k_block_sums(const V* __restrict__ sv, int B, double* __restrict__ out) {
+  __shared__ double red[32];
+  const uint64_t base = (uint64_t)blockIdx.x << B;
+  const int len = 1 << B;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < len; i += blockDim.x) acc += abs2(sv[base + i]);
+  const double s = block_sum(acc, red);
+  if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
+// items: (block, first shot, count) triples.  The block's |a|^2 is scanned in a fixed order
+// (per-thread sequential runs, then a sequential scan of the run totals).
+template <typename V>
+__global__ void k_sample_resolve(const V* __restrict__ sv, int B, const int64_t* __restrict__ items,
+                                 const double* __restrict__ resid, uint64_t* __restrict__ out_off) {
+  extern __shared__ double cum[];
+  __shared__ double run_tot[1024];
+  const int64_t blk = items[3 * blockIdx.x], first = items[3 * blockIdx.x + 1], cnt = items[3 * blockIdx.x + 2];
+  const int len = 1 << B;
+  const int per = (len + blockDim.x - 1) / blockDim.x;
+  const uint64_t base = (uint64_t)blk << B;
+  const int lo = threadIdx.x * per;
+  double s = 0.0;
+  for (int i = lo; i < lo + per && i < len; i++) {
+    s += abs2(sv[base + i]);
+    cum[i] = s;
+  }
+  run_tot[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    for (int t = 0; t < (int)blockDim.x; t++) {
+      const double v = run_tot[t];
+      run_tot[t] = acc;
+      acc += v;
+    }
+  }
+  __syncthreads();
+  const double off = run_tot[threadIdx.x];
+  for (int i = lo; i < lo + per && i < len; i++) cum[i] += off;
+  __syncthreads();
+  for (int64_t sidx = threadIdx.x; sidx < cnt; sidx += blockDim.x) {
+    const double u = resid[first + sidx];
+    int a = 0, b = len;  // first i with cum[i] > u
+    while (a < b) {
+      const int mid = (a + b) >> 1;
+      if (cum[mid] > u)
+        b = mid;
+      else
+        a = mid + 1;
+    }
+    if (a >= len) {  // u at/after the block total (rounding): last element with mass
+      a = len - 1;
+      while (a > 0 && cum[a] == cum[a - 1]) a--;
+    }
+    out_off[first + sidx] = base + (uint64_t)a;
+  }
+}
+
+// ------------------------------------------------------------------ exchange over peer memory
+struct ExDev {
+  int nins;        // number of inserted bits (k m-bits + the split bit h)
+  int pos[9];      // insertion positions, ascending
+  int val_my[9];   // bit values on the local side
+  int val_peer[9]; // bit values on the partner side
+};
+
+__device__ __forceinline__ uint64_t insert_bit(uint64_t x, int p, int v) {
+  const uint64_t lo = x & ((1ull << p) - 1);
+  return ((x - lo) << 1) | ((uint64_t)v << p) | lo;
+}
+
+// Swap local[x] <-> remote[x'] for every compact index j (2^(nL - k - 1) of them).
+template <typename V>
+__global__ void k_exchange_peer(V* __restrict__ local, V* __restrict__ remote, uint64_t count, ExDev e) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < count; j += stride) {
+    uint64_t x = j, y = j;
+    for (int i = 0; i < e.nins; i++) {
+      x = insert_bit(x, e.pos[i], e.val_my[i]);
+      y = insert_bit(y, e.pos[i], e.val_peer[i]);
+    }
+    const V a = local[x];
+    const V b = remote[y];
+    local[x] = b;
+    remote[y] = a;
+  }
+}
+
+// ------------------------------------------------------------------ host helpers
+template <typename V, int G, int NT, int MINB>
+cudaError_t launch_section_t(V* sv, const int* prog, const V* coef, int T, int n_out, cudaStream_t st) {
+  static bool attr_set = false;
+  const size_t smem = sizeof(V) << T;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_section<V, G, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(sizeof(V) << SV_TMAX));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int threads = 1 << (T - SV_R_BITS < 0 ? 0 : T - SV_R_BITS);
+  k_section<V, G, NT, MINB><<<(unsigned)(1ull << n_out), threads, smem, st>>>(sv, prog, coef);
+  return cudaGetLastError();
+}
+
+inline unsigned grid_for(uint64_t work, int threads) {
+  uint64_t b = (work + threads - 1) / threads;
+  const uint64_t cap = 148ull * 16;
+  if (b > cap) b = cap;
+  if (b == 0) b = 1;
+  return (unsigned)b;
+}
+
+template <typename V>
+V to_v(const double* c);
+template <>
+double2 to_v<double2>(const double* c) {
+  return make_double2(c[0], c[1]);
+}
+template <>
+float2 to_v<float2>(const double* c) {
+  return make_float2((float)c[0], (float)c[1]);
+}
+
+template <typename V>
+cudaError_t launch_gate_t(V* sv, int nL, const GateArgs& g, cudaStream_t st) {
+  const int th = 256;
+  const uint64_t N = 1ull << nL;
+  switch (g.type) {
+    case SV_OP_U1:
+      k_gate_u1<V><<<grid_for(N / 2, th), th, 0, st>>>(sv, N / 2, g.q0, to_v<V>(g.m), to_v<V>(g.m + 2),
+                                                       to_v<V>(g.m + 4), to_v<V>(g.m + 6));
+      break;
+    case SV_OP_U2: {
+      Mat16<V> M;
+      for (int i = 0; i < 16; i++) M.m[i] = to_v<V>(g.m + 2 * i);
+      k_gate_u2<V><<<grid_for(N / 4, th), th, 0, st>>>(sv, N / 4, g.q0, g.q1, M);
+      break;
+    }
+    case SV_OP_DIAG:
+      k_gate_diag<V><<<grid_for(N, th), th, 0, st>>>(sv, N, g.q0, g.q1, to_v<V>(g.m), to_v<V>(g.m + 2),
+                                                     to_v<V>(g.m + 4), to_v<V>(g.m + 6));
+      break;
+    case 7:
+      k_gate_swap<V><<<grid_for(N / 4, th), th, 0, st>>>(sv, N / 4, g.q0, g.q1);
+      break;
+    default:
+      return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ public wrappers
+cudaError_t launch_section(bool dbl, void* sv, const int* prog_dev, const void* coef_dev, int T, int r, int n_out,
+                           cudaStream_t st) {
+  (void)r;
+  if (dbl) {
+    if (T <= 12) return launch_section_t<double2, 3, 256, 2>((double2*)sv, prog_dev, (const double2*)coef_dev, T, n_out, st);
+    if (T == 13) return launch_section_t<double2, 3, 512, 1>((double2*)sv, prog_dev, (const double2*)coef_dev, T, n_out, st);
+    return cudaErrorInvalidValue;
+  }
+  if (T <= 12) return launch_section_t<float2, 4, 256, 2>((float2*)sv, prog_dev, (const float2*)coef_dev, T, n_out, st);
+  if (T == 13) return launch_section_t<float2, 4, 512, 1>((float2*)sv, prog_dev, (const float2*)coef_dev, T, n_out, st);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_gate(bool dbl, void* sv, int nL, const GateArgs& g, cudaStream_t st) {
+  return dbl ? launch_gate_t<double2>((double2*)sv, nL, g, st) : launch_gate_t<float2>((float2*)sv, nL, g, st);
+}
+
+cudaError_t launch_set_basis(bool dbl, void* sv, int nL, int64_t off, cudaStream_t st) {
+  const size_t bytes = (dbl ? 16 : 8) * (size_t(1) << nL);
+  cudaError_t e = cudaMemsetAsync(sv, 0, bytes, st);
+  if (e != cudaSuccess || off < 0) return e;
+  if (dbl)
+    k_set_one<double2><<<1, 1, 0, st>>>((double2*)sv, off);
+  else
+    k_set_one<float2><<<1, 1, 0, st>>>((float2*)sv, off);
+  return cudaGetLastError();
+}
+
+size_t norm_scratch_doubles() { return kRedBlocks; }
+
+cudaError_t launch_norm(bool dbl, const void* sv, int nL, double* scratch, double* out_dev, cudaStream_t st) {
+  const uint64_t N = 1ull << nL;
+  if (dbl)
+    k_norm_partial<double2><<<kRedBlocks, kRedThreads, 0, st>>>((const double2*)sv, N, scratch);
+  else
+    k_norm_partial<float2><<<kRedBlocks, kRedThreads, 0, st>>>((const float2*)sv, N, scratch);
+  k_sum_partials<<<1, 1024, 0, st>>>(scratch, kRedBlocks, out_dev);
+  return cudaGetLastError();
+}
+
+static constexpr int kMargBlocks = 148 * 2;
+static constexpr int kMargSmemBits = 12;
+
+size_t marginal_scratch_doubles(int nq) { return nq <= kMargSmemBits ? (size_t)kMargBlocks << nq : 0; }
+
+cudaError_t launch_marginal(bool dbl, const void* sv, int nL, const int* qbits, int nq, double* scratch,
+                            double* out_dev, cudaStream_t st) {
+  if (nq > 24) return cudaErrorInvalidValue;
+  QBits q;
+  for (int i = 0; i < nq; i++) q.b[i] = qbits[i];
+  const uint64_t N = 1ull << nL;
+  const int bins = 1 << nq;
+  if (nq <= kMargSmemBits) {
+    const size_t smem = sizeof(double) * bins;
+    if (dbl)
+      k_marginal_smem<double2><<<kMargBlocks, 512, smem, st>>>((const double2*)sv, N, q, nq, scratch);
+    else
+      k_marginal_smem<float2><<<kMargBlocks, 512, smem, st>>>((const float2*)sv, N, q, nq, scratch);
+    k_reduce_bins<<<grid_for(bins, 256), 256, 0, st>>>(scratch, kMargBlocks, bins, out_dev);
+  } else {
+    cudaError_t e = cudaMemsetAsync(out_dev, 0, sizeof(double) * bins, st);
+    if (e != cudaSuccess) return e;
+    if (dbl)
+      k_marginal_global<double2><<<grid_for(N, 256), 256, 0, st>>>((const double2*)sv, N, q, nq, out_dev);
+    else
+      k_marginal_global<float2><<<grid_for(N, 256), 256, 0, st>>>((const float2*)sv, N, q, nq, out_dev);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_block_sums(bool dbl, const void* sv, int nL, int B, double* out_dev, cudaStream_t st) {
+  const unsigned blocks = (unsigned)(1ull << (nL - B));
+  if (dbl)
+    k_block_sums<double2><<<blocks, 256, 0, st>>>((const double2*)sv, B, out_dev);
+  else
+    k_block_sums<float2><<<blocks, 256, 0, st>>>((const float2*)sv, B, out_dev);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sample_resolve(bool dbl, const void* sv, int B, const int64_t* items, int n_items,
+                                  const double* resid, uint64_t* out_off, cudaStream_t st) {
+  if (n_items == 0) return cudaSuccess;
+  const size_t smem = sizeof(double) << B;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_sample_resolve<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    cudaFuncSetAttribute(k_sample_resolve<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    attr = true;
+  }
+  if (dbl)
+    k_sample_resolve<double2><<<n_items, 256, smem, st>>>((const double2*)sv, B, items, resid, out_off);
+  else
+    k_sample_resolve<float2><<<n_items, 256, smem, st>>>((const float2*)sv, B, items, resid, out_off);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather(bool dbl, const void* sv, const uint64_t* offs, size_t cnt, void* out, cudaStream_t st) {
+  if (cnt == 0) return cudaSuccess;
+  if (dbl)
+    k_gather<double2><<<grid_for(cnt, 256), 256, 0, st>>>((const double2*)sv, offs, cnt, (double2*)out);
+  else
+    k_gather<float2><<<grid_for(cnt, 256), 256, 0, st>>>((const float2*)sv, offs, cnt, (float2*)out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_exchange_peer(bool dbl, void* local, void* const* peer_bases, int rank, int nL,
+                                 const ExchangeArgs& a, cudaStream_t st, int* launches) {
+  // rank bits of this rank at the exchanged positions
+  int mine = 0;
+  for (int i = 0; i < a.k; i++) mine |= ((rank >> a.bsel[i]) & 1) << i;
+  const uint64_t count = 1ull << (nL - a.k - 1);
+  for (int mu = 0; mu < (1 << a.k); mu++) {
+    if (mu == mine) continue;
+    int partner = rank;
+    for (int i = 0; i < a.k; i++) partner = (partner & ~(1 << a.bsel[i])) | (((mu >> i) & 1) << a.bsel[i]);
+    // my block mu (local bits m = mu) <-> partner's block `mine`; pairs split by bit h
+    ExDev e{};
+    struct PV {
+      int p, vm, vp;
+    } ins[9];
+    int n = 0;
+    for (int i = 0; i < a.k; i++) ins[n++] = {a.m[i], (mu >> i) & 1, (mine >> i) & 1};
+    const int hv = rank < partner ? 0 : 1;
+    ins[n++] = {a.h, hv, hv};
+    for (int i = 1; i < n; i++)  // ascending positions
+      for (int j = i; j > 0 && ins[j].p < ins[j - 1].p; j--) {
+        PV t = ins[j];
+        ins[j] = ins[j - 1];
+        ins[j - 1] = t;
+      }
+    e.nins = n;
+    for (int i = 0; i < n; i++) {
+      e.pos[i] = ins[i].p;
+      e.val_my[i] = ins[i].vm;
+      e.val_peer[i] = ins[i].vp;
+    }
+    const int th = 256;
+    if (dbl)
+      k_exchange_peer<double2><<<grid_for(count, th), th, 0, st>>>((double2*)local, (double2*)peer_bases[partner],
+                                                                   count, e);
+    else
+      k_exchange_peer<float2><<<grid_for(count, th), th, 0, st>>>((float2*)local, (float2*)peer_bases[partner], count,
+                                                                  e);
+    if (launches) (*launches)++;
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) return err;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t launch_copy(bool dbl, void* dst, const void* src, size_t count, cudaStream_t st) {
+  return cudaMemcpyAsync(dst, src, count * (dbl ? 16 : 8), cudaMemcpyDeviceToDevice, st);
+}
+
+}  // namespace sv

@@ -1,0 +1,55 @@
+// kernels.cuh — launch interfaces of the sm_100a kernels (host-callable wrappers).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace sv {
+
+// K1: one launch per section (program at prog_dev + int_off, coefficients in amp dtype).
+// dbl selects fp64 (double2 amplitudes) vs fp32 (float2).
+cudaError_t launch_section(bool dbl, void* sv, const int* prog_dev, const void* coef_dev, int T, int r, int n_out,
+                           cudaStream_t st);
+
+// K2: per-gate baseline, one pass over the shard per gate.  q0/q1 are memory bits;
+// diag codes follow program.h (rank bits pre-folded to constants).
+struct GateArgs {
+  int type;       // SV_OP_U1 / U2 / DIAG / SWAP(=7)
+  int q0, q1;
+  double m[32];   // complex coefficients (fp64; converted in the wrapper for fp32)
+};
+cudaError_t launch_gate(bool dbl, void* sv, int nL, const GateArgs& g, cudaStream_t st);
+
+// K6: |k>: zero the shard and write 1 at local offset `off` if owned.
+cudaError_t launch_set_basis(bool dbl, void* sv, int nL, int64_t off, cudaStream_t st);
+
+// K5: reductions.  Partial arrays are device scratch of the sizes returned by *_scratch.
+size_t norm_scratch_doubles();
+cudaError_t launch_norm(bool dbl, const void* sv, int nL, double* scratch, double* out_dev, cudaStream_t st);
+// histogram of |a|^2 over `nq` local memory bits (bin bit i <- memory bit qbits[i]); out has 2^nq doubles
+size_t marginal_scratch_doubles(int nq);
+cudaError_t launch_marginal(bool dbl, const void* sv, int nL, const int* qbits, int nq, double* scratch,
+                            double* out_dev, cudaStream_t st);
+// sums of |a|^2 over consecutive blocks of 2^B amplitudes
+cudaError_t launch_block_sums(bool dbl, const void* sv, int nL, int B, double* out_dev, cudaStream_t st);
+// resolve shots: for each of n_blocks work items (block id, first shot, shot count), CTA-scan the
+// block and binary-search each residual u; writes local offsets.
+cudaError_t launch_sample_resolve(bool dbl, const void* sv, int B, const int64_t* items, int n_items,
+                                  const double* resid, uint64_t* out_off, cudaStream_t st);
+
+// K7: out[i] = sv[offs[i]] if offs[i] != ~0 else 0.
+cudaError_t launch_gather(bool dbl, const void* sv, const uint64_t* offs, size_t cnt, void* out, cudaStream_t st);
+
+// Cross-GPU exchange of k local bits m[] with rank bits b[] (rank-bit indices), peer-memory swap.
+struct ExchangeArgs {
+  int k;
+  int m[8];       // local memory bits, ascending
+  int bsel[8];    // rank-bit index (0..g-1) paired with m[i]
+  int h;          // local bit (not in m) that splits each pair's work between the two ranks
+};
+cudaError_t launch_exchange_peer(bool dbl, void* local, void* const* peer_bases /*host array [world]*/, int rank,
+                                 int nL, const ExchangeArgs& a, cudaStream_t st, int* launches);
+// staging -> shard copy of `count` amplitudes at element offsets (for the NCCL exchange path)
+cudaError_t launch_copy(bool dbl, void* dst, const void* src, size_t count, cudaStream_t st);
+
+}  // namespace sv

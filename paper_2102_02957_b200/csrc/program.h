@@ -1,0 +1,59 @@
+// program.h — the per-section "program" the host compiles and the section kernel (K1) runs.
+//
+// A section (begin_blocking..end_blocking) is compiled into:
+//   * a TILE: T memory bits (the bits its non-diagonal gates touch, padded with the lowest free
+//     local bits so every tile is a union of >= 128-byte runs); one CTA owns one tile per launch
+//     and the grid enumerates the other local bits (out_bits);
+//   * PHASES: runs of gates whose non-diagonal qubits fit R_BITS "register" positions.  In a
+//     phase each thread holds 2^R_BITS amplitudes that differ only in those positions and applies
+//     the phase's gates in registers; shared memory is touched once per phase (load + store);
+//   * OPS: U2 / U1 / H1 / PERM on register slots, DIAG on any bit (tile position, out-of-tile
+//     local bit, or a rank bit folded to a constant on the host).
+// All records are plain ints so the same buffer serves host and device.
+#pragma once
+
+#define SV_R_BITS 4           // register positions per phase (16 amplitudes per thread)
+#define SV_TMAX 14            // max tile bits (fp64 T=13 -> 128 KiB smem)
+#define SV_MAX_OUT 48         // max out-of-tile local bits
+
+// op types
+#define SV_OP_U2 1      // a = slot0, b = slot1, coef -> 16 complex (row-major, s = bit(a) + 2 bit(b))
+#define SV_OP_U1 2      // a = slot, coef -> 4 complex (row-major)
+#define SV_OP_H1 3      // a = slot, coef -> 1 complex (scale s, real):  (x, y) -> (s(x+y), s(x-y))
+#define SV_OP_PERM2 4   // a = slot0, b = slot1, extra = packed permutation out[s] = in[(extra >> 2s) & 3]
+#define SV_OP_DIAG 5    // a = code0, b = code1, coef -> 4 complex d[s], s = bit(code0) + 2 bit(code1)
+#define SV_OP_DIAG_CP 6 // like DIAG with d0 = d1 = d2 = 1: only s == 3 is multiplied (coef -> d3)
+
+// DIAG bit codes
+#define SV_CODE_TILE(p) (p)           // tile position p (0 <= p < SV_TMAX)
+#define SV_CODE_OUT(mb) (100 + (mb))  // local memory bit mb outside the tile (per-CTA constant)
+#define SV_CODE_ZERO 200              // constant 0 (rank bit folded on the host, or unused)
+#define SV_CODE_ONE 201               // constant 1
+
+struct SvSecHeader {
+  int T;          // tile bits
+  int r;          // register bits per phase (<= SV_R_BITS)
+  int n_out;      // local memory bits outside the tile (grid = 2^n_out CTAs)
+  int n_phases;
+  int phase_off;  // int offset of the first SvPhase from the header
+  int op_off;     // int offset of the first SvOp from the header
+  int n_ops;
+  int pad;
+  int tile_bits[16];        // tile position -> memory bit (ascending)
+  int out_bits[SV_MAX_OUT]; // out-of-tile local memory bits (ascending) <- CTA index bits
+};
+
+struct SvPhase {
+  int R[SV_R_BITS];  // register slot -> tile position
+  int tpos[16];      // thread-index bit j -> tile position (T - r entries used)
+  int op_begin, op_count, pad0, pad1;
+};
+
+struct SvOp {
+  int type, a, b, coef;  // coef: index into the complex coefficient array (whole circuit)
+  int extra, pad0, pad1, pad2;
+};
+
+static_assert(sizeof(SvSecHeader) % 16 == 0, "header alignment");
+static_assert(sizeof(SvPhase) % 16 == 0, "phase alignment");
+static_assert(sizeof(SvOp) % 16 == 0, "op alignment");

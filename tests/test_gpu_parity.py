@@ -1,0 +1,185 @@
+"""GPU parity: libsv.so (C-ABI, sm_100a kernels) vs the CPU oracle on the same seeded inputs.
+
+Tolerances (north_star, DESIGN "Tolerances"): fp64 max|d| <= 1e-10; fp32 max|d| <= 1e-4 and
+||d||_2 <= 1e-5 * ||a||_2 (reading R15)."""
+import math
+
+import numpy as np
+import pytest
+
+import circuits as C
+import oracle as O
+
+from conftest import gpu_available
+
+pytestmark = pytest.mark.gpu
+
+sv = pytest.importorskip("paper_2102_02957_b200")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_gpu():
+    if not gpu_available():
+        pytest.skip("no CUDA device")
+    import torch
+    torch.cuda.set_device(0)
+
+
+def check(got, ref, prec):
+    d = np.abs(got.astype(np.complex128) - ref)
+    if prec == "fp64":
+        assert d.max() <= 1e-10, d.max()
+    else:
+        assert d.max() <= 1e-4, d.max()
+        assert np.linalg.norm(d) <= 1e-5 * max(1.0, np.linalg.norm(ref)), np.linalg.norm(d)
+
+
+def rand_state_records(n, seed):
+    return C.random_circuit(n, 4 * n, seed, kinds=("u3", "su4"))
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_qft10_cfg0(prec):
+    n, c = 10, 6
+    k = C.basis_index(1, n)
+    with sv.StateVector(n, c, prec) as s:
+        s.reset(k)
+        s.apply(C.qft(n))
+        got = s.state()
+    ref = O.apply_circuit(C.qft(n), n, basis=k)
+    check(got, ref, prec)
+    j = np.arange(1 << n)
+    closed = np.exp(2j * np.pi * ((j * k) % (1 << n)) / (1 << n)) / math.sqrt(1 << n)
+    check(got, closed, prec)
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_random_circuits(prec):
+    rng = np.random.default_rng(11)
+    for t in range(40):
+        n = int(rng.integers(2, 17))
+        c = int(rng.integers(2, n + 1)) if n >= 2 else 1
+        if prec == "fp64":
+            c = min(c, 13)
+        else:
+            c = min(c, 13)
+        circ = C.random_circuit(n, int(rng.integers(0, 120)), 500 + t)
+        with sv.StateVector(n, c, prec) as s:
+            s.apply(circ)
+            s.apply(circ[: len(circ) // 2])  # pi carried across calls
+            got = s.state()
+        ref = O.apply_circuit(circ[: len(circ) // 2], n, O.apply_circuit(circ, n))
+        check(got, ref, prec)
+
+
+@pytest.mark.parametrize("n,c", [(14, 12), (16, 8), (18, 12), (20, 10), (20, 13)])
+def test_qv_and_qft_mid(n, c):
+    for circ in (C.quantum_volume(n, 10, 1), C.qft(n)):
+        with sv.StateVector(n, c, "fp64") as s:
+            s.reset(C.basis_index(2, n))
+            s.apply(circ)
+            got = s.state()
+        check(got, O.apply_circuit(circ, n, basis=C.basis_index(2, n)), "fp64")
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_unblocked_baseline(prec):
+    n = 14
+    circ = C.random_circuit(n, 80, 9)
+    with sv.StateVector(n, 8, prec) as s:
+        s.apply(circ, flags=sv.SV_UNBLOCKED)
+        got = s.state()
+        st = s.stats()
+    check(got, O.apply_circuit(circ, n), prec)
+    assert st["sections"] == 0 and st["kernel_launches"] >= 80
+
+
+def test_restore_order_and_permutation():
+    n, c = 12, 5
+    circ = C.quantum_volume(n, 6, 4)
+    with sv.StateVector(n, c) as s:
+        s.apply(circ, flags=sv.SV_RESTORE_ORDER)
+        assert list(s.permutation()) == list(range(n))
+        got = s.state()
+    check(got, O.apply_circuit(circ, n), "fp64")
+
+
+def test_edge_cases():
+    # empty circuit, diagonal-only circuit, tiny n, c = n
+    for n, c in [(1, 1), (2, 2), (3, 2), (4, 4), (5, 3)]:
+        circ = C.random_circuit(n, 30, n, kinds=("u3", "u1") if n == 1 else ("u3", "cx", "cp", "swap", "su4", "u1", "d2"))
+        with sv.StateVector(n, c) as s:
+            s.apply(circ[:0])
+            s.apply(circ)
+            got = s.state()
+        check(got, O.apply_circuit(circ, n), "fp64")
+    circ = C.random_circuit(16, 200, 3, kinds=("cp", "u1", "d2"))
+    psi = C.random_circuit(16, 40, 4, kinds=("u3",))
+    with sv.StateVector(16, 4) as s:
+        s.apply(psi)
+        s.apply(circ)
+        got = s.state()
+    check(got, O.apply_circuit(circ, 16, O.apply_circuit(psi, 16)), "fp64")
+
+
+def test_readout_norm_probs_amplitudes():
+    n, c = 16, 10
+    circ = C.quantum_volume(n, 8, 3)
+    ref = O.apply_circuit(circ, n)
+    with sv.StateVector(n, c) as s:
+        s.apply(circ)
+        assert abs(s.norm() - 1.0) <= 1e-12
+        for Q in ([0], [15, 3], [0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15], [7, 2, 11]):
+            assert np.max(np.abs(s.probabilities(Q) - O.marginal(ref, Q))) <= 1e-13
+        idx = np.array([0, 1, 12345, (1 << n) - 1, 777], dtype=np.uint64)
+        assert np.max(np.abs(s.amplitudes(idx) - ref[idx.astype(np.int64)])) <= 1e-10
+
+
+def test_sampling():
+    n, c = 14, 8
+    # pi = identity (no blocking swaps needed: c = n) -> exact match with the oracle's inverse CDF
+    circ = C.quantum_volume(n, 6, 5)
+    with sv.StateVector(n, n) as s:
+        s.apply(circ)
+        assert list(s.permutation()) == list(range(n))
+        shots = s.sample(20000, 99)
+    ref = O.apply_circuit(circ, n)
+    us = C.sample_uniforms(99, 20000)
+    cdf = np.cumsum(np.abs(ref) ** 2)
+    near_edge = np.min(np.abs(cdf[None, :] - us[:, None]), axis=1) < 1e-12
+    exp = O.sample(ref, us)
+    assert np.array_equal(shots[~near_edge], exp[~near_edge])
+    # blocked (pi != id): distribution check (chi^2 over the 16 most likely outcomes + rest)
+    with sv.StateVector(n, c) as s:
+        s.apply(circ)
+        shots = s.sample(200000, 7)
+    p = np.abs(ref) ** 2
+    top = np.argsort(p)[::-1][:16]
+    obs = np.array([np.sum(shots == t) for t in top] + [0.0])
+    obs[-1] = len(shots) - obs[:-1].sum()
+    expv = np.concatenate([p[top], [1 - p[top].sum()]]) * len(shots)
+    chi2 = np.sum((obs - expv) ** 2 / expv)
+    assert chi2 < 45.0  # 16 dof, p ~ 1e-4
+
+
+def test_mirror_returns_to_basis_large():
+    n, c = 24, 12
+    k = C.basis_index(5, n)
+    with sv.StateVector(n, c) as s:
+        s.reset(k)
+        s.apply(C.mirror(C.quantum_volume(n, 10, 2)))
+        a = s.amplitudes(np.array([k], dtype=np.uint64))
+        assert abs(a[0] - 1.0) <= 1e-10
+        assert abs(s.norm() - 1.0) <= 1e-12
+
+
+@pytest.mark.slow
+def test_qv28_full_size_parity():
+    # BASELINE configs[1] at full size in the bench's launch configuration (c = 12), full compare.
+    n, c = 28, 12
+    circ = C.quantum_volume(n, 10, 1)
+    with sv.StateVector(n, c) as s:
+        s.apply(circ)
+        got = s.state()
+    ref = O.apply_circuit(circ, n)
+    check(got, ref, "fp64")

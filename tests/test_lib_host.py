@@ -1,0 +1,152 @@
+"""CPU tests of libsv.so: exports, the C++ blocking pass (bit-exact vs the oracle's independent
+pass) and the executor plan (semantics vs the dense oracle).  No GPU is needed: these entry
+points are host-only."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import circuits as C
+import oracle as O
+from oracle import blocking as B
+
+from blockutil import load_golden, parse_gates, triples
+from libutil import lib_tokens, memory_perm, plan_to_dense_records
+
+sv = pytest.importorskip("paper_2102_02957_b200")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    from paper_2102_02957_b200 import build
+    build.build()
+
+
+def test_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "sv.h")).read()
+    names = set(re.findall(r"^\s*(?:int|void|const char\*)\s+(sv_\w+)\s*\(", hdr, re.M))
+    assert len(names) >= 19
+    L = sv.lib()
+    for nm in names:
+        assert hasattr(L, nm), nm
+    assert set(names) == set(sv._lib.EXPORTS)
+
+
+def test_gate_dtype_matches_inputs():
+    assert sv.GATE_DTYPE == C.GATE_DTYPE
+
+
+def assert_same_pass(recs, n, c, flags=0, pi0=None):
+    toks_o, pi_o = B.block_circuit(triples(recs), n, c, pi0=pi0, flags=flags)
+    toks_l, pi_l = sv.block_circuit(recs, n, c, pi0=pi0, flags=flags)
+    assert lib_tokens(toks_l) == toks_o
+    assert list(pi_l) == list(pi_o)
+    # gate payloads are copied bit-for-bit from the input records
+    for r in toks_l:
+        if int(r["kind"]) in (C.U1, C.U2, C.D1, C.D2, C.SWAP) and int(r["pad"]) >= 0:
+            assert r["m"].tobytes() == recs[int(r["pad"])]["m"].tobytes()
+    return toks_l, pi_l
+
+
+@pytest.mark.parametrize("row", load_golden(os.path.join(ROOT, "tests", "golden", "blocking_traces.txt")))
+def test_pass_golden(row):
+    n, c, gates, expected, pi_expected = row
+    recs = parse_gates(gates, n)
+    toks, pi = sv.block_circuit(recs, n, c)
+    assert B.format_tokens(lib_tokens(toks)) == expected
+    assert list(pi) == pi_expected
+
+
+def test_pass_bit_exact_random_10k():
+    # bit-exact with the independent pass on >= 10^4 random circuits.
+    rng = np.random.default_rng(2024)
+    for t in range(10000):
+        n = int(rng.integers(2, 16))
+        c = int(rng.integers(2, n + 1))
+        ng = int(rng.integers(0, 40))
+        kinds = ("u3", "cx", "cp", "swap", "su4", "u1", "d2") if t % 2 else ("cx", "su4", "cp")
+        recs = C.random_circuit(n, ng, 77000 + t, kinds=kinds)
+        pi0 = rng.permutation(n) if t % 5 == 0 else None
+        flags = B.RESTORE_ORDER if t % 7 == 0 else 0
+        assert_same_pass(recs, n, c, flags=flags, pi0=pi0)
+
+
+@pytest.mark.parametrize("n,c", [(28, c) for c in range(8, 15)] + [(33, 12), (30, 10), (30, 12), (30, 13)])
+def test_pass_bit_exact_qv(n, c):
+    for seed in (1, 2, 3):
+        assert_same_pass(C.quantum_volume(n, 10, seed), n, c)
+
+
+@pytest.mark.parametrize("n,c", [(10, 6), (30, 10), (30, 11), (30, 12), (30, 13), (36, 12), (37, 12), (33, 12)])
+def test_pass_bit_exact_qft(n, c):
+    assert_same_pass(C.qft(n), n, c)
+
+
+def test_pass_errors():
+    with pytest.raises(sv.SvError, match="EINFEASIBLE"):
+        sv.block_circuit(C.records([C.gate(C.U2, 0, 1, np.eye(4))]), 4, 1)
+    with pytest.raises(sv.SvError, match="EINVAL"):
+        sv.block_circuit(C.records([C.gate(C.U2, 0, 0, np.eye(4))]), 4, 2)
+    with pytest.raises(sv.SvError, match="EINVAL"):
+        sv.block_circuit(C.records([C.gate(C.U1, 5, mat=np.eye(2))]), 4, 2)
+    bad = C.records([C.gate(C.U1, 0, mat=np.eye(2))])
+    bad["kind"] = 42
+    with pytest.raises(sv.SvError, match="EMALFORMED"):
+        sv.block_circuit(bad, 4, 2)
+
+
+def run_plan_dense(recs, n, c, g, flags=0, seed=0):
+    """Execute the library's plan densely (exchange = SWAP of memory bits) and compare with the
+    oracle on the original circuit, un-permuting through mu(q) = sigma[pi[q]]."""
+    plan, pi, sigma = sv.plan_circuit(recs, n, c, g, flags=flags)
+    nL = n - g
+    # structural checks: section gates only on local memory bits unless diagonal
+    inside = False
+    for r in plan:
+        k = int(r["kind"])
+        if k == C.BEGIN:
+            inside = True
+        elif k == C.END:
+            inside = False
+        elif k == 9:
+            assert not inside and int(r["q0"]) < nL <= int(r["q1"])
+        elif k in (C.U1, C.U2):
+            assert inside and int(r["q0"]) < nL and (k == C.U1 or int(r["q1"]) < nL)
+        elif k == C.SWAP:
+            assert flags & sv.SV_UNBLOCKED
+    rng = np.random.default_rng(seed)
+    psi = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+    psi /= np.linalg.norm(psi)
+    ref = O.apply_circuit(recs, n, psi)
+    mem = O.apply_circuit(plan_to_dense_records(plan), n, psi)
+    got = O.unpermute(mem, memory_perm(pi, sigma))
+    assert np.max(np.abs(got - ref)) <= 1e-12
+    return plan
+
+
+@pytest.mark.parametrize("g", [0, 1, 2, 3])
+def test_plan_semantics_random(g):
+    rng = np.random.default_rng(10 + g)
+    for t in range(120):
+        n = int(rng.integers(max(3, g + 2), 12))
+        c = int(rng.integers(2, n - g + 1)) if n - g >= 2 else 1
+        recs = C.random_circuit(n, int(rng.integers(0, 60)), 3000 + t + 1000 * g)
+        run_plan_dense(recs, n, c, g, flags=B.RESTORE_ORDER if t % 3 == 0 else 0, seed=t)
+
+
+@pytest.mark.parametrize("g", [0, 1, 2])
+def test_plan_semantics_qv_qft(g):
+    run_plan_dense(C.quantum_volume(10, 10, 1), 10, 5, g)
+    plan = run_plan_dense(C.qft(10), 10, 6, g)
+    if g == 0:  # single GPU: no data ever moves between sections
+        assert not any(int(r["kind"]) == 9 for r in plan)
+
+
+def test_plan_unblocked_matches():
+    recs = C.random_circuit(8, 50, 5)
+    plan = run_plan_dense(recs, 8, 4, 0, flags=sv.SV_UNBLOCKED)
+    assert sum(1 for r in plan if int(r["kind"]) == C.BEGIN) == 50
+    with pytest.raises(sv.SvError, match="EINFEASIBLE"):
+        sv.plan_circuit(C.records([C.gate(C.U1, 7, mat=C.H_MATRIX)]), 8, 4, 1, flags=sv.SV_UNBLOCKED)
