@@ -1,0 +1,366 @@
+#!/usr/bin/env python
+"""bench.py — the driver's benchmark contract for the cache-blocked state-vector hot path.
+
+    python bench.py --gpus N --steps K --warmup W [--impl reference] [--workload qv33]
+
+One STEP = one pass of the whole hot path over the workload: the host blocking
+pass + plan + program upload (a1-a3), every section kernel (a4, a7), every cross-GPU exchange
+(a5/a6), and a readout of marginal probabilities (a8), all through the C ABI of libsv.so.
+The default workload is BASELINE configs[3]: QV(33, depth 10, seed 1), fp64, chunk_bits 12,
+strong scaling over N GPUs (2^33 amplitudes = 128 GiB in total; it fits one B200).  The state
+(>= 4 GiB) is far larger than L2, so no flush is needed between steps.
+
+Rank 0 prints ONE JSON line.  `value` = input gates per second of the whole job, timed with
+CUDA events on the library's stream (max over ranks); `e2e` = the same metric measured through
+the public API with host buffers (gate list H2D, probabilities + amplitudes D2H) and a host
+clock; `roofline` = the section kernel (the dominant kernel) against its binding roofline;
+`cpu_baseline` = the CPU oracle on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import circuits as C  # noqa: E402
+
+METRIC = "QV/QFT circuit gates/s (fp64 state vector, cache-blocked)"
+FALLBACK_HBM_GBS = 6650.0
+# FP64 FMA pipe: 64 DFMA/clk/SM (measured 63.6 in tools/microbench.cu) x 148 SMs x 1.965 GHz x 2 flops
+FP64_PEAK_TFLOPS = 2 * 64 * 148 * 1.965e9 / 1e12
+
+
+# ----------------------------------------------------------------------------- workloads
+def workload(name: str, world: int):
+    g = world.bit_length() - 1
+    if name == "qv33":
+        n = 33
+        return dict(name="qv33", desc="QV(33, depth 10, seed 1) fp64, strong scaling", n=n,
+                    gates=C.quantum_volume(n, 10, 1), basis=0, scaling="strong")
+    if name == "qv28":
+        return dict(name="qv28", desc="QV(28, depth 10, seed 1) fp64", n=28,
+                    gates=C.quantum_volume(28, 10, 1), basis=0, scaling="strong")
+    if name == "qft30":
+        return dict(name="qft30", desc="QFT(30) fp64 on |splitmix64(1) mod 2^30>", n=30, gates=C.qft(30),
+                    basis=C.basis_index(1, 30), scaling="strong")
+    if name == "qft_weak":
+        n = 33 + g
+        return dict(name="qft_weak", desc=f"QFT({n}) fp64, 2^33 amplitudes per GPU (weak)", n=n, gates=C.qft(n),
+                    basis=C.basis_index(1, n), scaling="weak")
+    if name == "qv_weak":
+        n = 30 + g
+        return dict(name="qv_weak", desc=f"QV({n}, 10, 1) fp64, 2^30 amplitudes per GPU (weak)", n=n,
+                    gates=C.quantum_volume(n, 10, 1), basis=0, scaling="weak")
+    raise SystemExit(f"unknown workload {name}")
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d.get("hbm_gbs", FALLBACK_HBM_GBS)), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = "index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) < 9:
+                continue
+            for nm, v in zip(names, r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        load = [s for s in sm if s > 600] or sm
+        return {"sm_mhz": float(np.median(load)) if load else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- oracle timing
+def oracle_sample(wl, target_s: float = 15.0, max_gates: int = None):
+    """Time the CPU oracle (as it stands) on the first m gates of the workload from its basis
+    state; m is chosen from a one-gate probe so the sample takes ~target_s."""
+    import oracle as O
+    n = wl["n"]
+    gates = wl["gates"]
+    a = O.basis_state(n, wl["basis"])
+    t0 = time.perf_counter()
+    a = O.apply_circuit(gates[:1], n, a)
+    per = time.perf_counter() - t0
+    m = max(1, min(len(gates) - 1, int(target_s / max(per, 1e-6))))
+    if max_gates:
+        m = min(m, max_gates)
+    t0 = time.perf_counter()
+    O.apply_circuit(gates[1:1 + m], n, a)
+    dt = time.perf_counter() - t0
+    del a
+    return m, dt, per
+
+
+def cores():
+    v = os.environ.get("OMP_NUM_THREADS")
+    return int(v) if v else (len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count())
+
+
+def run_reference(args):
+    """--impl reference: the oracle (plain C + OpenMP, no blocking) timed on the host cores, each step
+    a bounded sample of the same workload (rank 0 only under torchrun)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    wl = workload(args.workload, args.gpus)
+    import oracle as O
+    n, gates = wl["n"], wl["gates"]
+    a = O.basis_state(n, wl["basis"])
+    t0 = time.perf_counter()
+    a = O.apply_circuit(gates[:1], n, a)
+    per = time.perf_counter() - t0
+    m = max(1, min(len(gates), int(args.ref_step_s / max(per, 1e-6))))
+    gi = 1
+    times = []
+    for it in range(args.warmup + args.steps):
+        sel = [(gi + j) % len(gates) for j in range(m)]
+        gi = (gi + m) % len(gates)
+        t0 = time.perf_counter()
+        a = O.apply_circuit(gates[sel], n, a)
+        dt = time.perf_counter() - t0
+        if it >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    value = args.steps * m / tot
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": wl["scaling"], "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded QV/QFT generator)",
+            "config": {"workload": wl["desc"], "n_qubits": n, "gates_per_step": m, "chunk_bits": None},
+            "cpu_baseline": {"value": value, "unit": "gates/s", "cores": cores(), "kind": "oracle",
+                             "sample": f"{m} gates of {wl['desc']} per step from its basis state (dense C oracle, OpenMP)"},
+            "e2e": {"value": value, "unit": "gates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2102_02957_b200 as sv
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    wl = workload(args.workload, world)
+    n, gates = wl["n"], wl["gates"]
+    c = args.chunk_bits
+    stream = torch.cuda.Stream()
+    uid = None
+    if world > 1:
+        u = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            u.copy_(torch.tensor(np.frombuffer(sv.nccl_unique_id(), dtype=np.uint8).copy()))
+        dist.broadcast(u, 0)
+        uid = bytes(u.cpu().numpy().tobytes())
+    s = sv.StateVector(n, c, args.precision, rank=rank, world=world, nccl_id=uid, stream=stream.cuda_stream)
+    Q = list(range(min(10, n)))
+
+    def step():
+        s.apply(gates)
+        s.probabilities(Q)
+
+    s.reset(wl["basis"])
+    for _ in range(args.warmup):
+        step()
+    s.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- timed region (device time, CUDA events on the library's stream)
+    s.reset_stats()
+    s.set_timing(True)
+    clk = ClockSampler(local)
+    clk.start()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    e1.synchronize()
+    barrier()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1)
+    st = s.stats()
+    s.set_timing(False)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = len(gates) / (ms_step / 1e3)
+
+    # ---- roofline of the dominant kernel (section kernel K1)
+    hbm_peak, hbm_src = peaks()
+    roof = None
+    if st["timed_sections"]:
+        t_launch = st["section_ms"] / st["timed_sections"] / 1e3
+        bytes_l = st["section_bytes"] / st["timed_sections"]
+        flops_l = st["section_flops"] / st["timed_sections"]
+        t_hbm = bytes_l / (hbm_peak * 1e9)
+        t_alu = flops_l / (FP64_PEAK_TFLOPS * 1e12) if args.precision == "fp64" else flops_l / (2 * FP64_PEAK_TFLOPS * 1e12)
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "section_traffic.json")
+        if os.path.exists(prof):
+            try:
+                traffic = json.load(open(prof)).get(wl["name"])
+            except Exception:
+                traffic = None
+        if t_hbm >= t_alu:
+            ach = bytes_l / t_launch / 1e9
+            roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
+                    "frac": round(ach / hbm_peak, 4), "traffic": traffic, "peak_source": hbm_src}
+        else:
+            ach = flops_l / t_launch / 1e12
+            pk = FP64_PEAK_TFLOPS if args.precision == "fp64" else 2 * FP64_PEAK_TFLOPS
+            roof = {"bound": "alu", "achieved": round(ach, 3), "peak": round(pk, 2), "unit": "TFLOP/s",
+                    "frac": round(ach / pk, 4), "traffic": traffic,
+                    "peak_source": "derived: 64 DFMA/clk/SM x 148 SMs x 1.965 GHz x 2 (DESIGN.md Roofline)"}
+        roof.update({"kernel": "k_section", "launches_timed": st["timed_sections"],
+                     "avg_launch_ms": round(t_launch * 1e3, 4), "alg_bytes_per_launch": bytes_l,
+                     "alg_flops_per_launch": flops_l,
+                     "hbm_frac_of_measured": round(bytes_l / t_launch / 1e9 / hbm_peak, 4),
+                     "section_share_of_step": round(st["section_ms"] / ms, 4)})
+
+    # ---- e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        idx = np.arange(0, 1 << n, max(1, (1 << n) // 1024), dtype=np.uint64)[:1024]
+        h2d = gates.nbytes + idx.nbytes
+        d2h = (8 << len(Q)) + idx.size * (16 if args.precision == "fp64" else 8)
+        times = []
+        for it in range(args.e2e_steps + 1):
+            barrier()
+            t0 = time.perf_counter()
+            s.reset(wl["basis"])
+            s.apply(gates)
+            s.probabilities(Q)
+            s.amplitudes(idx)
+            dt = time.perf_counter() - t0
+            if world > 1:
+                t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                dt = float(t.item())
+            if it > 0:
+                times.append(dt)
+        e2e = {"value": len(gates) / (sum(times) / len(times)), "unit": "gates/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "steps": len(times)}
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        m, dt, per = oracle_sample(wl, target_s=args.cpu_target_s)
+        cpu = {"value": m / dt, "unit": "gates/s", "cores": cores(), "kind": "oracle",
+               "sample": f"gates 2..{m + 1} of {wl['desc']} from its basis state ({m} gates, {dt:.1f} s; dense C oracle, OpenMP)"}
+
+    line = {"metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": wl["scaling"],
+            "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32",
+            "data": "synthetic (seeded QV/QFT generator, circuits/gen.py)",
+            "config": {"workload": wl["desc"], "n_qubits": n, "gates": int(len(gates)), "chunk_bits": c,
+                       "precision": args.precision, "parallelism": f"state sharded over {world} GPU(s)",
+                       "l2": "state >= 4 GiB per GPU >> 126 MB L2 (no flush needed)",
+                       "step": "sv_apply_circuit (pass+plan+upload+sections+exchanges) + sv_probabilities(10 qubits)"},
+            "amp_updates_per_s": value * (1 << n),
+            "sections_per_step": st["sections"] / args.steps, "exchanges_per_step": st["exchanges"] / args.steps,
+            "exchange_bytes_per_rank_per_step": st["bytes_sent"] / args.steps,
+            "exchange_ms_per_step": st["exchange_ms"] / args.steps,
+            "host_pass_ms": st["pass_ms"],
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(st["kernel_launches"]), "clocks": clocks}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    s.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="qv33")
+    ap.add_argument("--chunk-bits", type=int, default=12)
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-target-s", type=float, default=15.0)
+    ap.add_argument("--ref-step-s", type=float, default=8.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # contract: W >= 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

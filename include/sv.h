@@ -89,6 +89,13 @@ typedef struct sv_stats {
   uint64_t kernel_launches;   /* library kernels launched                                     */
   double pass_ms;             /* host time in the blocking pass + planning (last call)        */
   double apply_ms;            /* host wall time of the last sv_apply_circuit                   */
+  /* device-side accounting (filled when timing is enabled with sv_set_timing) */
+  uint64_t timed_sections;    /* section launches timed with CUDA events                       */
+  double section_ms;          /* summed event time of those section launches                   */
+  double exchange_ms;         /* summed event time of cross-GPU exchange steps                 */
+  double gate_ms;             /* summed event time of per-gate (unblocked) launches            */
+  double section_bytes;       /* algorithmic HBM bytes of the timed sections (2 x shard each)  */
+  double section_flops;       /* algorithmic flops of the timed sections (DESIGN "Roofline")   */
 } sv_stats;
 
 /* ---- lifetime ------------------------------------------------------------------------- */
@@ -132,7 +139,12 @@ int sv_probabilities(sv_handle h, const int32_t* qubits, int nq, double* host_ou
 int sv_sample(sv_handle h, size_t shots, uint64_t seed, uint64_t* host_out);
 /* logical_to_physical[q] = paper-physical position of logical qubit q (the pass's pi). */
 int sv_get_permutation(sv_handle h, int32_t* logical_to_physical);
+/* Cumulative counters since creation / the last sv_stats_reset (synchronizes when timing). */
 int sv_stats_get(sv_handle h, sv_stats* out);
+int sv_stats_reset(sv_handle h);
+/* enable != 0: bracket every section / exchange / per-gate launch with CUDA events on the
+ * handle's stream and accumulate device times into sv_stats (small overhead per launch). */
+int sv_set_timing(sv_handle h, int enable);
 const char* sv_last_error(sv_handle h);
 
 /* ---- host-only (no GPU needed; used for parity of the pass and the plan) -------------- */

@@ -32,12 +32,14 @@ class Stats(ctypes.Structure):
     _fields_ = [("circuits", ctypes.c_uint64), ("gates", ctypes.c_uint64), ("sections", ctypes.c_uint64),
                 ("chunk_swaps", ctypes.c_uint64), ("exchanges", ctypes.c_uint64),
                 ("exchange_batches", ctypes.c_uint64), ("bytes_sent", ctypes.c_uint64),
-                ("kernel_launches", ctypes.c_uint64), ("pass_ms", ctypes.c_double), ("apply_ms", ctypes.c_double)]
+                ("kernel_launches", ctypes.c_uint64), ("pass_ms", ctypes.c_double), ("apply_ms", ctypes.c_double),
+                ("timed_sections", ctypes.c_uint64), ("section_ms", ctypes.c_double), ("exchange_ms", ctypes.c_double),
+                ("gate_ms", ctypes.c_double), ("section_bytes", ctypes.c_double), ("section_flops", ctypes.c_double)]
 
 
 EXPORTS = ["sv_create", "sv_create_dist", "sv_destroy", "sv_nccl_unique_id", "sv_reset", "sv_apply_circuit",
            "sv_synchronize", "sv_get_amplitudes", "sv_get_state", "sv_norm", "sv_probabilities", "sv_sample",
-           "sv_get_permutation", "sv_stats_get", "sv_last_error", "sv_block_circuit", "sv_plan_circuit", "sv_free",
+           "sv_get_permutation", "sv_stats_get", "sv_stats_reset", "sv_set_timing", "sv_last_error", "sv_block_circuit", "sv_plan_circuit", "sv_free",
            "sv_abi_version"]
 
 _lib = None
@@ -70,6 +72,8 @@ def lib():
         "sv_sample": ([vp, sz, u64, vp], i32),
         "sv_get_permutation": ([vp, ip], i32),
         "sv_stats_get": ([vp, ctypes.POINTER(Stats)], i32),
+        "sv_stats_reset": ([vp], i32),
+        "sv_set_timing": ([vp, i32], i32),
         "sv_last_error": ([vp], ctypes.c_char_p),
         "sv_block_circuit": ([vp, sz, i32, i32, ip, u32, hp, ctypes.POINTER(sz), ip], i32),
         "sv_plan_circuit": ([vp, sz, i32, i32, i32, ip, ip, u32, hp, ctypes.POINTER(sz), ip, ip], i32),
@@ -231,6 +235,12 @@ class StateVector:
         out = np.zeros(self.n, dtype=np.int32)
         self._check(lib().sv_get_permutation(self._h, _ip(out)))
         return out
+
+    def set_timing(self, enable: bool = True):
+        self._check(lib().sv_set_timing(self._h, 1 if enable else 0))
+
+    def reset_stats(self):
+        self._check(lib().sv_stats_reset(self._h))
 
     def stats(self) -> dict:
         s = Stats()

@@ -91,6 +91,16 @@ struct sv_state {
   Program prog;
   sv_stats stats{};
   std::string err;
+
+  // optional per-launch device timing (sv_set_timing)
+  struct TRec {
+    cudaEvent_t a, b;
+    int kind;  // 0 section, 1 exchange, 2 gate
+    double bytes, flops;
+  };
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<TRec> trecs;
 };
 
 namespace {
@@ -300,6 +310,54 @@ int gate_step(sv_state* h, const sv_gate& gm) {
   return SV_OK;
 }
 
+cudaEvent_t ev_get(sv_state* h) {
+  if (!h->ev_pool.empty()) {
+    cudaEvent_t e = h->ev_pool.back();
+    h->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+cudaEvent_t tstart(sv_state* h) {
+  if (!h->timing) return nullptr;
+  cudaEvent_t e = ev_get(h);
+  cudaEventRecord(e, h->st);
+  return e;
+}
+
+void tend(sv_state* h, cudaEvent_t a, int kind, double bytes, double flops) {
+  if (!a) return;
+  cudaEvent_t b = ev_get(h);
+  cudaEventRecord(b, h->st);
+  h->trecs.push_back({a, b, kind, bytes, flops});
+}
+
+int drain_timing(sv_state* h) {
+  if (h->trecs.empty()) return SV_OK;
+  CUDA_TRY(h, cudaEventSynchronize(h->trecs.back().b));
+  for (auto& r : h->trecs) {
+    float ms = 0.f;
+    CUDA_TRY(h, cudaEventElapsedTime(&ms, r.a, r.b));
+    if (r.kind == 0) {
+      h->stats.timed_sections++;
+      h->stats.section_ms += ms;
+      h->stats.section_bytes += r.bytes;
+      h->stats.section_flops += r.flops;
+    } else if (r.kind == 1) {
+      h->stats.exchange_ms += ms;
+    } else {
+      h->stats.gate_ms += ms;
+    }
+    h->ev_pool.push_back(r.a);
+    h->ev_pool.push_back(r.b);
+  }
+  h->trecs.clear();
+  return SV_OK;
+}
+
 int check_handle(sv_state* h) {
   if (!h) return fail(nullptr, SV_EINVAL, "null handle");
   CUDA_TRY(h, cudaSetDevice(h->device));
@@ -479,6 +537,11 @@ int sv_destroy(sv_handle h) {
     if (b->p) cudaFreeHost(b->p);
   if (h->own_sv && h->sv) cudaFree(h->sv);
   if (h->ev_upload) cudaEventDestroy(h->ev_upload);
+  for (auto& r : h->trecs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   if (h->own_stream && h->st) cudaStreamDestroy(h->st);
   cudaGetLastError();
   delete h;
@@ -527,19 +590,28 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
   size_t si = 0;
   for (const Step& st : steps) {
     switch (st.type) {
-      case Step::EXCHANGE:
+      case Step::EXCHANGE: {
+        cudaEvent_t t = tstart(h);
         if (int rc = do_exchange(h, st.ex, flags)) return rc;
+        tend(h, t, 1, 0.0, 0.0);
         break;
+      }
       case Step::SECTION: {
         const Launch& L = h->prog.launches[si++];
+        cudaEvent_t t = tstart(h);
         CUDA_TRY(h, launch_section(h->dbl, h->sv, (const int*)h->d_prog.p + L.int_off, h->d_coef.p, L.T, L.r, L.n_out, h->st));
+        const double amps = (double)(1ull << h->nL);
+        tend(h, t, 0, 2.0 * amps * (double)h->amp, L.flops_per_amp * amps);
         h->stats.kernel_launches++;
         h->stats.sections++;
         break;
       }
-      case Step::GATE:
+      case Step::GATE: {
+        cudaEvent_t t = tstart(h);
         if (int rc = gate_step(h, st.gates[0])) return rc;
+        tend(h, t, 2, 0.0, 0.0);
         break;
+      }
     }
   }
   h->pi = pi;
@@ -559,7 +631,21 @@ int sv_get_permutation(sv_handle h, int32_t* out) {
 
 int sv_stats_get(sv_handle h, sv_stats* out) {
   if (!h || !out) return fail(h, SV_EINVAL, "null argument");
+  if (int rc = drain_timing(h)) return rc;
   *out = h->stats;
+  return SV_OK;
+}
+
+int sv_stats_reset(sv_handle h) {
+  if (!h) return fail(h, SV_EINVAL, "null handle");
+  if (int rc = drain_timing(h)) return rc;
+  h->stats = sv_stats{};
+  return SV_OK;
+}
+
+int sv_set_timing(sv_handle h, int enable) {
+  if (!h) return fail(h, SV_EINVAL, "null handle");
+  h->timing = enable != 0;
   return SV_OK;
 }
 

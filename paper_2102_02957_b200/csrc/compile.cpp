@@ -267,7 +267,14 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
       op_cursor++;
     }
   }
+  // algorithmic flops per amplitude: U2 4x4 complex matvec = 32, U1 = 16, H1 = 4, PERM = 0,
+  // DIAG = one complex multiply (6), DIAG_CP = one complex multiply on a quarter (1.5)
+  double fpa = 0.0;
+  for (const PGate& p : pg)
+    fpa += p.type == SV_OP_U2 ? 32.0 : p.type == SV_OP_U1 ? 16.0 : p.type == SV_OP_H1 ? 4.0
+         : p.type == SV_OP_DIAG ? 6.0 : p.type == SV_OP_DIAG_CP ? 1.5 : 0.0;
   Launch L;
+  L.flops_per_amp = fpa;
   L.int_off = base;
   L.T = T;
   L.r = r;

@@ -10,6 +10,7 @@ namespace sv {
 struct Launch {
   size_t int_off;  // start of the section's SvSecHeader in Program::ints
   int T, r, n_out, n_phases, n_ops;
+  double flops_per_amp;  // algorithmic flops per amplitude of the section (DESIGN "Roofline")
 };
 
 struct Program {

@@ -618,7 +618,7 @@ cudaError_t launch_section_t(V* sv, const int* prog, const V* coef, int T, int n
   const size_t smem = sizeof(V) << T;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(k_section<V, G, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(sizeof(V) << SV_TMAX));
+                                         (int)(sizeof(V) << 13));
     if (e != cudaSuccess) return e;
     attr_set = true;
   }

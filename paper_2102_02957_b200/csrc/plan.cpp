@@ -16,6 +16,8 @@ namespace sv {
 
 namespace {
 
+constexpr int kMaxTileBits = 13;  // one CTA tile: 2^13 amplitudes (128 KiB fp64)
+
 sv_gate to_memory(const sv_gate& t, const std::vector<int>& sigma) {
   sv_gate r = t;
   r.q0 = sigma[t.q0];
@@ -77,19 +79,55 @@ struct SectionMapper {
       steps.push_back(std::move(ex));
     }
     // 3. translate the section to memory bits; SWAPs relabel sigma for everything after them
-    Step s;
-    s.type = Step::SECTION;
+    std::vector<sv_gate> mem;
     for (const sv_gate& t : sec) {
       if (t.kind == SV_SWAP) {
         relabel(t.q0, t.q1);
         continue;
       }
-      s.gates.push_back(to_memory(t, sigma));
+      mem.push_back(to_memory(t, sigma));
     }
-    if (!s.gates.empty()) {
-      ctr.sections++;
-      steps.push_back(std::move(s));
+    if (mem.empty()) return;
+    uint64_t act = 0;
+    for (const sv_gate& m : mem)
+      if (!is_diag(m.kind)) act |= qmask(m);
+    if (__builtin_popcountll(act) <= kMaxTileBits) {
+      push_section(std::move(mem));
+      return;
     }
+    // More active bits than one tile holds (chunk_bits > kMaxTileBits): split the section with
+    // the same pass at c = kMaxTileBits on memory bits.  Its chunk_swaps are relabels of an
+    // inner frame whose inverse keeps every gate on its own memory bit, so only the grouping is
+    // used (each inner section's gates are the originals, by index).
+    std::vector<sv_gate> in = mem;
+    for (size_t i = 0; i < in.size(); i++) in[i].pad = (int32_t)i;
+    std::vector<int> ipi(nL);
+    for (int b = 0; b < nL; b++) ipi[b] = b;
+    std::vector<sv_gate> toks;
+    Status st = block_pass(in.data(), in.size(), nL, kMaxTileBits, ipi, 0, toks);
+    if (!st.good()) {  // cannot happen for valid sections; keep the section whole
+      push_section(std::move(mem));
+      return;
+    }
+    std::vector<sv_gate> cur;
+    for (const sv_gate& t : toks) {
+      if (t.kind == SV_BEGIN) {
+        cur.clear();
+      } else if (t.kind == SV_END) {
+        if (!cur.empty()) push_section(std::move(cur));
+        cur.clear();
+      } else if (t.kind != SV_CHUNK_SWAP) {
+        cur.push_back(mem[t.pad]);
+      }
+    }
+  }
+
+  void push_section(std::vector<sv_gate> gates) {
+    Step s;
+    s.type = Step::SECTION;
+    s.gates = std::move(gates);
+    ctr.sections++;
+    steps.push_back(std::move(s));
   }
 };
 

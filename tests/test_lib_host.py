@@ -150,3 +150,20 @@ def test_plan_unblocked_matches():
     assert sum(1 for r in plan if int(r["kind"]) == C.BEGIN) == 50
     with pytest.raises(sv.SvError, match="EINFEASIBLE"):
         sv.plan_circuit(C.records([C.gate(C.U1, 7, mat=C.H_MATRIX)]), 8, 4, 1, flags=sv.SV_UNBLOCKED)
+
+
+def test_plan_splits_wide_sections():
+    # chunk_bits above the 13-bit tile limit: sections are split (same pass at c = 13), never wider
+    n = 18
+    recs = C.quantum_volume(n, 8, 2)
+    plan = run_plan_dense(recs, n, 16, 0)
+    act, widest = set(), 0
+    for r in plan:
+        k = int(r["kind"])
+        if k == C.BEGIN:
+            act = set()
+        elif k == C.END:
+            widest = max(widest, len(act))
+        elif k in (C.U1, C.U2):
+            act |= {int(r["q0"])} | ({int(r["q1"])} if k == C.U2 else set())
+    assert widest <= 13

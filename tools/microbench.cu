@@ -48,6 +48,30 @@ __global__ void dmma_kernel(double* out, int iters) {
   for (int i = 0; i < 4; i++) s += c[i][0] + c[i][1];
   if (s == 123.456) out[0] = s;
 }
+// DMMA and DFMA interleaved: if the FP64 tensor path and the FMA pipe are separate units, the
+// combined FMA rate exceeds either alone.
+__global__ void mixed_kernel(double* out, int iters, double a0, double b0) {
+  double a = threadIdx.x * 1e-3, b = 0.5;
+  double c[4][2];
+  double x[8];
+  for (int i = 0; i < 4; i++) { c[i][0] = 0; c[i][1] = 0; }
+  for (int i = 0; i < 8; i++) x[i] = threadIdx.x + i;
+  for (int it = 0; it < iters; it++) {
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+#pragma unroll
+      for (int i = 0; i < 8; i++) x[i] = fma(x[i], a0, b0);
+  }
+  double s = 0;
+  for (int i = 0; i < 4; i++) s += c[i][0] + c[i][1];
+  for (int i = 0; i < 8; i++) s += x[i];
+  if (s == 123.456) out[0] = s;
+}
+
 __global__ void smem_kernel(double* out, int iters) {
   extern __shared__ double2 sm[];
   int n = 4096;
@@ -103,6 +127,15 @@ int main() {
     cudaEventRecord(e1); CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1);
     double fmas = (double)blocks * (threads / 32) * iters * 4 * 256.0;
     printf("{\"bench\":\"dmma_m8n8k4\",\"ms\":%.3f,\"fma_per_s\":%.4e,\"tflops\":%.2f}\n", ms, fmas / (ms * 1e-3), 2 * fmas / (ms * 1e-3) / 1e12);
+  }
+  for (int rep = 0; rep < 2; rep++) {
+    int iters = 20000, blocks = sms * 4, threads = 256;
+    cudaEventRecord(e0);
+    mixed_kernel<<<blocks, threads>>>(dout, iters, 0.999, 1e-3);
+    cudaEventRecord(e1); CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1);
+    double mma_fmas = (double)blocks * (threads / 32) * iters * 4 * 256.0;
+    double dfmas = (double)blocks * threads * iters * 32;
+    printf("{\"bench\":\"dmma+dfma\",\"ms\":%.3f,\"total_fma_per_s\":%.4e,\"mma_share\":%.2f}\n", ms, (mma_fmas + dfmas) / (ms * 1e-3), mma_fmas / (mma_fmas + dfmas));
   }
   CK(cudaFuncSetAttribute(smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
   for (int rep = 0; rep < 2; rep++) {
