@@ -577,18 +577,22 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
   if (!s.good()) return fail(h, s);
   h->prog.clear();
   const int T_default = 12;
-  for (const Step& st : steps) {
-    if (st.type != Step::SECTION) continue;
-    Status cs = compile_section(st.gates, h->nL, h->rank, h->g, T_default, h->dbl ? 3 : 4, h->prog);
-    if (!cs.good()) return fail(h, cs);
-    const Launch& L = h->prog.launches.back();
-    if (L.T > 13)
-      return fail(h, SV_ECAPACITY, "a section needs a tile larger than shared memory (lower chunk_bits)");
+  std::vector<size_t> launch_end(steps.size(), 0);  // one past the last launch of each step
+  for (size_t i = 0; i < steps.size(); i++) {
+    const Step& st = steps[i];
+    if (st.type == Step::SECTION) {
+      Status cs = compile_section_split(st.gates, h->nL, h->rank, h->g, T_default, h->dbl ? 3 : 4, h->prog);
+      if (!cs.good()) return fail(h, cs);
+      if (h->prog.launches.back().T > 13)
+        return fail(h, SV_ECAPACITY, "a section needs a tile larger than shared memory (lower chunk_bits)");
+    }
+    launch_end[i] = h->prog.launches.size();
   }
   h->stats.pass_ms = now_ms() - t0;
   if (int rc = upload_program(h)) return rc;
   size_t si = 0;
-  for (const Step& st : steps) {
+  for (size_t i = 0; i < steps.size(); i++) {
+    const Step& st = steps[i];
     switch (st.type) {
       case Step::EXCHANGE: {
         cudaEvent_t t = tstart(h);
@@ -597,13 +601,17 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
         break;
       }
       case Step::SECTION: {
-        const Launch& L = h->prog.launches[si++];
-        cudaEvent_t t = tstart(h);
-        CUDA_TRY(h, launch_section(h->dbl, h->sv, (const int*)h->d_prog.p + L.int_off, h->d_coef.p, L.T, L.r, L.n_out, h->st));
-        const double amps = (double)(1ull << h->nL);
-        tend(h, t, 0, 2.0 * amps * (double)h->amp, L.flops_per_amp * amps);
-        h->stats.kernel_launches++;
-        h->stats.sections++;
+        for (; si < launch_end[i]; si++) {
+          const Launch& L = h->prog.launches[si];
+          cudaEvent_t t = tstart(h);
+          CUDA_TRY(h, launch_section(h->dbl, h->sv, (const int*)h->d_prog.p + L.int_off, L.int_count,
+                                     (const char*)h->d_coef.p + L.coef_off * h->amp, L.coef_count, L.T, L.n_out,
+                                     L.n_phases, L.flags, h->st));
+          const double amps = (double)(1ull << h->nL);
+          tend(h, t, 0, 2.0 * amps * (double)h->amp, L.flops_per_amp * amps);
+          h->stats.kernel_launches++;
+          h->stats.sections++;
+        }
         break;
       }
       case Step::GATE: {

@@ -43,17 +43,20 @@ inline bool is_perm4(const double* m, int* perm) {  // 4x4 permutation matrix wi
 
 struct PGate {  // a gate on tile positions
   int type;
-  int a, b;          // slots are assigned later; here: positions (U*) or codes (DIAG)
-  uint32_t pmask;    // tile positions it touches (for dependencies)
+  int a, b;        // positions (U*/PERM) or memory-bit codes (DIAG: -1-mb local, 200/201 const)
+  uint32_t pmask;  // tile positions it touches (for dependencies)
   bool diag;
-  int coef;          // offset (in complex numbers) into Program::coefs
+  int src;         // index into the section's gate list (payload source)
   int extra;
 };
+
+constexpr int kDiagLocal = -1;  // DIAG operand: -(1 + memory bit)
 
 }  // namespace
 
 Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int world_log2, int T_default,
                        int swizzle_bits, Program& prog) {
+  (void)world_log2;
   // ---- tile bits
   uint64_t active = 0;
   for (const sv_gate& g : gates) {
@@ -84,35 +87,20 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
     }
   const int r = std::min(SV_R_BITS, T);
 
-  auto code_of = [&](int mb) -> int {
-    if (mb >= nL) return ((rank >> (mb - nL)) & 1) ? SV_CODE_ONE : SV_CODE_ZERO;
-    if (pos_of[mb] >= 0) return SV_CODE_TILE(pos_of[mb]);
-    return SV_CODE_OUT(mb);
-  };
-  auto push_coef = [&](const double* m, int count) -> int {
-    const int at = (int)(prog.coefs.size() / 2);
-    prog.coefs.insert(prog.coefs.end(), m, m + 2 * count);
-    return at;
-  };
-
   // ---- gates on positions
   std::vector<PGate> pg;
   pg.reserve(gates.size());
-  for (const sv_gate& g : gates) {
+  size_t ncoef = 0;
+  for (size_t gi = 0; gi < gates.size(); gi++) {
+    const sv_gate& g = gates[gi];
     PGate p{};
-    p.extra = 0;
+    p.src = (int)gi;
     switch (g.kind) {
       case SV_U1:
         p.a = pos_of[g.q0];
         p.pmask = 1u << p.a;
-        if (is_h_like(g.m)) {
-          p.type = SV_OP_H1;
-          const double s[2] = {g.m[0], 0.0};
-          p.coef = push_coef(s, 1);
-        } else {
-          p.type = SV_OP_U1;
-          p.coef = push_coef(g.m, 4);
-        }
+        p.type = is_h_like(g.m) ? SV_OP_H1 : SV_OP_U1;
+        ncoef += p.type == SV_OP_H1 ? 1 : 4;
         break;
       case SV_U2: {
         p.a = pos_of[g.q0];
@@ -122,32 +110,28 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
         if (is_perm4(g.m, perm)) {
           p.type = SV_OP_PERM2;
           p.extra = perm[0] | (perm[1] << 2) | (perm[2] << 4) | (perm[3] << 6);
-          p.coef = 0;
         } else {
           p.type = SV_OP_U2;
-          p.coef = push_coef(g.m, 16);
+          ncoef += 16;
         }
         break;
       }
       case SV_D1:
       case SV_D2: {
         p.diag = true;
-        p.a = code_of(g.q0);
-        p.b = g.kind == SV_D2 ? code_of(g.q1) : SV_CODE_ZERO;
-        p.pmask = 0;
-        if (p.a < 100) p.pmask |= 1u << p.a;
-        if (p.b < 100) p.pmask |= 1u << p.b;
-        double d[8] = {1, 0, 1, 0, 1, 0, 1, 0};
-        std::memcpy(d, g.m, sizeof(double) * (g.kind == SV_D2 ? 8 : 4));
-        const bool cp = g.kind == SV_D2 && d[0] == 1.0 && d[1] == 0.0 && d[2] == 1.0 && d[3] == 0.0 &&
-                        d[4] == 1.0 && d[5] == 0.0;
-        if (cp) {
-          p.type = SV_OP_DIAG_CP;
-          p.coef = push_coef(d + 6, 1);
-        } else {
-          p.type = SV_OP_DIAG;
-          p.coef = push_coef(d, 4);
-        }
+        auto operand = [&](int mb) {
+          if (mb >= nL) return ((rank >> (mb - nL)) & 1) ? SV_CODE_ONE : SV_CODE_ZERO;
+          return kDiagLocal - mb;
+        };
+        p.a = operand(g.q0);
+        p.b = g.kind == SV_D2 ? operand(g.q1) : SV_CODE_ZERO;
+        for (int x : {p.a, p.b})
+          if (x < 0 && pos_of[kDiagLocal - x] >= 0) p.pmask |= 1u << pos_of[kDiagLocal - x];
+        const double* d = g.m;
+        const bool cp = g.kind == SV_D2 && d[0] == 1.0 && d[1] == 0.0 && d[2] == 1.0 && d[3] == 0.0 && d[4] == 1.0 &&
+                        d[5] == 0.0;
+        p.type = cp ? SV_OP_DIAG_CP : SV_OP_DIAG;
+        ncoef += cp ? 1 : 4;
         break;
       }
       default:
@@ -155,6 +139,8 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
     }
     pg.push_back(p);
   }
+  const size_t coef_cap = swizzle_bits == 3 ? SV_CONST_COEF64 : SV_CONST_COEF32;
+  if (ncoef > coef_cap) return Status::err(kTooBig, "section coefficients exceed the constant budget");
 
   // ---- phase schedule
   struct Ph {
@@ -190,8 +176,10 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
       }
     }
     if (ph.ops.empty()) return Status::err(SV_EINFEASIBLE, "internal: phase schedule made no progress");
-    // pad the register set with the highest free positions (keeps low positions as thread bits)
-    for (int pos = T - 1; pos >= 0 && __builtin_popcount(rmask) < r; pos--) rmask |= 1u << pos;
+    // pad the register set with the highest free positions (keeps low positions as thread bits,
+    // so lanes walk contiguous memory)
+    for (int pos = T - 1; pos >= 0 && __builtin_popcount(rmask) < r; pos--)
+      if (!((rmask >> pos) & 1)) rmask |= 1u << pos;
     for (int pos = 0; pos < T; pos++)
       if ((rmask >> pos) & 1) ph.R.push_back(pos);
     phases.push_back(std::move(ph));
@@ -205,11 +193,14 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
 
   // ---- emit
   const size_t base = prog.ints.size();
+  const size_t cbase = prog.coefs.size() / 2;
   const int n_ops = (int)pg.size();
   const int header_ints = sizeof(SvSecHeader) / 4;
   const int phase_ints = sizeof(SvPhase) / 4;
   const int op_ints = sizeof(SvOp) / 4;
-  prog.ints.resize(base + header_ints + phase_ints * phases.size() + op_ints * n_ops, 0);
+  const size_t total_ints = header_ints + phase_ints * phases.size() + op_ints * (size_t)n_ops;
+  if (total_ints > SV_CONST_INTS) return Status::err(kTooBig, "section program exceeds the constant budget");
+  prog.ints.resize(base + total_ints, 0);
   SvSecHeader* H = reinterpret_cast<SvSecHeader*>(prog.ints.data() + base);
   H->T = T;
   H->r = r;
@@ -220,8 +211,14 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
   H->n_ops = n_ops;
   for (int j = 0; j < T; j++) H->tile_bits[j] = tile_bits[j];
   for (int j = 0; j < n_out; j++) H->out_bits[j] = out_bits[j];
+  auto push = [&](const double* m, int count) -> int {
+    const int at = (int)(prog.coefs.size() / 2 - cbase);
+    prog.coefs.insert(prog.coefs.end(), m, m + 2 * count);
+    return at;
+  };
 
   int op_cursor = 0;
+  bool lanes_contiguous_first = false, lanes_contiguous_last = false;
   for (size_t pi = 0; pi < phases.size(); pi++) {
     SvPhase* P = reinterpret_cast<SvPhase*>(prog.ints.data() + base + H->phase_off + phase_ints * pi);
     const Ph& ph = phases[pi];
@@ -248,25 +245,102 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
     }
     for (size_t i = 0; i < cand.size(); i++)
       if (!taken[i]) chosen.push_back(cand[i]);
-    for (size_t j = 0; j < chosen.size(); j++) P->tpos[j] = chosen[j];
+    int thread_of[SV_TMAX];
+    std::fill(thread_of, thread_of + SV_TMAX, -1);
+    for (size_t j = 0; j < chosen.size(); j++) {
+      P->tpos[j] = chosen[j];
+      thread_of[chosen[j]] = (int)j;
+    }
+    // lane group of 2^swizzle_bits threads walks one contiguous 128-byte run of HBM?
+    bool contiguous = (int)chosen.size() >= swizzle_bits;
+    for (int j = 0; contiguous && j < swizzle_bits; j++) contiguous = chosen[j] == j && tile_bits[j] == j;
+    if (pi == 0) lanes_contiguous_first = contiguous;
+    if (pi + 1 == phases.size()) lanes_contiguous_last = contiguous;
+
     P->op_begin = op_cursor;
     P->op_count = (int)ph.ops.size();
     for (int gi : ph.ops) {
       SvOp* O = reinterpret_cast<SvOp*>(prog.ints.data() + base + H->op_off + op_ints * op_cursor);
       const PGate& p = pg[gi];
+      const sv_gate& g = gates[p.src];
       O->type = p.type;
-      O->coef = p.coef;
       O->extra = p.extra;
-      if (p.diag) {
-        O->a = p.a;
-        O->b = p.b;
-      } else {
-        O->a = slot_of[p.a];
-        O->b = (p.type == SV_OP_U2 || p.type == SV_OP_PERM2) ? slot_of[p.b] : -1;
+      switch (p.type) {
+        case SV_OP_U2: {
+          int sa = slot_of[p.a], sb = slot_of[p.b];
+          double m[32];
+          std::memcpy(m, g.m, sizeof(m));
+          if (sa > sb) {  // canonical slot order: conjugate by the s=1 <-> s=2 permutation
+            static const int sw[4] = {0, 2, 1, 3};
+            for (int rr = 0; rr < 4; rr++)
+              for (int cc = 0; cc < 4; cc++) {
+                m[2 * (4 * rr + cc)] = g.m[2 * (4 * sw[rr] + sw[cc])];
+                m[2 * (4 * rr + cc) + 1] = g.m[2 * (4 * sw[rr] + sw[cc]) + 1];
+              }
+            std::swap(sa, sb);
+          }
+          O->a = sa;
+          O->b = sb;
+          O->coef = push(m, 16);
+          break;
+        }
+        case SV_OP_PERM2: {
+          int sa = slot_of[p.a], sb = slot_of[p.b];
+          if (sa > sb) {  // canonical slot order: relabel s = bit(a) + 2 bit(b) by swapping its bits
+            auto swb = [](int s) { return ((s & 1) << 1) | (s >> 1); };
+            int np = 0;
+            for (int s2 = 0; s2 < 4; s2++) np |= swb((p.extra >> (2 * swb(s2))) & 3) << (2 * s2);
+            O->extra = np;
+            std::swap(sa, sb);
+          }
+          O->a = sa;
+          O->b = sb;
+          O->coef = 0;
+          break;
+        }
+        case SV_OP_U1:
+          O->a = slot_of[p.a];
+          O->coef = push(g.m, 4);
+          break;
+        case SV_OP_H1: {
+          O->a = slot_of[p.a];
+          const double s[2] = {g.m[0], 0.0};
+          O->coef = push(s, 1);
+          break;
+        }
+        case SV_OP_DIAG:
+        case SV_OP_DIAG_CP: {
+          auto code = [&](int x) {
+            if (x >= 0) return x;  // constant
+            const int mb = kDiagLocal - x;
+            const int pos = pos_of[mb];
+            if (pos < 0) return SV_CODE_OUT(mb);
+            if (slot_of[pos] >= 0) return SV_CODE_SLOT(slot_of[pos]);
+            return SV_CODE_THREAD(thread_of[pos]);
+          };
+          int ca = code(p.a), cb = code(p.b);
+          double d[8] = {1, 0, 1, 0, 1, 0, 1, 0};
+          std::memcpy(d, g.m, sizeof(double) * (g.kind == SV_D2 ? 8 : 4));
+          // canonical form for the kernel: a register-slot operand comes first, two slots ascend
+          if (cb < 4 && (ca >= 4 || cb < ca)) {
+            std::swap(ca, cb);
+            std::swap(d[2], d[4]);  // d[s] with s = bit(a) + 2 bit(b): exchange s = 1 and s = 2
+            std::swap(d[3], d[5]);
+          }
+          O->a = ca;
+          O->b = cb;
+          if (p.type == SV_OP_DIAG_CP)
+            O->coef = push(d + 6, 1);
+          else
+            O->coef = push(d, 4);
+          break;
+        }
       }
       op_cursor++;
     }
   }
+  H->flags = (lanes_contiguous_first ? SV_FLAG_FIRST_DIRECT : 0) | (lanes_contiguous_last ? SV_FLAG_LAST_DIRECT : 0);
+
   // algorithmic flops per amplitude: U2 4x4 complex matvec = 32, U1 = 16, H1 = 4, PERM = 0,
   // DIAG = one complex multiply (6), DIAG_CP = one complex multiply on a quarter (1.5)
   double fpa = 0.0;
@@ -276,15 +350,34 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
   Launch L;
   L.flops_per_amp = fpa;
   L.int_off = base;
+  L.int_count = total_ints;
+  L.coef_off = cbase;
+  L.coef_count = prog.coefs.size() / 2 - cbase;
   L.T = T;
   L.r = r;
   L.n_out = n_out;
   L.n_phases = (int)phases.size();
   L.n_ops = n_ops;
+  L.flags = H->flags;
   prog.launches.push_back(L);
   // keep every section 16-byte aligned
   while (prog.ints.size() % 4) prog.ints.push_back(0);
   return Status::ok();
+}
+
+Status compile_section_split(const std::vector<sv_gate>& gates, int nL, int rank, int world_log2, int T_default,
+                             int swizzle_bits, Program& prog) {
+  const size_t ni = prog.ints.size(), nc = prog.coefs.size();
+  Status s = compile_section(gates, nL, rank, world_log2, T_default, swizzle_bits, prog);
+  if (s.code != kTooBig) return s;
+  prog.ints.resize(ni);
+  prog.coefs.resize(nc);
+  if (gates.size() < 2) return Status::err(SV_ECAPACITY, "a single gate exceeds the constant budget");
+  // Consecutive halves of the in-order gate list: each half is a valid section on its own.
+  const size_t h = gates.size() / 2;
+  std::vector<sv_gate> a(gates.begin(), gates.begin() + h), b(gates.begin() + h, gates.end());
+  if (Status sa = compile_section_split(a, nL, rank, world_log2, T_default, swizzle_bits, prog); !sa.good()) return sa;
+  return compile_section_split(b, nL, rank, world_log2, T_default, swizzle_bits, prog);
 }
 
 }  // namespace sv

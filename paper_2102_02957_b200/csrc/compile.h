@@ -7,9 +7,14 @@
 
 namespace sv {
 
+constexpr int kTooBig = -100;  // internal: section exceeds the __constant__ budget (split it)
+
 struct Launch {
-  size_t int_off;  // start of the section's SvSecHeader in Program::ints
-  int T, r, n_out, n_phases, n_ops;
+  size_t int_off;     // start of the section's SvSecHeader in Program::ints
+  size_t int_count;   // ints of header + phases + ops
+  size_t coef_off;    // first coefficient (complex index) of the section in Program::coefs
+  size_t coef_count;  // coefficients of the section
+  int T, r, n_out, n_phases, n_ops, flags;
   double flops_per_amp;  // algorithmic flops per amplitude of the section (DESIGN "Roofline")
 };
 
@@ -26,7 +31,11 @@ struct Program {
 
 // Compile one memory-frame section for this rank.  T_default: tile bits when the section needs
 // fewer; swizzle_bits: log2(amplitudes per 128-byte smem row) (3 for fp64, 4 for fp32).
+// compile_section_split splits sections whose program or coefficients exceed the __constant__
+// budget into consecutive in-order pieces (each its own launch).
 Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int world_log2, int T_default,
                        int swizzle_bits, Program& prog);
+Status compile_section_split(const std::vector<sv_gate>& gates, int nL, int rank, int world_log2, int T_default,
+                             int swizzle_bits, Program& prog);
 
 }  // namespace sv

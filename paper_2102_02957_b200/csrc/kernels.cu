@@ -1,9 +1,6 @@
 // kernels.cu — sm_100a kernels of the cache-blocked state-vector path.
 //
-//   K1 k_section      one HBM read + one HBM write of the shard per blocked section:
-//                     a CTA gathers its 2^T-amplitude tile into shared memory (XOR-fold swizzle),
-//                     runs the section's phases (each thread holds 16 amplitudes in registers and
-//                     applies every gate of the phase there), and writes the tile back once.
+//   (K1, the section kernel, is in section.cu)
 //   K2 k_gate_*       per-gate baseline: one pass per gate with the pair addressing of Listing 2
 //                     (P:242-254), 64-bit indices (the listing's 32-bit int would overflow).
 //   K5 reductions     norm, marginal probabilities, block masses and shot resolution.
@@ -15,6 +12,7 @@
 #include <cstdint>
 #include <cstring>
 
+#include "cplx.cuh"
 #include "kernels.cuh"
 #include "program.h"
 
@@ -23,355 +21,6 @@ namespace {
 
 constexpr int kRedBlocks = 148 * 8;  // fixed grid for deterministic reductions
 constexpr int kRedThreads = 256;
-
-// ------------------------------------------------------------------ complex helpers
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
-}
-__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
-}
-// acc + m * a
-__device__ __forceinline__ double2 cfma(double2 m, double2 a, double2 acc) {
-  acc.x = fma(m.x, a.x, acc.x);
-  acc.x = fma(-m.y, a.y, acc.x);
-  acc.y = fma(m.x, a.y, acc.y);
-  acc.y = fma(m.y, a.x, acc.y);
-  return acc;
-}
-__device__ __forceinline__ float2 cfma(float2 m, float2 a, float2 acc) {
-  acc.x = fmaf(m.x, a.x, acc.x);
-  acc.x = fmaf(-m.y, a.y, acc.x);
-  acc.y = fmaf(m.x, a.y, acc.y);
-  acc.y = fmaf(m.y, a.x, acc.y);
-  return acc;
-}
-__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
-__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
-__device__ __forceinline__ double abs2(double2 a) { return fma(a.x, a.x, a.y * a.y); }
-__device__ __forceinline__ double abs2(float2 a) { return (double)a.x * a.x + (double)a.y * a.y; }
-template <typename V> __device__ __forceinline__ V czero();
-template <> __device__ __forceinline__ double2 czero<double2>() { return make_double2(0.0, 0.0); }
-template <> __device__ __forceinline__ float2 czero<float2>() { return make_float2(0.f, 0.f); }
-template <typename V> __device__ __forceinline__ V cone();
-template <> __device__ __forceinline__ double2 cone<double2>() { return make_double2(1.0, 0.0); }
-template <> __device__ __forceinline__ float2 cone<float2>() { return make_float2(1.f, 0.f); }
-
-__device__ __forceinline__ double2 ldc(const double2* p) { return __ldg(p); }
-__device__ __forceinline__ float2 ldc(const float2* p) { return __ldg(p); }
-// volatile: keeps matrix elements out of long-lived registers (reloaded per use, L1 broadcast)
-__device__ __forceinline__ double2 ldv(const double2* p) {
-  double2 r;
-  asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
-  return r;
-}
-__device__ __forceinline__ float2 ldv(const float2* p) {
-  float2 r;
-  asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(r.x), "=f"(r.y) : "l"(p));
-  return r;
-}
-
-template <typename V>
-__device__ __forceinline__ V sel4(int s, V a0, V a1, V a2, V a3) {
-  return s == 0 ? a0 : (s == 1 ? a1 : (s == 2 ? a2 : a3));
-}
-
-// XOR-fold swizzle of a tile element index: the low G bits are XORed with every higher G-bit
-// group.  GF(2)-linear, so swz(a | b) = swz(a) ^ swz(b) for disjoint a, b.
-template <int G>
-__device__ __forceinline__ int swz(int i) {
-  int x = i >> G, f = 0;
-#pragma unroll
-  for (int j = 0; j < 5; j++) {
-    f ^= x;
-    x >>= G;
-  }
-  return i ^ (f & ((1 << G) - 1));
-}
-
-// ------------------------------------------------------------------ register-slot gates
-template <int S0, int S1, typename V>
-__device__ __forceinline__ void u2_slots(V (&v)[16], const V* __restrict__ m) {
-#pragma unroll
-  for (int q = 0; q < 16; q++) {
-    if (((q >> S0) & 1) || ((q >> S1) & 1)) continue;
-    const int i0 = q, i1 = q | (1 << S0), i2 = q | (1 << S1), i3 = q | (1 << S0) | (1 << S1);
-    const V a0 = v[i0], a1 = v[i1], a2 = v[i2], a3 = v[i3];
-#pragma unroll
-    for (int rr = 0; rr < 4; rr++) {
-      V acc = cmul(ldv(m + 4 * rr + 0), a0);
-      acc = cfma(ldv(m + 4 * rr + 1), a1, acc);
-      acc = cfma(ldv(m + 4 * rr + 2), a2, acc);
-      acc = cfma(ldv(m + 4 * rr + 3), a3, acc);
-      v[rr == 0 ? i0 : (rr == 1 ? i1 : (rr == 2 ? i2 : i3))] = acc;
-    }
-  }
-}
-
-template <typename V>
-__device__ __forceinline__ void op_u2(V (&v)[16], int a, int b, const V* __restrict__ m) {
-  switch (a * 4 + b) {
-    case 1: u2_slots<0, 1>(v, m); break;
-    case 2: u2_slots<0, 2>(v, m); break;
-    case 3: u2_slots<0, 3>(v, m); break;
-    case 4: u2_slots<1, 0>(v, m); break;
-    case 6: u2_slots<1, 2>(v, m); break;
-    case 7: u2_slots<1, 3>(v, m); break;
-    case 8: u2_slots<2, 0>(v, m); break;
-    case 9: u2_slots<2, 1>(v, m); break;
-    case 11: u2_slots<2, 3>(v, m); break;
-    case 12: u2_slots<3, 0>(v, m); break;
-    case 13: u2_slots<3, 1>(v, m); break;
-    case 14: u2_slots<3, 2>(v, m); break;
-    default: break;
-  }
-}
-
-template <int S, typename V>
-__device__ __forceinline__ void u1_slot(V (&v)[16], const V* __restrict__ m) {
-  const V m0 = ldc(m), m1 = ldc(m + 1), m2 = ldc(m + 2), m3 = ldc(m + 3);
-#pragma unroll
-  for (int q = 0; q < 16; q++) {
-    if ((q >> S) & 1) continue;
-    const V a0 = v[q], a1 = v[q | (1 << S)];
-    v[q] = cfma(m1, a1, cmul(m0, a0));
-    v[q | (1 << S)] = cfma(m3, a1, cmul(m2, a0));
-  }
-}
-
-template <typename V>
-__device__ __forceinline__ void op_u1(V (&v)[16], int a, const V* __restrict__ m) {
-  switch (a) {
-    case 0: u1_slot<0>(v, m); break;
-    case 1: u1_slot<1>(v, m); break;
-    case 2: u1_slot<2>(v, m); break;
-    case 3: u1_slot<3>(v, m); break;
-    default: break;
-  }
-}
-
-template <int S, typename V, typename R>
-__device__ __forceinline__ void h1_slot(V (&v)[16], R s) {
-#pragma unroll
-  for (int q = 0; q < 16; q++) {
-    if ((q >> S) & 1) continue;
-    const V a0 = v[q], a1 = v[q | (1 << S)];
-    v[q] = cscale(cadd(a0, a1), s);
-    v[q | (1 << S)] = cscale(csub(a0, a1), s);
-  }
-}
-
-template <typename V, typename R>
-__device__ __forceinline__ void op_h1(V (&v)[16], int a, R s) {
-  switch (a) {
-    case 0: h1_slot<0>(v, s); break;
-    case 1: h1_slot<1>(v, s); break;
-    case 2: h1_slot<2>(v, s); break;
-    case 3: h1_slot<3>(v, s); break;
-    default: break;
-  }
-}
-
-template <int S0, int S1, typename V>
-__device__ __forceinline__ void perm_slots(V (&v)[16], int perm) {
-  const int p0 = perm & 3, p1 = (perm >> 2) & 3, p2 = (perm >> 4) & 3, p3 = (perm >> 6) & 3;
-#pragma unroll
-  for (int q = 0; q < 16; q++) {
-    if (((q >> S0) & 1) || ((q >> S1) & 1)) continue;
-    const int i0 = q, i1 = q | (1 << S0), i2 = q | (1 << S1), i3 = q | (1 << S0) | (1 << S1);
-    const V a0 = v[i0], a1 = v[i1], a2 = v[i2], a3 = v[i3];
-    v[i0] = sel4(p0, a0, a1, a2, a3);
-    v[i1] = sel4(p1, a0, a1, a2, a3);
-    v[i2] = sel4(p2, a0, a1, a2, a3);
-    v[i3] = sel4(p3, a0, a1, a2, a3);
-  }
-}
-
-template <typename V>
-__device__ __forceinline__ void op_perm(V (&v)[16], int a, int b, int perm) {
-  switch (a * 4 + b) {
-    case 1: perm_slots<0, 1>(v, perm); break;
-    case 2: perm_slots<0, 2>(v, perm); break;
-    case 3: perm_slots<0, 3>(v, perm); break;
-    case 4: perm_slots<1, 0>(v, perm); break;
-    case 6: perm_slots<1, 2>(v, perm); break;
-    case 7: perm_slots<1, 3>(v, perm); break;
-    case 8: perm_slots<2, 0>(v, perm); break;
-    case 9: perm_slots<2, 1>(v, perm); break;
-    case 11: perm_slots<2, 3>(v, perm); break;
-    case 12: perm_slots<3, 0>(v, perm); break;
-    case 13: perm_slots<3, 1>(v, perm); break;
-    case 14: perm_slots<3, 2>(v, perm); break;
-    default: break;
-  }
-}
-
-__device__ __forceinline__ int code_bit(int code, int idx, uint64_t tile_off) {
-  if (code < 100) return (idx >> code) & 1;
-  if (code < 200) return (int)((tile_off >> (code - 100)) & 1ull);
-  return code - 200;
-}
-
-// ------------------------------------------------------------------ K1: section kernel
-template <typename V, int G, int NT, int MINB>
-__global__ void __launch_bounds__(NT, MINB)
-    k_section(V* __restrict__ sv, const int* __restrict__ prog, const V* __restrict__ coef) {
-  using R = decltype(V().x);
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  V* sm = reinterpret_cast<V*>(smem_raw);
-  const SvSecHeader* H = reinterpret_cast<const SvSecHeader*>(prog);
-  const int T = H->T, r = H->r, n_out = H->n_out;
-  const int nt_log = T - r;
-  const int nreg = 1 << r;
-  const int tid = threadIdx.x;
-
-  uint64_t tile_off = 0;
-  {
-    const uint64_t bid = blockIdx.x;
-    for (int j = 0; j < n_out; j++) tile_off |= ((bid >> j) & 1ull) << H->out_bits[j];
-  }
-  uint64_t off_t = 0;
-  for (int j = 0; j < nt_log; j++) off_t |= (uint64_t)((tid >> j) & 1) << H->tile_bits[j];
-  uint64_t hb[SV_R_BITS];
-  int hs[SV_R_BITS];
-#pragma unroll
-  for (int j = 0; j < SV_R_BITS; j++) {
-    hb[j] = j < r ? (1ull << H->tile_bits[nt_log + j]) : 0ull;
-    hs[j] = j < r ? swz<G>(1 << (nt_log + j)) : 0;
-  }
-  const int pt = swz<G>(tid);
-
-  V v[16];
-  const V* src = sv + (tile_off | off_t);
-#pragma unroll
-  for (int k = 0; k < 16; k++) {
-    v[k] = czero<V>();
-    if (k < nreg) {
-      uint64_t o = 0;
-#pragma unroll
-      for (int j = 0; j < SV_R_BITS; j++)
-        if ((k >> j) & 1) o |= hb[j];
-      v[k] = src[o];
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < 16; k++) {
-    if (k < nreg) {
-      int x = pt;
-#pragma unroll
-      for (int j = 0; j < SV_R_BITS; j++)
-        if ((k >> j) & 1) x ^= hs[j];
-      sm[x] = v[k];
-    }
-  }
-  __syncthreads();
-
-  const SvPhase* P = reinterpret_cast<const SvPhase*>(prog + H->phase_off);
-  const SvOp* O = reinterpret_cast<const SvOp*>(prog + H->op_off);
-  const int nph = H->n_phases;
-  for (int ph = 0; ph < nph; ph++) {
-    const SvPhase* p = P + ph;
-    int base = 0;
-    for (int j = 0; j < nt_log; j++) base |= ((tid >> j) & 1) << p->tpos[j];
-    const int pb = swz<G>(base);
-    int rb[SV_R_BITS], w[SV_R_BITS];
-#pragma unroll
-    for (int s = 0; s < SV_R_BITS; s++) {
-      rb[s] = s < r ? (1 << p->R[s]) : 0;
-      w[s] = swz<G>(rb[s]);
-    }
-#pragma unroll
-    for (int k = 0; k < 16; k++) {
-      if (k < nreg) {
-        int x = pb;
-#pragma unroll
-        for (int s = 0; s < SV_R_BITS; s++)
-          if ((k >> s) & 1) x ^= w[s];
-        v[k] = sm[x];
-      }
-    }
-    const int ob = p->op_begin, oc = p->op_count;
-    for (int oi = 0; oi < oc; oi++) {
-      const int4 h = __ldg(reinterpret_cast<const int4*>(O + ob + oi));
-      const int4 h2 = __ldg(reinterpret_cast<const int4*>(O + ob + oi) + 1);
-      const int type = h.x, a = h.y, b = h.z;
-      const V* c = coef + h.w;
-      switch (type) {
-        case SV_OP_U2: op_u2(v, a, b, c); break;
-        case SV_OP_U1: op_u1(v, a, c); break;
-        case SV_OP_H1: op_h1(v, a, (R)ldc(c).x); break;
-        case SV_OP_PERM2: op_perm(v, a, b, h2.x); break;
-        case SV_OP_DIAG: {
-          const V d0 = ldc(c), d1 = ldc(c + 1), d2 = ldc(c + 2), d3 = ldc(c + 3);
-#pragma unroll
-          for (int k = 0; k < 16; k++) {
-            if (k < nreg) {
-              int idx = base;
-#pragma unroll
-              for (int s = 0; s < SV_R_BITS; s++)
-                if ((k >> s) & 1) idx |= rb[s];
-              const int sidx = code_bit(a, idx, tile_off) | (code_bit(b, idx, tile_off) << 1);
-              v[k] = cmul(v[k], sel4(sidx, d0, d1, d2, d3));
-            }
-          }
-          break;
-        }
-        case SV_OP_DIAG_CP: {
-          const V d3 = ldc(c);
-#pragma unroll
-          for (int k = 0; k < 16; k++) {
-            if (k < nreg) {
-              int idx = base;
-#pragma unroll
-              for (int s = 0; s < SV_R_BITS; s++)
-                if ((k >> s) & 1) idx |= rb[s];
-              if (code_bit(a, idx, tile_off) & code_bit(b, idx, tile_off)) v[k] = cmul(v[k], d3);
-            }
-          }
-          break;
-        }
-        default: break;
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < 16; k++) {
-      if (k < nreg) {
-        int x = pb;
-#pragma unroll
-        for (int s = 0; s < SV_R_BITS; s++)
-          if ((k >> s) & 1) x ^= w[s];
-        sm[x] = v[k];
-      }
-    }
-    __syncthreads();
-  }
-
-#pragma unroll
-  for (int k = 0; k < 16; k++) {
-    if (k < nreg) {
-      int x = pt;
-#pragma unroll
-      for (int j = 0; j < SV_R_BITS; j++)
-        if ((k >> j) & 1) x ^= hs[j];
-      v[k] = sm[x];
-    }
-  }
-  V* dst = sv + (tile_off | off_t);
-#pragma unroll
-  for (int k = 0; k < 16; k++) {
-    if (k < nreg) {
-      uint64_t o = 0;
-#pragma unroll
-      for (int j = 0; j < SV_R_BITS; j++)
-        if ((k >> j) & 1) o |= hb[j];
-      dst[o] = v[k];
-    }
-  }
-}
 
 // ------------------------------------------------------------------ K2: per-gate baseline
 template <typename V>
@@ -612,21 +261,6 @@ __global__ void k_exchange_peer(V* __restrict__ local, V* __restrict__ remote, u
 }
 
 // ------------------------------------------------------------------ host helpers
-template <typename V, int G, int NT, int MINB>
-cudaError_t launch_section_t(V* sv, const int* prog, const V* coef, int T, int n_out, cudaStream_t st) {
-  static bool attr_set = false;
-  const size_t smem = sizeof(V) << T;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_section<V, G, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(sizeof(V) << 13));
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  const int threads = 1 << (T - SV_R_BITS < 0 ? 0 : T - SV_R_BITS);
-  k_section<V, G, NT, MINB><<<(unsigned)(1ull << n_out), threads, smem, st>>>(sv, prog, coef);
-  return cudaGetLastError();
-}
-
 inline unsigned grid_for(uint64_t work, int threads) {
   uint64_t b = (work + threads - 1) / threads;
   const uint64_t cap = 148ull * 16;
@@ -677,19 +311,6 @@ cudaError_t launch_gate_t(V* sv, int nL, const GateArgs& g, cudaStream_t st) {
 }  // namespace
 
 // ------------------------------------------------------------------ public wrappers
-cudaError_t launch_section(bool dbl, void* sv, const int* prog_dev, const void* coef_dev, int T, int r, int n_out,
-                           cudaStream_t st) {
-  (void)r;
-  if (dbl) {
-    if (T <= 12) return launch_section_t<double2, 3, 256, 2>((double2*)sv, prog_dev, (const double2*)coef_dev, T, n_out, st);
-    if (T == 13) return launch_section_t<double2, 3, 512, 1>((double2*)sv, prog_dev, (const double2*)coef_dev, T, n_out, st);
-    return cudaErrorInvalidValue;
-  }
-  if (T <= 12) return launch_section_t<float2, 4, 256, 2>((float2*)sv, prog_dev, (const float2*)coef_dev, T, n_out, st);
-  if (T == 13) return launch_section_t<float2, 4, 512, 1>((float2*)sv, prog_dev, (const float2*)coef_dev, T, n_out, st);
-  return cudaErrorInvalidValue;
-}
-
 cudaError_t launch_gate(bool dbl, void* sv, int nL, const GateArgs& g, cudaStream_t st) {
   return dbl ? launch_gate_t<double2>((double2*)sv, nL, g, st) : launch_gate_t<float2>((float2*)sv, nL, g, st);
 }

@@ -6,29 +6,41 @@
 //     and the grid enumerates the other local bits (out_bits);
 //   * PHASES: runs of gates whose non-diagonal qubits fit R_BITS "register" positions.  In a
 //     phase each thread holds 2^R_BITS amplitudes that differ only in those positions and applies
-//     the phase's gates in registers; shared memory is touched once per phase (load + store);
-//   * OPS: U2 / U1 / H1 / PERM on register slots, DIAG on any bit (tile position, out-of-tile
-//     local bit, or a rank bit folded to a constant on the host).
-// All records are plain ints so the same buffer serves host and device.
+//     the phase's gates in registers; shared memory is touched once per phase boundary, and the
+//     first / last phase read / write HBM directly when their lane bits are the tile's low bits;
+//   * OPS: U2 / U1 / H1 / PERM on register slots, DIAG on any bit (register slot, thread bit,
+//     out-of-tile local bit, or a rank bit folded to a constant on the host).
+// The program and the section's coefficients are copied into __constant__ memory before each
+// launch, so every warp reads them through uniform registers (LDCU) — matrices never occupy
+// vector registers or the LSU.
 #pragma once
 
 #define SV_R_BITS 4           // register positions per phase (16 amplitudes per thread)
 #define SV_TMAX 14            // max tile bits (fp64 T=13 -> 128 KiB smem)
 #define SV_MAX_OUT 48         // max out-of-tile local bits
 
+// __constant__ budget per section launch
+#define SV_CONST_INTS 4096    // 16 KiB of program
+#define SV_CONST_COEF64 2048  // 32 KiB of fp64 complex coefficients
+#define SV_CONST_COEF32 1024  // 8 KiB of fp32 complex coefficients
+
 // op types
-#define SV_OP_U2 1      // a = slot0, b = slot1, coef -> 16 complex (row-major, s = bit(a) + 2 bit(b))
+#define SV_OP_U2 1      // a = slot0 < b = slot1, coef -> 16 complex (row-major, s = bit(a) + 2 bit(b))
 #define SV_OP_U1 2      // a = slot, coef -> 4 complex (row-major)
 #define SV_OP_H1 3      // a = slot, coef -> 1 complex (scale s, real):  (x, y) -> (s(x+y), s(x-y))
 #define SV_OP_PERM2 4   // a = slot0, b = slot1, extra = packed permutation out[s] = in[(extra >> 2s) & 3]
 #define SV_OP_DIAG 5    // a = code0, b = code1, coef -> 4 complex d[s], s = bit(code0) + 2 bit(code1)
 #define SV_OP_DIAG_CP 6 // like DIAG with d0 = d1 = d2 = 1: only s == 3 is multiplied (coef -> d3)
 
-// DIAG bit codes
-#define SV_CODE_TILE(p) (p)           // tile position p (0 <= p < SV_TMAX)
+// DIAG bit codes (per phase)
+#define SV_CODE_SLOT(s) (s)           // register slot s (0..3): bit = (k >> s) & 1
+#define SV_CODE_THREAD(j) (32 + (j))  // thread-index bit j: bit = (tid >> j) & 1
 #define SV_CODE_OUT(mb) (100 + (mb))  // local memory bit mb outside the tile (per-CTA constant)
 #define SV_CODE_ZERO 200              // constant 0 (rank bit folded on the host, or unused)
 #define SV_CODE_ONE 201               // constant 1
+
+#define SV_FLAG_FIRST_DIRECT 1        // first phase loads straight from HBM
+#define SV_FLAG_LAST_DIRECT 2         // last phase stores straight to HBM
 
 struct SvSecHeader {
   int T;          // tile bits
@@ -38,7 +50,7 @@ struct SvSecHeader {
   int phase_off;  // int offset of the first SvPhase from the header
   int op_off;     // int offset of the first SvOp from the header
   int n_ops;
-  int pad;
+  int flags;      // SV_FLAG_*
   int tile_bits[16];        // tile position -> memory bit (ascending)
   int out_bits[SV_MAX_OUT]; // out-of-tile local memory bits (ascending) <- CTA index bits
 };
@@ -50,7 +62,7 @@ struct SvPhase {
 };
 
 struct SvOp {
-  int type, a, b, coef;  // coef: index into the complex coefficient array (whole circuit)
+  int type, a, b, coef;  // coef: index into the section's coefficients
   int extra, pad0, pad1, pad2;
 };
 

@@ -1,0 +1,424 @@
+// section.cu — K1, the section kernel: one HBM read + one HBM write of the shard per blocked
+// section (Listing 4 "for all chunks: apply gates of the blocking section").
+//
+// One CTA owns one 2^T-amplitude tile (a gather over the section's memory bits, program.h).
+// Each thread holds 16 amplitudes in registers that differ in the phase's 4 register positions
+// and applies every gate of the phase there; phases are separated by one shared-memory round
+// trip (XOR-fold swizzled, conflict-free for the lane groups the host chose); the first and last
+// phase talk to HBM directly when their lane bits are the tile's low memory bits.  The program
+// and the matrices live in __constant__ memory and reach the FMA pipe through uniform registers.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "cplx.cuh"
+#include "kernels.cuh"
+#include "program.h"
+
+namespace sv {
+
+__constant__ int c_prog[SV_CONST_INTS];
+__constant__ double2 c_coef64[SV_CONST_COEF64];
+__constant__ float2 c_coef32[SV_CONST_COEF32];
+
+namespace {
+
+template <typename V>
+__device__ __forceinline__ V cc(int i);
+template <>
+__device__ __forceinline__ double2 cc<double2>(int i) {
+  return c_coef64[i];
+}
+template <>
+__device__ __forceinline__ float2 cc<float2>(int i) {
+  return c_coef32[i];
+}
+
+// XOR-fold swizzle of a tile element index: the low G bits are XORed with every higher G-bit
+// group.  GF(2)-linear, so swz(a | b) = swz(a) ^ swz(b) for disjoint a, b.
+template <int G>
+__device__ __forceinline__ int swz(int i) {
+  int x = i >> G, f = 0;
+#pragma unroll
+  for (int j = 0; j < 5; j++) {
+    f ^= x;
+    x >>= G;
+  }
+  return i ^ (f & ((1 << G) - 1));
+}
+
+// ---------------------------------------------------------------- gates on register slots
+template <int S0, int S1, typename V>
+__device__ __forceinline__ void u2_slots(V (&v)[16], int cb) {
+#pragma unroll
+  for (int q = 0; q < 16; q++) {
+    if (((q >> S0) & 1) || ((q >> S1) & 1)) continue;
+    const int i0 = q, i1 = q | (1 << S0), i2 = q | (1 << S1), i3 = q | (1 << S0) | (1 << S1);
+    const V a0 = v[i0], a1 = v[i1], a2 = v[i2], a3 = v[i3];
+#pragma unroll
+    for (int rr = 0; rr < 4; rr++) {
+      V acc = cmul(cc<V>(cb + 4 * rr + 0), a0);
+      acc = cfma(cc<V>(cb + 4 * rr + 1), a1, acc);
+      acc = cfma(cc<V>(cb + 4 * rr + 2), a2, acc);
+      acc = cfma(cc<V>(cb + 4 * rr + 3), a3, acc);
+      v[rr == 0 ? i0 : (rr == 1 ? i1 : (rr == 2 ? i2 : i3))] = acc;
+    }
+  }
+}
+
+template <int S, typename V>
+__device__ __forceinline__ void u1_slot(V (&v)[16], int cb) {
+#pragma unroll
+  for (int q = 0; q < 16; q++) {
+    if ((q >> S) & 1) continue;
+    const V a0 = v[q], a1 = v[q | (1 << S)];
+    v[q] = cfma(cc<V>(cb + 1), a1, cmul(cc<V>(cb), a0));
+    v[q | (1 << S)] = cfma(cc<V>(cb + 3), a1, cmul(cc<V>(cb + 2), a0));
+  }
+}
+
+template <int S, typename V, typename R>
+__device__ __forceinline__ void h1_slot(V (&v)[16], R s) {
+#pragma unroll
+  for (int q = 0; q < 16; q++) {
+    if ((q >> S) & 1) continue;
+    const V a0 = v[q], a1 = v[q | (1 << S)];
+    v[q] = cscale(cadd(a0, a1), s);
+    v[q | (1 << S)] = cscale(csub(a0, a1), s);
+  }
+}
+
+template <int S0, int S1, typename V>
+__device__ __forceinline__ void perm_slots(V (&v)[16], int perm) {
+  const int p0 = perm & 3, p1 = (perm >> 2) & 3, p2 = (perm >> 4) & 3, p3 = (perm >> 6) & 3;
+#pragma unroll
+  for (int q = 0; q < 16; q++) {
+    if (((q >> S0) & 1) || ((q >> S1) & 1)) continue;
+    const int i0 = q, i1 = q | (1 << S0), i2 = q | (1 << S1), i3 = q | (1 << S0) | (1 << S1);
+    const V a0 = v[i0], a1 = v[i1], a2 = v[i2], a3 = v[i3];
+    v[i0] = sel4(p0, a0, a1, a2, a3);
+    v[i1] = sel4(p1, a0, a1, a2, a3);
+    v[i2] = sel4(p2, a0, a1, a2, a3);
+    v[i3] = sel4(p3, a0, a1, a2, a3);
+  }
+}
+
+// diagonal factors on register slots
+template <int S, typename V>
+__device__ __forceinline__ void d1_slot(V (&v)[16], V d0, V d1) {
+#pragma unroll
+  for (int k = 0; k < 16; k++) v[k] = cmul(v[k], ((k >> S) & 1) ? d1 : d0);
+}
+template <int S0, int S1, typename V>
+__device__ __forceinline__ void d2_slots(V (&v)[16], V d0, V d1, V d2, V d3) {
+#pragma unroll
+  for (int k = 0; k < 16; k++) v[k] = cmul(v[k], sel4(((k >> S0) & 1) | (((k >> S1) & 1) << 1), d0, d1, d2, d3));
+}
+template <int S0, int S1, typename V>
+__device__ __forceinline__ void cp_slots(V (&v)[16], V d3) {
+#pragma unroll
+  for (int k = 0; k < 16; k++)
+    if (((k >> S0) & 1) && ((k >> S1) & 1)) v[k] = cmul(v[k], d3);
+}
+template <int S, typename V>
+__device__ __forceinline__ void cp_slot(V (&v)[16], V d3) {
+#pragma unroll
+  for (int k = 0; k < 16; k++)
+    if ((k >> S) & 1) v[k] = cmul(v[k], d3);
+}
+template <typename V>
+__device__ __forceinline__ void scale_all(V (&v)[16], V f) {
+#pragma unroll
+  for (int k = 0; k < 16; k++) v[k] = cmul(v[k], f);
+}
+
+// dispatch on a canonical slot pair a < b (6 cases) / a single slot (4 cases)
+#define SV_PAIR_SWITCH(a, b, CALL)        \
+  switch ((a) * 4 + (b)) {                \
+    case 1: CALL(0, 1); break;            \
+    case 2: CALL(0, 2); break;            \
+    case 3: CALL(0, 3); break;            \
+    case 6: CALL(1, 2); break;            \
+    case 7: CALL(1, 3); break;            \
+    case 11: CALL(2, 3); break;           \
+    default: break;                       \
+  }
+#define SV_SLOT_SWITCH(a, CALL) \
+  switch (a) {                  \
+    case 0: CALL(0); break;     \
+    case 1: CALL(1); break;     \
+    case 2: CALL(2); break;     \
+    case 3: CALL(3); break;     \
+    default: break;             \
+  }
+
+// value of a non-slot DIAG bit code for this thread / tile
+__device__ __forceinline__ int code_val(int code, int tid, uint64_t tile_off) {
+  if (code < 100) return (tid >> (code - 32)) & 1;
+  if (code < 200) return (int)((tile_off >> (code - 100)) & 1ull);
+  return code - 200;
+}
+
+template <typename V, typename R>
+__device__ __forceinline__ void run_op(V (&v)[16], int oi, int tid, uint64_t tile_off) {
+  const int type = c_prog[oi], a = c_prog[oi + 1], b = c_prog[oi + 2], cb = c_prog[oi + 3];
+  switch (type) {
+    case SV_OP_U2: {
+#define CALL_U2(x, y) u2_slots<x, y>(v, cb)
+      SV_PAIR_SWITCH(a, b, CALL_U2)
+#undef CALL_U2
+      break;
+    }
+    case SV_OP_U1: {
+#define CALL_U1(x) u1_slot<x>(v, cb)
+      SV_SLOT_SWITCH(a, CALL_U1)
+#undef CALL_U1
+      break;
+    }
+    case SV_OP_H1: {
+      const R s = cc<V>(cb).x;
+#define CALL_H1(x) h1_slot<x>(v, s)
+      SV_SLOT_SWITCH(a, CALL_H1)
+#undef CALL_H1
+      break;
+    }
+    case SV_OP_PERM2: {
+      const int perm = c_prog[oi + 4];
+#define CALL_P(x, y) perm_slots<x, y>(v, perm)
+      SV_PAIR_SWITCH(a, b, CALL_P)
+#undef CALL_P
+      break;
+    }
+    case SV_OP_DIAG: {
+      const V d0 = cc<V>(cb), d1 = cc<V>(cb + 1), d2 = cc<V>(cb + 2), d3 = cc<V>(cb + 3);
+      if (a < 4 && b < 4) {
+#define CALL_D2(x, y) d2_slots<x, y>(v, d0, d1, d2, d3)
+        SV_PAIR_SWITCH(a, b, CALL_D2)
+#undef CALL_D2
+      } else if (a < 4) {
+        const int tb = code_val(b, tid, tile_off);
+        const V e0 = tb ? d2 : d0, e1 = tb ? d3 : d1;
+#define CALL_D1(x) d1_slot<x>(v, e0, e1)
+        SV_SLOT_SWITCH(a, CALL_D1)
+#undef CALL_D1
+      } else {
+        const int s = code_val(a, tid, tile_off) | (code_val(b, tid, tile_off) << 1);
+        scale_all(v, sel4(s, d0, d1, d2, d3));
+      }
+      break;
+    }
+    case SV_OP_DIAG_CP: {
+      const V d3 = cc<V>(cb);
+      if (a < 4 && b < 4) {
+#define CALL_CP2(x, y) cp_slots<x, y>(v, d3)
+        SV_PAIR_SWITCH(a, b, CALL_CP2)
+#undef CALL_CP2
+      } else if (a < 4) {
+        if (code_val(b, tid, tile_off)) {
+#define CALL_CP1(x) cp_slot<x>(v, d3)
+          SV_SLOT_SWITCH(a, CALL_CP1)
+#undef CALL_CP1
+        }
+      } else if (code_val(a, tid, tile_off) & code_val(b, tid, tile_off)) {
+        scale_all(v, d3);
+      }
+      break;
+    }
+    default:
+      break;
+  }
+}
+
+// header field offsets (ints) — see SvSecHeader
+constexpr int kH_T = 0, kH_R = 1, kH_NOUT = 2, kH_NPH = 3, kH_PHOFF = 4, kH_OPOFF = 5, kH_FLAGS = 7;
+constexpr int kH_TILE = 8, kH_OUT = 24;
+constexpr int kPhaseInts = sizeof(SvPhase) / 4, kOpInts = sizeof(SvOp) / 4;
+
+template <typename V, int G, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_section(V* __restrict__ sv) {
+  using R = decltype(V().x);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* sm = reinterpret_cast<V*>(smem_raw);
+  const int T = c_prog[kH_T], r = c_prog[kH_R], n_out = c_prog[kH_NOUT], nph = c_prog[kH_NPH];
+  const int phoff = c_prog[kH_PHOFF], opoff = c_prog[kH_OPOFF], flags = c_prog[kH_FLAGS];
+  const int nt_log = T - r;
+  const int nreg = 1 << r;
+  const int tid = threadIdx.x;
+
+  uint64_t tile_off = 0;
+  {
+    const uint64_t bid = blockIdx.x;
+    for (int j = 0; j < n_out; j++) tile_off |= ((bid >> j) & 1ull) << c_prog[kH_OUT + j];
+  }
+
+  V v[16];
+#pragma unroll
+  for (int k = 0; k < 16; k++) v[k] = czero<V>();
+
+  const bool first_direct = flags & SV_FLAG_FIRST_DIRECT;
+  const bool last_direct = flags & SV_FLAG_LAST_DIRECT;
+  // load-order mapping (used when a boundary phase is not direct): element i = tid + (k << nt_log)
+  const int pt = swz<G>(tid);
+  if (!first_direct) {
+    uint64_t off_t = 0;
+    for (int j = 0; j < nt_log; j++) off_t |= (uint64_t)((tid >> j) & 1) << c_prog[kH_TILE + j];
+    const V* src = sv + (tile_off | off_t);
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+      if (k < nreg) {
+        uint64_t o = 0;
+#pragma unroll
+        for (int j = 0; j < SV_R_BITS; j++)
+          if ((k >> j) & 1) o |= 1ull << c_prog[kH_TILE + nt_log + j];
+        v[k] = src[o];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+      if (k < nreg) {
+        int x = pt;
+#pragma unroll
+        for (int j = 0; j < SV_R_BITS; j++)
+          if ((k >> j) & 1) x ^= swz<G>(1 << (nt_log + j));
+        sm[x] = v[k];
+      }
+    }
+    __syncthreads();
+  }
+
+  for (int ph = 0; ph < nph; ph++) {
+    const int P = phoff + ph * kPhaseInts;
+    const bool direct_in = ph == 0 && first_direct;
+    const bool direct_out = ph == nph - 1 && last_direct;
+    int base = 0;
+    for (int j = 0; j < nt_log; j++) base |= ((tid >> j) & 1) << c_prog[P + SV_R_BITS + j];
+    const int pb = swz<G>(base);
+    if (direct_in) {
+      uint64_t mb = 0;
+      for (int j = 0; j < nt_log; j++) mb |= (uint64_t)((tid >> j) & 1) << c_prog[kH_TILE + c_prog[P + SV_R_BITS + j]];
+      const V* src = sv + (tile_off | mb);
+#pragma unroll
+      for (int k = 0; k < 16; k++) {
+        if (k < nreg) {
+          uint64_t o = 0;
+#pragma unroll
+          for (int s = 0; s < SV_R_BITS; s++)
+            if ((k >> s) & 1) o |= 1ull << c_prog[kH_TILE + c_prog[P + s]];
+          v[k] = src[o];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 16; k++) {
+        if (k < nreg) {
+          int x = pb;
+#pragma unroll
+          for (int s = 0; s < SV_R_BITS; s++)
+            if ((k >> s) & 1) x ^= swz<G>(1 << c_prog[P + s]);
+          v[k] = sm[x];
+        }
+      }
+    }
+    const int ob = c_prog[P + SV_R_BITS + 16], oc = c_prog[P + SV_R_BITS + 17];
+    for (int o = 0; o < oc; o++) run_op<V, R>(v, opoff + (ob + o) * kOpInts, tid, tile_off);
+    if (direct_out) {
+      uint64_t mb = 0;
+      for (int j = 0; j < nt_log; j++) mb |= (uint64_t)((tid >> j) & 1) << c_prog[kH_TILE + c_prog[P + SV_R_BITS + j]];
+      V* dst = sv + (tile_off | mb);
+#pragma unroll
+      for (int k = 0; k < 16; k++) {
+        if (k < nreg) {
+          uint64_t o = 0;
+#pragma unroll
+          for (int s = 0; s < SV_R_BITS; s++)
+            if ((k >> s) & 1) o |= 1ull << c_prog[kH_TILE + c_prog[P + s]];
+          dst[o] = v[k];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 16; k++) {
+        if (k < nreg) {
+          int x = pb;
+#pragma unroll
+          for (int s = 0; s < SV_R_BITS; s++)
+            if ((k >> s) & 1) x ^= swz<G>(1 << c_prog[P + s]);
+          sm[x] = v[k];
+        }
+      }
+      __syncthreads();
+    }
+  }
+
+  if (!last_direct) {
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+      if (k < nreg) {
+        int x = pt;
+#pragma unroll
+        for (int j = 0; j < SV_R_BITS; j++)
+          if ((k >> j) & 1) x ^= swz<G>(1 << (nt_log + j));
+        v[k] = sm[x];
+      }
+    }
+    uint64_t off_t = 0;
+    for (int j = 0; j < nt_log; j++) off_t |= (uint64_t)((tid >> j) & 1) << c_prog[kH_TILE + j];
+    V* dst = sv + (tile_off | off_t);
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+      if (k < nreg) {
+        uint64_t o = 0;
+#pragma unroll
+        for (int j = 0; j < SV_R_BITS; j++)
+          if ((k >> j) & 1) o |= 1ull << c_prog[kH_TILE + nt_log + j];
+        dst[o] = v[k];
+      }
+    }
+  }
+}
+
+template <typename V, int G, int NT, int MINB>
+cudaError_t launch_t(V* sv, int T, int n_out, size_t smem, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_section<V, G, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(sizeof(V) << 13));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int threads = 1 << (T > SV_R_BITS ? T - SV_R_BITS : 0);
+  k_section<V, G, NT, MINB><<<(unsigned)(1ull << n_out), threads, smem, st>>>(sv);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_section(bool dbl, void* sv, const int* prog_dev, size_t int_count, const void* coef_dev,
+                           size_t coef_count, int T, int n_out, int n_phases, int flags, cudaStream_t st) {
+  if (int_count > SV_CONST_INTS) return cudaErrorInvalidValue;
+  cudaError_t e = cudaMemcpyToSymbolAsync(c_prog, prog_dev, int_count * sizeof(int), 0, cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return e;
+  if (coef_count) {
+    if (dbl) {
+      if (coef_count > SV_CONST_COEF64) return cudaErrorInvalidValue;
+      e = cudaMemcpyToSymbolAsync(c_coef64, coef_dev, coef_count * sizeof(double2), 0, cudaMemcpyDeviceToDevice, st);
+    } else {
+      if (coef_count > SV_CONST_COEF32) return cudaErrorInvalidValue;
+      e = cudaMemcpyToSymbolAsync(c_coef32, coef_dev, coef_count * sizeof(float2), 0, cudaMemcpyDeviceToDevice, st);
+    }
+    if (e != cudaSuccess) return e;
+  }
+  const bool no_smem = n_phases == 1 && (flags & SV_FLAG_FIRST_DIRECT) && (flags & SV_FLAG_LAST_DIRECT);
+  if (dbl) {
+    const size_t smem = no_smem ? 0 : sizeof(double2) << T;
+    if (T <= 12) return launch_t<double2, 3, 256, 2>((double2*)sv, T, n_out, smem, st);
+    if (T == 13) return launch_t<double2, 3, 512, 1>((double2*)sv, T, n_out, smem, st);
+    return cudaErrorInvalidValue;
+  }
+  const size_t smem = no_smem ? 0 : sizeof(float2) << T;
+  if (T <= 12) return launch_t<float2, 4, 256, 2>((float2*)sv, T, n_out, smem, st);
+  if (T == 13) return launch_t<float2, 4, 512, 1>((float2*)sv, T, n_out, smem, st);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace sv
