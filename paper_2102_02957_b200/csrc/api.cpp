@@ -580,7 +580,7 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
   std::vector<size_t> launch_end(steps.size(), 0);  // one past the last launch of each step
   for (size_t i = 0; i < steps.size(); i++) {
     const Step& st = steps[i];
-    if (st.type == Step::SECTION) {
+    if (st.type == Step::SECTION && h->nL >= SV_R_BITS) {
       Status cs = compile_section_split(st.gates, h->nL, h->rank, h->g, T_default, h->dbl ? 3 : 4, h->prog);
       if (!cs.good()) return fail(h, cs);
       if (h->prog.launches.back().T > 13)
@@ -601,6 +601,11 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
         break;
       }
       case Step::SECTION: {
+        if (h->nL < SV_R_BITS) {  // shards of < 16 amplitudes: per-gate kernels (no tile to block)
+          for (const sv_gate& gm : st.gates)
+            if (int rc = gate_step(h, gm)) return rc;
+          break;
+        }
         for (; si < launch_end[i]; si++) {
           const Launch& L = h->prog.launches[si];
           cudaEvent_t t = tstart(h);

@@ -211,6 +211,8 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
   H->n_ops = n_ops;
   for (int j = 0; j < T; j++) H->tile_bits[j] = tile_bits[j];
   for (int j = 0; j < n_out; j++) H->out_bits[j] = out_bits[j];
+  for (int j = 0; j < r; j++) H->lw[j] = sv_swz_host(1 << (T - r + j), swizzle_bits);
+  for (int j = 0; j < T - r; j++) H->ltw[j] = sv_swz_host(1 << j, swizzle_bits);
   auto push = [&](const double* m, int count) -> int {
     const int at = (int)(prog.coefs.size() / 2 - cbase);
     prog.coefs.insert(prog.coefs.end(), m, m + 2 * count);
@@ -226,6 +228,8 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
     std::fill(slot_of, slot_of + SV_TMAX, -1);
     for (int s = 0; s < r; s++) {
       P->R[s] = ph.R[s];
+      P->rw[s] = sv_swz_host(1 << ph.R[s], swizzle_bits);
+      P->rmb[s] = tile_bits[ph.R[s]];
       slot_of[ph.R[s]] = s;
     }
     // thread bits: the first `swizzle_bits` get distinct residues mod swizzle_bits so a group of
@@ -249,6 +253,8 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
     std::fill(thread_of, thread_of + SV_TMAX, -1);
     for (size_t j = 0; j < chosen.size(); j++) {
       P->tpos[j] = chosen[j];
+      P->tw[j] = sv_swz_host(1 << chosen[j], swizzle_bits);
+      P->tmb[j] = tile_bits[chosen[j]];
       thread_of[chosen[j]] = (int)j;
     }
     // lane group of 2^swizzle_bits threads walks one contiguous 128-byte run of HBM?

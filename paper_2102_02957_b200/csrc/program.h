@@ -53,12 +53,29 @@ struct SvSecHeader {
   int flags;      // SV_FLAG_*
   int tile_bits[16];        // tile position -> memory bit (ascending)
   int out_bits[SV_MAX_OUT]; // out-of-tile local memory bits (ascending) <- CTA index bits
+  int lw[SV_R_BITS];        // load-order mapping: swz(1 << (T - r + j)) of register bit j
+  int ltw[16];              // load-order mapping: swz(1 << j) of thread bit j
 };
 
+// XOR-fold swizzle of a tile element index (host and device): the low G bits are XORed with
+// every higher G-bit group.  GF(2)-linear, so swz(a | b) = swz(a) ^ swz(b) for disjoint a, b.
+inline int sv_swz_host(int i, int G) {
+  int x = i >> G, f = 0;
+  for (int j = 0; j < 6; j++) {
+    f ^= x;
+    x >>= G;
+  }
+  return i ^ (f & ((1 << G) - 1));
+}
+
 struct SvPhase {
-  int R[SV_R_BITS];  // register slot -> tile position
-  int tpos[16];      // thread-index bit j -> tile position (T - r entries used)
+  int R[SV_R_BITS];    // register slot -> tile position
+  int rw[SV_R_BITS];   // swz(1 << R[s]): smem offset contribution of register slot s
+  int rmb[SV_R_BITS];  // memory bit of register slot s (direct HBM phases)
   int op_begin, op_count, pad0, pad1;
+  int tpos[16];        // thread-index bit j -> tile position (T - r entries used)
+  int tw[16];          // swz(1 << tpos[j])
+  int tmb[16];         // memory bit of thread bit j
 };
 
 struct SvOp {

@@ -229,20 +229,32 @@ __device__ __forceinline__ void run_op(V (&v)[16], int oi, int tid, uint64_t til
   }
 }
 
-// header field offsets (ints) — see SvSecHeader
-constexpr int kH_T = 0, kH_R = 1, kH_NOUT = 2, kH_NPH = 3, kH_PHOFF = 4, kH_OPOFF = 5, kH_FLAGS = 7;
-constexpr int kH_TILE = 8, kH_OUT = 24;
+// header / phase field offsets (ints) — see SvSecHeader / SvPhase
+constexpr int kH_T = 0, kH_NOUT = 2, kH_NPH = 3, kH_PHOFF = 4, kH_OPOFF = 5;
+constexpr int kH_TILE = 8, kH_OUT = 24, kH_LW = 72, kH_LTW = 76;
+constexpr int kP_RW = 4, kP_RMB = 8, kP_OPB = 12, kP_OPC = 13, kP_TW = 32, kP_TMB = 48;
 constexpr int kPhaseInts = sizeof(SvPhase) / 4, kOpInts = sizeof(SvOp) / 4;
+static_assert(sizeof(SvSecHeader) / 4 == kH_LTW + 16, "header layout");
+static_assert(kPhaseInts == 64, "phase layout");
 
-template <typename V, int G, int NT, int MINB>
+// x ^ (the XOR of w[s] over the set bits s of the compile-time register index k)
+template <int K>
+__device__ __forceinline__ int xk(int x, const int (&w)[SV_R_BITS]) {
+#pragma unroll
+  for (int s = 0; s < SV_R_BITS; s++)
+    if ((K >> s) & 1) x ^= w[s];
+  return x;
+}
+
+template <typename V, int G, int NT, int MINB, bool FIRST, bool LAST>
 __global__ void __launch_bounds__(NT, MINB) k_section(V* __restrict__ sv) {
   using R = decltype(V().x);
+  constexpr int RB = SV_R_BITS;  // the host guarantees T >= RB, so every phase has RB register slots
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V* sm = reinterpret_cast<V*>(smem_raw);
-  const int T = c_prog[kH_T], r = c_prog[kH_R], n_out = c_prog[kH_NOUT], nph = c_prog[kH_NPH];
-  const int phoff = c_prog[kH_PHOFF], opoff = c_prog[kH_OPOFF], flags = c_prog[kH_FLAGS];
-  const int nt_log = T - r;
-  const int nreg = 1 << r;
+  const int T = c_prog[kH_T], n_out = c_prog[kH_NOUT], nph = c_prog[kH_NPH];
+  const int phoff = c_prog[kH_PHOFF], opoff = c_prog[kH_OPOFF];
+  const int nt_log = T - RB;
   const int tid = threadIdx.x;
 
   uint64_t tile_off = 0;
@@ -252,143 +264,134 @@ __global__ void __launch_bounds__(NT, MINB) k_section(V* __restrict__ sv) {
   }
 
   V v[16];
+  // load-order mapping for the non-direct boundaries: element i = tid + (k << nt_log)
+  int pt = 0;
+  uint64_t off_t = 0;
+  int lw[RB];
+  int64_t lo[RB];
+  if constexpr (!(FIRST && LAST)) {
+    for (int j = 0; j < nt_log; j++) {
+      const int bit = (tid >> j) & 1;
+      pt ^= bit ? c_prog[kH_LTW + j] : 0;
+      off_t |= (uint64_t)bit << c_prog[kH_TILE + j];
+    }
 #pragma unroll
-  for (int k = 0; k < 16; k++) v[k] = czero<V>();
-
-  const bool first_direct = flags & SV_FLAG_FIRST_DIRECT;
-  const bool last_direct = flags & SV_FLAG_LAST_DIRECT;
-  // load-order mapping (used when a boundary phase is not direct): element i = tid + (k << nt_log)
-  const int pt = swz<G>(tid);
-  if (!first_direct) {
-    uint64_t off_t = 0;
-    for (int j = 0; j < nt_log; j++) off_t |= (uint64_t)((tid >> j) & 1) << c_prog[kH_TILE + j];
+    for (int s = 0; s < RB; s++) {
+      lw[s] = c_prog[kH_LW + s];
+      lo[s] = (int64_t)1 << c_prog[kH_TILE + nt_log + s];
+    }
+  }
+  if constexpr (FIRST) {  // phase 0 reads HBM directly in its own register mapping
+    const int P = phoff;
+    uint64_t mb = 0;
+    for (int j = 0; j < nt_log; j++) mb |= (uint64_t)((tid >> j) & 1) << c_prog[P + kP_TMB + j];
+    const V* src = sv + (tile_off | mb);
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+      int64_t o = 0;
+#pragma unroll
+      for (int s = 0; s < RB; s++)
+        if ((k >> s) & 1) o |= (int64_t)1 << c_prog[P + kP_RMB + s];
+      v[k] = src[o];
+    }
+  } else {  // coalesced load-order read, scattered into the swizzled tile
     const V* src = sv + (tile_off | off_t);
 #pragma unroll
     for (int k = 0; k < 16; k++) {
-      if (k < nreg) {
-        uint64_t o = 0;
+      int64_t o = 0;
 #pragma unroll
-        for (int j = 0; j < SV_R_BITS; j++)
-          if ((k >> j) & 1) o |= 1ull << c_prog[kH_TILE + nt_log + j];
-        v[k] = src[o];
-      }
+      for (int s = 0; s < RB; s++)
+        if ((k >> s) & 1) o |= lo[s];
+      v[k] = src[o];
     }
-#pragma unroll
-    for (int k = 0; k < 16; k++) {
-      if (k < nreg) {
-        int x = pt;
-#pragma unroll
-        for (int j = 0; j < SV_R_BITS; j++)
-          if ((k >> j) & 1) x ^= swz<G>(1 << (nt_log + j));
-        sm[x] = v[k];
-      }
-    }
+#define SV_STS(K) sm[xk<K>(pt, lw)] = v[K];
+    SV_STS(0) SV_STS(1) SV_STS(2) SV_STS(3) SV_STS(4) SV_STS(5) SV_STS(6) SV_STS(7)
+    SV_STS(8) SV_STS(9) SV_STS(10) SV_STS(11) SV_STS(12) SV_STS(13) SV_STS(14) SV_STS(15)
+#undef SV_STS
     __syncthreads();
   }
 
   for (int ph = 0; ph < nph; ph++) {
     const int P = phoff + ph * kPhaseInts;
-    const bool direct_in = ph == 0 && first_direct;
-    const bool direct_out = ph == nph - 1 && last_direct;
-    int base = 0;
-    for (int j = 0; j < nt_log; j++) base |= ((tid >> j) & 1) << c_prog[P + SV_R_BITS + j];
-    const int pb = swz<G>(base);
-    if (direct_in) {
-      uint64_t mb = 0;
-      for (int j = 0; j < nt_log; j++) mb |= (uint64_t)((tid >> j) & 1) << c_prog[kH_TILE + c_prog[P + SV_R_BITS + j]];
-      const V* src = sv + (tile_off | mb);
-#pragma unroll
-      for (int k = 0; k < 16; k++) {
-        if (k < nreg) {
-          uint64_t o = 0;
-#pragma unroll
-          for (int s = 0; s < SV_R_BITS; s++)
-            if ((k >> s) & 1) o |= 1ull << c_prog[kH_TILE + c_prog[P + s]];
-          v[k] = src[o];
-        }
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < 16; k++) {
-        if (k < nreg) {
-          int x = pb;
-#pragma unroll
-          for (int s = 0; s < SV_R_BITS; s++)
-            if ((k >> s) & 1) x ^= swz<G>(1 << c_prog[P + s]);
-          v[k] = sm[x];
-        }
-      }
+    const bool direct_in = FIRST && ph == 0;
+    const bool direct_out = LAST && ph == nph - 1;
+    int pb = 0;
+    uint64_t mb = 0;
+    for (int j = 0; j < nt_log; j++) {
+      const int bit = (tid >> j) & 1;
+      pb ^= bit ? c_prog[P + kP_TW + j] : 0;
+      if constexpr (LAST) mb |= (uint64_t)bit << c_prog[P + kP_TMB + j];
     }
-    const int ob = c_prog[P + SV_R_BITS + 16], oc = c_prog[P + SV_R_BITS + 17];
+    int w[RB];
+#pragma unroll
+    for (int s = 0; s < RB; s++) w[s] = c_prog[P + kP_RW + s];
+    if (!direct_in) {
+#define SV_LDS(K) v[K] = sm[xk<K>(pb, w)];
+      SV_LDS(0) SV_LDS(1) SV_LDS(2) SV_LDS(3) SV_LDS(4) SV_LDS(5) SV_LDS(6) SV_LDS(7)
+      SV_LDS(8) SV_LDS(9) SV_LDS(10) SV_LDS(11) SV_LDS(12) SV_LDS(13) SV_LDS(14) SV_LDS(15)
+#undef SV_LDS
+    }
+    const int ob = c_prog[P + kP_OPB], oc = c_prog[P + kP_OPC];
     for (int o = 0; o < oc; o++) run_op<V, R>(v, opoff + (ob + o) * kOpInts, tid, tile_off);
-    if (direct_out) {
-      uint64_t mb = 0;
-      for (int j = 0; j < nt_log; j++) mb |= (uint64_t)((tid >> j) & 1) << c_prog[kH_TILE + c_prog[P + SV_R_BITS + j]];
+    if (direct_out) {  // the last phase writes HBM directly in its own register mapping
       V* dst = sv + (tile_off | mb);
 #pragma unroll
       for (int k = 0; k < 16; k++) {
-        if (k < nreg) {
-          uint64_t o = 0;
+        int64_t o = 0;
 #pragma unroll
-          for (int s = 0; s < SV_R_BITS; s++)
-            if ((k >> s) & 1) o |= 1ull << c_prog[kH_TILE + c_prog[P + s]];
-          dst[o] = v[k];
-        }
+        for (int s = 0; s < RB; s++)
+          if ((k >> s) & 1) o |= (int64_t)1 << c_prog[P + kP_RMB + s];
+        dst[o] = v[k];
       }
     } else {
-#pragma unroll
-      for (int k = 0; k < 16; k++) {
-        if (k < nreg) {
-          int x = pb;
-#pragma unroll
-          for (int s = 0; s < SV_R_BITS; s++)
-            if ((k >> s) & 1) x ^= swz<G>(1 << c_prog[P + s]);
-          sm[x] = v[k];
-        }
-      }
+#define SV_STS(K) sm[xk<K>(pb, w)] = v[K];
+      SV_STS(0) SV_STS(1) SV_STS(2) SV_STS(3) SV_STS(4) SV_STS(5) SV_STS(6) SV_STS(7)
+      SV_STS(8) SV_STS(9) SV_STS(10) SV_STS(11) SV_STS(12) SV_STS(13) SV_STS(14) SV_STS(15)
+#undef SV_STS
       __syncthreads();
     }
   }
 
-  if (!last_direct) {
-#pragma unroll
-    for (int k = 0; k < 16; k++) {
-      if (k < nreg) {
-        int x = pt;
-#pragma unroll
-        for (int j = 0; j < SV_R_BITS; j++)
-          if ((k >> j) & 1) x ^= swz<G>(1 << (nt_log + j));
-        v[k] = sm[x];
-      }
-    }
-    uint64_t off_t = 0;
-    for (int j = 0; j < nt_log; j++) off_t |= (uint64_t)((tid >> j) & 1) << c_prog[kH_TILE + j];
+  if constexpr (!LAST) {
+#define SV_LDS(K) v[K] = sm[xk<K>(pt, lw)];
+    SV_LDS(0) SV_LDS(1) SV_LDS(2) SV_LDS(3) SV_LDS(4) SV_LDS(5) SV_LDS(6) SV_LDS(7)
+    SV_LDS(8) SV_LDS(9) SV_LDS(10) SV_LDS(11) SV_LDS(12) SV_LDS(13) SV_LDS(14) SV_LDS(15)
+#undef SV_LDS
     V* dst = sv + (tile_off | off_t);
 #pragma unroll
     for (int k = 0; k < 16; k++) {
-      if (k < nreg) {
-        uint64_t o = 0;
+      int64_t o = 0;
 #pragma unroll
-        for (int j = 0; j < SV_R_BITS; j++)
-          if ((k >> j) & 1) o |= 1ull << c_prog[kH_TILE + nt_log + j];
-        dst[o] = v[k];
-      }
+      for (int s = 0; s < RB; s++)
+        if ((k >> s) & 1) o |= lo[s];
+      dst[o] = v[k];
     }
   }
 }
 
-template <typename V, int G, int NT, int MINB>
-cudaError_t launch_t(V* sv, int T, int n_out, size_t smem, cudaStream_t st) {
+template <typename V, int G, int NT, int MINB, bool FIRST, bool LAST>
+cudaError_t launch_v(V* sv, int T, int n_out, size_t smem, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_section<V, G, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(sizeof(V) << 13));
+    cudaError_t e = cudaFuncSetAttribute(k_section<V, G, NT, MINB, FIRST, LAST>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(V) << 13));
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int threads = 1 << (T > SV_R_BITS ? T - SV_R_BITS : 0);
-  k_section<V, G, NT, MINB><<<(unsigned)(1ull << n_out), threads, smem, st>>>(sv);
+  const int threads = 1 << (T - SV_R_BITS);
+  k_section<V, G, NT, MINB, FIRST, LAST><<<(unsigned)(1ull << n_out), threads, smem, st>>>(sv);
   return cudaGetLastError();
+}
+
+// Direct-HBM boundary phases are compile-time variants.  (first direct, last via smem) is run as
+// the all-smem variant: ptxas keeps the coefficient loads on the uniform datapath in the other
+// three shapes only (checked by tests/test_sass.py).
+template <typename V, int G, int NT, int MINB>
+cudaError_t launch_t(V* sv, int T, int n_out, int flags, size_t smem, cudaStream_t st) {
+  const bool f = flags & SV_FLAG_FIRST_DIRECT, l = flags & SV_FLAG_LAST_DIRECT;
+  if (f && l) return launch_v<V, G, NT, MINB, true, true>(sv, T, n_out, smem, st);
+  if (l) return launch_v<V, G, NT, MINB, false, true>(sv, T, n_out, smem, st);
+  return launch_v<V, G, NT, MINB, false, false>(sv, T, n_out, smem, st);
 }
 
 }  // namespace
@@ -408,16 +411,17 @@ cudaError_t launch_section(bool dbl, void* sv, const int* prog_dev, size_t int_c
     }
     if (e != cudaSuccess) return e;
   }
+  if (T < SV_R_BITS) return cudaErrorInvalidValue;  // tiny shards run per-gate kernels instead
   const bool no_smem = n_phases == 1 && (flags & SV_FLAG_FIRST_DIRECT) && (flags & SV_FLAG_LAST_DIRECT);
   if (dbl) {
     const size_t smem = no_smem ? 0 : sizeof(double2) << T;
-    if (T <= 12) return launch_t<double2, 3, 256, 2>((double2*)sv, T, n_out, smem, st);
-    if (T == 13) return launch_t<double2, 3, 512, 1>((double2*)sv, T, n_out, smem, st);
+    if (T <= 12) return launch_t<double2, 3, 256, 2>((double2*)sv, T, n_out, flags, smem, st);
+    if (T == 13) return launch_t<double2, 3, 512, 1>((double2*)sv, T, n_out, flags, smem, st);
     return cudaErrorInvalidValue;
   }
   const size_t smem = no_smem ? 0 : sizeof(float2) << T;
-  if (T <= 12) return launch_t<float2, 4, 256, 2>((float2*)sv, T, n_out, smem, st);
-  if (T == 13) return launch_t<float2, 4, 512, 1>((float2*)sv, T, n_out, smem, st);
+  if (T <= 12) return launch_t<float2, 4, 256, 2>((float2*)sv, T, n_out, flags, smem, st);
+  if (T == 13) return launch_t<float2, 4, 512, 1>((float2*)sv, T, n_out, flags, smem, st);
   return cudaErrorInvalidValue;
 }
 
