@@ -96,6 +96,8 @@ typedef struct sv_stats {
   double gate_ms;             /* summed event time of per-gate (unblocked) launches            */
   double section_bytes;       /* algorithmic HBM bytes of the timed sections (2 x shard each)  */
   double section_flops;       /* algorithmic flops of the timed sections (DESIGN "Roofline")   */
+  uint64_t compactions;       /* standalone memory-bit swap passes (tile coalescing fallback)  */
+  uint64_t store_swaps;       /* memory-bit swaps fused into section stores (free)            */
 } sv_stats;
 
 /* ---- lifetime ------------------------------------------------------------------------- */

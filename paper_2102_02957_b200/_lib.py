@@ -34,7 +34,8 @@ class Stats(ctypes.Structure):
                 ("exchange_batches", ctypes.c_uint64), ("bytes_sent", ctypes.c_uint64),
                 ("kernel_launches", ctypes.c_uint64), ("pass_ms", ctypes.c_double), ("apply_ms", ctypes.c_double),
                 ("timed_sections", ctypes.c_uint64), ("section_ms", ctypes.c_double), ("exchange_ms", ctypes.c_double),
-                ("gate_ms", ctypes.c_double), ("section_bytes", ctypes.c_double), ("section_flops", ctypes.c_double)]
+                ("gate_ms", ctypes.c_double), ("section_bytes", ctypes.c_double), ("section_flops", ctypes.c_double),
+                ("compactions", ctypes.c_uint64), ("store_swaps", ctypes.c_uint64)]
 
 
 EXPORTS = ["sv_create", "sv_create_dist", "sv_destroy", "sv_nccl_unique_id", "sv_reset", "sv_apply_circuit",

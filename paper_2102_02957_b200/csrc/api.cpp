@@ -358,6 +358,17 @@ int drain_timing(sv_state* h) {
   return SV_OK;
 }
 
+// physical swap of memory bits m1 <-> m2 (both local), one pass over half of the shard
+int swap_step(sv_state* h, int m1, int m2) {
+  GateArgs a{};
+  a.type = 7;
+  a.q0 = m1;
+  a.q1 = m2;
+  CUDA_TRY(h, launch_gate(h->dbl, h->sv, h->nL, a, h->st));
+  h->stats.kernel_launches++;
+  return SV_OK;
+}
+
 int check_handle(sv_state* h) {
   if (!h) return fail(nullptr, SV_EINVAL, "null handle");
   CUDA_TRY(h, cudaSetDevice(h->device));
@@ -573,15 +584,17 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
   std::vector<int> pi = h->pi, sigma = h->sigma;
   std::vector<Step> steps;
   PlanCounters ctr;
-  Status s = make_plan(gates, n_gates, h->n, h->c, h->g, pi, sigma, flags, steps, ctr);
+  PlanLayout lay;
+  lay.low_bits = h->dbl ? 3 : 4;  // 128-byte runs
+  Status s = make_plan(gates, n_gates, h->n, h->c, h->g, pi, sigma, flags, steps, ctr, lay);
   if (!s.good()) return fail(h, s);
   h->prog.clear();
-  const int T_default = 12;
+  const int T_default = lay.tile_default;
   std::vector<size_t> launch_end(steps.size(), 0);  // one past the last launch of each step
   for (size_t i = 0; i < steps.size(); i++) {
     const Step& st = steps[i];
     if (st.type == Step::SECTION && h->nL >= SV_R_BITS) {
-      Status cs = compile_section_split(st.gates, h->nL, h->rank, h->g, T_default, h->dbl ? 3 : 4, h->prog);
+      Status cs = compile_section_split(st.gates, h->nL, h->rank, h->g, T_default, lay.low_bits, st.swaps, h->prog);
       if (!cs.good()) return fail(h, cs);
       if (h->prog.launches.back().T > 13)
         return fail(h, SV_ECAPACITY, "a section needs a tile larger than shared memory (lower chunk_bits)");
@@ -604,6 +617,8 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
         if (h->nL < SV_R_BITS) {  // shards of < 16 amplitudes: per-gate kernels (no tile to block)
           for (const sv_gate& gm : st.gates)
             if (int rc = gate_step(h, gm)) return rc;
+          for (const auto& sw : st.swaps)
+            if (int rc = swap_step(h, sw.first, sw.second)) return rc;
           break;
         }
         for (; si < launch_end[i]; si++) {
@@ -625,6 +640,14 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
         tend(h, t, 2, 0.0, 0.0);
         break;
       }
+      case Step::COMPACT: {  // standalone memory-bit swap passes that keep the next tile coalesced
+        cudaEvent_t t = tstart(h);
+        for (const auto& sw : st.swaps)
+          if (int rc = swap_step(h, sw.first, sw.second)) return rc;
+        tend(h, t, 2, 0.0, 0.0);
+        h->stats.compactions += st.swaps.size();
+        break;
+      }
     }
   }
   h->pi = pi;
@@ -632,6 +655,7 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
   h->stats.circuits++;
   h->stats.gates += n_gates;
   h->stats.chunk_swaps += ctr.chunk_swaps;
+  h->stats.store_swaps += ctr.store_swaps;
   h->stats.apply_ms = now_ms() - t0;
   return SV_OK;
 }
@@ -921,6 +945,15 @@ int sv_plan_circuit(const sv_gate* gates, size_t n_gates, int n, int c, int worl
         r.pad = (int32_t)i;
         recs.push_back(r);
       }
+    } else if (st.type == Step::COMPACT) {  // physical memory-bit swaps: SWAP records outside sections
+      for (const auto& sw : st.swaps) {
+        sv_gate r = mk;
+        r.kind = SV_SWAP;
+        r.q0 = sw.first;
+        r.q1 = sw.second;
+        r.pad = (int32_t)i;
+        recs.push_back(r);
+      }
     } else {
       sv_gate b = mk;
       b.kind = SV_BEGIN;
@@ -930,6 +963,14 @@ int sv_plan_circuit(const sv_gate* gates, size_t n_gates, int n, int c, int worl
       for (const sv_gate& gm : st.gates) recs.push_back(gm);
       b.kind = SV_END;
       recs.push_back(b);
+      for (const auto& sw : st.swaps) {  // swaps fused into the section's store, right after it
+        sv_gate r = mk;
+        r.kind = SV_SWAP;
+        r.q0 = sw.first;
+        r.q1 = sw.second;
+        r.pad = (int32_t)i;
+        recs.push_back(r);
+      }
     }
   }
   sv_gate* buf = (sv_gate*)std::malloc(sizeof(sv_gate) * std::max<size_t>(recs.size(), 1));

@@ -2,6 +2,7 @@
 #pragma once
 #include <cstdint>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/sv.h"
@@ -48,16 +49,38 @@ struct ExPair {
   int b;  // rank memory bit (>= nL)
 };
 struct Step {
-  enum Type { EXCHANGE = 0, SECTION = 1, GATE = 2 } type;
+  enum Type { EXCHANGE = 0, SECTION = 1, GATE = 2, COMPACT = 3 } type;
   std::vector<ExPair> ex;        // EXCHANGE
   std::vector<sv_gate> gates;    // SECTION / GATE: memory-frame gates (no SWAP inside SECTION)
+  // SECTION: memory-bit transpositions fused into the section's store (both bits in its tile);
+  // COMPACT: memory-bit transpositions done by a standalone swap pass (local bits).
+  std::vector<std::pair<int, int>> swaps;
 };
 struct PlanCounters {
-  uint64_t sections = 0, chunk_swaps = 0, exchanges = 0, exchange_batches = 0;
+  uint64_t sections = 0, chunk_swaps = 0, exchanges = 0, exchange_batches = 0, compactions = 0, store_swaps = 0;
 };
+// Layout policy knobs of the planner (plan.cpp).
+struct PlanLayout {
+  int low_bits = 3;    // memory bits every section tile should contain (3: 128-byte fp64 runs)
+  int max_tile = 13;   // largest tile (bits) one CTA holds
+  int tile_default = 12;
+};
+
+// The tile a section runs on (memory-bit mask), shared by the planner and the compiler: the
+// active bits, plus the lowest `low_bits` memory bits when that still fits max_tile, padded with
+// the lowest remaining local bits up to tile_default.
+inline uint64_t choose_tile(uint64_t active, int nL, const PlanLayout& L) {
+  const int nlow = L.low_bits < nL ? L.low_bits : nL;
+  uint64_t want = active | ((1ull << nlow) - 1);
+  if (__builtin_popcountll(want) > L.max_tile) want = active;
+  const int td = L.tile_default < nL ? L.tile_default : nL;
+  for (int b = 0; b < nL && __builtin_popcountll(want) < td; b++) want |= 1ull << b;
+  return want;
+}
 // Runs the pass (unless SV_UNBLOCKED) and maps it onto memory bits: every chunk_swap / SWAP is a
 // relabel of sigma; data moves only where a section needs a rank bit (DESIGN "Executor mapping").
 Status make_plan(const sv_gate* g, size_t count, int n, int c, int world_log2, std::vector<int>& pi,
-                 std::vector<int>& sigma, uint32_t flags, std::vector<Step>& steps, PlanCounters& ctr);
+                 std::vector<int>& sigma, uint32_t flags, std::vector<Step>& steps, PlanCounters& ctr,
+                 const PlanLayout& layout = PlanLayout());
 
 }  // namespace sv

@@ -7,7 +7,10 @@
 // Reordering only qubit-disjoint gates is the same legality rule the pass uses.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <utility>
 
 #include "common.h"
 #include "compile.h"
@@ -51,11 +54,12 @@ struct PGate {  // a gate on tile positions
 };
 
 constexpr int kDiagLocal = -1;  // DIAG operand: -(1 + memory bit)
+constexpr int kMaxTile = 13;    // 2^13 amplitudes: 128 KiB fp64 / 64 KiB fp32 of shared memory
 
 }  // namespace
 
 Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int world_log2, int T_default,
-                       int swizzle_bits, Program& prog) {
+                       int swizzle_bits, const std::vector<std::pair<int, int>>& store_swaps, Program& prog) {
   (void)world_log2;
   // ---- tile bits
   uint64_t active = 0;
@@ -67,10 +71,15 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
     if (b1 >= 0) active |= 1ull << b1;
   }
   const int nA = __builtin_popcountll(active);
-  int T = std::max(std::min(T_default, nL), nA);
-  if (T > SV_TMAX) return Status::err(SV_ECAPACITY, "section needs more tile bits than shared memory holds");
-  uint64_t tile = active;
-  for (int b = 0; b < nL && __builtin_popcountll(tile) < T; b++) tile |= 1ull << b;
+  // The tile always includes the lowest memory bits (128-byte runs: 8 fp64 / 16 fp32 amplitudes)
+  // when they fit; the planner (plan.cpp) arranges that they do.
+  PlanLayout lay;
+  lay.low_bits = swizzle_bits;
+  lay.max_tile = kMaxTile;
+  lay.tile_default = T_default;
+  const uint64_t tile = choose_tile(active, nL, lay);
+  const int T = __builtin_popcountll(tile);
+  if (T > kMaxTile) return Status::err(SV_ECAPACITY, "section needs more tile bits than shared memory holds");
   int tile_bits[16], pos_of[64];
   std::fill(pos_of, pos_of + 64, -1);
   int t = 0;
@@ -209,10 +218,37 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
   H->phase_off = header_ints;
   H->op_off = header_ints + phase_ints * (int)phases.size();
   H->n_ops = n_ops;
-  for (int j = 0; j < T; j++) H->tile_bits[j] = tile_bits[j];
+  int store_bits[16];
+  for (int j = 0; j < T; j++) store_bits[j] = tile_bits[j];
+  for (const auto& sw : store_swaps) {  // physical bit swaps fused into the store (plan.cpp)
+    const int p1 = sw.first < 64 ? pos_of[sw.first] : -1, p2 = sw.second < 64 ? pos_of[sw.second] : -1;
+    if (p1 < 0 || p2 < 0) return Status::err(SV_EMALFORMED, "internal: store swap outside the tile");
+    std::swap(store_bits[p1], store_bits[p2]);
+  }
+  for (int j = 0; j < T; j++) {
+    H->tile_bits[j] = tile_bits[j];
+    H->store_bits[j] = store_bits[j];
+  }
   for (int j = 0; j < n_out; j++) H->out_bits[j] = out_bits[j];
-  for (int j = 0; j < r; j++) H->lw[j] = sv_swz_host(1 << (T - r + j), swizzle_bits);
-  for (int j = 0; j < T - r; j++) H->ltw[j] = sv_swz_host(1 << j, swizzle_bits);
+  auto fill_map = [&](SvMap& m, const int* tpos, const int* R, const int* bits) {
+    for (int j = 0; j < T - r; j++) {
+      m.tw[j] = sv_swz_host(1 << tpos[j], swizzle_bits);
+      m.tmb[j] = bits[tpos[j]];
+    }
+    for (int s = 0; s < r; s++) {
+      m.rw[s] = sv_swz_host(1 << R[s], swizzle_bits);
+      m.rmb[s] = bits[R[s]];
+    }
+  };
+  {  // boundary maps: lanes walk the lowest memory bits of the load / store side
+    int order[16];
+    for (int j = 0; j < T; j++) order[j] = j;
+    fill_map(H->load, order, order + (T - r), tile_bits);
+    std::sort(order, order + T, [&](int a, int b) { return store_bits[a] < store_bits[b]; });
+    fill_map(H->store, order, order + (T - r), tile_bits);
+    for (int j = 0; j < T - r; j++) H->store.tmb[j] = store_bits[order[j]];
+    for (int s = 0; s < r; s++) H->store.rmb[s] = store_bits[order[T - r + s]];
+  }
   auto push = [&](const double* m, int count) -> int {
     const int at = (int)(prog.coefs.size() / 2 - cbase);
     prog.coefs.insert(prog.coefs.end(), m, m + 2 * count);
@@ -229,7 +265,6 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
     for (int s = 0; s < r; s++) {
       P->R[s] = ph.R[s];
       P->rw[s] = sv_swz_host(1 << ph.R[s], swizzle_bits);
-      P->rmb[s] = tile_bits[ph.R[s]];
       slot_of[ph.R[s]] = s;
     }
     // thread bits: the first `swizzle_bits` get distinct residues mod swizzle_bits so a group of
@@ -254,14 +289,23 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
     for (size_t j = 0; j < chosen.size(); j++) {
       P->tpos[j] = chosen[j];
       P->tw[j] = sv_swz_host(1 << chosen[j], swizzle_bits);
-      P->tmb[j] = tile_bits[chosen[j]];
       thread_of[chosen[j]] = (int)j;
     }
-    // lane group of 2^swizzle_bits threads walks one contiguous 128-byte run of HBM?
-    bool contiguous = (int)chosen.size() >= swizzle_bits;
-    for (int j = 0; contiguous && j < swizzle_bits; j++) contiguous = chosen[j] == j && tile_bits[j] == j;
-    if (pi == 0) lanes_contiguous_first = contiguous;
-    if (pi + 1 == phases.size()) lanes_contiguous_last = contiguous;
+    // a direct HBM boundary needs lane j of each 2^swizzle_bits group on memory bit j (128 B runs)
+    auto lanes_on_low_bits = [&](const int* bits) {
+      if ((int)chosen.size() < swizzle_bits) return false;
+      for (int j = 0; j < swizzle_bits; j++)
+        if (bits[chosen[j]] != j) return false;
+      return true;
+    };
+    if (pi == 0) {
+      lanes_contiguous_first = lanes_on_low_bits(tile_bits);
+      fill_map(H->din, chosen.data(), ph.R.data(), tile_bits);
+    }
+    if (pi + 1 == phases.size()) {
+      lanes_contiguous_last = lanes_on_low_bits(store_bits);
+      fill_map(H->dout, chosen.data(), ph.R.data(), store_bits);
+    }
 
     P->op_begin = op_cursor;
     P->op_count = (int)ph.ops.size();
@@ -353,6 +397,20 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
   for (const PGate& p : pg)
     fpa += p.type == SV_OP_U2 ? 32.0 : p.type == SV_OP_U1 ? 16.0 : p.type == SV_OP_H1 ? 4.0
          : p.type == SV_OP_DIAG ? 6.0 : p.type == SV_OP_DIAG_CP ? 1.5 : 0.0;
+  if (std::getenv("SV_DEBUG_PLAN")) {  // per-section compile report (analysis aid)
+    int cnt[8] = {0}, diag_kind[3] = {0};  // diag operands: slot-slot, slot-other, other-other
+    for (int i = 0; i < n_ops; i++) {
+      const SvOp* O = reinterpret_cast<const SvOp*>(prog.ints.data() + base + H->op_off + op_ints * i);
+      cnt[O->type]++;
+      if (O->type == SV_OP_DIAG || O->type == SV_OP_DIAG_CP) diag_kind[(O->a >= 4) + (O->b >= 4)]++;
+    }
+    std::fprintf(stderr,
+                 "[sv] section T=%d phases=%zu ops=%d U2=%d U1=%d H1=%d PERM=%d DIAG=%d CP=%d (ss=%d so=%d oo=%d) "
+                 "flags=%d flops/amp=%.1f low-tile-bits=%d%d%d%d\n",
+                 T, phases.size(), n_ops, cnt[SV_OP_U2], cnt[SV_OP_U1], cnt[SV_OP_H1], cnt[SV_OP_PERM2],
+                 cnt[SV_OP_DIAG], cnt[SV_OP_DIAG_CP], diag_kind[0], diag_kind[1], diag_kind[2], H->flags, fpa,
+                 (int)(tile & 1), (int)((tile >> 1) & 1), (int)((tile >> 2) & 1), (int)((tile >> 3) & 1));
+  }
   Launch L;
   L.flops_per_amp = fpa;
   L.int_off = base;
@@ -372,9 +430,9 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
 }
 
 Status compile_section_split(const std::vector<sv_gate>& gates, int nL, int rank, int world_log2, int T_default,
-                             int swizzle_bits, Program& prog) {
+                             int swizzle_bits, const std::vector<std::pair<int, int>>& store_swaps, Program& prog) {
   const size_t ni = prog.ints.size(), nc = prog.coefs.size();
-  Status s = compile_section(gates, nL, rank, world_log2, T_default, swizzle_bits, prog);
+  Status s = compile_section(gates, nL, rank, world_log2, T_default, swizzle_bits, store_swaps, prog);
   if (s.code != kTooBig) return s;
   prog.ints.resize(ni);
   prog.coefs.resize(nc);
@@ -382,8 +440,9 @@ Status compile_section_split(const std::vector<sv_gate>& gates, int nL, int rank
   // Consecutive halves of the in-order gate list: each half is a valid section on its own.
   const size_t h = gates.size() / 2;
   std::vector<sv_gate> a(gates.begin(), gates.begin() + h), b(gates.begin() + h, gates.end());
-  if (Status sa = compile_section_split(a, nL, rank, world_log2, T_default, swizzle_bits, prog); !sa.good()) return sa;
-  return compile_section_split(b, nL, rank, world_log2, T_default, swizzle_bits, prog);
+  if (Status sa = compile_section_split(a, nL, rank, world_log2, T_default, swizzle_bits, {}, prog); !sa.good())
+    return sa;
+  return compile_section_split(b, nL, rank, world_log2, T_default, swizzle_bits, store_swaps, prog);
 }
 
 }  // namespace sv

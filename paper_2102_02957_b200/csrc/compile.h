@@ -1,5 +1,6 @@
 // compile.h — section compiler interface (host).
 #pragma once
+#include <utility>
 #include <vector>
 
 #include "common.h"
@@ -33,9 +34,10 @@ struct Program {
 // fewer; swizzle_bits: log2(amplitudes per 128-byte smem row) (3 for fp64, 4 for fp32).
 // compile_section_split splits sections whose program or coefficients exceed the __constant__
 // budget into consecutive in-order pieces (each its own launch).
+// store_swaps: memory-bit transpositions (both bits in the tile) fused into the final store.
 Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int world_log2, int T_default,
-                       int swizzle_bits, Program& prog);
+                       int swizzle_bits, const std::vector<std::pair<int, int>>& store_swaps, Program& prog);
 Status compile_section_split(const std::vector<sv_gate>& gates, int nL, int rank, int world_log2, int T_default,
-                             int swizzle_bits, Program& prog);
+                             int swizzle_bits, const std::vector<std::pair<int, int>>& store_swaps, Program& prog);
 
 }  // namespace sv

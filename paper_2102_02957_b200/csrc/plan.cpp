@@ -3,10 +3,15 @@
 // The paper executes chunk_swaps by moving amplitudes between chunks.
 // Here every chunk_swap, and every SWAP inside a section, is a pure RELABEL of sigma (the map
 // paper-physical qubit -> memory bit): mem[mu'(y)] = mem[mu(tau_ab(y))] exactly when sigma' is
-// sigma with entries a and b exchanged (DESIGN "Executor mapping").  Data moves only when a
-// section needs a qubit whose memory bit is a rank bit (>= nL); then that rank bit is
-// physically exchanged with a local memory bit no gate of the section uses (the highest such
-// bit, so exchanged blocks are contiguous), one grouped exchange per section.
+// sigma with entries a and b exchanged (DESIGN "Executor mapping").  Data moves only
+//   * when a section needs a qubit whose memory bit is a rank bit (>= nL): that rank
+//     bit is exchanged with a local memory bit no gate of the section uses (EXCHANGE step);
+//   * to keep section tiles coalesced: every tile should contain the lowest memory bits.  The
+//     planner looks one section ahead and fuses bit swaps into the current section's store so
+//     the next section's qubits land on low memory bits (free: same addresses, permuted); when a
+//     section still cannot hold its qubits plus the low bits, a standalone swap pass moves them
+//     (COMPACT step).  A physical swap of memory bits plus the matching relabel of sigma leaves
+//     the logical state unchanged, so none of this changes what the circuit computes.
 #include <algorithm>
 #include <cstring>
 
@@ -16,8 +21,6 @@ namespace sv {
 
 namespace {
 
-constexpr int kMaxTileBits = 13;  // one CTA tile: 2^13 amplitudes (128 KiB fp64)
-
 sv_gate to_memory(const sv_gate& t, const std::vector<int>& sigma) {
   sv_gate r = t;
   r.q0 = sigma[t.q0];
@@ -25,15 +28,21 @@ sv_gate to_memory(const sv_gate& t, const std::vector<int>& sigma) {
   return r;
 }
 
-struct SectionMapper {
+struct Block {
+  std::vector<std::pair<int, int>> relabels;  // chunk_swaps (paper qubits) before the section
+  std::vector<sv_gate> gates;                  // section gates on paper qubits
+};
+
+struct Planner {
   int n, nL;
+  const PlanLayout& L;
   std::vector<int>& sigma;
   std::vector<int> owner;  // owner[m] = paper qubit whose memory bit is m
   std::vector<Step>& steps;
   PlanCounters& ctr;
 
-  SectionMapper(int n_, int nL_, std::vector<int>& s, std::vector<Step>& st, PlanCounters& c)
-      : n(n_), nL(nL_), sigma(s), owner(n_), steps(st), ctr(c) {
+  Planner(int n_, int nL_, const PlanLayout& lay, std::vector<int>& s, std::vector<Step>& st, PlanCounters& c)
+      : n(n_), nL(nL_), L(lay), sigma(s), owner(n_), steps(st), ctr(c) {
     for (int p = 0; p < n; p++) owner[sigma[p]] = p;
   }
 
@@ -42,26 +51,40 @@ struct SectionMapper {
     owner[sigma[a]] = a;
     owner[sigma[b]] = b;
   }
+  void swap_bits(int m1, int m2) { relabel(owner[m1], owner[m2]); }  // after a physical swap
 
-  void section(const std::vector<sv_gate>& sec) {
-    // 1. memory bits the section's non-diagonal gates touch (SWAPs are relabels, walked virtually)
-    std::vector<int> v = sigma;
+  // Memory bits the block's non-diagonal gates touch under the map v (SWAPs walked virtually),
+  // and the rank bits among them in order of first use.
+  static uint64_t needed(const Block& b, std::vector<int> v, int nL, std::vector<int>* rank_bits) {
     uint64_t need = 0;
-    std::vector<int> rank_bits;  // in order of first use
-    for (const sv_gate& t : sec) {
+    for (const sv_gate& t : b.gates) {
       if (t.kind == SV_SWAP) {
         std::swap(v[t.q0], v[t.q1]);
         continue;
       }
       if (is_diag(t.kind)) continue;
-      int bits[2] = {v[t.q0], is_two(t.kind) ? v[t.q1] : -1};
-      for (int b : bits) {
-        if (b < 0) continue;
-        if (!((need >> b) & 1) && b >= nL) rank_bits.push_back(b);
-        need |= 1ull << b;
+      const int bits[2] = {v[t.q0], is_two(t.kind) ? v[t.q1] : -1};
+      for (int bb : bits) {
+        if (bb < 0) continue;
+        if (rank_bits && !((need >> bb) & 1) && bb >= nL) rank_bits->push_back(bb);
+        need |= 1ull << bb;
       }
     }
-    // 2. bring needed rank bits onto local memory bits (one grouped exchange)
+    return need;
+  }
+
+  void run(const std::vector<Block>& blocks) {
+    for (size_t i = 0; i < blocks.size(); i++) {
+      for (const auto& rl : blocks[i].relabels) relabel(rl.first, rl.second);
+      section(blocks, i);
+    }
+  }
+
+  void section(const std::vector<Block>& blocks, size_t i) {
+    const Block& B = blocks[i];
+    // 1. bring needed rank bits onto local memory bits (one grouped exchange)
+    std::vector<int> rank_bits;
+    uint64_t need = needed(B, sigma, nL, &rank_bits);
     if (!rank_bits.empty()) {
       Step ex;
       ex.type = Step::EXCHANGE;
@@ -72,60 +95,106 @@ struct SectionMapper {
         // m >= 0 is guaranteed: the section needs at most c <= nL local bits in total
         taken |= 1ull << m;
         ex.ex.push_back({m, b});
-        relabel(owner[m], owner[b]);
+        swap_bits(m, b);
       }
       ctr.exchanges += ex.ex.size();
       ctr.exchange_batches++;
       steps.push_back(std::move(ex));
+      need = needed(B, sigma, nL, nullptr);
+    }
+    // 2. coalescing: the tile must hold the section's bits and the low memory bits
+    const int nlow = std::min(L.low_bits, nL);
+    const uint64_t low = (1ull << nlow) - 1;
+    int cnt = __builtin_popcountll(need);
+    if (cnt <= L.max_tile && cnt + __builtin_popcountll(low & ~need) > L.max_tile) {
+      Step cp;
+      cp.type = Step::COMPACT;
+      int over = cnt + __builtin_popcountll(low & ~need) - L.max_tile;
+      for (int l = 0; l < nlow && over > 0; l++) {
+        if ((need >> l) & 1) continue;
+        int h = nL - 1;
+        while (h >= nlow && !((need >> h) & 1)) h--;
+        if (h < nlow) break;
+        cp.swaps.push_back({l, h});
+        swap_bits(l, h);
+        need = (need & ~(1ull << h)) | (1ull << l);
+        over--;
+      }
+      ctr.compactions += cp.swaps.size();
+      if (!cp.swaps.empty()) steps.push_back(std::move(cp));
     }
     // 3. translate the section to memory bits; SWAPs relabel sigma for everything after them
     std::vector<sv_gate> mem;
-    for (const sv_gate& t : sec) {
+    for (const sv_gate& t : B.gates) {
       if (t.kind == SV_SWAP) {
         relabel(t.q0, t.q1);
         continue;
       }
       mem.push_back(to_memory(t, sigma));
     }
-    if (mem.empty()) return;
     uint64_t act = 0;
     for (const sv_gate& m : mem)
       if (!is_diag(m.kind)) act |= qmask(m);
-    if (__builtin_popcountll(act) <= kMaxTileBits) {
-      push_section(std::move(mem));
-      return;
-    }
-    // More active bits than one tile holds (chunk_bits > kMaxTileBits): split the section with
-    // the same pass at c = kMaxTileBits on memory bits.  Its chunk_swaps are relabels of an
-    // inner frame whose inverse keeps every gate on its own memory bit, so only the grouping is
-    // used (each inner section's gates are the originals, by index).
-    std::vector<sv_gate> in = mem;
-    for (size_t i = 0; i < in.size(); i++) in[i].pad = (int32_t)i;
-    std::vector<int> ipi(nL);
-    for (int b = 0; b < nL; b++) ipi[b] = b;
-    std::vector<sv_gate> toks;
-    Status st = block_pass(in.data(), in.size(), nL, kMaxTileBits, ipi, 0, toks);
-    if (!st.good()) {  // cannot happen for valid sections; keep the section whole
-      push_section(std::move(mem));
-      return;
-    }
-    std::vector<sv_gate> cur;
-    for (const sv_gate& t : toks) {
-      if (t.kind == SV_BEGIN) {
-        cur.clear();
-      } else if (t.kind == SV_END) {
-        if (!cur.empty()) push_section(std::move(cur));
-        cur.clear();
-      } else if (t.kind != SV_CHUNK_SWAP) {
-        cur.push_back(mem[t.pad]);
+    // 4. look ahead: fuse swaps into this section's store that put the next section's qubits on
+    //    the low memory bits (both bits of each swap lie in this section's tile)
+    std::vector<std::pair<int, int>> sw;
+    if (!mem.empty() && i + 1 < blocks.size() && __builtin_popcountll(act) <= L.max_tile) {
+      const uint64_t tile = choose_tile(act, nL, L);
+      std::vector<int> v = sigma;
+      for (const auto& rl : blocks[i + 1].relabels) std::swap(v[rl.first], v[rl.second]);
+      const uint64_t nxt = needed(blocks[i + 1], v, nL, nullptr) & ((nL >= 64) ? ~0ull : ((1ull << nL) - 1));
+      if (__builtin_popcountll(nxt) <= L.max_tile) {
+        uint64_t cand = nxt & tile & ~low;  // next-section bits we can pull down now
+        for (int l = 0; l < nlow && cand; l++) {
+          if (((nxt >> l) & 1) || !((tile >> l) & 1)) continue;
+          const int x = 63 - __builtin_clzll(cand);  // highest candidate
+          cand &= ~(1ull << x);
+          sw.push_back({l, x});
+        }
       }
     }
+    if (mem.empty()) {
+      return;
+    }
+    if (__builtin_popcountll(act) <= L.max_tile) {
+      push_section(std::move(mem), sw);
+    } else {
+      // More active bits than one tile holds (chunk_bits > max_tile): split the section with the
+      // same pass at c = max_tile - low_bits on memory bits (room for the coalescing bits).  Its chunk_swaps are relabels of an inner frame
+      // whose inverse keeps every gate on its own memory bit, so only the grouping is used (each
+      // inner section's gates are the originals, by index).
+      std::vector<sv_gate> in = mem;
+      for (size_t k = 0; k < in.size(); k++) in[k].pad = (int32_t)k;
+      std::vector<int> ipi(nL);
+      for (int b = 0; b < nL; b++) ipi[b] = b;
+      std::vector<sv_gate> toks;
+      Status st = block_pass(in.data(), in.size(), nL, std::max(2, L.max_tile - nlow), ipi, 0, toks);
+      if (!st.good()) {  // cannot happen for valid sections; keep the section whole
+        push_section(std::move(mem), {});
+      } else {
+        std::vector<sv_gate> cur;
+        for (const sv_gate& t : toks) {
+          if (t.kind == SV_BEGIN) {
+            cur.clear();
+          } else if (t.kind == SV_END) {
+            if (!cur.empty()) push_section(std::move(cur), {});
+            cur.clear();
+          } else if (t.kind != SV_CHUNK_SWAP) {
+            cur.push_back(mem[t.pad]);
+          }
+        }
+      }
+      sw.clear();
+    }
+    for (const auto& s : sw) swap_bits(s.first, s.second);
+    ctr.store_swaps += sw.size();
   }
 
-  void push_section(std::vector<sv_gate> gates) {
+  void push_section(std::vector<sv_gate> gates, const std::vector<std::pair<int, int>>& sw) {
     Step s;
     s.type = Step::SECTION;
     s.gates = std::move(gates);
+    s.swaps = sw;
     ctr.sections++;
     steps.push_back(std::move(s));
   }
@@ -134,7 +203,8 @@ struct SectionMapper {
 }  // namespace
 
 Status make_plan(const sv_gate* g, size_t count, int n, int c, int world_log2, std::vector<int>& pi,
-                 std::vector<int>& sigma, uint32_t flags, std::vector<Step>& steps, PlanCounters& ctr) {
+                 std::vector<int>& sigma, uint32_t flags, std::vector<Step>& steps, PlanCounters& ctr,
+                 const PlanLayout& layout) {
   const int nL = n - world_log2;
   if (world_log2 < 0 || nL < 1) return Status::err(SV_EINVAL, "world too large for n");
   if (c < 1 || c > nL) return Status::err(SV_EINVAL, "chunk_bits must satisfy 1 <= c <= n - log2(world)");
@@ -163,28 +233,32 @@ Status make_plan(const sv_gate* g, size_t count, int n, int c, int world_log2, s
   tokens.reserve(count * 2 + 16);
   if (Status s = block_pass(g, count, n, c, pi, flags, tokens); !s.good()) return s;
 
-  SectionMapper mapper(n, nL, sigma, steps, ctr);
-  std::vector<sv_gate> sec;
+  std::vector<Block> blocks;
+  Block cur;
   bool inside = false;
+  std::vector<std::pair<int, int>> trailing;  // chunk_swaps after the last section
   for (const sv_gate& t : tokens) {
     switch (t.kind) {
       case SV_CHUNK_SWAP:
-        mapper.relabel(t.q0, t.q1);
+        cur.relabels.push_back({t.q0, t.q1});
         ctr.chunk_swaps++;
         break;
       case SV_BEGIN:
-        sec.clear();
         inside = true;
         break;
       case SV_END:
         if (!inside) return Status::err(SV_EMALFORMED, "END without BEGIN");
-        mapper.section(sec);
+        blocks.push_back(std::move(cur));
+        cur = Block();
         inside = false;
         break;
       default:
-        sec.push_back(t);
+        cur.gates.push_back(t);
     }
   }
+  Planner planner(n, nL, layout, sigma, steps, ctr);
+  planner.run(blocks);
+  for (const auto& rl : cur.relabels) planner.relabel(rl.first, rl.second);  // trailing chunk_swaps
   return Status::ok();
 }
 

@@ -42,19 +42,31 @@
 #define SV_FLAG_FIRST_DIRECT 1        // first phase loads straight from HBM
 #define SV_FLAG_LAST_DIRECT 2         // last phase stores straight to HBM
 
+// A thread/register <-> tile mapping used at a tile boundary: smem offsets (swizzled) and the
+// HBM memory bit of every thread bit j and register slot s.
+struct SvMap {
+  int tw[16];
+  int rw[SV_R_BITS];
+  int tmb[16];
+  int rmb[SV_R_BITS];
+};
+
 struct SvSecHeader {
   int T;          // tile bits
-  int r;          // register bits per phase (<= SV_R_BITS)
+  int r;          // register bits per phase (== SV_R_BITS)
   int n_out;      // local memory bits outside the tile (grid = 2^n_out CTAs)
   int n_phases;
   int phase_off;  // int offset of the first SvPhase from the header
   int op_off;     // int offset of the first SvOp from the header
   int n_ops;
   int flags;      // SV_FLAG_*
-  int tile_bits[16];        // tile position -> memory bit (ascending)
+  int tile_bits[16];        // tile position -> memory bit on LOAD (ascending)
+  int store_bits[16];       // tile position -> memory bit on STORE (a permutation of tile_bits)
   int out_bits[SV_MAX_OUT]; // out-of-tile local memory bits (ascending) <- CTA index bits
-  int lw[SV_R_BITS];        // load-order mapping: swz(1 << (T - r + j)) of register bit j
-  int ltw[16];              // load-order mapping: swz(1 << j) of thread bit j
+  SvMap load;               // non-direct initial load: lanes walk the lowest load memory bits
+  SvMap store;              // non-direct final store: lanes walk the lowest store memory bits
+  SvMap din;                // direct first phase: phase-0 mapping, load memory bits
+  SvMap dout;               // direct last phase: last-phase mapping, store memory bits
 };
 
 // XOR-fold swizzle of a tile element index (host and device): the low G bits are XORed with
@@ -71,11 +83,9 @@ inline int sv_swz_host(int i, int G) {
 struct SvPhase {
   int R[SV_R_BITS];    // register slot -> tile position
   int rw[SV_R_BITS];   // swz(1 << R[s]): smem offset contribution of register slot s
-  int rmb[SV_R_BITS];  // memory bit of register slot s (direct HBM phases)
   int op_begin, op_count, pad0, pad1;
   int tpos[16];        // thread-index bit j -> tile position (T - r entries used)
   int tw[16];          // swz(1 << tpos[j])
-  int tmb[16];         // memory bit of thread bit j
 };
 
 struct SvOp {

@@ -9,6 +9,7 @@
 // and the matrices live in __constant__ memory and reach the FMA pipe through uniform registers.
 #include <cuda_runtime.h>
 
+#include <cstddef>
 #include <cstdint>
 
 #include "cplx.cuh"
@@ -229,13 +230,17 @@ __device__ __forceinline__ void run_op(V (&v)[16], int oi, int tid, uint64_t til
   }
 }
 
-// header / phase field offsets (ints) — see SvSecHeader / SvPhase
-constexpr int kH_T = 0, kH_NOUT = 2, kH_NPH = 3, kH_PHOFF = 4, kH_OPOFF = 5;
-constexpr int kH_TILE = 8, kH_OUT = 24, kH_LW = 72, kH_LTW = 76;
-constexpr int kP_RW = 4, kP_RMB = 8, kP_OPB = 12, kP_OPC = 13, kP_TW = 32, kP_TMB = 48;
+// header / phase / map field offsets (ints)
+constexpr int kH_T = offsetof(SvSecHeader, T) / 4, kH_NOUT = offsetof(SvSecHeader, n_out) / 4;
+constexpr int kH_NPH = offsetof(SvSecHeader, n_phases) / 4, kH_PHOFF = offsetof(SvSecHeader, phase_off) / 4;
+constexpr int kH_OPOFF = offsetof(SvSecHeader, op_off) / 4, kH_OUT = offsetof(SvSecHeader, out_bits) / 4;
+constexpr int kH_LOAD = offsetof(SvSecHeader, load) / 4, kH_STORE = offsetof(SvSecHeader, store) / 4;
+constexpr int kH_DIN = offsetof(SvSecHeader, din) / 4, kH_DOUT = offsetof(SvSecHeader, dout) / 4;
+constexpr int kM_TW = offsetof(SvMap, tw) / 4, kM_RW = offsetof(SvMap, rw) / 4;
+constexpr int kM_TMB = offsetof(SvMap, tmb) / 4, kM_RMB = offsetof(SvMap, rmb) / 4;
+constexpr int kP_RW = offsetof(SvPhase, rw) / 4, kP_OPB = offsetof(SvPhase, op_begin) / 4;
+constexpr int kP_OPC = offsetof(SvPhase, op_count) / 4, kP_TW = offsetof(SvPhase, tw) / 4;
 constexpr int kPhaseInts = sizeof(SvPhase) / 4, kOpInts = sizeof(SvOp) / 4;
-static_assert(sizeof(SvSecHeader) / 4 == kH_LTW + 16, "header layout");
-static_assert(kPhaseInts == 64, "phase layout");
 
 // x ^ (the XOR of w[s] over the set bits s of the compile-time register index k)
 template <int K>
@@ -244,6 +249,53 @@ __device__ __forceinline__ int xk(int x, const int (&w)[SV_R_BITS]) {
   for (int s = 0; s < SV_R_BITS; s++)
     if ((K >> s) & 1) x ^= w[s];
   return x;
+}
+
+// Swizzled shared-memory offsets of this thread's register-0 amplitude (x) and of each register
+// slot (w) under the mapping whose thread-bit offsets start at c_prog[tw] and slot offsets at
+// c_prog[rw].
+__device__ __forceinline__ void smem_map(int tw, int rw, int nt_log, int tid, int& x, int (&w)[SV_R_BITS]) {
+  x = 0;
+  for (int j = 0; j < nt_log; j++) x ^= ((tid >> j) & 1) ? c_prog[tw + j] : 0;
+#pragma unroll
+  for (int s = 0; s < SV_R_BITS; s++) w[s] = c_prog[rw + s];
+}
+
+// HBM element offset of this thread's register-0 amplitude under map M (tile base included)
+__device__ __forceinline__ uint64_t hbm_base(int M, int nt_log, int tid, uint64_t tile_off) {
+  uint64_t mb = tile_off;
+  for (int j = 0; j < nt_log; j++) mb |= (uint64_t)((tid >> j) & 1) << c_prog[M + kM_TMB + j];
+  return mb;
+}
+
+template <typename V>
+__device__ __forceinline__ void hbm_load(V (&v)[16], const V* __restrict__ src, int M) {
+  int64_t ro[SV_R_BITS];
+#pragma unroll
+  for (int s = 0; s < SV_R_BITS; s++) ro[s] = (int64_t)1 << c_prog[M + kM_RMB + s];
+#pragma unroll
+  for (int k = 0; k < 16; k++) {
+    int64_t o = 0;
+#pragma unroll
+    for (int s = 0; s < SV_R_BITS; s++)
+      if ((k >> s) & 1) o |= ro[s];
+    v[k] = src[o];
+  }
+}
+
+template <typename V>
+__device__ __forceinline__ void hbm_store(const V (&v)[16], V* __restrict__ dst, int M) {
+  int64_t ro[SV_R_BITS];
+#pragma unroll
+  for (int s = 0; s < SV_R_BITS; s++) ro[s] = (int64_t)1 << c_prog[M + kM_RMB + s];
+#pragma unroll
+  for (int k = 0; k < 16; k++) {
+    int64_t o = 0;
+#pragma unroll
+    for (int s = 0; s < SV_R_BITS; s++)
+      if ((k >> s) & 1) o |= ro[s];
+    dst[o] = v[k];
+  }
 }
 
 template <typename V, int G, int NT, int MINB, bool FIRST, bool LAST>
@@ -264,47 +316,13 @@ __global__ void __launch_bounds__(NT, MINB) k_section(V* __restrict__ sv) {
   }
 
   V v[16];
-  // load-order mapping for the non-direct boundaries: element i = tid + (k << nt_log)
-  int pt = 0;
-  uint64_t off_t = 0;
-  int lw[RB];
-  int64_t lo[RB];
-  if constexpr (!(FIRST && LAST)) {
-    for (int j = 0; j < nt_log; j++) {
-      const int bit = (tid >> j) & 1;
-      pt ^= bit ? c_prog[kH_LTW + j] : 0;
-      off_t |= (uint64_t)bit << c_prog[kH_TILE + j];
-    }
-#pragma unroll
-    for (int s = 0; s < RB; s++) {
-      lw[s] = c_prog[kH_LW + s];
-      lo[s] = (int64_t)1 << c_prog[kH_TILE + nt_log + s];
-    }
-  }
   if constexpr (FIRST) {  // phase 0 reads HBM directly in its own register mapping
-    const int P = phoff;
-    uint64_t mb = 0;
-    for (int j = 0; j < nt_log; j++) mb |= (uint64_t)((tid >> j) & 1) << c_prog[P + kP_TMB + j];
-    const V* src = sv + (tile_off | mb);
-#pragma unroll
-    for (int k = 0; k < 16; k++) {
-      int64_t o = 0;
-#pragma unroll
-      for (int s = 0; s < RB; s++)
-        if ((k >> s) & 1) o |= (int64_t)1 << c_prog[P + kP_RMB + s];
-      v[k] = src[o];
-    }
-  } else {  // coalesced load-order read, scattered into the swizzled tile
-    const V* src = sv + (tile_off | off_t);
-#pragma unroll
-    for (int k = 0; k < 16; k++) {
-      int64_t o = 0;
-#pragma unroll
-      for (int s = 0; s < RB; s++)
-        if ((k >> s) & 1) o |= lo[s];
-      v[k] = src[o];
-    }
-#define SV_STS(K) sm[xk<K>(pt, lw)] = v[K];
+    hbm_load(v, sv + hbm_base(kH_DIN, nt_log, tid, tile_off), kH_DIN);
+  } else {  // lanes walk the lowest load memory bits; scatter into the swizzled tile
+    hbm_load(v, sv + hbm_base(kH_LOAD, nt_log, tid, tile_off), kH_LOAD);
+    int x, w[RB];
+    smem_map(kH_LOAD + kM_TW, kH_LOAD + kM_RW, nt_log, tid, x, w);
+#define SV_STS(K) sm[xk<K>(x, w)] = v[K];
     SV_STS(0) SV_STS(1) SV_STS(2) SV_STS(3) SV_STS(4) SV_STS(5) SV_STS(6) SV_STS(7)
     SV_STS(8) SV_STS(9) SV_STS(10) SV_STS(11) SV_STS(12) SV_STS(13) SV_STS(14) SV_STS(15)
 #undef SV_STS
@@ -315,16 +333,8 @@ __global__ void __launch_bounds__(NT, MINB) k_section(V* __restrict__ sv) {
     const int P = phoff + ph * kPhaseInts;
     const bool direct_in = FIRST && ph == 0;
     const bool direct_out = LAST && ph == nph - 1;
-    int pb = 0;
-    uint64_t mb = 0;
-    for (int j = 0; j < nt_log; j++) {
-      const int bit = (tid >> j) & 1;
-      pb ^= bit ? c_prog[P + kP_TW + j] : 0;
-      if constexpr (LAST) mb |= (uint64_t)bit << c_prog[P + kP_TMB + j];
-    }
-    int w[RB];
-#pragma unroll
-    for (int s = 0; s < RB; s++) w[s] = c_prog[P + kP_RW + s];
+    int pb, w[RB];
+    smem_map(P + kP_TW, P + kP_RW, nt_log, tid, pb, w);
     if (!direct_in) {
 #define SV_LDS(K) v[K] = sm[xk<K>(pb, w)];
       SV_LDS(0) SV_LDS(1) SV_LDS(2) SV_LDS(3) SV_LDS(4) SV_LDS(5) SV_LDS(6) SV_LDS(7)
@@ -333,16 +343,8 @@ __global__ void __launch_bounds__(NT, MINB) k_section(V* __restrict__ sv) {
     }
     const int ob = c_prog[P + kP_OPB], oc = c_prog[P + kP_OPC];
     for (int o = 0; o < oc; o++) run_op<V, R>(v, opoff + (ob + o) * kOpInts, tid, tile_off);
-    if (direct_out) {  // the last phase writes HBM directly in its own register mapping
-      V* dst = sv + (tile_off | mb);
-#pragma unroll
-      for (int k = 0; k < 16; k++) {
-        int64_t o = 0;
-#pragma unroll
-        for (int s = 0; s < RB; s++)
-          if ((k >> s) & 1) o |= (int64_t)1 << c_prog[P + kP_RMB + s];
-        dst[o] = v[k];
-      }
+    if (direct_out) {  // the last phase writes HBM directly (store memory bits, same mapping)
+      hbm_store(v, sv + hbm_base(kH_DOUT, nt_log, tid, tile_off), kH_DOUT);
     } else {
 #define SV_STS(K) sm[xk<K>(pb, w)] = v[K];
       SV_STS(0) SV_STS(1) SV_STS(2) SV_STS(3) SV_STS(4) SV_STS(5) SV_STS(6) SV_STS(7)
@@ -352,20 +354,14 @@ __global__ void __launch_bounds__(NT, MINB) k_section(V* __restrict__ sv) {
     }
   }
 
-  if constexpr (!LAST) {
-#define SV_LDS(K) v[K] = sm[xk<K>(pt, lw)];
+  if constexpr (!LAST) {  // gather in store order (lanes walk the lowest store memory bits)
+    int x, w[RB];
+    smem_map(kH_STORE + kM_TW, kH_STORE + kM_RW, nt_log, tid, x, w);
+#define SV_LDS(K) v[K] = sm[xk<K>(x, w)];
     SV_LDS(0) SV_LDS(1) SV_LDS(2) SV_LDS(3) SV_LDS(4) SV_LDS(5) SV_LDS(6) SV_LDS(7)
     SV_LDS(8) SV_LDS(9) SV_LDS(10) SV_LDS(11) SV_LDS(12) SV_LDS(13) SV_LDS(14) SV_LDS(15)
 #undef SV_LDS
-    V* dst = sv + (tile_off | off_t);
-#pragma unroll
-    for (int k = 0; k < 16; k++) {
-      int64_t o = 0;
-#pragma unroll
-      for (int s = 0; s < RB; s++)
-        if ((k >> s) & 1) o |= lo[s];
-      dst[o] = v[k];
-    }
+    hbm_store(v, sv + hbm_base(kH_STORE, nt_log, tid, tile_off), kH_STORE);
   }
 }
 

@@ -102,20 +102,26 @@ def run_plan_dense(recs, n, c, g, flags=0, seed=0):
     oracle on the original circuit, un-permuting through mu(q) = sigma[pi[q]]."""
     plan, pi, sigma = sv.plan_circuit(recs, n, c, g, flags=flags)
     nL = n - g
-    # structural checks: section gates only on local memory bits unless diagonal
+    # structural checks: section gates only on local memory bits unless diagonal; SWAP records
+    # outside sections are physical memory-bit swaps (compaction / fused store swaps) on local
+    # bits; every section tile can hold its bits plus the three lowest memory bits (coalescing)
     inside = False
+    act = set()
     for r in plan:
         k = int(r["kind"])
         if k == C.BEGIN:
-            inside = True
+            inside, act = True, set()
         elif k == C.END:
             inside = False
+            if len(act) <= 13 and nL >= 3:
+                assert len(act | {0, 1, 2}) <= 13
         elif k == 9:
             assert not inside and int(r["q0"]) < nL <= int(r["q1"])
         elif k in (C.U1, C.U2):
             assert inside and int(r["q0"]) < nL and (k == C.U1 or int(r["q1"]) < nL)
+            act |= {int(r["q0"])} | ({int(r["q1"])} if k == C.U2 else set())
         elif k == C.SWAP:
-            assert flags & sv.SV_UNBLOCKED
+            assert (flags & sv.SV_UNBLOCKED) or (not inside and int(r["q0"]) < nL and int(r["q1"]) < nL)
     rng = np.random.default_rng(seed)
     psi = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
     psi /= np.linalg.norm(psi)
