@@ -5,11 +5,21 @@
 // shares a tile position with it and its non-diagonal positions fit the R_BITS register slots;
 // diagonal gates join whenever their dependencies allow (they act per amplitude).
 // Reordering only qubit-disjoint gates is the same legality rule the pass uses.
+//
+// Diagonal fusion: inside a phase every diagonal gate is sunk as late as its tile positions
+// allow (past non-diagonal gates on other positions), and each run of diagonal gates becomes one
+// DIAGSET: the product of all its factors, decomposed into terms c^[S subset k][J subset tid]
+// [O subset tile] over register slots S, thread bits J and out-of-tile bits O.  Terms without
+// thread bits are evaluated once per warp (lanes 0..15, one register subset S each), so a QFT
+// section's hundreds of controlled phases cost a few complex multiplies per amplitude.
 #include <algorithm>
 #include <cmath>
+#include <complex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <tuple>
 #include <utility>
 
 #include "common.h"
@@ -18,6 +28,8 @@
 namespace sv {
 
 namespace {
+
+typedef std::complex<double> cd;
 
 inline bool is_h_like(const double* m) {  // s * [[1, 1], [1, -1]], s real: exact check only
   for (int i = 0; i < 4; i++)
@@ -46,7 +58,7 @@ inline bool is_perm4(const double* m, int* perm) {  // 4x4 permutation matrix wi
 
 struct PGate {  // a gate on tile positions
   int type;
-  int a, b;        // positions (U*/PERM) or memory-bit codes (DIAG: -1-mb local, 200/201 const)
+  int a, b;        // positions (U*/PERM) or memory-bit operands (DIAG: -1-mb local, 200/201 const)
   uint32_t pmask;  // tile positions it touches (for dependencies)
   bool diag;
   int src;         // index into the section's gate list (payload source)
@@ -55,6 +67,14 @@ struct PGate {  // a gate on tile positions
 
 constexpr int kDiagLocal = -1;  // DIAG operand: -(1 + memory bit)
 constexpr int kMaxTile = 13;    // 2^13 amplitudes: 128 KiB fp64 / 64 KiB fp32 of shared memory
+
+// One factor term of a DIAGSET: coef applies where slots S, thread bits J and out bits O are all 1.
+struct TermKey {
+  int S;
+  uint32_t J;
+  uint64_t O;
+  bool operator<(const TermKey& o) const { return std::tie(S, J, O) < std::tie(o.S, o.J, o.O); }
+};
 
 }  // namespace
 
@@ -70,7 +90,6 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
     active |= 1ull << b0;
     if (b1 >= 0) active |= 1ull << b1;
   }
-  const int nA = __builtin_popcountll(active);
   // The tile always includes the lowest memory bits (128-byte runs: 8 fp64 / 16 fp32 amplitudes)
   // when they fit; the planner (plan.cpp) arranges that they do.
   PlanLayout lay;
@@ -99,7 +118,6 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
   // ---- gates on positions
   std::vector<PGate> pg;
   pg.reserve(gates.size());
-  size_t ncoef = 0;
   for (size_t gi = 0; gi < gates.size(); gi++) {
     const sv_gate& g = gates[gi];
     PGate p{};
@@ -109,7 +127,6 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
         p.a = pos_of[g.q0];
         p.pmask = 1u << p.a;
         p.type = is_h_like(g.m) ? SV_OP_H1 : SV_OP_U1;
-        ncoef += p.type == SV_OP_H1 ? 1 : 4;
         break;
       case SV_U2: {
         p.a = pos_of[g.q0];
@@ -121,7 +138,6 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
           p.extra = perm[0] | (perm[1] << 2) | (perm[2] << 4) | (perm[3] << 6);
         } else {
           p.type = SV_OP_U2;
-          ncoef += 16;
         }
         break;
       }
@@ -140,7 +156,6 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
         const bool cp = g.kind == SV_D2 && d[0] == 1.0 && d[1] == 0.0 && d[2] == 1.0 && d[3] == 0.0 && d[4] == 1.0 &&
                         d[5] == 0.0;
         p.type = cp ? SV_OP_DIAG_CP : SV_OP_DIAG;
-        ncoef += cp ? 1 : 4;
         break;
       }
       default:
@@ -148,8 +163,6 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
     }
     pg.push_back(p);
   }
-  const size_t coef_cap = swizzle_bits == 3 ? SV_CONST_COEF64 : SV_CONST_COEF32;
-  if (ncoef > coef_cap) return Status::err(kTooBig, "section coefficients exceed the constant budget");
 
   // ---- phase schedule
   struct Ph {
@@ -200,24 +213,96 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
     phases.push_back(ph);
   }
 
-  // ---- emit
-  const size_t base = prog.ints.size();
-  const size_t cbase = prog.coefs.size() / 2;
-  const int n_ops = (int)pg.size();
+  // ---- per phase: thread-bit order, then the op items (single ops or fused diagonal runs)
+  struct Item {
+    int gate = -1;           // single op: index into pg
+    std::vector<int> group;  // DIAGSET: indices into pg
+  };
+  struct PhaseOut {
+    std::vector<int> chosen;  // thread bit j -> tile position
+    int slot_of[SV_TMAX], thread_of[SV_TMAX];
+    std::vector<Item> items;
+  };
+  std::vector<PhaseOut> pout(phases.size());
+  for (size_t pi = 0; pi < phases.size(); pi++) {
+    const Ph& ph = phases[pi];
+    PhaseOut& po = pout[pi];
+    std::fill(po.slot_of, po.slot_of + SV_TMAX, -1);
+    std::fill(po.thread_of, po.thread_of + SV_TMAX, -1);
+    for (int s = 0; s < r; s++) po.slot_of[ph.R[s]] = s;
+    // thread bits: the first `swizzle_bits` get distinct residues mod swizzle_bits so a group of
+    // 2^swizzle_bits lanes hits distinct 16-/8-byte bank groups under the XOR-fold swizzle.
+    std::vector<int> cand;
+    for (int pos = 0; pos < T; pos++)
+      if (po.slot_of[pos] < 0) cand.push_back(pos);
+    uint32_t used_res = 0;
+    std::vector<bool> taken(cand.size(), false);
+    for (size_t i = 0; i < cand.size() && (int)po.chosen.size() < swizzle_bits; i++) {
+      const int res = cand[i] % swizzle_bits;
+      if (!((used_res >> res) & 1)) {
+        used_res |= 1u << res;
+        po.chosen.push_back(cand[i]);
+        taken[i] = true;
+      }
+    }
+    for (size_t i = 0; i < cand.size(); i++)
+      if (!taken[i]) po.chosen.push_back(cand[i]);
+    for (size_t j = 0; j < po.chosen.size(); j++) po.thread_of[po.chosen[j]] = (int)j;
+    // sink diagonal ops: each waits until a later non-diagonal op shares a tile position
+    std::vector<int> sink;
+    auto flush = [&](uint32_t mask, bool all) {
+      std::vector<int> keep, go;
+      for (int gi : sink) ((all || (pg[gi].pmask & mask)) ? go : keep).push_back(gi);
+      sink.swap(keep);
+      if (go.empty()) return;
+      Item it;
+      if (go.size() == 1) {
+        const PGate& p = pg[go[0]];
+        // a lone diagonal whose operands are register slots / constants stays a plain op
+        auto slotish = [&](int x) { return x >= 0 || po.slot_of[pos_of[kDiagLocal - x]] >= 0; };
+        auto in_tile = [&](int x) { return x >= 0 || pos_of[kDiagLocal - x] >= 0; };
+        if (in_tile(p.a) && in_tile(p.b) && slotish(p.a) && slotish(p.b)) {
+          it.gate = go[0];
+          po.items.push_back(it);
+          return;
+        }
+      }
+      it.group = go;
+      po.items.push_back(it);
+    };
+    for (int gi : ph.ops) {
+      if (pg[gi].diag) {
+        sink.push_back(gi);
+        continue;
+      }
+      flush(pg[gi].pmask, false);
+      Item it;
+      it.gate = gi;
+      po.items.push_back(it);
+    }
+    flush(0, true);
+  }
+
+  // ---- sizes
   const int header_ints = sizeof(SvSecHeader) / 4;
   const int phase_ints = sizeof(SvPhase) / 4;
   const int op_ints = sizeof(SvOp) / 4;
-  const size_t total_ints = header_ints + phase_ints * phases.size() + op_ints * (size_t)n_ops;
-  if (total_ints > SV_CONST_INTS) return Status::err(kTooBig, "section program exceeds the constant budget");
-  prog.ints.resize(base + total_ints, 0);
-  SvSecHeader* H = reinterpret_cast<SvSecHeader*>(prog.ints.data() + base);
-  H->T = T;
-  H->r = r;
-  H->n_out = n_out;
-  H->n_phases = (int)phases.size();
-  H->phase_off = header_ints;
-  H->op_off = header_ints + phase_ints * (int)phases.size();
-  H->n_ops = n_ops;
+  size_t n_items = 0;
+  for (const auto& po : pout) n_items += po.items.size();
+
+  // ---- emit
+  const size_t base = prog.ints.size();
+  const size_t cbase = prog.coefs.size() / 2;
+  const size_t ops_end = header_ints + phase_ints * phases.size() + op_ints * n_items;
+  prog.ints.resize(base + ops_end, 0);
+  auto H = [&]() { return reinterpret_cast<SvSecHeader*>(prog.ints.data() + base); };
+  H()->T = T;
+  H()->r = r;
+  H()->n_out = n_out;
+  H()->n_phases = (int)phases.size();
+  H()->phase_off = header_ints;
+  H()->op_off = header_ints + phase_ints * (int)phases.size();
+  H()->n_ops = (int)n_items;
   int store_bits[16];
   for (int j = 0; j < T; j++) store_bits[j] = tile_bits[j];
   for (const auto& sw : store_swaps) {  // physical bit swaps fused into the store (plan.cpp)
@@ -226,10 +311,10 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
     std::swap(store_bits[p1], store_bits[p2]);
   }
   for (int j = 0; j < T; j++) {
-    H->tile_bits[j] = tile_bits[j];
-    H->store_bits[j] = store_bits[j];
+    H()->tile_bits[j] = tile_bits[j];
+    H()->store_bits[j] = store_bits[j];
   }
-  for (int j = 0; j < n_out; j++) H->out_bits[j] = out_bits[j];
+  for (int j = 0; j < n_out; j++) H()->out_bits[j] = out_bits[j];
   auto fill_map = [&](SvMap& m, const int* tpos, const int* R, const int* bits) {
     for (int j = 0; j < T - r; j++) {
       m.tw[j] = sv_swz_host(1 << tpos[j], swizzle_bits);
@@ -243,172 +328,252 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
   {  // boundary maps: lanes walk the lowest memory bits of the load / store side
     int order[16];
     for (int j = 0; j < T; j++) order[j] = j;
-    fill_map(H->load, order, order + (T - r), tile_bits);
+    fill_map(H()->load, order, order + (T - r), tile_bits);
     std::sort(order, order + T, [&](int a, int b) { return store_bits[a] < store_bits[b]; });
-    fill_map(H->store, order, order + (T - r), tile_bits);
-    for (int j = 0; j < T - r; j++) H->store.tmb[j] = store_bits[order[j]];
-    for (int s = 0; s < r; s++) H->store.rmb[s] = store_bits[order[T - r + s]];
+    fill_map(H()->store, order, order + (T - r), tile_bits);
+    for (int j = 0; j < T - r; j++) H()->store.tmb[j] = store_bits[order[j]];
+    for (int s = 0; s < r; s++) H()->store.rmb[s] = store_bits[order[T - r + s]];
   }
   auto push = [&](const double* m, int count) -> int {
     const int at = (int)(prog.coefs.size() / 2 - cbase);
     prog.coefs.insert(prog.coefs.end(), m, m + 2 * count);
     return at;
   };
+  auto push_c = [&](cd c) -> int {
+    const double m[2] = {c.real(), c.imag()};
+    return push(m, 1);
+  };
 
+  double fpa = 0.0;  // algorithmic flops per amplitude of the section (DESIGN "Roofline")
   int op_cursor = 0;
   bool lanes_contiguous_first = false, lanes_contiguous_last = false;
+  int n_diagset = 0, n_diag_fused = 0;
   for (size_t pi = 0; pi < phases.size(); pi++) {
-    SvPhase* P = reinterpret_cast<SvPhase*>(prog.ints.data() + base + H->phase_off + phase_ints * pi);
+    SvPhase* P = reinterpret_cast<SvPhase*>(prog.ints.data() + base + H()->phase_off + phase_ints * pi);
     const Ph& ph = phases[pi];
-    int slot_of[SV_TMAX];
-    std::fill(slot_of, slot_of + SV_TMAX, -1);
+    const PhaseOut& po = pout[pi];
     for (int s = 0; s < r; s++) {
       P->R[s] = ph.R[s];
       P->rw[s] = sv_swz_host(1 << ph.R[s], swizzle_bits);
-      slot_of[ph.R[s]] = s;
     }
-    // thread bits: the first `swizzle_bits` get distinct residues mod swizzle_bits so a group of
-    // 2^swizzle_bits lanes hits distinct 16-/8-byte bank groups under the XOR-fold swizzle.
-    std::vector<int> cand, chosen;
-    for (int pos = 0; pos < T; pos++)
-      if (slot_of[pos] < 0) cand.push_back(pos);
-    uint32_t used_res = 0;
-    std::vector<bool> taken(cand.size(), false);
-    for (size_t i = 0; i < cand.size() && (int)chosen.size() < swizzle_bits; i++) {
-      const int res = cand[i] % swizzle_bits;
-      if (!((used_res >> res) & 1)) {
-        used_res |= 1u << res;
-        chosen.push_back(cand[i]);
-        taken[i] = true;
-      }
-    }
-    for (size_t i = 0; i < cand.size(); i++)
-      if (!taken[i]) chosen.push_back(cand[i]);
-    int thread_of[SV_TMAX];
-    std::fill(thread_of, thread_of + SV_TMAX, -1);
-    for (size_t j = 0; j < chosen.size(); j++) {
-      P->tpos[j] = chosen[j];
-      P->tw[j] = sv_swz_host(1 << chosen[j], swizzle_bits);
-      thread_of[chosen[j]] = (int)j;
+    for (size_t j = 0; j < po.chosen.size(); j++) {
+      P->tpos[j] = po.chosen[j];
+      P->tw[j] = sv_swz_host(1 << po.chosen[j], swizzle_bits);
     }
     // a direct HBM boundary needs lane j of each 2^swizzle_bits group on memory bit j (128 B runs)
     auto lanes_on_low_bits = [&](const int* bits) {
-      if ((int)chosen.size() < swizzle_bits) return false;
+      if ((int)po.chosen.size() < swizzle_bits) return false;
       for (int j = 0; j < swizzle_bits; j++)
-        if (bits[chosen[j]] != j) return false;
+        if (bits[po.chosen[j]] != j) return false;
       return true;
     };
     if (pi == 0) {
       lanes_contiguous_first = lanes_on_low_bits(tile_bits);
-      fill_map(H->din, chosen.data(), ph.R.data(), tile_bits);
+      fill_map(H()->din, po.chosen.data(), ph.R.data(), tile_bits);
     }
     if (pi + 1 == phases.size()) {
       lanes_contiguous_last = lanes_on_low_bits(store_bits);
-      fill_map(H->dout, chosen.data(), ph.R.data(), store_bits);
+      fill_map(H()->dout, po.chosen.data(), ph.R.data(), store_bits);
     }
-
+    P = reinterpret_cast<SvPhase*>(prog.ints.data() + base + H()->phase_off + phase_ints * pi);
     P->op_begin = op_cursor;
-    P->op_count = (int)ph.ops.size();
-    for (int gi : ph.ops) {
-      SvOp* O = reinterpret_cast<SvOp*>(prog.ints.data() + base + H->op_off + op_ints * op_cursor);
-      const PGate& p = pg[gi];
-      const sv_gate& g = gates[p.src];
-      O->type = p.type;
-      O->extra = p.extra;
-      switch (p.type) {
-        case SV_OP_U2: {
-          int sa = slot_of[p.a], sb = slot_of[p.b];
-          double m[32];
-          std::memcpy(m, g.m, sizeof(m));
-          if (sa > sb) {  // canonical slot order: conjugate by the s=1 <-> s=2 permutation
-            static const int sw[4] = {0, 2, 1, 3};
-            for (int rr = 0; rr < 4; rr++)
-              for (int cc = 0; cc < 4; cc++) {
-                m[2 * (4 * rr + cc)] = g.m[2 * (4 * sw[rr] + sw[cc])];
-                m[2 * (4 * rr + cc) + 1] = g.m[2 * (4 * sw[rr] + sw[cc]) + 1];
-              }
-            std::swap(sa, sb);
-          }
-          O->a = sa;
-          O->b = sb;
-          O->coef = push(m, 16);
-          break;
-        }
-        case SV_OP_PERM2: {
-          int sa = slot_of[p.a], sb = slot_of[p.b];
-          if (sa > sb) {  // canonical slot order: relabel s = bit(a) + 2 bit(b) by swapping its bits
-            auto swb = [](int s) { return ((s & 1) << 1) | (s >> 1); };
-            int np = 0;
-            for (int s2 = 0; s2 < 4; s2++) np |= swb((p.extra >> (2 * swb(s2))) & 3) << (2 * s2);
-            O->extra = np;
-            std::swap(sa, sb);
-          }
-          O->a = sa;
-          O->b = sb;
-          O->coef = 0;
-          break;
-        }
-        case SV_OP_U1:
-          O->a = slot_of[p.a];
-          O->coef = push(g.m, 4);
-          break;
-        case SV_OP_H1: {
-          O->a = slot_of[p.a];
-          const double s[2] = {g.m[0], 0.0};
-          O->coef = push(s, 1);
-          break;
-        }
-        case SV_OP_DIAG:
-        case SV_OP_DIAG_CP: {
-          auto code = [&](int x) {
-            if (x >= 0) return x;  // constant
-            const int mb = kDiagLocal - x;
-            const int pos = pos_of[mb];
-            if (pos < 0) return SV_CODE_OUT(mb);
-            if (slot_of[pos] >= 0) return SV_CODE_SLOT(slot_of[pos]);
-            return SV_CODE_THREAD(thread_of[pos]);
+    P->op_count = (int)po.items.size();
+
+    // operand code in this phase's mapping
+    auto code = [&](int x) {
+      if (x >= 0) return x;  // constant
+      const int mb = kDiagLocal - x;
+      const int pos = pos_of[mb];
+      if (pos < 0) return SV_CODE_OUT(mb);
+      if (po.slot_of[pos] >= 0) return SV_CODE_SLOT(po.slot_of[pos]);
+      return SV_CODE_THREAD(po.thread_of[pos]);
+    };
+
+    for (const Item& it : po.items) {
+      SvOp op{};
+      if (!it.group.empty()) {  // ---------------------------------------------------- DIAGSET
+        std::map<TermKey, cd> terms;
+        auto add = [&](int ca, int cb, cd c, bool need_a, bool need_b) {
+          TermKey k{0, 0u, 0ull};
+          auto cond = [&](int x) -> bool {  // false: the term never applies
+            if (x == SV_CODE_ZERO) return false;
+            if (x == SV_CODE_ONE) return true;
+            if (x < 4) k.S |= 1 << x;
+            else if (x < 100) k.J |= 1u << (x - 32);
+            else k.O |= 1ull << (x - 100);
+            return true;
           };
-          int ca = code(p.a), cb = code(p.b);
-          double d[8] = {1, 0, 1, 0, 1, 0, 1, 0};
-          std::memcpy(d, g.m, sizeof(double) * (g.kind == SV_D2 ? 8 : 4));
-          // canonical form for the kernel: a register-slot operand comes first, two slots ascend
-          if (cb < 4 && (ca >= 4 || cb < ca)) {
-            std::swap(ca, cb);
-            std::swap(d[2], d[4]);  // d[s] with s = bit(a) + 2 bit(b): exchange s = 1 and s = 2
-            std::swap(d[3], d[5]);
-          }
-          O->a = ca;
-          O->b = cb;
-          if (p.type == SV_OP_DIAG_CP)
-            O->coef = push(d + 6, 1);
+          if (need_a && !cond(ca)) return;
+          if (need_b && !cond(cb)) return;
+          auto f = terms.find(k);
+          if (f == terms.end())
+            terms[k] = c;
           else
-            O->coef = push(d, 4);
-          break;
+            f->second *= c;
+        };
+        for (int gi : it.group) {
+          const PGate& p = pg[gi];
+          const sv_gate& g = gates[p.src];
+          const int ca = code(p.a), cb = code(p.b);
+          auto cval = [&](int i) { return cd(g.m[2 * i], g.m[2 * i + 1]); };
+          if (p.type == SV_OP_DIAG_CP) {
+            add(ca, cb, cval(3), true, true);
+          } else if (g.kind == SV_D1) {
+            add(ca, cb, cval(0), false, false);
+            add(ca, cb, cval(1) / cval(0), true, false);
+          } else {  // general 2-qubit diagonal: d0 * (d1/d0)^a * (d2/d0)^b * (d3 d0 / (d1 d2))^(ab)
+            const cd d0 = cval(0), d1 = cval(1), d2 = cval(2), d3 = cval(3);
+            add(ca, cb, d0, false, false);
+            add(ca, cb, d1 / d0, true, false);
+            add(ca, cb, d2 / d0, false, true);
+            add(ca, cb, d3 * d0 / (d1 * d2), true, true);
+          }
+          n_diag_fused++;
+        }
+        // descriptor: [mask][cta offsets 17][thread offsets 17] then terms
+        std::vector<cd> cst(16, cd(1.0, 0.0));
+        std::vector<std::vector<std::pair<uint64_t, cd>>> cta(16);
+        std::vector<std::vector<std::tuple<uint32_t, uint64_t, cd>>> thr(16);
+        for (const auto& kv : terms) {
+          const TermKey& k = kv.first;
+          if (k.J == 0 && k.O == 0)
+            cst[k.S] *= kv.second;
+          else if (k.J == 0)
+            cta[k.S].push_back({k.O, kv.second});
+          else
+            thr[k.S].push_back(std::make_tuple(k.J, k.O, kv.second));
+        }
+        int mask = 0;
+        for (int S = 0; S < 16; S++)
+          if (cst[S] != cd(1.0, 0.0) || !cta[S].empty() || !thr[S].empty()) mask |= 1 << S;
+        const size_t desc = prog.ints.size() - base;
+        prog.ints.push_back(mask);
+        const size_t cta_off = prog.ints.size();
+        prog.ints.resize(prog.ints.size() + 34, 0);
+        const int c0 = (int)(prog.coefs.size() / 2 - cbase);
+        for (int S = 0; S < 16; S++) push_c(cst[S]);
+        // cta terms: (O_lo, O_hi, coef)
+        for (int S = 0; S < 16; S++) {
+          prog.ints[cta_off + S] = (int)(prog.ints.size() - base);
+          for (const auto& tm : cta[S]) {
+            prog.ints.push_back((int)(tm.first & 0xffffffffu));
+            prog.ints.push_back((int)(tm.first >> 32));
+            prog.ints.push_back(push_c(tm.second));
+          }
+        }
+        prog.ints[cta_off + 16] = (int)(prog.ints.size() - base);
+        for (int S = 0; S < 16; S++) {
+          prog.ints[cta_off + 17 + S] = (int)(prog.ints.size() - base);
+          for (const auto& tm : thr[S]) {
+            prog.ints.push_back((int)std::get<0>(tm));
+            prog.ints.push_back((int)(std::get<1>(tm) & 0xffffffffu));
+            prog.ints.push_back((int)(std::get<1>(tm) >> 32));
+            prog.ints.push_back(push_c(std::get<2>(tm)));
+          }
+        }
+        prog.ints[cta_off + 33] = (int)(prog.ints.size() - base);
+        op.type = SV_OP_DIAGSET;
+        op.a = (int)desc;
+        op.coef = c0;
+        // flops: per active subset S one complex multiply on the 2^(4-|S|)/16 of the registers it
+        // covers, plus one complex multiply per thread term per thread (16 amplitudes)
+        for (int S = 0; S < 16; S++)
+          if ((mask >> S) & 1) fpa += 6.0 * (1 << (4 - __builtin_popcount(S))) / 16.0 + 6.0 * thr[S].size() / 16.0;
+        n_diagset++;
+      } else {  // ---------------------------------------------------------------- single op
+        const PGate& p = pg[it.gate];
+        const sv_gate& g = gates[p.src];
+        op.type = p.type;
+        op.extra = p.extra;
+        switch (p.type) {
+          case SV_OP_U2: {
+            int sa = po.slot_of[p.a], sb = po.slot_of[p.b];
+            double m[32];
+            std::memcpy(m, g.m, sizeof(m));
+            if (sa > sb) {  // canonical slot order: conjugate by the s=1 <-> s=2 permutation
+              static const int sw[4] = {0, 2, 1, 3};
+              for (int rr = 0; rr < 4; rr++)
+                for (int cc = 0; cc < 4; cc++) {
+                  m[2 * (4 * rr + cc)] = g.m[2 * (4 * sw[rr] + sw[cc])];
+                  m[2 * (4 * rr + cc) + 1] = g.m[2 * (4 * sw[rr] + sw[cc]) + 1];
+                }
+              std::swap(sa, sb);
+            }
+            op.a = sa;
+            op.b = sb;
+            op.coef = push(m, 16);
+            fpa += 32.0;
+            break;
+          }
+          case SV_OP_PERM2: {
+            int sa = po.slot_of[p.a], sb = po.slot_of[p.b];
+            if (sa > sb) {  // canonical slot order: relabel s = bit(a) + 2 bit(b) by swapping its bits
+              auto swb = [](int s) { return ((s & 1) << 1) | (s >> 1); };
+              int np = 0;
+              for (int s2 = 0; s2 < 4; s2++) np |= swb((p.extra >> (2 * swb(s2))) & 3) << (2 * s2);
+              op.extra = np;
+              std::swap(sa, sb);
+            }
+            op.a = sa;
+            op.b = sb;
+            op.coef = 0;
+            break;
+          }
+          case SV_OP_U1:
+            op.a = po.slot_of[p.a];
+            op.coef = push(g.m, 4);
+            fpa += 16.0;
+            break;
+          case SV_OP_H1: {
+            op.a = po.slot_of[p.a];
+            const double s[2] = {g.m[0], 0.0};
+            op.coef = push(s, 1);
+            fpa += 4.0;
+            break;
+          }
+          case SV_OP_DIAG:
+          case SV_OP_DIAG_CP: {
+            int ca = code(p.a), cb = code(p.b);
+            double d[8] = {1, 0, 1, 0, 1, 0, 1, 0};
+            std::memcpy(d, g.m, sizeof(double) * (g.kind == SV_D2 ? 8 : 4));
+            // canonical form for the kernel: a register-slot operand comes first, two slots ascend
+            if (cb < 4 && (ca >= 4 || cb < ca)) {
+              std::swap(ca, cb);
+              std::swap(d[2], d[4]);  // d[s] with s = bit(a) + 2 bit(b): exchange s = 1 and s = 2
+              std::swap(d[3], d[5]);
+            }
+            op.a = ca;
+            op.b = cb;
+            if (p.type == SV_OP_DIAG_CP) {
+              op.coef = push(d + 6, 1);
+              fpa += 1.5;
+            } else {
+              op.coef = push(d, 4);
+              fpa += 6.0;
+            }
+            break;
+          }
         }
       }
+      std::memcpy(prog.ints.data() + base + H()->op_off + op_ints * op_cursor, &op, sizeof(op));
       op_cursor++;
     }
   }
-  H->flags = (lanes_contiguous_first ? SV_FLAG_FIRST_DIRECT : 0) | (lanes_contiguous_last ? SV_FLAG_LAST_DIRECT : 0);
+  H()->flags = (lanes_contiguous_first ? SV_FLAG_FIRST_DIRECT : 0) | (lanes_contiguous_last ? SV_FLAG_LAST_DIRECT : 0);
+  const size_t total_ints = prog.ints.size() - base;
+  const size_t ncoef = prog.coefs.size() / 2 - cbase;
+  const size_t coef_cap = swizzle_bits == 3 ? SV_CONST_COEF64 : SV_CONST_COEF32;
+  if (total_ints > SV_CONST_INTS || ncoef > coef_cap) {
+    prog.ints.resize(base);
+    prog.coefs.resize(cbase * 2);
+    return Status::err(kTooBig, "section program exceeds the constant budget");
+  }
 
-  // algorithmic flops per amplitude: U2 4x4 complex matvec = 32, U1 = 16, H1 = 4, PERM = 0,
-  // DIAG = one complex multiply (6), DIAG_CP = one complex multiply on a quarter (1.5)
-  double fpa = 0.0;
-  for (const PGate& p : pg)
-    fpa += p.type == SV_OP_U2 ? 32.0 : p.type == SV_OP_U1 ? 16.0 : p.type == SV_OP_H1 ? 4.0
-         : p.type == SV_OP_DIAG ? 6.0 : p.type == SV_OP_DIAG_CP ? 1.5 : 0.0;
   if (std::getenv("SV_DEBUG_PLAN")) {  // per-section compile report (analysis aid)
-    int cnt[8] = {0}, diag_kind[3] = {0};  // diag operands: slot-slot, slot-other, other-other
-    for (int i = 0; i < n_ops; i++) {
-      const SvOp* O = reinterpret_cast<const SvOp*>(prog.ints.data() + base + H->op_off + op_ints * i);
-      cnt[O->type]++;
-      if (O->type == SV_OP_DIAG || O->type == SV_OP_DIAG_CP) diag_kind[(O->a >= 4) + (O->b >= 4)]++;
-    }
     std::fprintf(stderr,
-                 "[sv] section T=%d phases=%zu ops=%d U2=%d U1=%d H1=%d PERM=%d DIAG=%d CP=%d (ss=%d so=%d oo=%d) "
-                 "flags=%d flops/amp=%.1f low-tile-bits=%d%d%d%d\n",
-                 T, phases.size(), n_ops, cnt[SV_OP_U2], cnt[SV_OP_U1], cnt[SV_OP_H1], cnt[SV_OP_PERM2],
-                 cnt[SV_OP_DIAG], cnt[SV_OP_DIAG_CP], diag_kind[0], diag_kind[1], diag_kind[2], H->flags, fpa,
+                 "[sv] section T=%d phases=%zu items=%zu gates=%zu diagsets=%d fused_diag=%d flags=%d "
+                 "flops/amp=%.1f ints=%zu coefs=%zu low-tile-bits=%d%d%d%d\n",
+                 T, phases.size(), n_items, gates.size(), n_diagset, n_diag_fused, H()->flags, fpa, total_ints, ncoef,
                  (int)(tile & 1), (int)((tile >> 1) & 1), (int)((tile >> 2) & 1), (int)((tile >> 3) & 1));
   }
   Launch L;
@@ -416,13 +581,13 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
   L.int_off = base;
   L.int_count = total_ints;
   L.coef_off = cbase;
-  L.coef_count = prog.coefs.size() / 2 - cbase;
+  L.coef_count = ncoef;
   L.T = T;
   L.r = r;
   L.n_out = n_out;
   L.n_phases = (int)phases.size();
-  L.n_ops = n_ops;
-  L.flags = H->flags;
+  L.n_ops = (int)n_items;
+  L.flags = H()->flags;
   prog.launches.push_back(L);
   // keep every section 16-byte aligned
   while (prog.ints.size() % 4) prog.ints.push_back(0);

@@ -153,6 +153,71 @@ __device__ __forceinline__ void scale_all(V (&v)[16], V f) {
     default: break;             \
   }
 
+// multiply every register k that contains slot subset S by f
+template <int S, typename V>
+__device__ __forceinline__ void scale_subset(V (&v)[16], V f) {
+#pragma unroll
+  for (int k = 0; k < 16; k++)
+    if ((k & S) == S) v[k] = cmul(v[k], f);
+}
+
+template <typename V>
+__device__ __forceinline__ V shfl_c(V x, int src) {
+  x.x = __shfl_sync(0xffffffffu, x.x, src);
+  x.y = __shfl_sync(0xffffffffu, x.y, src);
+  return x;
+}
+
+__device__ __forceinline__ uint64_t mask64(int lo, int hi) { return (uint64_t)(uint32_t)lo | ((uint64_t)(uint32_t)hi << 32); }
+
+// Fused diagonal run (SV_OP_DIAGSET, program.h): per-CTA terms are evaluated by lanes 0..15 of
+// every warp (lane = register subset S) and broadcast with shuffles; per-thread terms by each
+// thread; then each non-trivial subset scales the registers that contain it.
+template <typename V>
+__device__ __forceinline__ void diagset(V (&v)[16], int desc, int cb, int tid, uint64_t tile_off) {
+  const int mask = c_prog[desc];
+  const int lane = tid & 31;
+  V mine = cone<V>();
+  if (lane < 16 && ((mask >> lane) & 1)) {
+    const int e = c_prog[desc + 2 + lane];
+    for (int t = c_prog[desc + 1 + lane]; t < e; t += 3) {
+      const uint64_t O = mask64(c_prog[t], c_prog[t + 1]);
+      const V c = cc<V>(c_prog[t + 2]);
+      if ((tile_off & O) == O) mine = cmul(mine, c);
+    }
+  }
+#pragma unroll
+  for (int S = 0; S < 16; S++) {
+    if (!((mask >> S) & 1)) continue;
+    V g = cmul(shfl_c(mine, S), cc<V>(cb + S));
+    const int e = c_prog[desc + 19 + S];
+    for (int t = c_prog[desc + 18 + S]; t < e; t += 4) {
+      const int J = c_prog[t];
+      const uint64_t O = mask64(c_prog[t + 1], c_prog[t + 2]);
+      const V c = cc<V>(c_prog[t + 3]);  // uniform load, outside the per-thread condition
+      if ((tid & J) == J && (tile_off & O) == O) g = cmul(g, c);
+    }
+    switch (S) {
+      case 0: scale_subset<0>(v, g); break;
+      case 1: scale_subset<1>(v, g); break;
+      case 2: scale_subset<2>(v, g); break;
+      case 3: scale_subset<3>(v, g); break;
+      case 4: scale_subset<4>(v, g); break;
+      case 5: scale_subset<5>(v, g); break;
+      case 6: scale_subset<6>(v, g); break;
+      case 7: scale_subset<7>(v, g); break;
+      case 8: scale_subset<8>(v, g); break;
+      case 9: scale_subset<9>(v, g); break;
+      case 10: scale_subset<10>(v, g); break;
+      case 11: scale_subset<11>(v, g); break;
+      case 12: scale_subset<12>(v, g); break;
+      case 13: scale_subset<13>(v, g); break;
+      case 14: scale_subset<14>(v, g); break;
+      default: scale_subset<15>(v, g); break;
+    }
+  }
+}
+
 // value of a non-slot DIAG bit code for this thread / tile
 __device__ __forceinline__ int code_val(int code, int tid, uint64_t tile_off) {
   if (code < 100) return (tid >> (code - 32)) & 1;
@@ -225,6 +290,9 @@ __device__ __forceinline__ void run_op(V (&v)[16], int oi, int tid, uint64_t til
       }
       break;
     }
+    case SV_OP_DIAGSET:
+      diagset(v, a, cb, tid, tile_off);
+      break;
     default:
       break;
   }
