@@ -986,3 +986,69 @@ int sv_plan_circuit(const sv_gate* gates, size_t n_gates, int n, int c, int worl
 }
 
 }  // extern "C"
+
+extern "C" int sv_compile_circuit(const sv_gate* gates, size_t n_gates, int n, int c, int world_log2, int rank,
+                                  sv_precision prec, const int32_t* pi0, const int32_t* sigma0, uint32_t flags,
+                                  int64_t** steps_out, size_t* n_steps,
+                                  int32_t** ints_out, size_t* n_ints, double** coefs_out, size_t* n_coefs,
+                                  int32_t* pi_final, int32_t* sigma_final) {
+  if (!steps_out || !n_steps || !ints_out || !n_ints || !coefs_out || !n_coefs || (n_gates && !gates))
+    return fail(nullptr, SV_EINVAL, "null argument");
+  if (n < 1 || n > 63 || world_log2 < 0 || world_log2 >= n) return fail(nullptr, SV_EINVAL, "bad n / world");
+  const int nL = n - world_log2;
+  std::vector<int> pi(n), sigma(n);
+  for (int q = 0; q < n; q++) {
+    pi[q] = pi0 ? pi0[q] : q;
+    sigma[q] = sigma0 ? sigma0[q] : q;
+  }
+  std::vector<Step> steps;
+  PlanCounters ctr;
+  PlanLayout lay;
+  lay.low_bits = prec == SV_FP64 ? 3 : 4;
+  Status s = make_plan(gates, n_gates, n, c, world_log2, pi, sigma, flags, steps, ctr, lay);
+  if (!s.good()) return fail(nullptr, s);
+  Program prog;
+  std::vector<int64_t> rec;
+  auto put = [&](std::initializer_list<int64_t> v) {
+    int64_t r[8] = {0};
+    int i = 0;
+    for (int64_t x : v) r[i++] = x;
+    rec.insert(rec.end(), r, r + 8);
+  };
+  for (size_t i = 0; i < steps.size(); i++) {
+    const Step& st = steps[i];
+    if (st.type == Step::EXCHANGE) {
+      for (const ExPair& p : st.ex) put({0, p.m, p.b, (int64_t)i});
+    } else if (st.type == Step::COMPACT) {
+      for (const auto& sw : st.swaps) put({3, sw.first, sw.second});
+    } else if (st.type == Step::GATE || nL < SV_R_BITS) {
+      for (const sv_gate& gm : st.gates) put({2, gm.kind, gm.q0, gm.q1, gm.pad});
+      for (const auto& sw : st.swaps) put({3, sw.first, sw.second});
+    } else {
+      const size_t first = prog.launches.size();
+      Status cs = compile_section_split(st.gates, nL, rank, world_log2, lay.tile_default, lay.low_bits, st.swaps, prog);
+      if (!cs.good()) return fail(nullptr, cs);
+      for (size_t k = first; k < prog.launches.size(); k++) {
+        const Launch& L = prog.launches[k];
+        put({1, (int64_t)L.int_off, (int64_t)L.int_count, (int64_t)L.coef_off, (int64_t)L.coef_count, L.T, L.n_out,
+             L.flags});
+      }
+    }
+  }
+  auto dup = [](const void* src, size_t bytes) {
+    void* p = std::malloc(bytes ? bytes : 1);
+    if (p && bytes) std::memcpy(p, src, bytes);
+    return p;
+  };
+  *steps_out = (int64_t*)dup(rec.data(), rec.size() * sizeof(int64_t));
+  *n_steps = rec.size() / 8;
+  *ints_out = (int32_t*)dup(prog.ints.data(), prog.ints.size() * sizeof(int));
+  *n_ints = prog.ints.size();
+  *coefs_out = (double*)dup(prog.coefs.data(), prog.coefs.size() * sizeof(double));
+  *n_coefs = prog.coefs.size() / 2;
+  for (int q = 0; q < n; q++) {
+    if (pi_final) pi_final[q] = pi[q];
+    if (sigma_final) sigma_final[q] = sigma[q];
+  }
+  return SV_OK;
+}

@@ -177,8 +177,9 @@ template <typename V>
 __device__ __forceinline__ void diagset(V (&v)[16], int desc, int cb, int tid, uint64_t tile_off) {
   const int mask = c_prog[desc];
   const int lane = tid & 31;
+  const bool full_warp = blockDim.x >= 32;  // tiny tiles (T < 9) have fewer than 32 threads
   V mine = cone<V>();
-  if (lane < 16 && ((mask >> lane) & 1)) {
+  if (full_warp && lane < 16 && ((mask >> lane) & 1)) {
     const int e = c_prog[desc + 2 + lane];
     for (int t = c_prog[desc + 1 + lane]; t < e; t += 3) {
       const uint64_t O = mask64(c_prog[t], c_prog[t + 1]);
@@ -189,7 +190,18 @@ __device__ __forceinline__ void diagset(V (&v)[16], int desc, int cb, int tid, u
 #pragma unroll
   for (int S = 0; S < 16; S++) {
     if (!((mask >> S) & 1)) continue;
-    V g = cmul(shfl_c(mine, S), cc<V>(cb + S));
+    V g;
+    if (full_warp) {
+      g = cmul(shfl_c(mine, S), cc<V>(cb + S));
+    } else {  // every thread walks the per-CTA terms itself
+      g = cc<V>(cb + S);
+      const int e0 = c_prog[desc + 2 + S];
+      for (int t = c_prog[desc + 1 + S]; t < e0; t += 3) {
+        const uint64_t O = mask64(c_prog[t], c_prog[t + 1]);
+        const V c = cc<V>(c_prog[t + 2]);
+        if ((tile_off & O) == O) g = cmul(g, c);
+      }
+    }
     const int e = c_prog[desc + 19 + S];
     for (int t = c_prog[desc + 18 + S]; t < e; t += 4) {
       const int J = c_prog[t];

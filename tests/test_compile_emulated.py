@@ -1,0 +1,80 @@
+"""The section compiler on CPU: programs from sv_compile_circuit, executed by tests/emulator.py
+(which mirrors section.cu's data flow and checks its invariants), must reproduce the oracle."""
+import numpy as np
+import pytest
+
+import circuits as C
+import oracle as O
+
+from emulator import run
+
+sv = pytest.importorskip("paper_2102_02957_b200")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    from paper_2102_02957_b200 import build
+    build.build()
+
+
+def emulate(recs, n, c, g=0, precision="fp64", seed=0, flags=0, pi0=None, sigma0=None, psi=None):
+    """Run the compiled programs on a random (or given) logical state; returns (steps, pi, sigma, logical out)."""
+    steps, ints, coefs, pi, sigma = sv.compile_circuit(recs, n, c, g, 0, precision, flags, pi0, sigma0)
+    if psi is None:
+        rng = np.random.default_rng(seed)
+        psi = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+        psi /= np.linalg.norm(psi)
+    mu0 = list(range(n)) if pi0 is None else [int(sigma0[int(p)]) for p in pi0]
+    mem = np.empty_like(psi)
+    mem[:] = psi[O.unpermute(np.arange(1 << n).astype(np.complex128), mu0).real.astype(np.int64).argsort()]
+
+    def gate_fn(m, st):
+        rec = np.array(recs[int(st[4])], dtype=C.GATE_DTYPE)
+        rec["q0"], rec["q1"] = int(st[2]), int(st[3])
+        m[:] = O.apply_circuit(C.records([rec]), n, m)
+
+    run(steps, ints, coefs, mem, gate_fn=gate_fn)
+    got = O.unpermute(mem, [int(sigma[int(p)]) for p in pi])
+    ref = O.apply_circuit(recs, n, psi)
+    err = np.max(np.abs(got - ref))
+    assert err <= 1e-12, err
+    return steps, pi, sigma, got
+
+
+def test_two_applies_carry_the_permutations():
+    # the GPU test_random_circuits pattern: a second circuit starts from the first one's pi/sigma
+    rng = np.random.default_rng(11)
+    for t in range(40):
+        n = int(rng.integers(2, 17))
+        c = min(int(rng.integers(2, n + 1)), 13)
+        circ = C.random_circuit(n, int(rng.integers(0, 120)), 500 + t)
+        _, pi, sigma, out = emulate(circ, n, c, seed=t)
+        emulate(circ[: len(circ) // 2], n, c, pi0=pi, sigma0=sigma, psi=out)
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_random_circuits_emulated(prec):
+    rng = np.random.default_rng(31)
+    for t in range(25):
+        n = int(rng.integers(4, 15))
+        c = int(rng.integers(2, n + 1))
+        recs = C.random_circuit(n, int(rng.integers(1, 90)), 900 + t)
+        emulate(recs, n, c, precision=prec, seed=t)
+
+
+def test_diagonal_heavy_emulated():
+    for t, (n, c) in enumerate([(12, 4), (14, 6), (13, 12), (10, 3)]):
+        psi_recs = C.random_circuit(n, 20, 50 + t, kinds=("u3", "su4"))
+        recs = np.concatenate([psi_recs, C.random_circuit(n, 150, 60 + t, kinds=("cp", "u1", "d2", "u3"))])
+        emulate(recs, n, c, seed=t)
+
+
+@pytest.mark.parametrize("n,c", [(12, 6), (14, 8), (14, 12), (16, 12)])
+def test_qft_qv_emulated(n, c):
+    emulate(C.qft(n), n, c)
+    emulate(C.quantum_volume(n, 6, 2), n, c)
+
+
+def test_ghz_permutation_ops_emulated():
+    emulate(C.ghz(12), 12, 5)
+    emulate(C.mirror(C.random_circuit(9, 60, 4, kinds=("cx", "swap", "u3"))), 9, 4)
