@@ -164,18 +164,19 @@ int sv_plan_circuit(const sv_gate* gates, size_t n_gates, int n, int chunk_bits,
                     const int32_t* pi0, const int32_t* sigma0, uint32_t flags, sv_gate** out,
                     size_t* n_out, int32_t* pi_final, int32_t* sigma_final);
 /* The section programs sv_apply_circuit would launch for rank `rank` of 2^world_log2 GPUs, for
- * testing the section compiler without a GPU.  *steps: n_steps records of 8 int64:
- *   {1, int_off, int_count, coef_off, coef_count, T, n_out, flags}  a section launch
+ * testing the section compiler without a GPU.  *steps: n_steps records of 12 int64:
+ *   {1, int_off, int_count, coef_off, coef_count, T, n_out, flags, aux_off, aux_count}  a launch
  *   {3, m1, m2, 0, ...}                                            a memory-bit swap pass
  *   {0, m, b, batch, 0, ...}                                       an exchange pair
  *   {2, kind, q0, q1, gate index, 0, ...}                          a per-gate launch
- * *ints / *coefs: the programs (program.h layout) and fp64 complex coefficients.  pi_final /
+ * *ints / *coefs / *aux: the programs (program.h layout), fp64 complex coefficients (constant
+ * bank) and fp64 complex DIAGSET factor tables (global memory).  pi_final /
  * sigma_final as in sv_plan_circuit.  All outputs are freed with sv_free. */
 int sv_compile_circuit(const sv_gate* gates, size_t n_gates, int n, int chunk_bits, int world_log2,
                        int rank, sv_precision prec, const int32_t* pi0, const int32_t* sigma0,
                        uint32_t flags, int64_t** steps, size_t* n_steps,
                        int32_t** ints, size_t* n_ints, double** coefs, size_t* n_coefs,
-                       int32_t* pi_final, int32_t* sigma_final);
+                       double** aux, size_t* n_aux, int32_t* pi_final, int32_t* sigma_final);
 void sv_free(void* p);
 /* ABI version (for the binding's check). */
 int sv_abi_version(void);

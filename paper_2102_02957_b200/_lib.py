@@ -80,7 +80,7 @@ def lib():
         "sv_block_circuit": ([vp, sz, i32, i32, ip, u32, hp, ctypes.POINTER(sz), ip], i32),
         "sv_plan_circuit": ([vp, sz, i32, i32, i32, ip, ip, u32, hp, ctypes.POINTER(sz), ip, ip], i32),
         "sv_compile_circuit": ([vp, sz, i32, i32, i32, i32, i32, ip, ip, u32, hp, ctypes.POINTER(sz), hp, ctypes.POINTER(sz),
-                                hp, ctypes.POINTER(sz), ip, ip], i32),
+                                hp, ctypes.POINTER(sz), hp, ctypes.POINTER(sz), ip, ip], i32),
         "sv_free": ([vp], None),
         "sv_abi_version": ([], i32),
     }
@@ -151,10 +151,10 @@ def plan_circuit(gates, n: int, c: int, world_log2: int, pi0=None, sigma0=None, 
 def compile_circuit(gates, n: int, c: int, world_log2: int = 0, rank: int = 0, precision: str = "fp64",
                     flags: int = 0, pi0=None, sigma0=None):
     """Host-only: the section programs sv_apply_circuit would launch (sv_compile_circuit) ->
-    (steps int64[k, 8], ints int32[], coefs complex128[], pi_final, sigma_final)."""
+    (steps int64[k, 12], ints int32[], coefs complex128[], aux complex128[], pi_final, sigma_final)."""
     g = as_gates(gates)
-    st, ni, co = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
-    nst, nin, nco = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
+    st, ni, co, ax = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+    nst, nin, nco, nax = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
     pif = np.zeros(n, dtype=np.int32)
     sgf = np.zeros(n, dtype=np.int32)
     prec = {"fp64": SV_FP64, "fp32": SV_FP32}[precision]
@@ -163,16 +163,18 @@ def compile_circuit(gates, n: int, c: int, world_log2: int = 0, rank: int = 0, p
     rc = lib().sv_compile_circuit(g.ctypes.data if len(g) else None, len(g), n, c, world_log2, rank, prec,
                                   None if p0 is None else _ip(p0), None if s0 is None else _ip(s0), flags,
                                   ctypes.byref(st), ctypes.byref(nst), ctypes.byref(ni), ctypes.byref(nin),
-                                  ctypes.byref(co), ctypes.byref(nco), _ip(pif), _ip(sgf))
+                                  ctypes.byref(co), ctypes.byref(nco), ctypes.byref(ax), ctypes.byref(nax),
+                                  _ip(pif), _ip(sgf))
     check(rc)
     try:
-        steps = np.frombuffer(ctypes.string_at(st.value, nst.value * 64), dtype=np.int64).reshape(-1, 8).copy()
+        steps = np.frombuffer(ctypes.string_at(st.value, nst.value * 96), dtype=np.int64).reshape(-1, 12).copy()
         ints = np.frombuffer(ctypes.string_at(ni.value, nin.value * 4), dtype=np.int32).copy()
         coefs = np.frombuffer(ctypes.string_at(co.value, nco.value * 16), dtype=np.complex128).copy()
+        aux = np.frombuffer(ctypes.string_at(ax.value, nax.value * 16), dtype=np.complex128).copy()
     finally:
-        for p in (st, ni, co):
+        for p in (st, ni, co, ax):
             lib().sv_free(p)
-    return steps, ints, coefs, pif, sgf
+    return steps, ints, coefs, aux, pif, sgf
 
 
 def nccl_unique_id() -> bytes:

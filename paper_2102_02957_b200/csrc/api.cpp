@@ -77,7 +77,7 @@ struct sv_state {
   bool own_stream = false;
   std::vector<int> pi, sigma;
 
-  DevBuf d_prog, d_coef, d_scratch, d_small, d_tmp, d_tmp2, d_stage;
+  DevBuf d_prog, d_coef, d_aux, d_scratch, d_small, d_tmp, d_tmp2, d_stage;
   PinBuf h_stage, h_stage2;
   cudaEvent_t ev_upload = nullptr;
   bool upload_pending = false;
@@ -253,24 +253,30 @@ int do_exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags) {
 
 int upload_program(sv_state* h) {
   const size_t ib = h->prog.ints.size() * sizeof(int);
-  const size_t ncoef = h->prog.coefs.size() / 2;
-  const size_t cb = ncoef * h->amp;
-  if (ib + cb == 0) return SV_OK;
+  const size_t ncoef = h->prog.coefs.size() / 2, naux = h->prog.aux.size() / 2;
+  const size_t cb = ncoef * h->amp, ab = naux * h->amp;
+  if (ib + cb + ab == 0) return SV_OK;
   if (h->upload_pending) CUDA_TRY(h, cudaEventSynchronize(h->ev_upload));  // staging reuse
-  if (int rc = ensure_pin(h, h->h_stage, ib + cb + 64)) return rc;
+  const size_t c_at = (ib + 15) & ~size_t(15), a_at = (c_at + cb + 15) & ~size_t(15);
+  if (int rc = ensure_pin(h, h->h_stage, a_at + ab + 64)) return rc;
   if (int rc = ensure_dev(h, h->d_prog, ib + 16)) return rc;
   if (int rc = ensure_dev(h, h->d_coef, cb + 16)) return rc;
+  if (int rc = ensure_dev(h, h->d_aux, ab + 16)) return rc;
   char* s = (char*)h->h_stage.p;
   std::memcpy(s, h->prog.ints.data(), ib);
-  char* cs = s + ((ib + 15) & ~size_t(15));
-  if (h->dbl) {
-    std::memcpy(cs, h->prog.coefs.data(), cb);
-  } else {
-    float* f = (float*)cs;
-    for (size_t i = 0; i < 2 * ncoef; i++) f[i] = (float)h->prog.coefs[i];
-  }
+  auto put = [&](char* dst, const std::vector<double>& src, size_t n) {
+    if (h->dbl) {
+      std::memcpy(dst, src.data(), n * 16);
+    } else {  // round to nearest fp32 on upload
+      float* f = (float*)dst;
+      for (size_t i = 0; i < 2 * n; i++) f[i] = (float)src[i];
+    }
+  };
+  put(s + c_at, h->prog.coefs, ncoef);
+  put(s + a_at, h->prog.aux, naux);
   if (ib) CUDA_TRY(h, cudaMemcpyAsync(h->d_prog.p, s, ib, cudaMemcpyHostToDevice, h->st));
-  if (cb) CUDA_TRY(h, cudaMemcpyAsync(h->d_coef.p, cs, cb, cudaMemcpyHostToDevice, h->st));
+  if (cb) CUDA_TRY(h, cudaMemcpyAsync(h->d_coef.p, s + c_at, cb, cudaMemcpyHostToDevice, h->st));
+  if (ab) CUDA_TRY(h, cudaMemcpyAsync(h->d_aux.p, s + a_at, ab, cudaMemcpyHostToDevice, h->st));
   CUDA_TRY(h, cudaEventRecord(h->ev_upload, h->st));
   h->upload_pending = true;
   return SV_OK;
@@ -542,7 +548,7 @@ int sv_destroy(sv_handle h) {
   if (h->st) cudaStreamSynchronize(h->st);
   for (void* p : h->ipc_opened) cudaIpcCloseMemHandle(p);
   if (h->comm && h->nc) h->nc->CommDestroy(h->comm);
-  for (DevBuf* b : {&h->d_prog, &h->d_coef, &h->d_scratch, &h->d_small, &h->d_tmp, &h->d_tmp2, &h->d_stage})
+  for (DevBuf* b : {&h->d_prog, &h->d_coef, &h->d_aux, &h->d_scratch, &h->d_small, &h->d_tmp, &h->d_tmp2, &h->d_stage})
     if (b->p) cudaFree(b->p);
   for (PinBuf* b : {&h->h_stage, &h->h_stage2})
     if (b->p) cudaFreeHost(b->p);
@@ -625,8 +631,9 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
           const Launch& L = h->prog.launches[si];
           cudaEvent_t t = tstart(h);
           CUDA_TRY(h, launch_section(h->dbl, h->sv, (const int*)h->d_prog.p + L.int_off, L.int_count,
-                                     (const char*)h->d_coef.p + L.coef_off * h->amp, L.coef_count, L.T, L.n_out,
-                                     L.n_phases, L.flags, h->st));
+                                     (const char*)h->d_coef.p + L.coef_off * h->amp, L.coef_count,
+                                     (const char*)h->d_aux.p + L.aux_off * h->amp, L.T, L.n_out, L.n_phases,
+                                     L.flags, h->st));
           const double amps = (double)(1ull << h->nL);
           tend(h, t, 0, 2.0 * amps * (double)h->amp, L.flops_per_amp * amps);
           h->stats.kernel_launches++;
@@ -991,8 +998,9 @@ extern "C" int sv_compile_circuit(const sv_gate* gates, size_t n_gates, int n, i
                                   sv_precision prec, const int32_t* pi0, const int32_t* sigma0, uint32_t flags,
                                   int64_t** steps_out, size_t* n_steps,
                                   int32_t** ints_out, size_t* n_ints, double** coefs_out, size_t* n_coefs,
-                                  int32_t* pi_final, int32_t* sigma_final) {
-  if (!steps_out || !n_steps || !ints_out || !n_ints || !coefs_out || !n_coefs || (n_gates && !gates))
+                                  double** aux_out, size_t* n_aux, int32_t* pi_final, int32_t* sigma_final) {
+  if (!steps_out || !n_steps || !ints_out || !n_ints || !coefs_out || !n_coefs || !aux_out || !n_aux ||
+      (n_gates && !gates))
     return fail(nullptr, SV_EINVAL, "null argument");
   if (n < 1 || n > 63 || world_log2 < 0 || world_log2 >= n) return fail(nullptr, SV_EINVAL, "bad n / world");
   const int nL = n - world_log2;
@@ -1010,10 +1018,10 @@ extern "C" int sv_compile_circuit(const sv_gate* gates, size_t n_gates, int n, i
   Program prog;
   std::vector<int64_t> rec;
   auto put = [&](std::initializer_list<int64_t> v) {
-    int64_t r[8] = {0};
+    int64_t r[12] = {0};
     int i = 0;
     for (int64_t x : v) r[i++] = x;
-    rec.insert(rec.end(), r, r + 8);
+    rec.insert(rec.end(), r, r + 12);
   };
   for (size_t i = 0; i < steps.size(); i++) {
     const Step& st = steps[i];
@@ -1031,7 +1039,7 @@ extern "C" int sv_compile_circuit(const sv_gate* gates, size_t n_gates, int n, i
       for (size_t k = first; k < prog.launches.size(); k++) {
         const Launch& L = prog.launches[k];
         put({1, (int64_t)L.int_off, (int64_t)L.int_count, (int64_t)L.coef_off, (int64_t)L.coef_count, L.T, L.n_out,
-             L.flags});
+             L.flags, (int64_t)L.aux_off, (int64_t)L.aux_count});
       }
     }
   }
@@ -1041,11 +1049,13 @@ extern "C" int sv_compile_circuit(const sv_gate* gates, size_t n_gates, int n, i
     return p;
   };
   *steps_out = (int64_t*)dup(rec.data(), rec.size() * sizeof(int64_t));
-  *n_steps = rec.size() / 8;
+  *n_steps = rec.size() / 12;
   *ints_out = (int32_t*)dup(prog.ints.data(), prog.ints.size() * sizeof(int));
   *n_ints = prog.ints.size();
   *coefs_out = (double*)dup(prog.coefs.data(), prog.coefs.size() * sizeof(double));
   *n_coefs = prog.coefs.size() / 2;
+  *aux_out = (double*)dup(prog.aux.data(), prog.aux.size() * sizeof(double));
+  *n_aux = prog.aux.size() / 2;
   for (int q = 0; q < n; q++) {
     if (pi_final) pi_final[q] = pi[q];
     if (sigma_final) sigma_final[q] = sigma[q];

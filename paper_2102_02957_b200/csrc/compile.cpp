@@ -9,9 +9,11 @@
 // Diagonal fusion: inside a phase every diagonal gate is sunk as late as its tile positions
 // allow (past non-diagonal gates on other positions), and each run of diagonal gates becomes one
 // DIAGSET: the product of all its factors, decomposed into terms c^[S subset k][J subset tid]
-// [O subset tile] over register slots S, thread bits J and out-of-tile bits O.  Terms without
-// thread bits are evaluated once per warp (lanes 0..15, one register subset S each), so a QFT
-// section's hundreds of controlled phases cost a few complex multiplies per amplitude.
+// [O subset tile] over register slots S, thread bits J and out-of-tile bits O.  Terms on two
+// slots are constants (a 16-entry table); the rest belong to the empty set or one slot and are
+// tabulated per thread index on the host (constant and thread-bit terms) or evaluated once per
+// warp (out-of-tile terms), so a QFT section's hundreds of controlled phases cost a few complex
+// multiplies per amplitude.
 #include <algorithm>
 #include <cmath>
 #include <complex>
@@ -254,21 +256,22 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
       std::vector<int> keep, go;
       for (int gi : sink) ((all || (pg[gi].pmask & mask)) ? go : keep).push_back(gi);
       sink.swap(keep);
-      if (go.empty()) return;
-      Item it;
-      if (go.size() == 1) {
-        const PGate& p = pg[go[0]];
-        // a lone diagonal whose operands are register slots / constants stays a plain op
-        auto slotish = [&](int x) { return x >= 0 || po.slot_of[pos_of[kDiagLocal - x]] >= 0; };
-        auto in_tile = [&](int x) { return x >= 0 || pos_of[kDiagLocal - x] >= 0; };
+      // diagonals whose operands are all register slots / constants stay plain ops (a few
+      // complex multiplies on the registers); the rest of the run becomes one DIAGSET
+      auto in_tile = [&](int x) { return x >= 0 || pos_of[kDiagLocal - x] >= 0; };
+      auto slotish = [&](int x) { return x >= 0 || po.slot_of[pos_of[kDiagLocal - x]] >= 0; };
+      Item set;
+      for (int gi : go) {
+        const PGate& p = pg[gi];
         if (in_tile(p.a) && in_tile(p.b) && slotish(p.a) && slotish(p.b)) {
-          it.gate = go[0];
+          Item it;
+          it.gate = gi;
           po.items.push_back(it);
-          return;
+        } else {
+          set.group.push_back(gi);
         }
       }
-      it.group = go;
-      po.items.push_back(it);
+      if (!set.group.empty()) po.items.push_back(set);
     };
     for (int gi : ph.ops) {
       if (pg[gi].diag) {
@@ -281,6 +284,16 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
       po.items.push_back(it);
     }
     flush(0, true);
+    if (const char* dbg = std::getenv("SV_DEBUG_PLAN"); dbg && dbg[0] == '2') {
+      std::fprintf(stderr, "[sv]   phase %zu R=%d,%d,%d,%d:", pi, ph.R[0], ph.R[1], ph.R[2], ph.R[3]);
+      for (const Item& it : po.items) {
+        if (it.group.empty())
+          std::fprintf(stderr, " op%d", pg[it.gate].type);
+        else
+          std::fprintf(stderr, " SET[%zu]", it.group.size());
+      }
+      std::fprintf(stderr, "\n");
+    }
   }
 
   // ---- sizes
@@ -293,6 +306,7 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
   // ---- emit
   const size_t base = prog.ints.size();
   const size_t cbase = prog.coefs.size() / 2;
+  const size_t abase = prog.aux.size() / 2;
   const size_t ops_end = header_ints + phase_ints * phases.size() + op_ints * n_items;
   prog.ints.resize(base + ops_end, 0);
   auto H = [&]() { return reinterpret_cast<SvSecHeader*>(prog.ints.data() + base); };
@@ -430,55 +444,75 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
           }
           n_diag_fused++;
         }
-        // descriptor: [mask][cta offsets 17][thread offsets 17] then terms
-        std::vector<cd> cst(16, cd(1.0, 0.0));
-        std::vector<std::vector<std::pair<uint64_t, cd>>> cta(16);
-        std::vector<std::vector<std::tuple<uint32_t, uint64_t, cd>>> thr(16);
+        // Split the terms by register subset: |S| <= 1 (the empty set and the four slots, index
+        // si = 0..4) keep per-CTA / per-thread structure; |S| >= 2 terms come from both operands
+        // on register slots, so they are constants and fold into a 16-entry table LAMBDA[k].
+        const int nthr = 1 << (T - r);
+        std::vector<cd> lam(16, cd(1.0, 0.0));
+        bool has_lam = false;
+        std::vector<std::vector<cd>> tab(5, std::vector<cd>(nthr, cd(1.0, 0.0)));
+        std::vector<std::vector<std::pair<uint64_t, cd>>> cta(5);
+        std::vector<std::tuple<int, uint32_t, uint64_t, cd>> mixed;
         for (const auto& kv : terms) {
           const TermKey& k = kv.first;
-          if (k.J == 0 && k.O == 0)
-            cst[k.S] *= kv.second;
-          else if (k.J == 0)
-            cta[k.S].push_back({k.O, kv.second});
-          else
-            thr[k.S].push_back(std::make_tuple(k.J, k.O, kv.second));
+          const int pc = __builtin_popcount(k.S);
+          if (pc >= 2) {
+            if (k.J || k.O) return Status::err(SV_EMALFORMED, "internal: diagonal term on >2 operands");
+            for (int kk = 0; kk < 16; kk++)
+              if ((kk & k.S) == k.S) lam[kk] *= kv.second;
+            has_lam = true;
+            continue;
+          }
+          const int si = pc == 0 ? 0 : 1 + __builtin_ctz(k.S);
+          if (k.O == 0) {  // constant or thread-bit term: tabulated per thread index
+            for (int tid = 0; tid < nthr; tid++)
+              if (((uint32_t)tid & k.J) == k.J) tab[si][tid] *= kv.second;
+          } else if (k.J == 0) {
+            cta[si].push_back({k.O, kv.second});
+          } else {
+            mixed.push_back(std::make_tuple(si, k.J, k.O, kv.second));
+          }
         }
-        int mask = 0;
-        for (int S = 0; S < 16; S++)
-          if (cst[S] != cd(1.0, 0.0) || !cta[S].empty() || !thr[S].empty()) mask |= 1 << S;
         const size_t desc = prog.ints.size() - base;
-        prog.ints.push_back(mask);
-        const size_t cta_off = prog.ints.size();
-        prog.ints.resize(prog.ints.size() + 34, 0);
-        const int c0 = (int)(prog.coefs.size() / 2 - cbase);
-        for (int S = 0; S < 16; S++) push_c(cst[S]);
-        // cta terms: (O_lo, O_hi, coef)
-        for (int S = 0; S < 16; S++) {
-          prog.ints[cta_off + S] = (int)(prog.ints.size() - base);
-          for (const auto& tm : cta[S]) {
+        const int aux0 = (int)(prog.aux.size() / 2 - abase);
+        for (int si = 0; si < 5; si++)
+          for (int tid = 0; tid < nthr; tid++) {
+            prog.aux.push_back(tab[si][tid].real());
+            prog.aux.push_back(tab[si][tid].imag());
+          }
+        prog.ints.push_back(has_lam ? 1 : 0);
+        prog.ints.push_back(aux0);
+        const size_t off = prog.ints.size();
+        prog.ints.resize(prog.ints.size() + 8, 0);
+        for (int si = 0; si < 5; si++) {  // per-CTA terms: (out-bit mask lo, hi, coef)
+          prog.ints[off + si] = (int)(prog.ints.size() - base);
+          for (const auto& tm : cta[si]) {
             prog.ints.push_back((int)(tm.first & 0xffffffffu));
             prog.ints.push_back((int)(tm.first >> 32));
             prog.ints.push_back(push_c(tm.second));
           }
         }
-        prog.ints[cta_off + 16] = (int)(prog.ints.size() - base);
-        for (int S = 0; S < 16; S++) {
-          prog.ints[cta_off + 17 + S] = (int)(prog.ints.size() - base);
-          for (const auto& tm : thr[S]) {
-            prog.ints.push_back((int)std::get<0>(tm));
-            prog.ints.push_back((int)(std::get<1>(tm) & 0xffffffffu));
-            prog.ints.push_back((int)(std::get<1>(tm) >> 32));
-            prog.ints.push_back(push_c(std::get<2>(tm)));
-          }
+        prog.ints[off + 5] = (int)(prog.ints.size() - base);
+        prog.ints[off + 6] = (int)(prog.ints.size() - base);  // mixed terms: (si, J, O lo, O hi, coef)
+        for (const auto& tm : mixed) {
+          prog.ints.push_back(std::get<0>(tm));
+          prog.ints.push_back((int)std::get<1>(tm));
+          prog.ints.push_back((int)(std::get<2>(tm) & 0xffffffffu));
+          prog.ints.push_back((int)(std::get<2>(tm) >> 32));
+          prog.ints.push_back(push_c(std::get<3>(tm)));
         }
-        prog.ints[cta_off + 33] = (int)(prog.ints.size() - base);
+        prog.ints[off + 7] = (int)(prog.ints.size() - base);
+        int lam0 = 0;
+        if (has_lam) {
+          lam0 = (int)(prog.coefs.size() / 2 - cbase);
+          for (int kk = 0; kk < 16; kk++) push_c(lam[kk]);
+        }
         op.type = SV_OP_DIAGSET;
         op.a = (int)desc;
-        op.coef = c0;
-        // flops: per active subset S one complex multiply on the 2^(4-|S|)/16 of the registers it
-        // covers, plus one complex multiply per thread term per thread (16 amplitudes)
-        for (int S = 0; S < 16; S++)
-          if ((mask >> S) & 1) fpa += 6.0 * (1 << (4 - __builtin_popcount(S))) / 16.0 + 6.0 * thr[S].size() / 16.0;
+        op.coef = lam0;
+        // flops per amplitude: build the 16 register factors from the five subset factors (~16
+        // complex multiplies per thread), apply them (16), LAMBDA (16), per-thread mixed terms
+        fpa += (6.0 * (32 + (has_lam ? 16 : 0) + mixed.size() + 5)) / 16.0;
         n_diagset++;
       } else {  // ---------------------------------------------------------------- single op
         const PGate& p = pg[it.gate];
@@ -566,6 +600,7 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
   if (total_ints > SV_CONST_INTS || ncoef > coef_cap) {
     prog.ints.resize(base);
     prog.coefs.resize(cbase * 2);
+    prog.aux.resize(abase * 2);
     return Status::err(kTooBig, "section program exceeds the constant budget");
   }
 
@@ -582,6 +617,8 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
   L.int_count = total_ints;
   L.coef_off = cbase;
   L.coef_count = ncoef;
+  L.aux_off = abase;
+  L.aux_count = prog.aux.size() / 2 - abase;
   L.T = T;
   L.r = r;
   L.n_out = n_out;
@@ -596,11 +633,12 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
 
 Status compile_section_split(const std::vector<sv_gate>& gates, int nL, int rank, int world_log2, int T_default,
                              int swizzle_bits, const std::vector<std::pair<int, int>>& store_swaps, Program& prog) {
-  const size_t ni = prog.ints.size(), nc = prog.coefs.size();
+  const size_t ni = prog.ints.size(), nc = prog.coefs.size(), na = prog.aux.size();
   Status s = compile_section(gates, nL, rank, world_log2, T_default, swizzle_bits, store_swaps, prog);
   if (s.code != kTooBig) return s;
   prog.ints.resize(ni);
   prog.coefs.resize(nc);
+  prog.aux.resize(na);
   if (gates.size() < 2) return Status::err(SV_ECAPACITY, "a single gate exceeds the constant budget");
   // Consecutive halves of the in-order gate list: each half is a valid section on its own.
   const size_t h = gates.size() / 2;

@@ -15,17 +15,21 @@ struct Launch {
   size_t int_count;   // ints of header + phases + ops
   size_t coef_off;    // first coefficient (complex index) of the section in Program::coefs
   size_t coef_count;  // coefficients of the section
+  size_t aux_off;     // first complex of the section's DIAGSET factor tables in Program::aux
+  size_t aux_count;
   int T, r, n_out, n_phases, n_ops, flags;
   double flops_per_amp;  // algorithmic flops per amplitude of the section (DESIGN "Roofline")
 };
 
 struct Program {
   std::vector<int> ints;       // headers, phases, ops of every section, concatenated
-  std::vector<double> coefs;   // complex coefficients (re, im) in fp64
+  std::vector<double> coefs;   // complex coefficients (re, im) in fp64 (-> __constant__)
+  std::vector<double> aux;     // DIAGSET per-thread factor tables (re, im) in fp64 (-> global)
   std::vector<Launch> launches;
   void clear() {
     ints.clear();
     coefs.clear();
+    aux.clear();
     launches.clear();
   }
 };

@@ -31,14 +31,14 @@
 #define SV_OP_PERM2 4   // a = slot0, b = slot1, extra = packed permutation out[s] = in[(extra >> 2s) & 3]
 #define SV_OP_DIAG 5    // a = code0, b = code1, coef -> 4 complex d[s], s = bit(code0) + 2 bit(code1)
 #define SV_OP_DIAG_CP 6 // like DIAG with d0 = d1 = d2 = 1: only s == 3 is multiplied (coef -> d3)
-#define SV_OP_DIAGSET 7 // fused run of diagonal gates: a = descriptor offset, coef -> 16 constant
-                        // factors per register subset S; descriptor (ints, from the header):
-                        //   [0] mask of non-trivial subsets S (16 bits)
-                        //   [1+S] / [17]   begin of S's per-CTA terms / end   (3 ints each:
-                        //                  out-bit mask lo, hi, coef): apply if tile has all bits
-                        //   [18+S] / [34]  begin of S's per-thread terms / end (4 ints each:
-                        //                  thread-bit mask, out-bit mask lo, hi, coef)
-                        // register k is multiplied by the factor of every S with S subset of k
+#define SV_OP_DIAGSET 7 // fused run of diagonal gates: a = descriptor offset (ints from the header),
+                        // coef -> LAMBDA[16] (if flag bit 0); descriptor:
+                        //   [0] flags (bit 0: LAMBDA present)   [1] aux offset of 5 thread tables
+                        //   [2+i] / [7] per-CTA terms of subset i (i = 0: empty set, 1+s: slot s),
+                        //               3 ints each: out-bit mask lo, hi, coef (apply if set)
+                        //   [8] / [9]   per-thread mixed terms, 5 ints: i, thread mask, out lo, hi, coef
+                        // register k is multiplied by LAMBDA[k] * F_0 * prod_{s in k} F_{1+s},
+                        // F_i = (per-CTA terms) * table_i[tid] * (matching mixed terms)
 
 // DIAG bit codes (per phase)
 #define SV_CODE_SLOT(s) (s)           // register slot s (0..3): bit = (k >> s) & 1

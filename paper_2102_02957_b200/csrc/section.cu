@@ -170,62 +170,66 @@ __device__ __forceinline__ V shfl_c(V x, int src) {
 
 __device__ __forceinline__ uint64_t mask64(int lo, int hi) { return (uint64_t)(uint32_t)lo | ((uint64_t)(uint32_t)hi << 32); }
 
-// Fused diagonal run (SV_OP_DIAGSET, program.h): per-CTA terms are evaluated by lanes 0..15 of
-// every warp (lane = register subset S) and broadcast with shuffles; per-thread terms by each
-// thread; then each non-trivial subset scales the registers that contain it.
+// Fused diagonal run (SV_OP_DIAGSET, program.h).  The five subset factors F_i (empty set and the
+// four register slots) are: per-CTA out-bit terms (lanes 0..4 of each warp, broadcast by shuffle)
+// x the host-built per-thread table x rare mixed terms; the 16 register factors are products of
+// them built as A[k & 3] * B[k >> 2] with no branches, so v stays in place.
 template <typename V>
-__device__ __forceinline__ void diagset(V (&v)[16], int desc, int cb, int tid, uint64_t tile_off) {
-  const int mask = c_prog[desc];
+__device__ __forceinline__ V cta_factor(int b, int e, uint64_t tile_off) {
+  V f = cone<V>();
+  for (int t = b; t < e; t += 3) {
+    const uint64_t O = mask64(c_prog[t], c_prog[t + 1]);
+    const V c = cc<V>(c_prog[t + 2]);
+    if ((tile_off & O) == O) f = cmul(f, c);
+  }
+  return f;
+}
+
+template <typename V>
+__device__ __forceinline__ void diagset(V (&v)[16], int desc, int cb, int tid, uint64_t tile_off,
+                                        const V* __restrict__ aux) {
+  const int flags = c_prog[desc];
+  const V* tab = aux + c_prog[desc + 1];
+  const int nthr = blockDim.x;
   const int lane = tid & 31;
-  const bool full_warp = blockDim.x >= 32;  // tiny tiles (T < 9) have fewer than 32 threads
-  V mine = cone<V>();
-  if (full_warp && lane < 16 && ((mask >> lane) & 1)) {
-    const int e = c_prog[desc + 2 + lane];
-    for (int t = c_prog[desc + 1 + lane]; t < e; t += 3) {
-      const uint64_t O = mask64(c_prog[t], c_prog[t + 1]);
-      const V c = cc<V>(c_prog[t + 2]);
-      if ((tile_off & O) == O) mine = cmul(mine, c);
+  V F[5];
+  if (blockDim.x >= 32) {
+    V mine = cone<V>();
+    if (lane < 5) mine = cta_factor<V>(c_prog[desc + 2 + lane], c_prog[desc + 3 + lane], tile_off);
+#pragma unroll
+    for (int i = 0; i < 5; i++) F[i] = cmul(shfl_c(mine, i), tab[i * nthr + tid]);
+  } else {  // tiny tiles (T < 9): fewer than 32 threads, every thread walks the terms itself
+#pragma unroll
+    for (int i = 0; i < 5; i++)
+      F[i] = cmul(cta_factor<V>(c_prog[desc + 2 + i], c_prog[desc + 3 + i], tile_off), tab[i * nthr + tid]);
+  }
+  const int me = c_prog[desc + 9];
+  for (int t = c_prog[desc + 8]; t < me; t += 5) {
+    const int si = c_prog[t], J = c_prog[t + 1];
+    const uint64_t O = mask64(c_prog[t + 2], c_prog[t + 3]);
+    const V c = cc<V>(c_prog[t + 4]);
+    if ((tid & J) == J && (tile_off & O) == O) {
+#pragma unroll
+      for (int i = 0; i < 5; i++)
+        if (si == i) F[i] = cmul(F[i], c);
     }
   }
+  // A[lo] = F_0 * prod_{s in lo} F_{1+s} (slots 0, 1); B[hi] = prod_{s in hi} F_{3+s} (slots 2, 3)
+  const V A0 = F[0], A1 = cmul(F[0], F[1]), A2 = cmul(F[0], F[2]), A3 = cmul(A1, F[2]);
+  const V B1 = F[3], B2 = F[4], B3 = cmul(F[3], F[4]);
+  if (flags & 1) {
 #pragma unroll
-  for (int S = 0; S < 16; S++) {
-    if (!((mask >> S) & 1)) continue;
-    V g;
-    if (full_warp) {
-      g = cmul(shfl_c(mine, S), cc<V>(cb + S));
-    } else {  // every thread walks the per-CTA terms itself
-      g = cc<V>(cb + S);
-      const int e0 = c_prog[desc + 2 + S];
-      for (int t = c_prog[desc + 1 + S]; t < e0; t += 3) {
-        const uint64_t O = mask64(c_prog[t], c_prog[t + 1]);
-        const V c = cc<V>(c_prog[t + 2]);
-        if ((tile_off & O) == O) g = cmul(g, c);
-      }
+    for (int k = 0; k < 16; k++) {
+      const V a = (k & 3) == 0 ? A0 : (k & 3) == 1 ? A1 : (k & 3) == 2 ? A2 : A3;
+      const V f = (k >> 2) == 0 ? a : cmul(a, (k >> 2) == 1 ? B1 : (k >> 2) == 2 ? B2 : B3);
+      v[k] = cmul(v[k], cmul(f, cc<V>(cb + k)));
     }
-    const int e = c_prog[desc + 19 + S];
-    for (int t = c_prog[desc + 18 + S]; t < e; t += 4) {
-      const int J = c_prog[t];
-      const uint64_t O = mask64(c_prog[t + 1], c_prog[t + 2]);
-      const V c = cc<V>(c_prog[t + 3]);  // uniform load, outside the per-thread condition
-      if ((tid & J) == J && (tile_off & O) == O) g = cmul(g, c);
-    }
-    switch (S) {
-      case 0: scale_subset<0>(v, g); break;
-      case 1: scale_subset<1>(v, g); break;
-      case 2: scale_subset<2>(v, g); break;
-      case 3: scale_subset<3>(v, g); break;
-      case 4: scale_subset<4>(v, g); break;
-      case 5: scale_subset<5>(v, g); break;
-      case 6: scale_subset<6>(v, g); break;
-      case 7: scale_subset<7>(v, g); break;
-      case 8: scale_subset<8>(v, g); break;
-      case 9: scale_subset<9>(v, g); break;
-      case 10: scale_subset<10>(v, g); break;
-      case 11: scale_subset<11>(v, g); break;
-      case 12: scale_subset<12>(v, g); break;
-      case 13: scale_subset<13>(v, g); break;
-      case 14: scale_subset<14>(v, g); break;
-      default: scale_subset<15>(v, g); break;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+      const V a = (k & 3) == 0 ? A0 : (k & 3) == 1 ? A1 : (k & 3) == 2 ? A2 : A3;
+      const V f = (k >> 2) == 0 ? a : cmul(a, (k >> 2) == 1 ? B1 : (k >> 2) == 2 ? B2 : B3);
+      v[k] = cmul(v[k], f);
     }
   }
 }
@@ -238,7 +242,7 @@ __device__ __forceinline__ int code_val(int code, int tid, uint64_t tile_off) {
 }
 
 template <typename V, typename R>
-__device__ __forceinline__ void run_op(V (&v)[16], int oi, int tid, uint64_t tile_off) {
+__device__ __forceinline__ void run_op(V (&v)[16], int oi, int tid, uint64_t tile_off, const V* __restrict__ aux) {
   const int type = c_prog[oi], a = c_prog[oi + 1], b = c_prog[oi + 2], cb = c_prog[oi + 3];
   switch (type) {
     case SV_OP_U2: {
@@ -303,7 +307,7 @@ __device__ __forceinline__ void run_op(V (&v)[16], int oi, int tid, uint64_t til
       break;
     }
     case SV_OP_DIAGSET:
-      diagset(v, a, cb, tid, tile_off);
+      diagset(v, a, cb, tid, tile_off, aux);
       break;
     default:
       break;
@@ -379,7 +383,7 @@ __device__ __forceinline__ void hbm_store(const V (&v)[16], V* __restrict__ dst,
 }
 
 template <typename V, int G, int NT, int MINB, bool FIRST, bool LAST>
-__global__ void __launch_bounds__(NT, MINB) k_section(V* __restrict__ sv) {
+__global__ void __launch_bounds__(NT, MINB) k_section(V* __restrict__ sv, const V* __restrict__ aux) {
   using R = decltype(V().x);
   constexpr int RB = SV_R_BITS;  // the host guarantees T >= RB, so every phase has RB register slots
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -422,7 +426,7 @@ __global__ void __launch_bounds__(NT, MINB) k_section(V* __restrict__ sv) {
 #undef SV_LDS
     }
     const int ob = c_prog[P + kP_OPB], oc = c_prog[P + kP_OPC];
-    for (int o = 0; o < oc; o++) run_op<V, R>(v, opoff + (ob + o) * kOpInts, tid, tile_off);
+    for (int o = 0; o < oc; o++) run_op<V, R>(v, opoff + (ob + o) * kOpInts, tid, tile_off, aux);
     if (direct_out) {  // the last phase writes HBM directly (store memory bits, same mapping)
       hbm_store(v, sv + hbm_base(kH_DOUT, nt_log, tid, tile_off), kH_DOUT);
     } else {
@@ -446,7 +450,7 @@ __global__ void __launch_bounds__(NT, MINB) k_section(V* __restrict__ sv) {
 }
 
 template <typename V, int G, int NT, int MINB, bool FIRST, bool LAST>
-cudaError_t launch_v(V* sv, int T, int n_out, size_t smem, cudaStream_t st) {
+cudaError_t launch_v(V* sv, const V* aux, int T, int n_out, size_t smem, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(k_section<V, G, NT, MINB, FIRST, LAST>,
@@ -455,7 +459,7 @@ cudaError_t launch_v(V* sv, int T, int n_out, size_t smem, cudaStream_t st) {
     attr_set = true;
   }
   const int threads = 1 << (T - SV_R_BITS);
-  k_section<V, G, NT, MINB, FIRST, LAST><<<(unsigned)(1ull << n_out), threads, smem, st>>>(sv);
+  k_section<V, G, NT, MINB, FIRST, LAST><<<(unsigned)(1ull << n_out), threads, smem, st>>>(sv, aux);
   return cudaGetLastError();
 }
 
@@ -463,17 +467,18 @@ cudaError_t launch_v(V* sv, int T, int n_out, size_t smem, cudaStream_t st) {
 // the all-smem variant: ptxas keeps the coefficient loads on the uniform datapath in the other
 // three shapes only (checked by tests/test_sass.py).
 template <typename V, int G, int NT, int MINB>
-cudaError_t launch_t(V* sv, int T, int n_out, int flags, size_t smem, cudaStream_t st) {
+cudaError_t launch_t(V* sv, const V* aux, int T, int n_out, int flags, size_t smem, cudaStream_t st) {
   const bool f = flags & SV_FLAG_FIRST_DIRECT, l = flags & SV_FLAG_LAST_DIRECT;
-  if (f && l) return launch_v<V, G, NT, MINB, true, true>(sv, T, n_out, smem, st);
-  if (l) return launch_v<V, G, NT, MINB, false, true>(sv, T, n_out, smem, st);
-  return launch_v<V, G, NT, MINB, false, false>(sv, T, n_out, smem, st);
+  if (f && l) return launch_v<V, G, NT, MINB, true, true>(sv, aux, T, n_out, smem, st);
+  if (l) return launch_v<V, G, NT, MINB, false, true>(sv, aux, T, n_out, smem, st);
+  return launch_v<V, G, NT, MINB, false, false>(sv, aux, T, n_out, smem, st);
 }
 
 }  // namespace
 
 cudaError_t launch_section(bool dbl, void* sv, const int* prog_dev, size_t int_count, const void* coef_dev,
-                           size_t coef_count, int T, int n_out, int n_phases, int flags, cudaStream_t st) {
+                           size_t coef_count, const void* aux_dev, int T, int n_out, int n_phases, int flags,
+                           cudaStream_t st) {
   if (int_count > SV_CONST_INTS) return cudaErrorInvalidValue;
   cudaError_t e = cudaMemcpyToSymbolAsync(c_prog, prog_dev, int_count * sizeof(int), 0, cudaMemcpyDeviceToDevice, st);
   if (e != cudaSuccess) return e;
@@ -491,13 +496,13 @@ cudaError_t launch_section(bool dbl, void* sv, const int* prog_dev, size_t int_c
   const bool no_smem = n_phases == 1 && (flags & SV_FLAG_FIRST_DIRECT) && (flags & SV_FLAG_LAST_DIRECT);
   if (dbl) {
     const size_t smem = no_smem ? 0 : sizeof(double2) << T;
-    if (T <= 12) return launch_t<double2, 3, 256, 2>((double2*)sv, T, n_out, flags, smem, st);
-    if (T == 13) return launch_t<double2, 3, 512, 1>((double2*)sv, T, n_out, flags, smem, st);
+    if (T <= 12) return launch_t<double2, 3, 256, 2>((double2*)sv, (const double2*)aux_dev, T, n_out, flags, smem, st);
+    if (T == 13) return launch_t<double2, 3, 512, 1>((double2*)sv, (const double2*)aux_dev, T, n_out, flags, smem, st);
     return cudaErrorInvalidValue;
   }
   const size_t smem = no_smem ? 0 : sizeof(float2) << T;
-  if (T <= 12) return launch_t<float2, 4, 256, 2>((float2*)sv, T, n_out, flags, smem, st);
-  if (T == 13) return launch_t<float2, 4, 512, 1>((float2*)sv, T, n_out, flags, smem, st);
+  if (T <= 12) return launch_t<float2, 4, 256, 2>((float2*)sv, (const float2*)aux_dev, T, n_out, flags, smem, st);
+  if (T == 13) return launch_t<float2, 4, 512, 1>((float2*)sv, (const float2*)aux_dev, T, n_out, flags, smem, st);
   return cudaErrorInvalidValue;
 }
 

@@ -24,7 +24,7 @@ def _bits(x, b):
     return (x >> b) & 1
 
 
-def run_section(mem, prog, coefs, n_out, T, flags):
+def run_section(mem, prog, coefs, n_out, T, flags, aux=None):
     nt = 1 << (T - 4)
     tids = np.arange(nt)
     first = bool(flags & 1) and bool(flags & 2)  # launch_t runs (first direct, last smem) as smem-only
@@ -69,7 +69,7 @@ def run_section(mem, prog, coefs, n_out, T, flags):
                 v = sm[x].copy()
             ob, oc = prog[P + P_OPB], prog[P + P_OPC]
             for o in range(oc):
-                apply_op(v, prog, coefs, opoff + (ob + o) * OP_INTS, tids, tile_off)
+                apply_op(v, prog, coefs, opoff + (ob + o) * OP_INTS, tids, tile_off, aux)
             if last and ph == nph - 1:
                 stored = hbm(H_DOUT, tile_off)
                 mem[stored] = v
@@ -93,7 +93,7 @@ def _bitval(code, k, tids, tile_off):
     return np.full((len(tids), 16), code - 200)
 
 
-def apply_op(v, prog, coefs, oi, tids, tile_off):
+def apply_op(v, prog, coefs, oi, tids, tile_off, aux=None):
     typ, a, b, cb, extra = (int(x) for x in prog[oi:oi + 5])
     if typ == U2:
         m = coefs[cb:cb + 16].reshape(4, 4)
@@ -134,23 +134,30 @@ def apply_op(v, prog, coefs, oi, tids, tile_off):
         v[both] *= coefs[cb]
     elif typ == DIAGSET:
         d = a
-        mask = int(prog[d])
-        for S in range(16):
-            if not (mask >> S) & 1:
-                continue
-            g = np.full(len(tids), coefs[cb + S], dtype=np.complex128)
-            for t in range(int(prog[d + 1 + S]), int(prog[d + 2 + S]), 3):
+        flags, aux0 = int(prog[d]), int(prog[d + 1])
+        nthr = len(tids)
+        F = []
+        for i in range(5):
+            f = 1.0 + 0j
+            for t in range(int(prog[d + 2 + i]), int(prog[d + 3 + i]), 3):
                 O = (int(prog[t]) & 0xffffffff) | ((int(prog[t + 1]) & 0xffffffff) << 32)
                 if tile_off & O == O:
-                    g *= coefs[int(prog[t + 2])]
-            for t in range(int(prog[d + 18 + S]), int(prog[d + 19 + S]), 4):
-                J = int(prog[t])
-                O = (int(prog[t + 1]) & 0xffffffff) | ((int(prog[t + 2]) & 0xffffffff) << 32)
-                if tile_off & O == O:
-                    sel = (tids & J) == J
-                    g[sel] *= coefs[int(prog[t + 3])]
-            ks = [k for k in range(16) if k & S == S]
-            v[:, ks] *= g[:, None]
+                    f *= coefs[int(prog[t + 2])]
+            F.append(f * aux[aux0 + i * nthr + tids])
+        for t in range(int(prog[d + 8]), int(prog[d + 9]), 5):
+            si, J = int(prog[t]), int(prog[t + 1])
+            O = (int(prog[t + 2]) & 0xffffffff) | ((int(prog[t + 3]) & 0xffffffff) << 32)
+            if tile_off & O == O:
+                sel = (tids & J) == J
+                F[si][sel] *= coefs[int(prog[t + 4])]
+        for k in range(16):
+            f = F[0].copy()
+            for s_ in range(4):
+                if (k >> s_) & 1:
+                    f *= F[1 + s_]
+            if flags & 1:
+                f *= coefs[cb + k]
+            v[:, k] *= f
     else:
         raise AssertionError(f"unknown op type {typ}")
 
@@ -163,13 +170,13 @@ def swap_bits(mem, m1, m2):
     mem[:] = mem[y]
 
 
-def run(steps, prog, coefs, mem, gates=None, gate_fn=None):
+def run(steps, prog, coefs, aux, mem, gate_fn=None):
     """Execute every step on the full memory-ordered state `mem` (in place)."""
     for st in steps:
         kind = int(st[0])
         if kind == 1:
-            off, cnt, coff, ccnt, T, n_out, flags = (int(x) for x in st[1:8])
-            run_section(mem, prog[off:off + cnt], coefs[coff:coff + ccnt], n_out, T, flags)
+            off, cnt, coff, ccnt, T, n_out, flags, aoff, acnt = (int(x) for x in st[1:10])
+            run_section(mem, prog[off:off + cnt], coefs[coff:coff + ccnt], n_out, T, flags, aux[aoff:aoff + acnt])
         elif kind in (0, 3):
             swap_bits(mem, int(st[1]), int(st[2]))
         elif kind == 2:

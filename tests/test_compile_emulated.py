@@ -19,7 +19,7 @@ def built():
 
 def emulate(recs, n, c, g=0, precision="fp64", seed=0, flags=0, pi0=None, sigma0=None, psi=None):
     """Run the compiled programs on a random (or given) logical state; returns (steps, pi, sigma, logical out)."""
-    steps, ints, coefs, pi, sigma = sv.compile_circuit(recs, n, c, g, 0, precision, flags, pi0, sigma0)
+    steps, ints, coefs, aux, pi, sigma = sv.compile_circuit(recs, n, c, g, 0, precision, flags, pi0, sigma0)
     if psi is None:
         rng = np.random.default_rng(seed)
         psi = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
@@ -33,7 +33,7 @@ def emulate(recs, n, c, g=0, precision="fp64", seed=0, flags=0, pi0=None, sigma0
         rec["q0"], rec["q1"] = int(st[2]), int(st[3])
         m[:] = O.apply_circuit(C.records([rec]), n, m)
 
-    run(steps, ints, coefs, mem, gate_fn=gate_fn)
+    run(steps, ints, coefs, aux, mem, gate_fn=gate_fn)
     got = O.unpermute(mem, [int(sigma[int(p)]) for p in pi])
     ref = O.apply_circuit(recs, n, psi)
     err = np.max(np.abs(got - ref))
