@@ -83,9 +83,7 @@ __device__ __forceinline__ void h1_slot(V (&v)[16], R s) {
 #pragma unroll
   for (int q = 0; q < 16; q++) {
     if ((q >> S) & 1) continue;
-    const V a0 = v[q], a1 = v[q | (1 << S)];
-    v[q] = cscale(cadd(a0, a1), s);
-    v[q | (1 << S)] = cscale(csub(a0, a1), s);
+    h_ip(v[q], v[q | (1 << S)], s);
   }
 }
 
@@ -108,29 +106,29 @@ __device__ __forceinline__ void perm_slots(V (&v)[16], int perm) {
 template <int S, typename V>
 __device__ __forceinline__ void d1_slot(V (&v)[16], V d0, V d1) {
 #pragma unroll
-  for (int k = 0; k < 16; k++) v[k] = cmul(v[k], ((k >> S) & 1) ? d1 : d0);
+  for (int k = 0; k < 16; k++) cmul_ip(v[k], ((k >> S) & 1) ? d1 : d0);
 }
 template <int S0, int S1, typename V>
 __device__ __forceinline__ void d2_slots(V (&v)[16], V d0, V d1, V d2, V d3) {
 #pragma unroll
-  for (int k = 0; k < 16; k++) v[k] = cmul(v[k], sel4(((k >> S0) & 1) | (((k >> S1) & 1) << 1), d0, d1, d2, d3));
+  for (int k = 0; k < 16; k++) cmul_ip(v[k], sel4(((k >> S0) & 1) | (((k >> S1) & 1) << 1), d0, d1, d2, d3));
 }
 template <int S0, int S1, typename V>
 __device__ __forceinline__ void cp_slots(V (&v)[16], V d3) {
 #pragma unroll
   for (int k = 0; k < 16; k++)
-    if (((k >> S0) & 1) && ((k >> S1) & 1)) v[k] = cmul(v[k], d3);
+    if (((k >> S0) & 1) && ((k >> S1) & 1)) cmul_ip(v[k], d3);
 }
 template <int S, typename V>
 __device__ __forceinline__ void cp_slot(V (&v)[16], V d3) {
 #pragma unroll
   for (int k = 0; k < 16; k++)
-    if ((k >> S) & 1) v[k] = cmul(v[k], d3);
+    if ((k >> S) & 1) cmul_ip(v[k], d3);
 }
 template <typename V>
 __device__ __forceinline__ void scale_all(V (&v)[16], V f) {
 #pragma unroll
-  for (int k = 0; k < 16; k++) v[k] = cmul(v[k], f);
+  for (int k = 0; k < 16; k++) cmul_ip(v[k], f);
 }
 
 // dispatch on a canonical slot pair a < b (6 cases) / a single slot (4 cases)
@@ -222,14 +220,14 @@ __device__ __forceinline__ void diagset(V (&v)[16], int desc, int cb, int tid, u
     for (int k = 0; k < 16; k++) {
       const V a = (k & 3) == 0 ? A0 : (k & 3) == 1 ? A1 : (k & 3) == 2 ? A2 : A3;
       const V f = (k >> 2) == 0 ? a : cmul(a, (k >> 2) == 1 ? B1 : (k >> 2) == 2 ? B2 : B3);
-      v[k] = cmul(v[k], cmul(f, cc<V>(cb + k)));
+      cmul_ip(v[k], cmul(f, cc<V>(cb + k)));
     }
   } else {
 #pragma unroll
     for (int k = 0; k < 16; k++) {
       const V a = (k & 3) == 0 ? A0 : (k & 3) == 1 ? A1 : (k & 3) == 2 ? A2 : A3;
       const V f = (k >> 2) == 0 ? a : cmul(a, (k >> 2) == 1 ? B1 : (k >> 2) == 2 ? B2 : B3);
-      v[k] = cmul(v[k], f);
+      cmul_ip(v[k], f);
     }
   }
 }
