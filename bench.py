@@ -131,13 +131,13 @@ def oracle_sample(wl, target_s: float = 15.0, max_gates: int = None):
     gates = wl["gates"]
     a = O.basis_state(n, wl["basis"])
     t0 = time.perf_counter()
-    a = O.apply_circuit(gates[:1], n, a)
+    O.apply_circuit(gates[:1], n, a, inplace=True)
     per = time.perf_counter() - t0
     m = max(1, min(len(gates) - 1, int(target_s / max(per, 1e-6))))
     if max_gates:
         m = min(m, max_gates)
     t0 = time.perf_counter()
-    O.apply_circuit(gates[1:1 + m], n, a)
+    O.apply_circuit(gates[1:1 + m], n, a, inplace=True)
     dt = time.perf_counter() - t0
     del a
     return m, dt, per
@@ -159,7 +159,7 @@ def run_reference(args):
     n, gates = wl["n"], wl["gates"]
     a = O.basis_state(n, wl["basis"])
     t0 = time.perf_counter()
-    a = O.apply_circuit(gates[:1], n, a)
+    O.apply_circuit(gates[:1], n, a, inplace=True)
     per = time.perf_counter() - t0
     m = max(1, min(len(gates), int(args.ref_step_s / max(per, 1e-6))))
     gi = 1
@@ -168,7 +168,7 @@ def run_reference(args):
         sel = [(gi + j) % len(gates) for j in range(m)]
         gi = (gi + m) % len(gates)
         t0 = time.perf_counter()
-        a = O.apply_circuit(gates[sel], n, a)
+        O.apply_circuit(gates[sel], n, a, inplace=True)
         dt = time.perf_counter() - t0
         if it >= args.warmup:
             times.append(dt)

@@ -79,10 +79,17 @@ def basis_state(n: int, k: int = 0) -> np.ndarray:
     return a
 
 
-def apply_circuit(recs: np.ndarray, n: int, psi: np.ndarray = None, basis: int = 0) -> np.ndarray:
+def apply_circuit(recs: np.ndarray, n: int, psi: np.ndarray = None, basis: int = 0, inplace: bool = False) -> np.ndarray:
     """Dense U_circuit |psi> (|basis> if psi is None).  recs: structured array of 272-byte records
-    (circuits.GATE_DTYPE layout); BEGIN/END are ignored and CHUNK_SWAP acts as SWAP."""
-    a = basis_state(n, basis) if psi is None else np.array(psi, dtype=np.complex128, copy=True)
+    (circuits.GATE_DTYPE layout); BEGIN/END are ignored and CHUNK_SWAP acts as SWAP.  inplace=True
+    updates a contiguous complex128 psi in place (for states too large to copy)."""
+    if psi is None:
+        a = basis_state(n, basis)
+    elif inplace:
+        assert psi.dtype == np.complex128 and psi.flags.c_contiguous
+        a = psi
+    else:
+        a = np.array(psi, dtype=np.complex128, copy=True)
     assert a.size == 1 << n
     recs = np.ascontiguousarray(recs)
     rc = lib().or_apply_circuit(_dp(a), n, recs.ctypes.data_as(ctypes.c_void_p), len(recs))
