@@ -633,7 +633,7 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
           CUDA_TRY(h, launch_section(h->dbl, h->sv, (const int*)h->d_prog.p + L.int_off, L.int_count,
                                      (const char*)h->d_coef.p + L.coef_off * h->amp, L.coef_count,
                                      (const char*)h->d_aux.p + L.aux_off * h->amp, L.T, L.n_out, L.n_phases,
-                                     L.flags, h->st));
+                                     L.flags, L.n_sets, h->st));
           const double amps = (double)(1ull << h->nL);
           tend(h, t, 0, 2.0 * amps * (double)h->amp, L.flops_per_amp * amps);
           h->stats.kernel_launches++;

@@ -358,6 +358,16 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
     return push(m, 1);
   };
 
+  // Hadamard scales: every H1 of the section multiplies all amplitudes by its real scale, a global
+  // scalar, so all but the last run as unscaled butterflies and the last applies the product.
+  int last_h1 = -1;
+  double h_scale = 1.0;
+  for (const auto& po : pout)
+    for (const Item& it : po.items)
+      if (it.group.empty() && pg[it.gate].type == SV_OP_H1) {
+        last_h1 = it.gate;
+        h_scale *= gates[pg[it.gate].src].m[0];
+      }
   double fpa = 0.0;  // algorithmic flops per amplitude of the section (DESIGN "Roofline")
   int op_cursor = 0;
   bool lanes_contiguous_first = false, lanes_contiguous_last = false;
@@ -480,7 +490,12 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
             prog.aux.push_back(tab[si][tid].real());
             prog.aux.push_back(tab[si][tid].imag());
           }
-        prog.ints.push_back(has_lam ? 1 : 0);
+        int set_idx = 255;  // per-CTA factors: computed once per CTA in the prologue if a slot is free
+        if (H()->n_sets < SV_MAX_SETS) {
+          set_idx = H()->n_sets++;
+          H()->set_desc[set_idx] = (int)desc;
+        }
+        prog.ints.push_back((has_lam ? 1 : 0) | (set_idx << 8));
         prog.ints.push_back(aux0);
         const size_t off = prog.ints.size();
         prog.ints.resize(prog.ints.size() + 8, 0);
@@ -560,9 +575,15 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
             break;
           case SV_OP_H1: {
             op.a = po.slot_of[p.a];
-            const double s[2] = {g.m[0], 0.0};
-            op.coef = push(s, 1);
-            fpa += 4.0;
+            if (it.gate == last_h1) {
+              const double s[2] = {h_scale, 0.0};
+              op.coef = push(s, 1);
+              fpa += 4.0;
+            } else {
+              op.type = SV_OP_H1U;
+              op.coef = 0;
+              fpa += 2.0;
+            }
             break;
           }
           case SV_OP_DIAG:
@@ -625,6 +646,7 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
   L.n_phases = (int)phases.size();
   L.n_ops = (int)n_items;
   L.flags = H()->flags;
+  L.n_sets = H()->n_sets;
   prog.launches.push_back(L);
   // keep every section 16-byte aligned
   while (prog.ints.size() % 4) prog.ints.push_back(0);

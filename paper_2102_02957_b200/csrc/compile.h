@@ -17,7 +17,7 @@ struct Launch {
   size_t coef_count;  // coefficients of the section
   size_t aux_off;     // first complex of the section's DIAGSET factor tables in Program::aux
   size_t aux_count;
-  int T, r, n_out, n_phases, n_ops, flags;
+  int T, r, n_out, n_phases, n_ops, flags, n_sets;
   double flops_per_amp;  // algorithmic flops per amplitude of the section (DESIGN "Roofline")
 };
 

@@ -35,6 +35,27 @@ __device__ __forceinline__ void cmul_ip(float2& v, float2 f) {
       : "+f"(v.x), "+f"(v.y)
       : "f"(f.x), "f"(f.y));
 }
+// (a, b) <- (a + b, a - b)
+__device__ __forceinline__ void hu_ip(double2& a, double2& b) {
+  asm("{\n\t.reg .f64 t1, t2;\n\t"
+      "sub.f64 t1, %0, %2;\n\t"
+      "sub.f64 t2, %1, %3;\n\t"
+      "add.f64 %0, %0, %2;\n\t"
+      "add.f64 %1, %1, %3;\n\t"
+      "mov.f64 %2, t1;\n\t"
+      "mov.f64 %3, t2;\n\t}"
+      : "+d"(a.x), "+d"(a.y), "+d"(b.x), "+d"(b.y));
+}
+__device__ __forceinline__ void hu_ip(float2& a, float2& b) {
+  asm("{\n\t.reg .f32 t1, t2;\n\t"
+      "sub.f32 t1, %0, %2;\n\t"
+      "sub.f32 t2, %1, %3;\n\t"
+      "add.f32 %0, %0, %2;\n\t"
+      "add.f32 %1, %1, %3;\n\t"
+      "mov.f32 %2, t1;\n\t"
+      "mov.f32 %3, t2;\n\t}"
+      : "+f"(a.x), "+f"(a.y), "+f"(b.x), "+f"(b.y));
+}
 // (a, b) <- (s (a + b), s (a - b))
 __device__ __forceinline__ void h_ip(double2& a, double2& b, double s) {
   asm("{\n\t.reg .f64 t1, t2;\n\t"

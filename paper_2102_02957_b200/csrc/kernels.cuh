@@ -11,7 +11,7 @@ namespace sv {
 // `st`, then launches 2^n_out CTAs.  dbl selects fp64 (double2 amplitudes) vs fp32 (float2).
 cudaError_t launch_section(bool dbl, void* sv, const int* prog_dev, size_t int_count, const void* coef_dev,
                            size_t coef_count, const void* aux_dev, int T, int n_out, int n_phases, int flags,
-                           cudaStream_t st);
+                           int n_sets, cudaStream_t st);
 
 // K2: per-gate baseline, one pass over the shard per gate.  q0/q1 are memory bits;
 // diag codes follow program.h (rank bits pre-folded to constants).

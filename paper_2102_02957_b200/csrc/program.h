@@ -18,6 +18,7 @@
 #define SV_R_BITS 4           // register positions per phase (16 amplitudes per thread)
 #define SV_TMAX 14            // max tile bits (fp64 T=13 -> 128 KiB smem)
 #define SV_MAX_OUT 48         // max out-of-tile local bits
+#define SV_MAX_SETS 6         // DIAGSETs per section with prologue-computed per-CTA factors (6 x 5 lanes)
 
 // __constant__ budget per section launch
 #define SV_CONST_INTS 4096    // 16 KiB of program
@@ -28,6 +29,8 @@
 #define SV_OP_U2 1      // a = slot0 < b = slot1, coef -> 16 complex (row-major, s = bit(a) + 2 bit(b))
 #define SV_OP_U1 2      // a = slot, coef -> 4 complex (row-major)
 #define SV_OP_H1 3      // a = slot, coef -> 1 complex (scale s, real):  (x, y) -> (s(x+y), s(x-y))
+#define SV_OP_H1U 8     // a = slot: unscaled butterfly (x, y) -> (x+y, x-y); the section's product of
+                        // Hadamard scales is applied once, by its last H1 op (a global scalar)
 #define SV_OP_PERM2 4   // a = slot0, b = slot1, extra = packed permutation out[s] = in[(extra >> 2s) & 3]
 #define SV_OP_DIAG 5    // a = code0, b = code1, coef -> 4 complex d[s], s = bit(code0) + 2 bit(code1)
 #define SV_OP_DIAG_CP 6 // like DIAG with d0 = d1 = d2 = 1: only s == 3 is multiplied (coef -> d3)
@@ -75,6 +78,9 @@ struct SvSecHeader {
   SvMap store;              // non-direct final store: lanes walk the lowest store memory bits
   SvMap din;                // direct first phase: phase-0 mapping, load memory bits
   SvMap dout;               // direct last phase: last-phase mapping, store memory bits
+  int n_sets;               // DIAGSETs whose per-CTA factors the CTA prologue computes (<= SV_MAX_SETS)
+  int set_desc[SV_MAX_SETS];  // their descriptor offsets; factors go to smem after the tile
+  int pad_sets[1];
 };
 
 // XOR-fold swizzle of a tile element index (host and device): the low G bits are XORed with

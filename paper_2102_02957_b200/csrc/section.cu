@@ -87,6 +87,15 @@ __device__ __forceinline__ void h1_slot(V (&v)[16], R s) {
   }
 }
 
+template <int S, typename V>
+__device__ __forceinline__ void hu_slot(V (&v)[16]) {
+#pragma unroll
+  for (int q = 0; q < 16; q++) {
+    if ((q >> S) & 1) continue;
+    hu_ip(v[q], v[q | (1 << S)]);
+  }
+}
+
 template <int S0, int S1, typename V>
 __device__ __forceinline__ void perm_slots(V (&v)[16], int perm) {
   const int p0 = perm & 3, p1 = (perm >> 2) & 3, p2 = (perm >> 4) & 3, p3 = (perm >> 6) & 3;
@@ -185,13 +194,17 @@ __device__ __forceinline__ V cta_factor(int b, int e, uint64_t tile_off) {
 
 template <typename V>
 __device__ __forceinline__ void diagset(V (&v)[16], int desc, int cb, int tid, uint64_t tile_off,
-                                        const V* __restrict__ aux) {
+                                        const V* __restrict__ aux, const V* ctaf) {
   const int flags = c_prog[desc];
   const V* tab = aux + c_prog[desc + 1];
   const int nthr = blockDim.x;
   const int lane = tid & 31;
+  const int set = (flags >> 8) & 255;
   V F[5];
-  if (blockDim.x >= 32) {
+  if (set != 255) {  // per-CTA factors computed once by the CTA prologue
+#pragma unroll
+    for (int i = 0; i < 5; i++) F[i] = cmul(ctaf[5 * set + i], tab[i * nthr + tid]);
+  } else if (blockDim.x >= 32) {
     V mine = cone<V>();
     if (lane < 5) mine = cta_factor<V>(c_prog[desc + 2 + lane], c_prog[desc + 3 + lane], tile_off);
 #pragma unroll
@@ -240,7 +253,8 @@ __device__ __forceinline__ int code_val(int code, int tid, uint64_t tile_off) {
 }
 
 template <typename V, typename R>
-__device__ __forceinline__ void run_op(V (&v)[16], int oi, int tid, uint64_t tile_off, const V* __restrict__ aux) {
+__device__ __forceinline__ void run_op(V (&v)[16], int oi, int tid, uint64_t tile_off, const V* __restrict__ aux,
+                                       const V* ctaf) {
   const int type = c_prog[oi], a = c_prog[oi + 1], b = c_prog[oi + 2], cb = c_prog[oi + 3];
   switch (type) {
     case SV_OP_U2: {
@@ -305,8 +319,14 @@ __device__ __forceinline__ void run_op(V (&v)[16], int oi, int tid, uint64_t til
       break;
     }
     case SV_OP_DIAGSET:
-      diagset(v, a, cb, tid, tile_off, aux);
+      diagset(v, a, cb, tid, tile_off, aux, ctaf);
       break;
+    case SV_OP_H1U: {
+#define CALL_HU(x) hu_slot<x>(v)
+      SV_SLOT_SWITCH(a, CALL_HU)
+#undef CALL_HU
+      break;
+    }
     default:
       break;
   }
@@ -323,6 +343,7 @@ constexpr int kM_TMB = offsetof(SvMap, tmb) / 4, kM_RMB = offsetof(SvMap, rmb) /
 constexpr int kP_RW = offsetof(SvPhase, rw) / 4, kP_OPB = offsetof(SvPhase, op_begin) / 4;
 constexpr int kP_OPC = offsetof(SvPhase, op_count) / 4, kP_TW = offsetof(SvPhase, tw) / 4;
 constexpr int kPhaseInts = sizeof(SvPhase) / 4, kOpInts = sizeof(SvOp) / 4;
+constexpr int kH_NSETS = offsetof(SvSecHeader, n_sets) / 4, kH_SETS = offsetof(SvSecHeader, set_desc) / 4;
 
 // x ^ (the XOR of w[s] over the set bits s of the compile-time register index k)
 template <int K>
@@ -397,6 +418,17 @@ __global__ void __launch_bounds__(NT, MINB) k_section(V* __restrict__ sv, const 
     for (int j = 0; j < n_out; j++) tile_off |= ((bid >> j) & 1ull) << c_prog[kH_OUT + j];
   }
 
+  // per-CTA DIAGSET factors (out-of-tile terms), computed once per CTA by warp 0 into smem
+  V* ctaf = reinterpret_cast<V*>(smem_raw + (sizeof(V) << T));
+  const int n_sets = c_prog[kH_NSETS];
+  if (n_sets > 0) {
+    if (tid < 5 * n_sets) {
+      const int d = c_prog[kH_SETS + tid / 5], i = tid % 5;
+      ctaf[tid] = cta_factor<V>(c_prog[d + 2 + i], c_prog[d + 3 + i], tile_off);
+    }
+    __syncthreads();
+  }
+
   V v[16];
   if constexpr (FIRST) {  // phase 0 reads HBM directly in its own register mapping
     hbm_load(v, sv + hbm_base(kH_DIN, nt_log, tid, tile_off), kH_DIN);
@@ -424,7 +456,7 @@ __global__ void __launch_bounds__(NT, MINB) k_section(V* __restrict__ sv, const 
 #undef SV_LDS
     }
     const int ob = c_prog[P + kP_OPB], oc = c_prog[P + kP_OPC];
-    for (int o = 0; o < oc; o++) run_op<V, R>(v, opoff + (ob + o) * kOpInts, tid, tile_off, aux);
+    for (int o = 0; o < oc; o++) run_op<V, R>(v, opoff + (ob + o) * kOpInts, tid, tile_off, aux, ctaf);
     if (direct_out) {  // the last phase writes HBM directly (store memory bits, same mapping)
       hbm_store(v, sv + hbm_base(kH_DOUT, nt_log, tid, tile_off), kH_DOUT);
     } else {
@@ -452,7 +484,7 @@ cudaError_t launch_v(V* sv, const V* aux, int T, int n_out, size_t smem, cudaStr
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(k_section<V, G, NT, MINB, FIRST, LAST>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(V) << 13));
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)((sizeof(V) << 13) + 5 * SV_MAX_SETS * sizeof(V)));
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -476,7 +508,7 @@ cudaError_t launch_t(V* sv, const V* aux, int T, int n_out, int flags, size_t sm
 
 cudaError_t launch_section(bool dbl, void* sv, const int* prog_dev, size_t int_count, const void* coef_dev,
                            size_t coef_count, const void* aux_dev, int T, int n_out, int n_phases, int flags,
-                           cudaStream_t st) {
+                           int n_sets, cudaStream_t st) {
   if (int_count > SV_CONST_INTS) return cudaErrorInvalidValue;
   cudaError_t e = cudaMemcpyToSymbolAsync(c_prog, prog_dev, int_count * sizeof(int), 0, cudaMemcpyDeviceToDevice, st);
   if (e != cudaSuccess) return e;
@@ -493,12 +525,14 @@ cudaError_t launch_section(bool dbl, void* sv, const int* prog_dev, size_t int_c
   if (T < SV_R_BITS) return cudaErrorInvalidValue;  // tiny shards run per-gate kernels instead
   const bool no_smem = n_phases == 1 && (flags & SV_FLAG_FIRST_DIRECT) && (flags & SV_FLAG_LAST_DIRECT);
   if (dbl) {
-    const size_t smem = no_smem ? 0 : sizeof(double2) << T;
+    const size_t smem = n_sets ? (sizeof(double2) << T) + 5 * SV_MAX_SETS * sizeof(double2)
+                               : (no_smem ? 0 : sizeof(double2) << T);
     if (T <= 12) return launch_t<double2, 3, 256, 2>((double2*)sv, (const double2*)aux_dev, T, n_out, flags, smem, st);
     if (T == 13) return launch_t<double2, 3, 512, 1>((double2*)sv, (const double2*)aux_dev, T, n_out, flags, smem, st);
     return cudaErrorInvalidValue;
   }
-  const size_t smem = no_smem ? 0 : sizeof(float2) << T;
+  const size_t smem = n_sets ? (sizeof(float2) << T) + 5 * SV_MAX_SETS * sizeof(float2)
+                             : (no_smem ? 0 : sizeof(float2) << T);
   if (T <= 12) return launch_t<float2, 4, 256, 2>((float2*)sv, (const float2*)aux_dev, T, n_out, flags, smem, st);
   if (T == 13) return launch_t<float2, 4, 512, 1>((float2*)sv, (const float2*)aux_dev, T, n_out, flags, smem, st);
   return cudaErrorInvalidValue;

@@ -16,7 +16,7 @@ H_LOAD, H_STORE, H_DIN, H_DOUT = 88, 128, 168, 208
 M_TW, M_RW, M_TMB, M_RMB = 0, 16, 20, 36
 PHASE_INTS, P_RW, P_OPB, P_OPC, P_TW = 44, 4, 8, 9, 28
 OP_INTS = 8
-U2, U1, H1, PERM2, DIAG, DIAG_CP, DIAGSET = 1, 2, 3, 4, 5, 6, 7
+U2, U1, H1, PERM2, DIAG, DIAG_CP, DIAGSET, H1U = 1, 2, 3, 4, 5, 6, 7, 8
 KS = np.arange(16)
 
 
@@ -116,6 +116,12 @@ def apply_op(v, prog, coefs, oi, tids, tile_off, aux=None):
                 continue
             x, y = v[:, q].copy(), v[:, q | 1 << a].copy()
             v[:, q], v[:, q | 1 << a] = s * (x + y), s * (x - y)
+    elif typ == H1U:
+        for q in range(16):
+            if (q >> a) & 1:
+                continue
+            x, y = v[:, q].copy(), v[:, q | 1 << a].copy()
+            v[:, q], v[:, q | 1 << a] = x + y, x - y
     elif typ == PERM2:
         perm = [(extra >> (2 * s)) & 3 for s in range(4)]
         for q in range(16):
@@ -134,7 +140,7 @@ def apply_op(v, prog, coefs, oi, tids, tile_off, aux=None):
         v[both] *= coefs[cb]
     elif typ == DIAGSET:
         d = a
-        flags, aux0 = int(prog[d]), int(prog[d + 1])
+        flags, aux0 = int(prog[d]) & 1, int(prog[d + 1])
         nthr = len(tids)
         F = []
         for i in range(5):
