@@ -91,6 +91,8 @@ struct sv_state {
   Program prog;
   sv_stats stats{};
   std::string err;
+  bool basis_pending = false;  // state is exactly |basis_index> (set by sv_reset)
+  uint64_t basis_index = 0;
 
   // optional per-launch device timing (sv_set_timing)
   struct TRec {
@@ -574,6 +576,8 @@ int sv_reset(sv_handle h, uint64_t k) {
   const int64_t off = owner == h->rank ? (int64_t)(k & ((1ull << h->nL) - 1)) : -1;
   CUDA_TRY(h, launch_set_basis(h->dbl, h->sv, h->nL, off, h->st));
   h->stats.kernel_launches += off >= 0 ? 1 : 0;
+  h->basis_pending = true;  // the next circuit may choose its memory layout freely (NEXT-2)
+  h->basis_index = k;
   return SV_OK;
 }
 
@@ -592,8 +596,24 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
   PlanCounters ctr;
   PlanLayout lay;
   lay.low_bits = h->dbl ? 3 : 4;  // 128-byte runs
-  Status s = make_plan(gates, n_gates, h->n, h->c, h->g, pi, sigma, flags, steps, ctr, lay);
+  lay.free_initial = h->basis_pending && !(flags & SV_UNBLOCKED);
+  std::vector<int> sigma0;
+  Status s = make_plan(gates, n_gates, h->n, h->c, h->g, pi, sigma, flags, steps, ctr, lay, &sigma0);
   if (!s.good()) return fail(h, s);
+  if (lay.free_initial && sigma0 != h->sigma) {
+    // relocate the single nonzero amplitude of |k> to its place under the chosen layout
+    uint64_t from = 0, to = 0;
+    for (int q = 0; q < h->n; q++) {
+      const uint64_t b = (h->basis_index >> q) & 1;
+      from |= b << h->sigma[h->pi[q]];
+      to |= b << sigma0[h->pi[q]];
+    }
+    const uint64_t lm = (1ull << h->nL) - 1;
+    if ((int)(from >> h->nL) == h->rank) CUDA_TRY(h, launch_set_amp(h->dbl, h->sv, (int64_t)(from & lm), 0.0, h->st));
+    if ((int)(to >> h->nL) == h->rank) CUDA_TRY(h, launch_set_amp(h->dbl, h->sv, (int64_t)(to & lm), 1.0, h->st));
+    h->stats.kernel_launches += 2;
+  }
+  h->basis_pending = false;
   h->prog.clear();
   const int T_default = lay.tile_default;
   std::vector<size_t> launch_end(steps.size(), 0);  // one past the last launch of each step

@@ -64,6 +64,7 @@ struct PlanLayout {
   int low_bits = 3;    // memory bits every section tile should contain (3: 128-byte fp64 runs)
   int max_tile = 13;   // largest tile (bits) one CTA holds
   int tile_default = 12;
+  bool free_initial = false;  // the state is a basis state: choose the initial sigma freely (NEXT-2)
 };
 
 // The tile a section runs on (memory-bit mask), shared by the planner and the compiler: the
@@ -81,6 +82,6 @@ inline uint64_t choose_tile(uint64_t active, int nL, const PlanLayout& L) {
 // relabel of sigma; data moves only where a section needs a rank bit (DESIGN "Executor mapping").
 Status make_plan(const sv_gate* g, size_t count, int n, int c, int world_log2, std::vector<int>& pi,
                  std::vector<int>& sigma, uint32_t flags, std::vector<Step>& steps, PlanCounters& ctr,
-                 const PlanLayout& layout = PlanLayout());
+                 const PlanLayout& layout = PlanLayout(), std::vector<int>* sigma_initial = nullptr);
 
 }  // namespace sv

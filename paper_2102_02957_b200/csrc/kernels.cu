@@ -93,6 +93,13 @@ __global__ void k_set_one(V* sv, int64_t off) {
 }
 
 template <typename V>
+__global__ void k_set_amp(V* sv, int64_t off, double re) {
+  V x = czero<V>();
+  x.x = re;
+  sv[off] = x;
+}
+
+template <typename V>
 __global__ void k_gather(const V* __restrict__ sv, const uint64_t* __restrict__ offs, size_t cnt, V* __restrict__ out) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < cnt; i += (size_t)gridDim.x * blockDim.x) {
     const uint64_t o = offs[i];
@@ -323,6 +330,14 @@ cudaError_t launch_set_basis(bool dbl, void* sv, int nL, int64_t off, cudaStream
     k_set_one<double2><<<1, 1, 0, st>>>((double2*)sv, off);
   else
     k_set_one<float2><<<1, 1, 0, st>>>((float2*)sv, off);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_set_amp(bool dbl, void* sv, int64_t off, double re, cudaStream_t st) {
+  if (dbl)
+    k_set_amp<double2><<<1, 1, 0, st>>>((double2*)sv, off, re);
+  else
+    k_set_amp<float2><<<1, 1, 0, st>>>((float2*)sv, off, re);
   return cudaGetLastError();
 }
 

@@ -22,6 +22,8 @@ struct GateArgs {
 };
 cudaError_t launch_gate(bool dbl, void* sv, int nL, const GateArgs& g, cudaStream_t st);
 
+// write the real value re at local offset off (one amplitude)
+cudaError_t launch_set_amp(bool dbl, void* sv, int64_t off, double re, cudaStream_t st);
 // K6: |k>: zero the shard and write 1 at local offset `off` if owned.
 cudaError_t launch_set_basis(bool dbl, void* sv, int nL, int64_t off, cudaStream_t st);
 

@@ -204,13 +204,14 @@ struct Planner {
 
 Status make_plan(const sv_gate* g, size_t count, int n, int c, int world_log2, std::vector<int>& pi,
                  std::vector<int>& sigma, uint32_t flags, std::vector<Step>& steps, PlanCounters& ctr,
-                 const PlanLayout& layout) {
+                 const PlanLayout& layout, std::vector<int>* sigma_initial) {
   const int nL = n - world_log2;
   if (world_log2 < 0 || nL < 1) return Status::err(SV_EINVAL, "world too large for n");
   if (c < 1 || c > nL) return Status::err(SV_EINVAL, "chunk_bits must satisfy 1 <= c <= n - log2(world)");
   if ((int)pi.size() != n || (int)sigma.size() != n) return Status::err(SV_EINVAL, "bad permutation length");
   if (Status s = validate_gates(g, count, n); !s.good()) return s;
 
+  if (sigma_initial) *sigma_initial = sigma;
   if (flags & SV_UNBLOCKED) {
     // Per-gate baseline: each gate is one step on memory bits mu(q) = sigma[pi[q]].
     for (size_t i = 0; i < count; i++) {
@@ -256,6 +257,27 @@ Status make_plan(const sv_gate* g, size_t count, int n, int c, int world_log2, s
         cur.gates.push_back(t);
     }
   }
+  if (layout.free_initial && !blocks.empty()) {
+    // NEXT-2 "free initial layout" (the paper's bit reordering): the state is a basis
+    // state, so sigma can be chosen freely at no data cost.  Put the first section's qubits on
+    // the lowest memory bits (its tile is then coalesced and no exchange is needed), keep every
+    // other qubit's relative order, then undo the first block's chunk_swap relabels.
+    std::vector<int> after = sigma;
+    for (const auto& rl : blocks[0].relabels) std::swap(after[rl.first], after[rl.second]);
+    const uint64_t need = Planner::needed(blocks[0], after, n, nullptr);
+    std::vector<int> order(n);  // paper qubits: needed first, each group by current memory bit
+    for (int p = 0; p < n; p++) order[p] = p;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+      const bool na = (need >> after[a]) & 1, nb = (need >> after[b]) & 1;
+      if (na != nb) return na;
+      return after[a] < after[b];
+    });
+    for (int i = 0; i < n; i++) after[order[i]] = i;
+    for (auto it = blocks[0].relabels.rbegin(); it != blocks[0].relabels.rend(); ++it)
+      std::swap(after[it->first], after[it->second]);
+    sigma = after;
+  }
+  if (sigma_initial) *sigma_initial = sigma;
   Planner planner(n, nL, layout, sigma, steps, ctr);
   planner.run(blocks);
   for (const auto& rl : cur.relabels) planner.relabel(rl.first, rl.second);  // trailing chunk_swaps
