@@ -67,6 +67,10 @@ typedef struct {
 #define SV_RESTORE_ORDER (1u << 1) /* append swaps returning the paper-physical order to logical */
 #define SV_EXCHANGE_NCCL (1u << 2) /* cross-GPU exchange by NCCL send/recv through a staging ring */
                                    /* instead of the peer-memory swap kernel                    */
+#define SV_FREE_LAYOUT   (1u << 3) /* sv_plan_circuit / sv_compile_circuit: plan as sv_apply_   */
+                                   /* circuit does right after sv_reset (the state is a basis   */
+                                   /* state, so the planner chooses the initial memory layout; */
+                                   /* sigma0 is ignored).  sv_apply_circuit decides this itself */
 
 /* Error codes. */
 #define SV_OK           0
@@ -77,6 +81,7 @@ typedef struct {
 #define SV_EMALFORMED  -4 /* malformed record / marker sequence                               */
 #define SV_ECUDA       -5 /* CUDA runtime failure                                              */
 #define SV_ENCCL       -6 /* NCCL failure or NCCL library not loadable                         */
+#define SV_EUNAVAILABLE -7 /* optional run-time component missing (NVRTC for sv_jit_compile_*) */
 
 typedef struct sv_stats {
   uint64_t circuits;          /* sv_apply_circuit calls                                       */
@@ -98,6 +103,11 @@ typedef struct sv_stats {
   double section_flops;       /* algorithmic flops of the timed sections (DESIGN "Roofline")   */
   uint64_t compactions;       /* standalone memory-bit swap passes (tile coalescing fallback)  */
   uint64_t store_swaps;       /* memory-bit swaps fused into section stores (free)            */
+  /* run-time specialised section kernels (NVRTC, environment SV_JIT=sync|async|0) */
+  uint64_t jit_launches;      /* section launches that ran a generated kernel                  */
+  uint64_t interp_launches;   /* section launches that ran the program interpreter             */
+  uint64_t jit_compiled;      /* kernels compiled by this process so far (cache misses)        */
+  double jit_compile_ms;      /* host time spent compiling them (process total)                */
 } sv_stats;
 
 /* ---- lifetime ------------------------------------------------------------------------- */
@@ -172,6 +182,14 @@ int sv_plan_circuit(const sv_gate* gates, size_t n_gates, int n, int chunk_bits,
  * *ints / *coefs / *aux: the programs (program.h layout), fp64 complex coefficients (constant
  * bank) and fp64 complex DIAGSET factor tables (global memory).  pi_final /
  * sigma_final as in sv_plan_circuit.  All outputs are freed with sv_free. */
+/* Host only (no GPU): generate the run-time specialised kernel of every section launch that
+ * sv_compile_circuit returns (same arguments) and compile it for sm_100a with NVRTC, as
+ * sv_apply_circuit does on first use (SV_JIT, jit.h).  *n_kernels / *compile_ms report the work;
+ * dump_dir (nullable) receives section_<i>.cu and section_<i>.cubin.  SV_EUNAVAILABLE if NVRTC
+ * cannot be loaded. */
+int sv_jit_compile_circuit(const sv_gate* gates, size_t n_gates, int n, int chunk_bits, int world_log2, int rank,
+                           sv_precision prec, uint32_t flags, const char* dump_dir, int* n_kernels,
+                           double* compile_ms);
 int sv_compile_circuit(const sv_gate* gates, size_t n_gates, int n, int chunk_bits, int world_log2,
                        int rank, sv_precision prec, const int32_t* pi0, const int32_t* sigma0,
                        uint32_t flags, int64_t** steps, size_t* n_steps,

@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libsv.so")
 GATE_DTYPE = np.dtype([("kind", "<i4"), ("q0", "<i4"), ("q1", "<i4"), ("pad", "<i4"), ("m", "<f8", (32,))])
 SV_U1, SV_U2, SV_D1, SV_D2, SV_SWAP, SV_CHUNK_SWAP, SV_BEGIN, SV_END, SV_EXCHANGE = range(1, 10)
 SV_FP32, SV_FP64 = 0, 1
-SV_UNBLOCKED, SV_RESTORE_ORDER, SV_EXCHANGE_NCCL = 1, 2, 4
+SV_UNBLOCKED, SV_RESTORE_ORDER, SV_EXCHANGE_NCCL, SV_FREE_LAYOUT = 1, 2, 4, 8
 ERRORS = {-1: "SV_EINVAL", -2: "SV_ECAPACITY", -3: "SV_EINFEASIBLE", -4: "SV_EMALFORMED", -5: "SV_ECUDA", -6: "SV_ENCCL"}
 
 
@@ -35,13 +35,15 @@ class Stats(ctypes.Structure):
                 ("kernel_launches", ctypes.c_uint64), ("pass_ms", ctypes.c_double), ("apply_ms", ctypes.c_double),
                 ("timed_sections", ctypes.c_uint64), ("section_ms", ctypes.c_double), ("exchange_ms", ctypes.c_double),
                 ("gate_ms", ctypes.c_double), ("section_bytes", ctypes.c_double), ("section_flops", ctypes.c_double),
-                ("compactions", ctypes.c_uint64), ("store_swaps", ctypes.c_uint64)]
+                ("compactions", ctypes.c_uint64), ("store_swaps", ctypes.c_uint64),
+                ("jit_launches", ctypes.c_uint64), ("interp_launches", ctypes.c_uint64),
+                ("jit_compiled", ctypes.c_uint64), ("jit_compile_ms", ctypes.c_double)]
 
 
 EXPORTS = ["sv_create", "sv_create_dist", "sv_destroy", "sv_nccl_unique_id", "sv_reset", "sv_apply_circuit",
            "sv_synchronize", "sv_get_amplitudes", "sv_get_state", "sv_norm", "sv_probabilities", "sv_sample",
            "sv_get_permutation", "sv_stats_get", "sv_stats_reset", "sv_set_timing", "sv_last_error", "sv_block_circuit", "sv_plan_circuit",
-           "sv_compile_circuit", "sv_free",
+           "sv_compile_circuit", "sv_jit_compile_circuit", "sv_free",
            "sv_abi_version"]
 
 _lib = None
@@ -81,6 +83,8 @@ def lib():
         "sv_plan_circuit": ([vp, sz, i32, i32, i32, ip, ip, u32, hp, ctypes.POINTER(sz), ip, ip], i32),
         "sv_compile_circuit": ([vp, sz, i32, i32, i32, i32, i32, ip, ip, u32, hp, ctypes.POINTER(sz), hp, ctypes.POINTER(sz),
                                 hp, ctypes.POINTER(sz), hp, ctypes.POINTER(sz), ip, ip], i32),
+        "sv_jit_compile_circuit": ([vp, sz, i32, i32, i32, i32, i32, u32, ctypes.c_char_p, ip,
+                                    ctypes.POINTER(ctypes.c_double)], i32),
         "sv_free": ([vp], None),
         "sv_abi_version": ([], i32),
     }
@@ -175,6 +179,20 @@ def compile_circuit(gates, n: int, c: int, world_log2: int = 0, rank: int = 0, p
         for p in (st, ni, co, ax):
             lib().sv_free(p)
     return steps, ints, coefs, aux, pif, sgf
+
+
+def jit_compile_circuit(gates, n: int, c: int, world_log2: int = 0, rank: int = 0, precision: str = "fp64",
+                        flags: int = 0, dump_dir: str = None):
+    """Host-only: NVRTC-compile the run-time specialised kernel of every section launch
+    (sv_jit_compile_circuit) -> (kernels, compile_ms)."""
+    g = as_gates(gates)
+    nk = np.zeros(1, dtype=np.int32)
+    ms = ctypes.c_double()
+    prec = {"fp64": SV_FP64, "fp32": SV_FP32}[precision]
+    rc = lib().sv_jit_compile_circuit(g.ctypes.data if len(g) else None, len(g), n, c, world_log2, rank, prec, flags,
+                                      dump_dir.encode() if dump_dir else None, _ip(nk), ctypes.byref(ms))
+    check(rc)
+    return int(nk[0]), ms.value
 
 
 def nccl_unique_id() -> bytes:

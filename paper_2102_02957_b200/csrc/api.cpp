@@ -19,6 +19,7 @@
 #include "comm.h"
 #include "common.h"
 #include "compile.h"
+#include "jit.h"
 #include "kernels.cuh"
 
 using namespace sv;
@@ -650,10 +651,18 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
         for (; si < launch_end[i]; si++) {
           const Launch& L = h->prog.launches[si];
           cudaEvent_t t = tstart(h);
-          CUDA_TRY(h, launch_section(h->dbl, h->sv, (const int*)h->d_prog.p + L.int_off, L.int_count,
-                                     (const char*)h->d_coef.p + L.coef_off * h->amp, L.coef_count,
-                                     (const char*)h->d_aux.p + L.aux_off * h->amp, L.T, L.n_out, L.n_phases,
-                                     L.flags, L.n_sets, h->st));
+          const int* pdev = (const int*)h->d_prog.p + L.int_off;
+          const char* cdev = (const char*)h->d_coef.p + L.coef_off * h->amp;
+          const char* adev = (const char*)h->d_aux.p + L.aux_off * h->amp;
+          cudaError_t je = cudaSuccess;
+          if (jit_launch_section(h->dbl, h->sv, h->prog.ints.data() + L.int_off, L, pdev, cdev, adev, h->st, &je)) {
+            CUDA_TRY(h, je);
+            h->stats.jit_launches++;
+          } else {
+            CUDA_TRY(h, launch_section(h->dbl, h->sv, pdev, L.int_count, cdev, L.coef_count, adev, L.T, L.n_out,
+                                       L.n_phases, L.flags, L.n_sets, h->st));
+            h->stats.interp_launches++;
+          }
           const double amps = (double)(1ull << h->nL);
           tend(h, t, 0, 2.0 * amps * (double)h->amp, L.flops_per_amp * amps);
           h->stats.kernel_launches++;
@@ -697,6 +706,9 @@ int sv_stats_get(sv_handle h, sv_stats* out) {
   if (!h || !out) return fail(h, SV_EINVAL, "null argument");
   if (int rc = drain_timing(h)) return rc;
   *out = h->stats;
+  const JitCounters jc = jit_counters();
+  out->jit_compiled = jc.compiled;
+  out->jit_compile_ms = jc.compile_ms;
   return SV_OK;
 }
 
@@ -956,7 +968,9 @@ int sv_plan_circuit(const sv_gate* gates, size_t n_gates, int n, int c, int worl
   }
   std::vector<Step> steps;
   PlanCounters ctr;
-  Status s = make_plan(gates, n_gates, n, c, world_log2, pi, sigma, flags, steps, ctr);
+  PlanLayout lay;
+  lay.free_initial = (flags & SV_FREE_LAYOUT) && !(flags & SV_UNBLOCKED);
+  Status s = make_plan(gates, n_gates, n, c, world_log2, pi, sigma, flags, steps, ctr, lay);
   if (!s.good()) return fail(nullptr, s);
   std::vector<sv_gate> recs;
   sv_gate mk;
@@ -1033,6 +1047,7 @@ extern "C" int sv_compile_circuit(const sv_gate* gates, size_t n_gates, int n, i
   PlanCounters ctr;
   PlanLayout lay;
   lay.low_bits = prec == SV_FP64 ? 3 : 4;
+  lay.free_initial = (flags & SV_FREE_LAYOUT) && !(flags & SV_UNBLOCKED);
   Status s = make_plan(gates, n_gates, n, c, world_log2, pi, sigma, flags, steps, ctr, lay);
   if (!s.good()) return fail(nullptr, s);
   Program prog;
@@ -1080,5 +1095,40 @@ extern "C" int sv_compile_circuit(const sv_gate* gates, size_t n_gates, int n, i
     if (pi_final) pi_final[q] = pi[q];
     if (sigma_final) sigma_final[q] = sigma[q];
   }
+  return SV_OK;
+}
+
+extern "C" int sv_jit_compile_circuit(const sv_gate* gates, size_t n_gates, int n, int c, int world_log2, int rank,
+                                      sv_precision prec, uint32_t flags, const char* dump_dir, int* n_kernels,
+                                      double* compile_ms) {
+  if (n_gates && !gates) return fail(nullptr, SV_EINVAL, "null gate array");
+  if (n < 1 || n > 63 || world_log2 < 0 || world_log2 >= n) return fail(nullptr, SV_EINVAL, "bad n / world");
+  const int nL = n - world_log2;
+  std::vector<int> pi(n), sigma(n);
+  for (int q = 0; q < n; q++) pi[q] = sigma[q] = q;
+  std::vector<Step> steps;
+  PlanCounters ctr;
+  PlanLayout lay;
+  lay.low_bits = prec == SV_FP64 ? 3 : 4;
+  lay.free_initial = (flags & SV_FREE_LAYOUT) && !(flags & SV_UNBLOCKED);
+  Status s = make_plan(gates, n_gates, n, c, world_log2, pi, sigma, flags, steps, ctr, lay);
+  if (!s.good()) return fail(nullptr, s);
+  Program prog;
+  for (const Step& st : steps) {
+    if (st.type != Step::SECTION || nL < SV_R_BITS) continue;
+    Status cs = compile_section_split(st.gates, nL, rank, world_log2, lay.tile_default, lay.low_bits, st.swaps, prog);
+    if (!cs.good()) return fail(nullptr, cs);
+  }
+  int k = 0;
+  double total = 0.0;
+  for (const Launch& L : prog.launches) {
+    double ms = 0.0;
+    Status js = jit_compile_only(prog.ints.data() + L.int_off, L, prec == SV_FP64, dump_dir, k, &ms);
+    if (!js.good()) return fail(nullptr, js);
+    total += ms;
+    k++;
+  }
+  if (n_kernels) *n_kernels = k;
+  if (compile_ms) *compile_ms = total;
   return SV_OK;
 }

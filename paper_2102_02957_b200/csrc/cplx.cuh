@@ -1,6 +1,8 @@
 // cplx.cuh — complex double2 / float2 helpers shared by the device kernels.
 #pragma once
+#ifndef __CUDACC_RTC__
 #include <cuda_runtime.h>
+#endif
 
 namespace sv {
 

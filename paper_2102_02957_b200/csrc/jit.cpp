@@ -1,0 +1,467 @@
+// jit.cpp — run-time specialised section kernels (see jit.h).
+//
+// The generated kernel is the interpreter kernel of section.cu with its loops over phases and
+// ops unrolled for one program: the same device building blocks (section_dev.cuh, embedded in
+// libsv.so as text by build.py) with every slot, map entry and coefficient offset an immediate.
+// NVRTC and the CUDA library API are reached through dlopen / the static runtime, so libsv.so
+// still loads on a host without a GPU or without NVRTC (the interpreter then runs).
+#include "jit.h"
+
+#include <dlfcn.h>
+#include <nvrtc.h>
+
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <cstdio>
+#include <cstdlib>
+#include <fstream>
+#include <cstring>
+#include <deque>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "program.h"
+
+namespace sv {
+namespace {
+
+#include "jit_headers.inc"  // kJitHeaderNames[], kJitHeaderTexts[], kJitHeaderCount (build.py)
+
+// ------------------------------------------------------------------------------------ NVRTC
+struct Nvrtc {
+  bool ok = false;
+  decltype(&nvrtcCreateProgram) create = nullptr;
+  decltype(&nvrtcDestroyProgram) destroy = nullptr;
+  decltype(&nvrtcCompileProgram) compile = nullptr;
+  decltype(&nvrtcGetProgramLogSize) log_size = nullptr;
+  decltype(&nvrtcGetProgramLog) log = nullptr;
+  decltype(&nvrtcGetCUBINSize) cubin_size = nullptr;
+  decltype(&nvrtcGetCUBIN) cubin = nullptr;
+  decltype(&nvrtcAddNameExpression) add_name = nullptr;
+  decltype(&nvrtcGetLoweredName) lowered = nullptr;
+};
+
+Nvrtc load_nvrtc() {
+  Nvrtc n;
+  void* h = nullptr;
+  for (const char* name : {"libnvrtc.so.12", "/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so"})
+    if ((h = dlopen(name, RTLD_NOW | RTLD_LOCAL))) break;
+  if (!h) return n;
+#define SV_SYM(field, sym) n.field = reinterpret_cast<decltype(n.field)>(dlsym(h, sym))
+  SV_SYM(create, "nvrtcCreateProgram");
+  SV_SYM(destroy, "nvrtcDestroyProgram");
+  SV_SYM(compile, "nvrtcCompileProgram");
+  SV_SYM(log_size, "nvrtcGetProgramLogSize");
+  SV_SYM(log, "nvrtcGetProgramLog");
+  SV_SYM(cubin_size, "nvrtcGetCUBINSize");
+  SV_SYM(cubin, "nvrtcGetCUBIN");
+  SV_SYM(add_name, "nvrtcAddNameExpression");
+  SV_SYM(lowered, "nvrtcGetLoweredName");
+#undef SV_SYM
+  n.ok = n.create && n.destroy && n.compile && n.log_size && n.log && n.cubin_size && n.cubin && n.add_name &&
+         n.lowered;
+  return n;
+}
+
+Nvrtc& nvrtc() {
+  static Nvrtc n = load_nvrtc();
+  return n;
+}
+
+enum Mode { kOff = 0, kSync = 1, kAsync = 2 };
+Mode mode() {
+  static const Mode m = [] {
+    const char* e = std::getenv("SV_JIT");
+    if (!e || !*e || !std::strcmp(e, "sync") || !std::strcmp(e, "1")) return kSync;
+    if (!std::strcmp(e, "async")) return kAsync;
+    return kOff;
+  }();
+  return m;
+}
+
+// ------------------------------------------------------------------------------------ source
+size_t smem_bytes(const Launch& L, bool dbl) {
+  const size_t amp = dbl ? 16 : 8;
+  const bool no_smem = L.n_phases == 1 && (L.flags & SV_FLAG_FIRST_DIRECT) && (L.flags & SV_FLAG_LAST_DIRECT);
+  if (L.n_sets) return (amp << L.T) + 5 * SV_MAX_SETS * amp;
+  return no_smem ? 0 : amp << L.T;
+}
+
+struct Gen {
+  std::ostringstream o;
+  int T = 0, ntl = 0;
+
+  template <typename X>
+  void arr(const char* type, const char* name, const X* v, int n) {
+    o << "    constexpr " << type << " " << name << "[" << (n > 0 ? n : 1) << "] = {";
+    if (n == 0) o << "0";
+    for (int i = 0; i < n; i++) o << (i ? ", " : "") << v[i];
+    o << "};\n";
+  }
+  // HBM element offset of register 0 (b) and of every register k (RO[k]) under map m
+  void hbm(const SvMap& m) {
+    long long ro[16];
+    for (int k = 0; k < 16; k++) {
+      ro[k] = 0;
+      for (int s = 0; s < SV_R_BITS; s++)
+        if ((k >> s) & 1) ro[k] |= 1ll << m.rmb[s];
+    }
+    arr("int", "TMB", m.tmb, ntl);
+    arr("long long", "RO", ro, 16);
+    o << "    uint64_t b = tile_off;\n"
+      << "#pragma unroll\n    for (int j = 0; j < " << ntl << "; j++) b |= (uint64_t)((tid >> j) & 1) << TMB[j];\n";
+  }
+  // swizzled smem offset of register 0 (x) and XOR offsets W[k] for thread-bit words tw, slot words rw
+  void smem(const int* tw, const int* rw) {
+    int w[16];
+    for (int k = 0; k < 16; k++) {
+      w[k] = 0;
+      for (int s = 0; s < SV_R_BITS; s++)
+        if ((k >> s) & 1) w[k] ^= rw[s];
+    }
+    arr("int", "TW", tw, ntl);
+    arr("int", "W", w, 16);
+    o << "    int x = 0;\n#pragma unroll\n    for (int j = 0; j < " << ntl
+      << "; j++) x ^= ((tid >> j) & 1) ? TW[j] : 0;\n";
+  }
+  void lds() { o << "#pragma unroll\n    for (int k = 0; k < 16; k++) v[k] = sm[x ^ W[k]];\n"; }
+  void sts() { o << "#pragma unroll\n    for (int k = 0; k < 16; k++) sm[x ^ W[k]] = v[k];\n"; }
+  void ldg() { o << "#pragma unroll\n    for (int k = 0; k < 16; k++) v[k] = psi[b + RO[k]];\n"; }
+  void stg() { o << "#pragma unroll\n    for (int k = 0; k < 16; k++) psi[b + RO[k]] = v[k];\n"; }
+};
+
+std::string gen_source(const int* p, const Launch& L, bool dbl) {
+  const SvSecHeader* H = reinterpret_cast<const SvSecHeader*>(p);
+  Gen g;
+  g.T = H->T;
+  g.ntl = H->T - SV_R_BITS;
+  const int nt = 1 << g.ntl;
+  const bool first = H->flags & SV_FLAG_FIRST_DIRECT, last = H->flags & SV_FLAG_LAST_DIRECT;
+  const int nph = H->n_phases;
+  auto& o = g.o;
+  o << "#include \"section_dev.cuh\"\nusing namespace sv;\ntypedef " << (dbl ? "double2" : "float2") << " V;\n";
+  o << "extern \"C\" __global__ void __launch_bounds__(" << nt << ", " << (H->T <= 12 ? 2 : 1)
+    << ") sv_sec(V* __restrict__ psi, const V* __restrict__ aux) {\n";
+  o << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n"
+    << "  V* sm = reinterpret_cast<V*>(smem_raw);\n"
+    << "  V* ctaf = reinterpret_cast<V*>(smem_raw + (sizeof(V) << " << H->T << "));\n"
+    << "  (void)sm; (void)ctaf; (void)aux;\n"
+    << "  const int tid = threadIdx.x;\n"
+    << "  const uint64_t bid = blockIdx.x;\n"
+    << "  uint64_t tile_off = 0;\n";
+  {
+    o << "  {\n";
+    g.arr("int", "OB", H->out_bits, H->n_out);
+    o << "#pragma unroll\n    for (int j = 0; j < " << H->n_out << "; j++) tile_off |= ((bid >> j) & 1ull) << OB[j];\n";
+    o << "  }\n";
+  }
+  if (H->n_sets > 0) {
+    o << "  for (int f = tid; f < " << 5 * H->n_sets << "; f += " << nt << ") {\n"
+      << "    const int d = c_prog[kH_SETS + f / 5], i = f % 5;\n"
+      << "    ctaf[f] = cta_factor<V>(c_prog[d + 2 + i], c_prog[d + 3 + i], tile_off);\n  }\n"
+      << "  __syncthreads();\n";
+  }
+  o << "  V v[16];\n";
+  if (!first) {
+    o << "  {  // load: lanes walk the lowest load memory bits, scatter into the swizzled tile\n";
+    g.hbm(H->load);
+    g.ldg();
+    g.smem(H->load.tw, H->load.rw);
+    g.sts();
+    o << "    __syncthreads();\n  }\n";
+  }
+  const SvPhase* ph = reinterpret_cast<const SvPhase*>(p + H->phase_off);
+  const SvOp* ops = reinterpret_cast<const SvOp*>(p + H->op_off);
+  for (int k = 0; k < nph; k++) {
+    const bool din = first && k == 0, dout = last && k == nph - 1;
+    o << "  {  // phase " << k << "\n";
+    if (din) {
+      g.hbm(H->din);
+      g.ldg();
+    }
+    if (!din || !dout) g.smem(ph[k].tw, ph[k].rw);
+    if (!din) g.lds();
+    for (int i = 0; i < ph[k].op_count; i++) {
+      const SvOp& op = ops[ph[k].op_begin + i];
+      o << "    op_c<" << op.type << ", " << op.a << ", " << op.b << ", " << op.coef << ", " << op.extra
+        << ">(v, tid, tile_off, aux, ctaf);\n";
+    }
+    if (dout) {
+      o << "    {\n";
+      g.hbm(H->dout);
+      g.stg();
+      o << "    }\n";
+    } else {
+      g.sts();
+      o << "    __syncthreads();\n";
+    }
+    o << "  }\n";
+  }
+  if (!last) {
+    o << "  {  // gather in store order, lanes walk the lowest store memory bits\n";
+    g.smem(H->store.tw, H->store.rw);
+    g.lds();
+    g.hbm(H->store);
+    g.stg();
+    o << "  }\n";
+  }
+  o << "}\n";
+  (void)L;
+  return o.str();
+}
+
+// ------------------------------------------------------------------------------------ cache
+struct Entry {
+  std::atomic<int> state{0};  // 0 pending, 1 ready, 2 failed
+  cudaLibrary_t lib = nullptr;
+  cudaKernel_t kern = nullptr;
+  void* c_prog = nullptr;
+  size_t c_prog_bytes = 0;
+  void* c_coef = nullptr;
+  size_t c_coef_bytes = 0;
+  std::string err;
+};
+
+struct Job {
+  std::shared_ptr<Entry> e;
+  std::string src;
+  int dev;
+  bool dbl;
+};
+
+std::mutex g_mu;
+std::unordered_map<std::string, std::shared_ptr<Entry>> g_cache;
+JitCounters g_ctr;
+
+// NVRTC: source -> sm_100a cubin (+ the lowered names of the __constant__ arrays)
+bool compile_cubin(const std::string& src, bool dbl, std::vector<char>& cubin, std::string& name_prog,
+                   std::string& name_coef, std::string& err) {
+  Nvrtc& N = nvrtc();
+  if (!N.ok) {
+    err = "NVRTC (libnvrtc.so.12) not found";
+    return false;
+  }
+  nvrtcProgram prog = nullptr;
+  if (N.create(&prog, src.c_str(), "sv_section_jit.cu", kJitHeaderCount, kJitHeaderTexts, kJitHeaderNames) !=
+      NVRTC_SUCCESS) {
+    err = "nvrtcCreateProgram failed";
+    return false;
+  }
+  const char* sym_prog = "&sv::c_prog";
+  const char* sym_coef = dbl ? "&sv::c_coef64" : "&sv::c_coef32";
+  N.add_name(prog, sym_prog);
+  N.add_name(prog, sym_coef);
+  const char* opts[] = {"-arch=sm_100a", "-std=c++17", "-lineinfo", "-DSV_JIT_KERNEL=1"};
+  const nvrtcResult rc = N.compile(prog, 4, opts);
+  if (rc != NVRTC_SUCCESS) {
+    size_t n = 0;
+    N.log_size(prog, &n);
+    std::string log(n, '\0');
+    if (n) N.log(prog, &log[0]);
+    err = "NVRTC compile failed: " + log.substr(0, 4000);
+    N.destroy(&prog);
+    return false;
+  }
+  size_t nc = 0;
+  N.cubin_size(prog, &nc);
+  cubin.resize(nc);
+  N.cubin(prog, cubin.data());
+  const char* lp = nullptr;
+  const char* lc = nullptr;
+  if (N.lowered(prog, sym_prog, &lp) == NVRTC_SUCCESS && lp) name_prog = lp;
+  if (N.lowered(prog, sym_coef, &lc) == NVRTC_SUCCESS && lc) name_coef = lc;
+  N.destroy(&prog);
+  return true;
+}
+
+void build_entry(Entry& e, const std::string& src, int dev, bool dbl) {
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<char> cubin;
+  std::string name_prog, name_coef;
+  if (!compile_cubin(src, dbl, cubin, name_prog, name_coef, e.err)) {
+    static std::once_flag once;
+    std::call_once(once, [&] { std::fprintf(stderr, "[sv] JIT disabled for this kernel: %s\n", e.err.c_str()); });
+    e.state = 2;
+    return;
+  }
+  cudaSetDevice(dev);
+  cudaError_t ce = cudaLibraryLoadData(&e.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+  if (ce == cudaSuccess) ce = cudaLibraryGetKernel(&e.kern, e.lib, "sv_sec");
+  if (ce != cudaSuccess) {
+    e.err = std::string("module load failed: ") + cudaGetErrorString(ce);
+    cudaGetLastError();
+    e.state = 2;
+    return;
+  }
+  if (!name_prog.empty() && cudaLibraryGetGlobal(&e.c_prog, &e.c_prog_bytes, e.lib, name_prog.c_str()) != cudaSuccess)
+    e.c_prog = nullptr;
+  if (!name_coef.empty() && cudaLibraryGetGlobal(&e.c_coef, &e.c_coef_bytes, e.lib, name_coef.c_str()) != cudaSuccess)
+    e.c_coef = nullptr;
+  cudaGetLastError();
+  const size_t amp = dbl ? 16 : 8;
+  ce = cudaFuncSetAttribute(reinterpret_cast<const void*>(e.kern), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)((amp << 13) + 5 * SV_MAX_SETS * amp));
+  if (ce != cudaSuccess) {
+    e.err = std::string("cudaFuncSetAttribute failed: ") + cudaGetErrorString(ce);
+    cudaGetLastError();
+    e.state = 2;
+    return;
+  }
+  const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_ctr.compiled++;
+    g_ctr.compile_ms += ms;
+  }
+  e.state = 1;
+}
+
+// background compiler (mode async)
+struct Worker {
+  std::mutex mu;
+  std::condition_variable cv, idle;
+  std::deque<Job> q;
+  bool stop = false, busy = false;
+  std::thread th;
+  Worker() {
+    th = std::thread([this] {
+      for (;;) {
+        Job j;
+        {
+          std::unique_lock<std::mutex> lk(mu);
+          cv.wait(lk, [this] { return stop || !q.empty(); });
+          if (stop) return;
+          j = std::move(q.front());
+          q.pop_front();
+          busy = true;
+        }
+        build_entry(*j.e, j.src, j.dev, j.dbl);
+        {
+          std::lock_guard<std::mutex> lk(mu);
+          busy = false;
+        }
+        idle.notify_all();
+      }
+    });
+  }
+  ~Worker() {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      stop = true;
+    }
+    cv.notify_all();
+    if (th.joinable()) th.join();
+  }
+  void push(Job j) {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      q.push_back(std::move(j));
+    }
+    cv.notify_one();
+  }
+  void wait() {
+    std::unique_lock<std::mutex> lk(mu);
+    idle.wait(lk, [this] { return q.empty() && !busy; });
+  }
+};
+
+Worker& worker() {
+  static Worker w;
+  return w;
+}
+
+}  // namespace
+
+std::string jit_source(const int* prog_host, const Launch& L, bool dbl) { return gen_source(prog_host, L, dbl); }
+
+Status jit_compile_only(const int* prog_host, const Launch& L, bool dbl, const char* dump_dir, int index,
+                        double* ms) {
+  const auto t0 = std::chrono::steady_clock::now();
+  const std::string src = gen_source(prog_host, L, dbl);
+  std::vector<char> cubin;
+  std::string np, nc, err;
+  const bool ok = compile_cubin(src, dbl, cubin, np, nc, err);
+  *ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  if (dump_dir) {
+    const std::string base = std::string(dump_dir) + "/section_" + std::to_string(index);
+    std::ofstream(base + ".cu") << src;
+    if (ok) std::ofstream(base + ".cubin", std::ios::binary).write(cubin.data(), (std::streamsize)cubin.size());
+  }
+  if (!ok) return Status::err(nvrtc().ok ? SV_EMALFORMED : SV_EUNAVAILABLE, err);
+  return Status::ok();
+}
+
+bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const Launch& L, const int* prog_dev,
+                        const void* coef_dev, const void* aux_dev, cudaStream_t st, cudaError_t* err) {
+  *err = cudaSuccess;
+  const Mode m = mode();
+  if (m == kOff || L.T < SV_R_BITS) return false;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::string key(reinterpret_cast<const char*>(prog_host), L.int_count * sizeof(int));
+  key.push_back(dbl ? 'd' : 'f');
+  key.append(reinterpret_cast<const char*>(&dev), sizeof(dev));
+  std::shared_ptr<Entry> e;
+  bool fresh = false;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_cache.find(key);
+    if (it == g_cache.end()) {
+      e = std::make_shared<Entry>();
+      g_cache.emplace(key, e);
+      fresh = true;
+    } else {
+      e = it->second;
+    }
+  }
+  if (fresh) {
+    if (m == kSync)
+      build_entry(*e, gen_source(prog_host, L, dbl), dev, dbl);
+    else
+      worker().push(Job{e, gen_source(prog_host, L, dbl), dev, dbl});
+  }
+  if (e->state.load() != 1) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_ctr.fallbacks++;
+    return false;
+  }
+  const size_t amp = dbl ? 16 : 8;
+  if (e->c_prog) {
+    if (L.int_count * sizeof(int) > e->c_prog_bytes) return false;
+    *err = cudaMemcpyAsync(e->c_prog, prog_dev, L.int_count * sizeof(int), cudaMemcpyDeviceToDevice, st);
+    if (*err != cudaSuccess) return true;
+  }
+  if (e->c_coef && L.coef_count) {
+    if (L.coef_count * amp > e->c_coef_bytes) return false;
+    *err = cudaMemcpyAsync(e->c_coef, coef_dev, L.coef_count * amp, cudaMemcpyDeviceToDevice, st);
+    if (*err != cudaSuccess) return true;
+  }
+  void* a0 = sv;
+  void* a1 = const_cast<void*>(aux_dev);
+  void* args[] = {&a0, &a1};
+  const unsigned grid = (unsigned)(1ull << L.n_out);
+  const unsigned threads = 1u << (L.T - SV_R_BITS);
+  *err = cudaLaunchKernel(reinterpret_cast<const void*>(e->kern), dim3(grid), dim3(threads), args,
+                          smem_bytes(L, dbl), st);
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_ctr.hits++;
+  }
+  return true;
+}
+
+void jit_wait() {
+  if (mode() == kAsync) worker().wait();
+}
+
+JitCounters jit_counters() {
+  std::lock_guard<std::mutex> lk(g_mu);
+  return g_ctr;
+}
+
+}  // namespace sv

@@ -1,0 +1,45 @@
+// jit.h — run-time specialised section kernels (host C++; NVRTC + CUDA library API).
+//
+// The interpreter kernel (section.cu) walks a section's program from __constant__ memory; every
+// op pays a dispatch and the register file is reshuffled at each dispatch merge point.  Here the
+// same program (compile.cpp, already checked by the emulator and the parity tests) is printed as
+// straight-line CUDA — slots, maps and coefficient offsets become immediates — and compiled
+// for sm_100a with NVRTC.  Kernels are cached by the program's structure (its ints; coefficient
+// values stay run-time data in __constant__ memory), so a circuit with the same shape reuses
+// them.  Mode (environment SV_JIT):
+//   "sync"  (default) compile on first use, then launch the generated kernel;
+//   "async" launch the interpreter while a background thread compiles;
+//   "0"     interpreter only.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+
+#include "compile.h"
+
+namespace sv {
+
+struct JitCounters {
+  uint64_t compiled = 0;   // kernels built by NVRTC
+  uint64_t hits = 0;       // launches that found their kernel ready
+  uint64_t fallbacks = 0;  // launches that ran the interpreter (mode async / 0, or no NVRTC)
+  double compile_ms = 0;   // host time spent in NVRTC + module load
+};
+
+// Launch one section with its generated kernel.  Returns false if the caller must run the
+// interpreter instead (mode, compile pending or NVRTC unavailable); *err is the launch status.
+bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const Launch& L, const int* prog_dev,
+                        const void* coef_dev, const void* aux_dev, cudaStream_t st, cudaError_t* err);
+
+// Block until background compiles have finished (mode async).
+void jit_wait();
+JitCounters jit_counters();
+// Generated source of one launch (tests / debugging).
+std::string jit_source(const int* prog_host, const Launch& L, bool dbl);
+// Host only: generate + NVRTC-compile one launch (no module load); optionally dump
+// <dump_dir>/section_<index>.cu / .cubin.
+Status jit_compile_only(const int* prog_host, const Launch& L, bool dbl, const char* dump_dir, int index, double* ms);
+
+}  // namespace sv

@@ -83,6 +83,7 @@ struct SvSecHeader {
   int pad_sets[1];
 };
 
+#ifndef __CUDACC_RTC__
 // XOR-fold swizzle of a tile element index (host and device): the low G bits are XORed with
 // every higher G-bit group.  GF(2)-linear, so swz(a | b) = swz(a) ^ swz(b) for disjoint a, b.
 inline int sv_swz_host(int i, int G) {
@@ -93,6 +94,7 @@ inline int sv_swz_host(int i, int G) {
   }
   return i ^ (f & ((1 << G) - 1));
 }
+#endif
 
 struct SvPhase {
   int R[SV_R_BITS];    // register slot -> tile position
@@ -110,3 +112,33 @@ struct SvOp {
 static_assert(sizeof(SvSecHeader) % 16 == 0, "header alignment");
 static_assert(sizeof(SvPhase) % 16 == 0, "phase alignment");
 static_assert(sizeof(SvOp) % 16 == 0, "op alignment");
+
+// Field offsets in ints, for device code (NVRTC has no offsetof): checked against the structs.
+constexpr int kH_T = 0, kH_R = 1, kH_NOUT = 2, kH_NPH = 3, kH_PHOFF = 4, kH_OPOFF = 5, kH_NOPS = 6, kH_FLAGS = 7;
+constexpr int kH_TILE = 8, kH_STOREB = 24, kH_OUT = 40, kH_LOAD = 88, kH_STORE = 128, kH_DIN = 168, kH_DOUT = 208;
+constexpr int kH_NSETS = 248, kH_SETS = 249;
+constexpr int kM_TW = 0, kM_RW = 16, kM_TMB = 20, kM_RMB = 36;
+constexpr int kP_RW = 4, kP_OPB = 8, kP_OPC = 9, kP_TW = 28;
+constexpr int kPhaseInts = sizeof(SvPhase) / 4, kOpInts = sizeof(SvOp) / 4;
+#ifndef __CUDACC_RTC__
+#include <cstddef>
+#define SV_OFF(S, f) (int)(offsetof(S, f) / 4)
+static_assert(SV_OFF(SvSecHeader, T) == kH_T && SV_OFF(SvSecHeader, r) == kH_R && SV_OFF(SvSecHeader, n_out) == kH_NOUT &&
+                  SV_OFF(SvSecHeader, n_phases) == kH_NPH && SV_OFF(SvSecHeader, phase_off) == kH_PHOFF &&
+                  SV_OFF(SvSecHeader, op_off) == kH_OPOFF && SV_OFF(SvSecHeader, n_ops) == kH_NOPS &&
+                  SV_OFF(SvSecHeader, flags) == kH_FLAGS,
+              "header scalars");
+static_assert(SV_OFF(SvSecHeader, tile_bits) == kH_TILE && SV_OFF(SvSecHeader, store_bits) == kH_STOREB &&
+                  SV_OFF(SvSecHeader, out_bits) == kH_OUT && SV_OFF(SvSecHeader, load) == kH_LOAD &&
+                  SV_OFF(SvSecHeader, store) == kH_STORE && SV_OFF(SvSecHeader, din) == kH_DIN &&
+                  SV_OFF(SvSecHeader, dout) == kH_DOUT && SV_OFF(SvSecHeader, n_sets) == kH_NSETS &&
+                  SV_OFF(SvSecHeader, set_desc) == kH_SETS,
+              "header arrays");
+static_assert(SV_OFF(SvMap, tw) == kM_TW && SV_OFF(SvMap, rw) == kM_RW && SV_OFF(SvMap, tmb) == kM_TMB &&
+                  SV_OFF(SvMap, rmb) == kM_RMB,
+              "map");
+static_assert(SV_OFF(SvPhase, rw) == kP_RW && SV_OFF(SvPhase, op_begin) == kP_OPB &&
+                  SV_OFF(SvPhase, op_count) == kP_OPC && SV_OFF(SvPhase, tw) == kP_TW,
+              "phase");
+#undef SV_OFF
+#endif

@@ -78,3 +78,22 @@ def test_qft_qv_emulated(n, c):
 def test_ghz_permutation_ops_emulated():
     emulate(C.ghz(12), 12, 5)
     emulate(C.mirror(C.random_circuit(9, 60, 4, kinds=("cx", "swap", "u3"))), 9, 4)
+
+
+def test_free_initial_layout_emulated():
+    # sv_apply_circuit right after sv_reset(0): the planner picks the initial layout (NEXT-2);
+    # |0> sits at memory address 0 under every layout, so the emulated start state is exact.
+    rng = np.random.default_rng(11)
+    for t in range(40):
+        n = int(rng.integers(2, 17))
+        c = min(int(rng.integers(2, n + 1)), 13)
+        circ = C.random_circuit(n, int(rng.integers(0, 120)), 500 + t)
+        psi = np.zeros(1 << n, dtype=np.complex128)
+        psi[0] = 1
+        for prec in ("fp64", "fp32"):
+            emulate(circ, n, c, precision=prec, flags=sv.SV_FREE_LAYOUT, psi=psi.copy())
+    for n, c in [(12, 6), (14, 12), (16, 12)]:
+        psi = np.zeros(1 << n, dtype=np.complex128)
+        psi[0] = 1
+        emulate(C.qft(n), n, c, flags=sv.SV_FREE_LAYOUT, psi=psi.copy())
+        emulate(C.quantum_volume(n, 6, 2), n, c, flags=sv.SV_FREE_LAYOUT, psi=psi.copy())
