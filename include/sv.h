@@ -190,6 +190,13 @@ int sv_plan_circuit(const sv_gate* gates, size_t n_gates, int n, int chunk_bits,
 int sv_jit_compile_circuit(const sv_gate* gates, size_t n_gates, int n, int chunk_bits, int world_log2, int rank,
                            sv_precision prec, uint32_t flags, const char* dump_dir, int* n_kernels,
                            double* compile_ms);
+/* Process-wide section-kernel mode: 0 = program interpreter only, 1 = run-time specialised
+ * kernels compiled on first use (default; in parallel for all sections of a circuit), 2 = same,
+ * compiled in the background while the interpreter runs.  -1 queries.  The environment variable
+ * SV_JIT=0|sync|async sets the initial mode.  Returns the previous mode. */
+int sv_jit_mode(int mode);
+/* Block until background (mode 2) compiles have finished. */
+int sv_jit_wait(void);
 int sv_compile_circuit(const sv_gate* gates, size_t n_gates, int n, int chunk_bits, int world_log2,
                        int rank, sv_precision prec, const int32_t* pi0, const int32_t* sigma0,
                        uint32_t flags, int64_t** steps, size_t* n_steps,

@@ -43,7 +43,7 @@ class Stats(ctypes.Structure):
 EXPORTS = ["sv_create", "sv_create_dist", "sv_destroy", "sv_nccl_unique_id", "sv_reset", "sv_apply_circuit",
            "sv_synchronize", "sv_get_amplitudes", "sv_get_state", "sv_norm", "sv_probabilities", "sv_sample",
            "sv_get_permutation", "sv_stats_get", "sv_stats_reset", "sv_set_timing", "sv_last_error", "sv_block_circuit", "sv_plan_circuit",
-           "sv_compile_circuit", "sv_jit_compile_circuit", "sv_free",
+           "sv_compile_circuit", "sv_jit_compile_circuit", "sv_jit_mode", "sv_jit_wait", "sv_free",
            "sv_abi_version"]
 
 _lib = None
@@ -85,6 +85,8 @@ def lib():
                                 hp, ctypes.POINTER(sz), hp, ctypes.POINTER(sz), ip, ip], i32),
         "sv_jit_compile_circuit": ([vp, sz, i32, i32, i32, i32, i32, u32, ctypes.c_char_p, ip,
                                     ctypes.POINTER(ctypes.c_double)], i32),
+        "sv_jit_mode": ([i32], i32),
+        "sv_jit_wait": ([], i32),
         "sv_free": ([vp], None),
         "sv_abi_version": ([], i32),
     }
@@ -193,6 +195,19 @@ def jit_compile_circuit(gates, n: int, c: int, world_log2: int = 0, rank: int = 
                                       dump_dir.encode() if dump_dir else None, _ip(nk), ctypes.byref(ms))
     check(rc)
     return int(nk[0]), ms.value
+
+
+JIT_OFF, JIT_SYNC, JIT_ASYNC = 0, 1, 2
+
+
+def jit_mode(mode: int = -1) -> int:
+    """Set (0 interpreter, 1 sync, 2 async) or query (-1) the process-wide section-kernel mode;
+    returns the previous mode (sv_jit_mode)."""
+    return int(lib().sv_jit_mode(mode))
+
+
+def jit_wait() -> None:
+    check(lib().sv_jit_wait())
 
 
 def nccl_unique_id() -> bytes:

@@ -629,6 +629,7 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
     launch_end[i] = h->prog.launches.size();
   }
   h->stats.pass_ms = now_ms() - t0;
+  jit_prepare(h->prog, h->dbl);  // run-time specialised kernels (jit.h): compile what is missing
   if (int rc = upload_program(h)) return rc;
   size_t si = 0;
   for (size_t i = 0; i < steps.size(); i++) {
@@ -1130,5 +1131,12 @@ extern "C" int sv_jit_compile_circuit(const sv_gate* gates, size_t n_gates, int 
   }
   if (n_kernels) *n_kernels = k;
   if (compile_ms) *compile_ms = total;
+  return SV_OK;
+}
+
+extern "C" int sv_jit_mode(int mode) { return jit_set_mode(mode); }
+
+extern "C" int sv_jit_wait(void) {
+  jit_wait();
   return SV_OK;
 }

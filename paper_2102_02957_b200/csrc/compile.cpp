@@ -215,6 +215,82 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
     phases.push_back(ph);
   }
 
+  // Shared-memory swizzle of this section: tile position p -> word (a GF(2)-linear, invertible
+  // map; every smem offset is an XOR of words).  p < G keeps 1 << p; p >= G adds a nonzero G-bit
+  // vector vec[p] to the low bits.  A 2^G-lane group then covers the 2^G 16- (fp64) or 8-byte
+  // (fp32) slots of a 128-byte wavefront exactly when its G lane bits carry independent vectors:
+  // the load map's lanes are positions 0..G-1, the store map's are the positions of the lowest
+  // store memory bits, and each phase picks G independent thread positions (below).  The vectors
+  // are searched so every phase's thread positions span GF(2)^G.
+  const int G = swizzle_bits;
+  int store_bits[16];
+  for (int j = 0; j < T; j++) store_bits[j] = tile_bits[j];
+  for (const auto& sw : store_swaps) {  // physical bit swaps fused into the store (plan.cpp)
+    const int p1 = sw.first < 64 ? pos_of[sw.first] : -1, p2 = sw.second < 64 ? pos_of[sw.second] : -1;
+    if (p1 < 0 || p2 < 0) return Status::err(SV_EMALFORMED, "internal: store swap outside the tile");
+    std::swap(store_bits[p1], store_bits[p2]);
+  }
+  int swz[SV_TMAX];
+  {
+    const int nseq = (1 << G) - 1;
+    auto span_of = [&](const int* v, const std::vector<int>& pos) {
+      uint32_t span = 1;
+      for (int p : pos) {
+        uint32_t g2 = span;
+        for (int u = 0; u < (1 << G); u++)
+          if ((span >> u) & 1) g2 |= 1u << (u ^ v[p]);
+        span = g2;
+      }
+      return span;
+    };
+    const uint32_t full = (1u << (1 << G)) - 1;  // all 2^G vectors reachable
+    int order[16];
+    for (int j = 0; j < T; j++) order[j] = j;
+    std::sort(order, order + T, [&](int a, int b) { return store_bits[a] < store_bits[b]; });
+    std::vector<int> store_lanes(order, order + std::min(G, T));
+    std::vector<std::vector<int>> thread_pos;
+    for (const Ph& ph : phases) {
+      std::vector<int> tp;
+      for (int pos = 0; pos < T; pos++)
+        if (std::find(ph.R.begin(), ph.R.end(), pos) == ph.R.end()) tp.push_back(pos);
+      thread_pos.push_back(tp);
+    }
+    auto score = [&](const int* v) {  // constraints met (higher is better)
+      int sc = 0;
+      if (T - r >= G && span_of(v, store_lanes) == full) sc += 1000;
+      for (const auto& tp : thread_pos)
+        if ((int)tp.size() >= G && span_of(v, tp) == full) sc++;
+      return sc;
+    };
+    int target = (T - r >= G ? 1000 : 0);
+    for (const auto& tp : thread_pos)
+      if ((int)tp.size() >= G) target++;
+    int vec[SV_TMAX], best[SV_TMAX];
+    uint64_t rng = 0x9E3779B97F4A7C15ull ^ ((uint64_t)T << 32) ^ phases.size();
+    int best_sc = -1;
+    for (int attempt = 0; attempt < 256 && best_sc < target; attempt++) {
+      for (int pos = 0; pos < T; pos++) {
+        if (pos < G) {
+          vec[pos] = 1 << pos;
+        } else if (attempt == 0) {
+          vec[pos] = 1 + (pos - G) % nseq;  // deterministic first try
+        } else {
+          rng ^= rng << 13;
+          rng ^= rng >> 7;
+          rng ^= rng << 17;
+          vec[pos] = 1 + (int)(rng % (uint64_t)nseq);
+        }
+      }
+      const int sc = score(vec);
+      if (sc > best_sc) {
+        best_sc = sc;
+        std::copy(vec, vec + T, best);
+      }
+    }
+    for (int pos = 0; pos < T; pos++) swz[pos] = pos < G ? (1 << pos) : ((1 << pos) | best[pos]);
+  }
+  auto low_vec = [&](int pos) { return swz[pos] & ((1 << G) - 1); };
+
   // ---- per phase: thread-bit order, then the op items (single ops or fused diagonal runs)
   struct Item {
     int gate = -1;           // single op: index into pg
@@ -232,20 +308,22 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
     std::fill(po.slot_of, po.slot_of + SV_TMAX, -1);
     std::fill(po.thread_of, po.thread_of + SV_TMAX, -1);
     for (int s = 0; s < r; s++) po.slot_of[ph.R[s]] = s;
-    // thread bits: the first `swizzle_bits` get distinct residues mod swizzle_bits so a group of
-    // 2^swizzle_bits lanes hits distinct 16-/8-byte bank groups under the XOR-fold swizzle.
+    // thread bits: the first G get linearly independent swizzle vectors (lowest positions first,
+    // so lanes walk the lowest memory bits where they can: direct HBM boundaries need that)
     std::vector<int> cand;
     for (int pos = 0; pos < T; pos++)
       if (po.slot_of[pos] < 0) cand.push_back(pos);
-    uint32_t used_res = 0;
     std::vector<bool> taken(cand.size(), false);
-    for (size_t i = 0; i < cand.size() && (int)po.chosen.size() < swizzle_bits; i++) {
-      const int res = cand[i] % swizzle_bits;
-      if (!((used_res >> res) & 1)) {
-        used_res |= 1u << res;
-        po.chosen.push_back(cand[i]);
-        taken[i] = true;
-      }
+    uint32_t span = 1;  // bit v set: vector v is an XOR of chosen vectors (v = 0 always)
+    for (size_t i = 0; i < cand.size() && (int)po.chosen.size() < G; i++) {
+      const int vec = low_vec(cand[i]);
+      if ((span >> vec) & 1) continue;
+      uint32_t grown = span;
+      for (int u = 0; u < (1 << G); u++)
+        if ((span >> u) & 1) grown |= 1u << (u ^ vec);
+      span = grown;
+      po.chosen.push_back(cand[i]);
+      taken[i] = true;
     }
     for (size_t i = 0; i < cand.size(); i++)
       if (!taken[i]) po.chosen.push_back(cand[i]);
@@ -317,13 +395,6 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
   H()->phase_off = header_ints;
   H()->op_off = header_ints + phase_ints * (int)phases.size();
   H()->n_ops = (int)n_items;
-  int store_bits[16];
-  for (int j = 0; j < T; j++) store_bits[j] = tile_bits[j];
-  for (const auto& sw : store_swaps) {  // physical bit swaps fused into the store (plan.cpp)
-    const int p1 = sw.first < 64 ? pos_of[sw.first] : -1, p2 = sw.second < 64 ? pos_of[sw.second] : -1;
-    if (p1 < 0 || p2 < 0) return Status::err(SV_EMALFORMED, "internal: store swap outside the tile");
-    std::swap(store_bits[p1], store_bits[p2]);
-  }
   for (int j = 0; j < T; j++) {
     H()->tile_bits[j] = tile_bits[j];
     H()->store_bits[j] = store_bits[j];
@@ -331,11 +402,11 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
   for (int j = 0; j < n_out; j++) H()->out_bits[j] = out_bits[j];
   auto fill_map = [&](SvMap& m, const int* tpos, const int* R, const int* bits) {
     for (int j = 0; j < T - r; j++) {
-      m.tw[j] = sv_swz_host(1 << tpos[j], swizzle_bits);
+      m.tw[j] = swz[tpos[j]];
       m.tmb[j] = bits[tpos[j]];
     }
     for (int s = 0; s < r; s++) {
-      m.rw[s] = sv_swz_host(1 << R[s], swizzle_bits);
+      m.rw[s] = swz[R[s]];
       m.rmb[s] = bits[R[s]];
     }
   };
@@ -378,11 +449,11 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
     const PhaseOut& po = pout[pi];
     for (int s = 0; s < r; s++) {
       P->R[s] = ph.R[s];
-      P->rw[s] = sv_swz_host(1 << ph.R[s], swizzle_bits);
+      P->rw[s] = swz[ph.R[s]];
     }
     for (size_t j = 0; j < po.chosen.size(); j++) {
       P->tpos[j] = po.chosen[j];
-      P->tw[j] = sv_swz_host(1 << po.chosen[j], swizzle_bits);
+      P->tw[j] = swz[po.chosen[j]];
     }
     // a direct HBM boundary needs lane j of each 2^swizzle_bits group on memory bit j (128 B runs)
     auto lanes_on_low_bits = [&](const int* bits) {

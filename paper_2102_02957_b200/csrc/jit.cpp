@@ -10,6 +10,7 @@
 #include <dlfcn.h>
 #include <nvrtc.h>
 
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
@@ -74,19 +75,36 @@ Nvrtc& nvrtc() {
 }
 
 enum Mode { kOff = 0, kSync = 1, kAsync = 2 };
+std::atomic<int> g_mode{-1};
 Mode mode() {
-  static const Mode m = [] {
+  int m = g_mode.load();
+  if (m < 0) {
     const char* e = std::getenv("SV_JIT");
-    if (!e || !*e || !std::strcmp(e, "sync") || !std::strcmp(e, "1")) return kSync;
-    if (!std::strcmp(e, "async")) return kAsync;
-    return kOff;
-  }();
-  return m;
+    m = (!e || !*e || !std::strcmp(e, "sync") || !std::strcmp(e, "1")) ? kSync : !std::strcmp(e, "async") ? kAsync : kOff;
+    int expect = -1;
+    g_mode.compare_exchange_strong(expect, m);
+    m = g_mode.load();
+  }
+  return (Mode)m;
 }
 
 // ------------------------------------------------------------------------------------ source
+// Pipelined variant (gen_source_pipelined): two warp groups per CTA work on alternate tiles of
+// a persistent CTA with three tile buffers in shared memory, each group loading its next tile
+// with cp.async while it computes the current one.
+constexpr int kPipeSetsBytes = 2 * 5 * SV_MAX_SETS;  // per-CTA factor slots (both groups), in amplitudes
+bool pipelined(const Launch& L, bool dbl) {
+  static const bool on = [] {
+    const char* e = std::getenv("SV_PIPE");
+    return !(e && e[0] == '0');
+  }();
+  const size_t amp = dbl ? 16 : 8;
+  return on && L.T >= 9 && L.T <= 12 && 3 * (amp << L.T) + kPipeSetsBytes * amp + 64 <= 227 * 1024;
+}
+
 size_t smem_bytes(const Launch& L, bool dbl) {
   const size_t amp = dbl ? 16 : 8;
+  if (pipelined(L, dbl)) return 3 * (amp << L.T) + kPipeSetsBytes * amp + 64;
   const bool no_smem = L.n_phases == 1 && (L.flags & SV_FLAG_FIRST_DIRECT) && (L.flags & SV_FLAG_LAST_DIRECT);
   if (L.n_sets) return (amp << L.T) + 5 * SV_MAX_SETS * amp;
   return no_smem ? 0 : amp << L.T;
@@ -135,7 +153,10 @@ struct Gen {
   void stg() { o << "#pragma unroll\n    for (int k = 0; k < 16; k++) psi[b + RO[k]] = v[k];\n"; }
 };
 
+std::string gen_source_pipelined(const int* p, const Launch& L, bool dbl);
+
 std::string gen_source(const int* p, const Launch& L, bool dbl) {
+  if (pipelined(L, dbl)) return gen_source_pipelined(p, L, dbl);
   const SvSecHeader* H = reinterpret_cast<const SvSecHeader*>(p);
   Gen g;
   g.T = H->T;
@@ -189,7 +210,7 @@ std::string gen_source(const int* p, const Launch& L, bool dbl) {
     for (int i = 0; i < ph[k].op_count; i++) {
       const SvOp& op = ops[ph[k].op_begin + i];
       o << "    op_c<" << op.type << ", " << op.a << ", " << op.b << ", " << op.coef << ", " << op.extra
-        << ">(v, tid, tile_off, aux, ctaf);\n";
+        << ">(v, tid, " << nt << ", tile_off, aux, ctaf);\n";
     }
     if (dout) {
       o << "    {\n";
@@ -215,6 +236,120 @@ std::string gen_source(const int* p, const Launch& L, bool dbl) {
   return o.str();
 }
 
+// Persistent CTA, two warp groups of 2^(T-4) threads, three tile buffers.  The CTA's tiles
+// j = 0, 1, 2, ... (tile blockIdx.x + j * gridDim.x) alternate between the groups and tile j
+// lives in buffer j % 3.  Buffer (j + 2) % 3 is released when the other group finishes tile
+// j - 1 (done[] in shared memory), and the group computing tile j then issues the cp.async
+// loads of its next tile j + 2 there: at the first phase boundary that sees the release, or at
+// the end of tile j.  Phase barriers are named barriers of the group, so the two groups drift
+// freely and one group's loads / shared-memory traffic overlap the other's arithmetic.
+std::string gen_source_pipelined(const int* p, const Launch& L, bool dbl) {
+  (void)L;
+  const SvSecHeader* H = reinterpret_cast<const SvSecHeader*>(p);
+  Gen g;
+  g.T = H->T;
+  g.ntl = H->T - SV_R_BITS;
+  const int nt = 1 << g.ntl;
+  const bool last = H->flags & SV_FLAG_LAST_DIRECT;
+  const int nph = H->n_phases;
+  auto& o = g.o;
+  o << "#include \"section_dev.cuh\"\nusing namespace sv;\ntypedef " << (dbl ? "double2" : "float2") << " V;\n";
+  o << "constexpr int NTG = " << nt << ", TILE = " << (1 << H->T) << ";\n";
+  o << "extern \"C\" __global__ void __launch_bounds__(" << 2 * nt
+    << ", 1) sv_sec(V* __restrict__ psi, const V* __restrict__ aux) {\n";
+  o << "  extern __shared__ __align__(128) unsigned char smem_raw[];\n"
+    << "  V* const bufs = reinterpret_cast<V*>(smem_raw);\n"
+    << "  V* const ctaf_all = bufs + 3 * TILE;\n"
+    << "  int* const done = reinterpret_cast<int*>(ctaf_all + " << kPipeSetsBytes << ");\n"
+    << "  const int grp = threadIdx.x / NTG, tid = threadIdx.x % NTG, bar = 1 + grp;\n"
+    << "  V* const ctaf = ctaf_all + grp * " << 5 * SV_MAX_SETS << ";\n"
+    << "  (void)ctaf; (void)aux;\n"
+    << "  constexpr unsigned long long NTILES = 1ull << " << H->n_out << ";\n";
+  g.arr("int", "OB", H->out_bits, H->n_out);
+  o << "  auto tile_of = [&](uint64_t t) {\n    uint64_t r = 0;\n#pragma unroll\n    for (int j = 0; j < "
+    << H->n_out << "; j++) r |= ((t >> j) & 1ull) << OB[j];\n    return r;\n  };\n"
+    << "  auto blk_of = [&](long long j) { return (uint64_t)blockIdx.x + (uint64_t)j * gridDim.x; };\n";
+  {  // load map: thread part of the HBM offset and of the swizzled smem offset (tile-invariant)
+    long long ro[16];
+    int w[16];
+    for (int k = 0; k < 16; k++) {
+      ro[k] = 0;
+      w[k] = 0;
+      for (int s = 0; s < SV_R_BITS; s++)
+        if ((k >> s) & 1) {
+          ro[k] |= 1ll << H->load.rmb[s];
+          w[k] ^= H->load.rw[s];
+        }
+    }
+    g.arr("int", "LTMB", H->load.tmb, g.ntl);
+    g.arr("int", "LTW", H->load.tw, g.ntl);
+    g.arr("long long", "LRO", ro, 16);
+    g.arr("int", "LW", w, 16);
+  }
+  o << "  uint64_t lb = 0;\n  int lx = 0;\n#pragma unroll\n  for (int j = 0; j < " << g.ntl
+    << "; j++) {\n    lb |= (uint64_t)((tid >> j) & 1) << LTMB[j];\n    lx ^= ((tid >> j) & 1) ? LTW[j] : 0;\n  }\n";
+  o << "  auto issue = [&](long long j) {\n    V* dst = bufs + (int)(j % 3) * TILE;\n"
+    << "    const V* src = psi + (tile_of(blk_of(j)) | lb);\n#pragma unroll\n"
+    << "    for (int k = 0; k < 16; k++) cp_async_v(dst + (lx ^ LW[k]), src + LRO[k]);\n    cp_async_commit();\n  };\n";
+  o << "  if (threadIdx.x < 3) done[threadIdx.x] = (int)threadIdx.x - 3;  // tile -3 + b 'finished' in buffer b\n"
+    << "  __syncthreads();\n"
+    << "  long long j = grp;\n  if (blk_of(j) < NTILES) issue(j);\n"
+    << "#pragma unroll 1\n"  // keep the tile body single: unrolling it doubles compile time and code
+    << "  for (; blk_of(j) < NTILES; j += 2) {\n"
+    << "    V* const sm = bufs + (int)(j % 3) * TILE;\n"
+    << "    const bool want = blk_of(j + 2) < NTILES;\n"
+    << "    int* const nxt_done = done + (int)((j + 2) % 3);\n"
+    << "    bool issued = false;\n"
+    << "    const uint64_t tile_off = tile_of(blk_of(j));\n";
+  if (H->n_sets > 0) {
+    o << "    for (int f = tid; f < " << 5 * H->n_sets << "; f += NTG) {\n"
+      << "      const int d = c_prog[kH_SETS + f / 5], i = f % 5;\n"
+      << "      ctaf[f] = cta_factor<V>(c_prog[d + 2 + i], c_prog[d + 3 + i], tile_off);\n    }\n";
+  }
+  o << "    cp_async_wait<0>();\n    group_sync<NTG>(bar);\n    V v[16];\n";
+  const SvPhase* ph = reinterpret_cast<const SvPhase*>(p + H->phase_off);
+  const SvOp* ops = reinterpret_cast<const SvOp*>(p + H->op_off);
+  for (int k = 0; k < nph; k++) {
+    const bool dout = last && k == nph - 1;
+    o << "  {  // phase " << k << "\n";
+    g.smem(ph[k].tw, ph[k].rw);
+    g.lds();
+    for (int i = 0; i < ph[k].op_count; i++) {
+      const SvOp& op = ops[ph[k].op_begin + i];
+      o << "    op_c<" << op.type << ", " << op.a << ", " << op.b << ", " << op.coef << ", " << op.extra
+        << ">(v, tid, NTG, tile_off, aux, ctaf);\n";
+    }
+    if (dout) {
+      o << "    {\n";
+      g.hbm(H->dout);
+      g.stg();
+      o << "    }\n";
+    } else {
+      g.sts();
+      o << "    if (want && !issued) {\n"
+        << "      if (group_sync_or<NTG>(bar, ld_volatile(nxt_done) >= j - 1)) {\n"
+        << "        issue(j + 2);\n        issued = true;\n      }\n"
+        << "    } else {\n      group_sync<NTG>(bar);\n    }\n";
+    }
+    o << "  }\n";
+  }
+  if (!last) {
+    o << "  {  // gather in store order, lanes walk the lowest store memory bits\n";
+    g.smem(H->store.tw, H->store.rw);
+    g.lds();
+    g.hbm(H->store);
+    g.stg();
+    o << "  }\n";
+  }
+  o << "    group_sync<NTG>(bar);  // every read of this buffer is done: release it\n"
+    << "    if (tid == 0) st_release(done + (int)(j % 3), (int)j);\n"
+    << "    if (want && !issued) {\n"
+    << "      while (ld_volatile(nxt_done) < j - 1) {\n      }\n"
+    << "      issue(j + 2);\n    }\n"
+    << "  }\n}\n";
+  return o.str();
+}
+
 // ------------------------------------------------------------------------------------ cache
 struct Entry {
   std::atomic<int> state{0};  // 0 pending, 1 ready, 2 failed
@@ -224,6 +359,7 @@ struct Entry {
   size_t c_prog_bytes = 0;
   void* c_coef = nullptr;
   size_t c_coef_bytes = 0;
+  uint64_t occ = 0;  // resident CTAs on the device (pipelined variant's grid)
   std::string err;
 };
 
@@ -305,7 +441,7 @@ void build_entry(Entry& e, const std::string& src, int dev, bool dbl) {
   cudaGetLastError();
   const size_t amp = dbl ? 16 : 8;
   ce = cudaFuncSetAttribute(reinterpret_cast<const void*>(e.kern), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)((amp << 13) + 5 * SV_MAX_SETS * amp));
+                            227 * 1024);  // the opt-in maximum; occupancy follows the launch size
   if (ce != cudaSuccess) {
     e.err = std::string("cudaFuncSetAttribute failed: ") + cudaGetErrorString(ce);
     cudaGetLastError();
@@ -396,6 +532,58 @@ Status jit_compile_only(const int* prog_host, const Launch& L, bool dbl, const c
   return Status::ok();
 }
 
+namespace {
+std::string make_key(const int* prog_host, const Launch& L, bool dbl, int dev) {
+  std::string key(reinterpret_cast<const char*>(prog_host), L.int_count * sizeof(int));
+  key.push_back(dbl ? 'd' : 'f');
+  key.append(reinterpret_cast<const char*>(&dev), sizeof(dev));
+  return key;
+}
+}  // namespace
+
+int jit_set_mode(int m) {
+  const int prev = mode();
+  if (m >= 0 && m <= 2) g_mode.store(m);
+  return prev;
+}
+
+void jit_prepare(const Program& prog, bool dbl) {
+  const Mode m = mode();
+  if (m == kOff) return;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::vector<std::pair<std::shared_ptr<Entry>, std::string>> todo;
+  for (const Launch& L : prog.launches) {
+    if (L.T < SV_R_BITS) continue;
+    const int* p = prog.ints.data() + L.int_off;
+    std::string key = make_key(p, L, dbl, dev);
+    std::shared_ptr<Entry> e;
+    {
+      std::lock_guard<std::mutex> lk(g_mu);
+      if (g_cache.count(key)) continue;
+      e = std::make_shared<Entry>();
+      g_cache.emplace(std::move(key), e);
+    }
+    todo.emplace_back(e, gen_source(p, L, dbl));
+  }
+  if (todo.empty()) return;
+  if (m == kAsync) {
+    for (auto& t : todo) worker().push(Job{t.first, std::move(t.second), dev, dbl});
+    return;
+  }
+  // sync: compile the missing kernels in parallel (NVRTC is thread-safe per program)
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const unsigned nth = std::min<unsigned>(hw, (unsigned)todo.size());
+  std::atomic<size_t> next{0};
+  auto run = [&] {
+    for (size_t i; (i = next.fetch_add(1)) < todo.size();) build_entry(*todo[i].first, todo[i].second, dev, dbl);
+  };
+  std::vector<std::thread> th;
+  for (unsigned t = 1; t < nth; t++) th.emplace_back(run);
+  run();
+  for (auto& t : th) t.join();
+}
+
 bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const Launch& L, const int* prog_dev,
                         const void* coef_dev, const void* aux_dev, cudaStream_t st, cudaError_t* err) {
   *err = cudaSuccess;
@@ -403,9 +591,7 @@ bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const Launch& 
   if (m == kOff || L.T < SV_R_BITS) return false;
   int dev = 0;
   cudaGetDevice(&dev);
-  std::string key(reinterpret_cast<const char*>(prog_host), L.int_count * sizeof(int));
-  key.push_back(dbl ? 'd' : 'f');
-  key.append(reinterpret_cast<const char*>(&dev), sizeof(dev));
+  std::string key = make_key(prog_host, L, dbl, dev);
   std::shared_ptr<Entry> e;
   bool fresh = false;
   {
@@ -444,8 +630,21 @@ bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const Launch& 
   void* a0 = sv;
   void* a1 = const_cast<void*>(aux_dev);
   void* args[] = {&a0, &a1};
-  const unsigned grid = (unsigned)(1ull << L.n_out);
-  const unsigned threads = 1u << (L.T - SV_R_BITS);
+  const unsigned threads = (pipelined(L, dbl) ? 2u : 1u) << (L.T - SV_R_BITS);
+  unsigned grid = (unsigned)(1ull << L.n_out);
+  if (pipelined(L, dbl)) {  // persistent: one wave of resident CTAs
+    if (e->occ == 0) {
+      int sms = 0, nb = 0;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, reinterpret_cast<const void*>(e->kern), (int)threads,
+                                                        smem_bytes(L, dbl)) != cudaSuccess || nb < 1)
+        nb = 1;
+      cudaGetLastError();
+      e->occ = (uint64_t)nb * (uint64_t)sms;
+    }
+    const uint64_t pairs = ((1ull << L.n_out) + 1) / 2;  // each CTA runs two groups
+    grid = (unsigned)std::min<uint64_t>(e->occ, std::max<uint64_t>(1, pairs));
+  }
   *err = cudaLaunchKernel(reinterpret_cast<const void*>(e->kern), dim3(grid), dim3(threads), args,
                           smem_bytes(L, dbl), st);
   {

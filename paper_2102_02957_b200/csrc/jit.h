@@ -33,6 +33,11 @@ struct JitCounters {
 bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const Launch& L, const int* prog_dev,
                         const void* coef_dev, const void* aux_dev, cudaStream_t st, cudaError_t* err);
 
+// Make sure every launch of the program has its kernel: mode sync compiles the missing ones in
+// parallel now, mode async queues them.
+void jit_prepare(const Program& prog, bool dbl);
+// Process-wide mode: 0 off, 1 sync, 2 async, -1 query; returns the previous mode.
+int jit_set_mode(int mode);
 // Block until background compiles have finished (mode async).
 void jit_wait();
 JitCounters jit_counters();

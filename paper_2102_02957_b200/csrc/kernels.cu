@@ -143,20 +143,66 @@ struct QBits {
   int b[24];
 };
 
+// Marginal probabilities, task form: a warp task fixes every memory bit except the 5 lane bits
+// (consecutive amplitudes: coalesced) and up to 6 "iteration" bits that are not marginal bits,
+// so each lane's bin is fixed for the whole task and it accumulates in a register; lanes then
+// reduce over their non-marginal lane bits by shuffles and one lane per bin adds to the
+// histogram (shared memory per CTA, or global for > 12 bits).  One atomic per bin per task.
+struct MargPlan {
+  int nq, nit, ntb;
+  uint32_t lane_q;  // lane bits (0..4) that are marginal bits
+  int qb[24];       // bin bit i <- memory bit qb[i]
+  int it_b[8];      // iteration bits (not marginal, >= 5)
+  int task_b[64];   // all other bits >= 5
+};
+
 template <typename V>
-__global__ void k_marginal_smem(const V* __restrict__ sv, uint64_t N, QBits q, int nq, double* __restrict__ partial) {
+__global__ void k_marginal_tasks(const V* __restrict__ sv, MargPlan p, double* __restrict__ dst, int use_smem) {
   extern __shared__ double hist[];
-  const int bins = 1 << nq;
-  for (int i = threadIdx.x; i < bins; i += blockDim.x) hist[i] = 0.0;
-  __syncthreads();
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < N; x += stride) {
+  const int bins = 1 << p.nq;
+  if (use_smem) {
+    for (int i = threadIdx.x; i < bins; i += blockDim.x) hist[i] = 0.0;
+    __syncthreads();
+  }
+  const int lane = threadIdx.x & 31;
+  int y_lane = 0;
+  for (int i = 0; i < p.nq; i++)
+    if (p.qb[i] < 5) y_lane |= ((lane >> p.qb[i]) & 1) << i;
+  const uint32_t nonq = ~p.lane_q & 31u;
+  const uint64_t ntasks = 1ull << p.ntb;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const int niter = 1 << p.nit;
+  for (uint64_t t = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ntasks; t += nwarps) {
+    uint64_t x0 = (uint64_t)lane;
+    for (int j = 0; j < p.ntb; j++) x0 |= ((t >> j) & 1ull) << p.task_b[j];
+    int y = y_lane;
+    for (int i = 0; i < p.nq; i++)
+      if (p.qb[i] >= 5) y |= (int)((x0 >> p.qb[i]) & 1ull) << i;
+    double acc = 0.0;
+#pragma unroll 8
+    for (int it = 0; it < niter; it++) {
+      uint64_t x = x0;
+      for (int j = 0; j < p.nit; j++) x |= (uint64_t)((it >> j) & 1) << p.it_b[j];
+      acc += abs2(sv[x]);
+    }
+#pragma unroll
+    for (int j = 0; j < 5; j++)
+      if ((nonq >> j) & 1) acc += __shfl_xor_sync(0xffffffffu, acc, 1 << j);
+    if ((lane & nonq) == 0) atomicAdd(&(use_smem ? hist : dst)[y], acc);
+  }
+  if (use_smem) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < bins; i += blockDim.x) dst[(size_t)blockIdx.x * bins + i] = hist[i];
+  }
+}
+
+template <typename V>
+__global__ void k_marginal_small(const V* __restrict__ sv, uint64_t N, QBits q, int nq, double* __restrict__ out) {
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < N; x += (uint64_t)gridDim.x * blockDim.x) {
     int y = 0;
     for (int i = 0; i < nq; i++) y |= (int)((x >> q.b[i]) & 1) << i;
-    atomicAdd(&hist[y], abs2(sv[x]));
+    atomicAdd(&out[y], abs2(sv[x]));
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < bins; i += blockDim.x) partial[(size_t)blockIdx.x * bins + i] = hist[i];
 }
 
 __global__ void k_reduce_bins(const double* __restrict__ partial, int blocks, int bins, double* __restrict__ out) {
@@ -164,16 +210,6 @@ __global__ void k_reduce_bins(const double* __restrict__ partial, int blocks, in
     double s = 0.0;
     for (int bk = 0; bk < blocks; bk++) s += partial[(size_t)bk * bins + y];
     out[y] = s;
-  }
-}
-
-template <typename V>
-__global__ void k_marginal_global(const V* __restrict__ sv, uint64_t N, QBits q, int nq, double* __restrict__ out) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < N; x += stride) {
-    uint64_t y = 0;
-    for (int i = 0; i < nq; i++) y |= ((x >> q.b[i]) & 1ull) << i;
-    atomicAdd(&out[y], abs2(sv[x]));
   }
 }
 
@@ -361,25 +397,45 @@ size_t marginal_scratch_doubles(int nq) { return nq <= kMargSmemBits ? (size_t)k
 cudaError_t launch_marginal(bool dbl, const void* sv, int nL, const int* qbits, int nq, double* scratch,
                             double* out_dev, cudaStream_t st) {
   if (nq > 24) return cudaErrorInvalidValue;
-  QBits q;
-  for (int i = 0; i < nq; i++) q.b[i] = qbits[i];
   const uint64_t N = 1ull << nL;
   const int bins = 1 << nq;
-  if (nq <= kMargSmemBits) {
-    const size_t smem = sizeof(double) * bins;
-    if (dbl)
-      k_marginal_smem<double2><<<kMargBlocks, 512, smem, st>>>((const double2*)sv, N, q, nq, scratch);
-    else
-      k_marginal_smem<float2><<<kMargBlocks, 512, smem, st>>>((const float2*)sv, N, q, nq, scratch);
-    k_reduce_bins<<<grid_for(bins, 256), 256, 0, st>>>(scratch, kMargBlocks, bins, out_dev);
-  } else {
+  if (nL < 11) {  // tiny shards: one atomic per amplitude
+    QBits q;
+    for (int i = 0; i < nq; i++) q.b[i] = qbits[i];
     cudaError_t e = cudaMemsetAsync(out_dev, 0, sizeof(double) * bins, st);
     if (e != cudaSuccess) return e;
     if (dbl)
-      k_marginal_global<double2><<<grid_for(N, 256), 256, 0, st>>>((const double2*)sv, N, q, nq, out_dev);
+      k_marginal_small<double2><<<grid_for(N, 256), 256, 0, st>>>((const double2*)sv, N, q, nq, out_dev);
     else
-      k_marginal_global<float2><<<grid_for(N, 256), 256, 0, st>>>((const float2*)sv, N, q, nq, out_dev);
+      k_marginal_small<float2><<<grid_for(N, 256), 256, 0, st>>>((const float2*)sv, N, q, nq, out_dev);
+    return cudaGetLastError();
   }
+  MargPlan p{};
+  p.nq = nq;
+  uint64_t qmask = 0;
+  for (int i = 0; i < nq; i++) {
+    p.qb[i] = qbits[i];
+    qmask |= 1ull << qbits[i];
+  }
+  p.lane_q = (uint32_t)(qmask & 31u);
+  for (int b = 5; b < nL; b++) {
+    if (!((qmask >> b) & 1) && p.nit < 6)
+      p.it_b[p.nit++] = b;
+    else
+      p.task_b[p.ntb++] = b;
+  }
+  const bool smem = nq <= kMargSmemBits;
+  if (!smem) {
+    cudaError_t e = cudaMemsetAsync(out_dev, 0, sizeof(double) * bins, st);
+    if (e != cudaSuccess) return e;
+  }
+  double* dst = smem ? scratch : out_dev;
+  const size_t shm = smem ? sizeof(double) * bins : 0;
+  if (dbl)
+    k_marginal_tasks<double2><<<kMargBlocks, 512, shm, st>>>((const double2*)sv, p, dst, smem ? 1 : 0);
+  else
+    k_marginal_tasks<float2><<<kMargBlocks, 512, shm, st>>>((const float2*)sv, p, dst, smem ? 1 : 0);
+  if (smem) k_reduce_bins<<<grid_for(bins, 256), 256, 0, st>>>(scratch, kMargBlocks, bins, out_dev);
   return cudaGetLastError();
 }
 

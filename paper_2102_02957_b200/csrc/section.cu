@@ -87,7 +87,7 @@ __device__ __forceinline__ void run_op(V (&v)[16], int oi, int tid, uint64_t til
       break;
     }
     case SV_OP_DIAGSET:
-      diagset(v, a, cb, tid, tile_off, aux, ctaf);
+      diagset(v, a, cb, tid, (int)blockDim.x, tile_off, aux, ctaf);
       break;
     case SV_OP_H1U: {
 #define CALL_HU(x) hu_slot<x>(v)

@@ -192,18 +192,17 @@ __device__ __forceinline__ V cta_factor(int b, int e, uint64_t tile_off) {
 }
 
 template <typename V>
-__device__ __forceinline__ void diagset(V (&v)[16], int desc, int cb, int tid, uint64_t tile_off,
+__device__ __forceinline__ void diagset(V (&v)[16], int desc, int cb, int tid, int nthr, uint64_t tile_off,
                                         const V* __restrict__ aux, const V* ctaf) {
   const int flags = c_prog[desc];
   const V* tab = aux + c_prog[desc + 1];
-  const int nthr = blockDim.x;
   const int lane = tid & 31;
   const int set = (flags >> 8) & 255;
   V F[5];
   if (set != 255) {  // per-CTA factors computed once by the CTA prologue
 #pragma unroll
     for (int i = 0; i < 5; i++) F[i] = cmul(ctaf[5 * set + i], tab[i * nthr + tid]);
-  } else if (blockDim.x >= 32) {
+  } else if (nthr >= 32) {
     V mine = cone<V>();
     if (lane < 5) mine = cta_factor<V>(c_prog[desc + 2 + lane], c_prog[desc + 3 + lane], tile_off);
 #pragma unroll
@@ -310,10 +309,46 @@ __device__ __forceinline__ void hbm_store(const V (&v)[16], V* __restrict__ dst,
   }
 }
 
+// Asynchronous global -> shared copies (cp.async, sm_80+): the pipelined generated kernels
+// (jit.cpp) load the next tile while the current one is computed.
+template <typename V>
+__device__ __forceinline__ void cp_async_v(V* smem, const V* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  if constexpr (sizeof(V) == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+// Named barrier over the NT threads of one warp group (id 1..15; 0 is __syncthreads)
+template <int NT>
+__device__ __forceinline__ void group_sync(int id) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(NT) : "memory");
+}
+// ... that also returns whether any thread of the group passed pred != 0
+template <int NT>
+__device__ __forceinline__ bool group_sync_or(int id, bool pred) {
+  int r;
+  asm volatile("{\n\t.reg .pred p, q;\n\tsetp.ne.s32 p, %1, 0;\n\tbar.red.or.pred q, %2, %3, p;\n\tselp.s32 %0, 1, 0, q;\n\t}"
+               : "=r"(r)
+               : "r"((int)pred), "r"(id), "n"(NT)
+               : "memory");
+  return r != 0;
+}
+__device__ __forceinline__ int ld_volatile(const int* p) { return *(const volatile int*)p; }
+__device__ __forceinline__ void st_release(int* p, int x) {
+  __threadfence_block();
+  *(volatile int*)p = x;
+}
+
 // Compile-time op (generated kernels): the same gate code as the interpreter's run_op, with the
 // op fields as template arguments, so slots and coefficient offsets are immediates.
 template <int TYPE, int A, int B, int CB, int X, typename V>
-__device__ __forceinline__ void op_c(V (&v)[16], int tid, uint64_t tile_off, const V* __restrict__ aux,
+__device__ __forceinline__ void op_c(V (&v)[16], int tid, int nthr, uint64_t tile_off, const V* __restrict__ aux,
                                      const V* ctaf) {
   if constexpr (TYPE == SV_OP_U2) {
     u2_slots<A, B>(v, CB);
@@ -344,7 +379,7 @@ __device__ __forceinline__ void op_c(V (&v)[16], int tid, uint64_t tile_off, con
       if (code_val(A, tid, tile_off) & code_val(B, tid, tile_off)) scale_all(v, cc<V>(CB));
     }
   } else if constexpr (TYPE == SV_OP_DIAGSET) {
-    diagset(v, A, CB, tid, tile_off, aux, ctaf);
+    diagset(v, A, CB, tid, nthr, tile_off, aux, ctaf);
   }
 }
 

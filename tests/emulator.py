@@ -189,3 +189,30 @@ def run(steps, prog, coefs, aux, mem, gate_fn=None):
             gate_fn(mem, st)
         else:
             raise AssertionError(kind)
+
+
+def smem_conflicts(prog, G):
+    """Boundary maps / phases of one section whose 2^G-lane groups would hit a 128-byte smem
+    wavefront with a repeated 16-byte (fp64, G=3) / 8-byte (fp32, G=4) slot: the low G bits of
+    the first G thread words must be linearly independent (the kernel's offsets are XORs of them)."""
+    T, nph, phoff = int(prog[H_T]), int(prog[H_NPH]), int(prog[H_PHOFF])
+    ntl = T - 4
+    mask = (1 << G) - 1
+    bad = []
+
+    def indep(words):
+        span = {0}
+        for w in words:
+            v = w & mask
+            if v in span:
+                return False
+            span |= {u ^ v for u in span}
+        return True
+
+    maps = [("load", H_LOAD + M_TW), ("store", H_STORE + M_TW)] + \
+           [(f"phase{k}", phoff + k * PHASE_INTS + P_TW) for k in range(nph)]
+    for name, tw in maps:
+        words = [int(prog[tw + j]) for j in range(min(G, ntl))]
+        if ntl >= G and not indep(words):
+            bad.append(name)
+    return bad

@@ -97,3 +97,17 @@ def test_free_initial_layout_emulated():
         psi[0] = 1
         emulate(C.qft(n), n, c, flags=sv.SV_FREE_LAYOUT, psi=psi.copy())
         emulate(C.quantum_volume(n, 6, 2), n, c, flags=sv.SV_FREE_LAYOUT, psi=psi.copy())
+
+
+@pytest.mark.parametrize("prec,G", [("fp64", 3), ("fp32", 4)])
+def test_section_smem_maps_conflict_free(prec, G):
+    # every shared-memory round trip of the QV / QFT workloads hits distinct 16-/8-byte slots per
+    # 128-byte wavefront (the per-section swizzle and thread-bit choice in compile.cpp)
+    from emulator import smem_conflicts
+    for recs, n, c in [(C.quantum_volume(22, 10, 1), 22, 12), (C.quantum_volume(22, 10, 2), 22, 10),
+                       (C.qft(22), 22, 12), (C.qft(22), 22, 10), (C.random_circuit(16, 200, 3), 16, 9)]:
+        steps, ints, coefs, aux, pi, sigma = sv.compile_circuit(recs, n, c, 0, 0, prec, sv.SV_FREE_LAYOUT)
+        for st in steps:
+            if st[0] == 1 and st[5] >= 4 + G:
+                bad = smem_conflicts(ints[st[1]:st[1] + st[2]], G)
+                assert not bad, (n, c, bad)

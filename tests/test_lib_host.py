@@ -173,3 +173,16 @@ def test_plan_splits_wide_sections():
         elif k in (C.U1, C.U2):
             act |= {int(r["q0"])} | ({int(r["q1"])} if k == C.U2 else set())
     assert widest <= 13
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_jit_sources_compile_for_sm100a(prec, tmp_path):
+    # the run-time specialised section kernels (jit.cpp) are generated and NVRTC-compiled on the
+    # host; the GPU parity tests then run them.  Both the plain and the pipelined variant appear.
+    n = 13
+    recs = np.concatenate([C.qft(n), C.quantum_volume(n, 4, 3), C.random_circuit(n, 60, 5, kinds=("cp", "u3", "d2"))])
+    k, ms = sv.jit_compile_circuit(recs, n, 10, precision=prec, flags=sv.SV_FREE_LAYOUT, dump_dir=str(tmp_path))
+    assert k >= 3
+    srcs = [open(p).read() for p in sorted(tmp_path.glob("section_*.cu"))]
+    assert len(srcs) == k and len(list(tmp_path.glob("section_*.cubin"))) == k
+    assert any("group_sync_or" in s for s in srcs)  # pipelined (T 9..12)
