@@ -95,8 +95,8 @@ Mode mode() {
 constexpr int kPipeSetsBytes = 2 * 5 * SV_MAX_SETS;  // per-CTA factor slots (both groups), in amplitudes
 bool pipelined(const Launch& L, bool dbl) {
   static const bool on = [] {
-    const char* e = std::getenv("SV_PIPE");
-    return !(e && e[0] == '0');
+    const char* e = std::getenv("SV_PIPE");  // opt-in: measured slower than two CTAs per SM
+    return e && e[0] == '1';
   }();
   const size_t amp = dbl ? 16 : 8;
   return on && L.T >= 9 && L.T <= 12 && 3 * (amp << L.T) + kPipeSetsBytes * amp + 64 <= 227 * 1024;
