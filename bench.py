@@ -6,7 +6,7 @@
 One STEP = one pass of the whole hot path over the workload: the host blocking
 pass + plan + program upload (a1-a3), every section kernel (a4, a7), every cross-GPU exchange
 (a5/a6), and a readout of marginal probabilities (a8), all through the C ABI of libsv.so.
-The default workload is BASELINE configs[3]: QV(33, depth 10, seed 1), fp64, chunk_bits 12,
+The default workload is BASELINE configs[3]: QV(33, depth 10, seed 1), fp64, chunk_bits 11,
 strong scaling over N GPUs (2^33 amplitudes = 128 GiB in total; it fits one B200).  The state
 (>= 4 GiB) is far larger than L2, so no flush is needed between steps.
 
@@ -45,21 +45,21 @@ def workload(name: str, world: int):
     if name == "qv33":
         n = 33
         return dict(name="qv33", desc="QV(33, depth 10, seed 1) fp64, strong scaling", n=n,
-                    gates=C.quantum_volume(n, 10, 1), basis=0, scaling="strong")
+                    gates=C.quantum_volume(n, 10, 1), basis=0, scaling="strong", chunk_bits=11)
     if name == "qv28":
         return dict(name="qv28", desc="QV(28, depth 10, seed 1) fp64", n=28,
-                    gates=C.quantum_volume(28, 10, 1), basis=0, scaling="strong")
+                    gates=C.quantum_volume(28, 10, 1), basis=0, scaling="strong", chunk_bits=11)
     if name == "qft30":
         return dict(name="qft30", desc="QFT(30) fp64 on |splitmix64(1) mod 2^30>", n=30, gates=C.qft(30),
-                    basis=C.basis_index(1, 30), scaling="strong")
+                    basis=C.basis_index(1, 30), scaling="strong", chunk_bits=10)
     if name == "qft_weak":
         n = 33 + g
         return dict(name="qft_weak", desc=f"QFT({n}) fp64, 2^33 amplitudes per GPU (weak)", n=n, gates=C.qft(n),
-                    basis=C.basis_index(1, n), scaling="weak")
+                    basis=C.basis_index(1, n), scaling="weak", chunk_bits=10)
     if name == "qv_weak":
         n = 30 + g
         return dict(name="qv_weak", desc=f"QV({n}, 10, 1) fp64, 2^30 amplitudes per GPU (weak)", n=n,
-                    gates=C.quantum_volume(n, 10, 1), basis=0, scaling="weak")
+                    gates=C.quantum_volume(n, 10, 1), basis=0, scaling="weak", chunk_bits=11)
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -203,7 +203,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     wl = workload(args.workload, world)
     n, gates = wl["n"], wl["gates"]
-    c = args.chunk_bits
+    c = args.chunk_bits if args.chunk_bits else wl["chunk_bits"]
     stream = torch.cuda.Stream()
     uid = None
     if world > 1:
@@ -280,7 +280,8 @@ def run_ours(args):
             roof = {"bound": "alu", "achieved": round(ach, 3), "peak": round(pk, 2), "unit": "TFLOP/s",
                     "frac": round(ach / pk, 4), "traffic": traffic,
                     "peak_source": "derived: 64 DFMA/clk/SM x 148 SMs x 1.965 GHz x 2 (DESIGN.md Roofline)"}
-        roof.update({"kernel": "k_section", "launches_timed": st["timed_sections"],
+        roof.update({"kernel": "sv_sec (run-time specialised section kernel; k_section when interpreted)",
+                     "launches_timed": st["timed_sections"],
                      "avg_launch_ms": round(t_launch * 1e3, 4), "alg_bytes_per_launch": bytes_l,
                      "alg_flops_per_launch": flops_l,
                      "hbm_frac_of_measured": round(bytes_l / t_launch / 1e9 / hbm_peak, 4),
@@ -317,6 +318,14 @@ def run_ours(args):
         cpu = {"value": m / dt, "unit": "gates/s", "cores": cores(), "kind": "oracle",
                "sample": f"gates 2..{m + 1} of {wl['desc']} from its basis state ({m} gates, {dt:.1f} s; dense C oracle, OpenMP)"}
 
+    # ---- cross-GPU exchanges against NVLink 5 (900 GB/s per direction per GPU)
+    nvl = None
+    if world > 1 and st["exchange_ms"] > 0:
+        gbs = st["bytes_sent"] / (st["exchange_ms"] / 1e3) / 1e9
+        nvl = {"achieved": round(gbs, 1), "peak": 900.0, "unit": "GB/s per direction", "frac": round(gbs / 900.0, 4),
+               "bytes_per_rank_per_step": st["bytes_sent"] / args.steps,
+               "share_of_step": round(st["exchange_ms"] / ms, 4)}
+
     line = {"metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": wl["scaling"],
             "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32",
@@ -330,7 +339,10 @@ def run_ours(args):
             "exchange_bytes_per_rank_per_step": st["bytes_sent"] / args.steps,
             "exchange_ms_per_step": st["exchange_ms"] / args.steps,
             "host_pass_ms": st["pass_ms"],
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "nvlink": nvl, "cpu_baseline": cpu, "e2e": e2e,
+            "section_kernels": {"generated": int(st["jit_launches"]), "interpreted": int(st["interp_launches"]),
+                                "compiled_total": int(st["jit_compiled"]),
+                                "compile_ms_total": round(st["jit_compile_ms"], 1)},
             "gpu_launches": int(st["kernel_launches"]), "clocks": clocks}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -348,7 +360,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="qv33")
-    ap.add_argument("--chunk-bits", type=int, default=12)
+    ap.add_argument("--chunk-bits", type=int, default=0, help="0: the workload's measured best (DESIGN.md)")
     ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)

@@ -597,6 +597,7 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
   PlanCounters ctr;
   PlanLayout lay;
   lay.low_bits = h->dbl ? 3 : 4;  // 128-byte runs
+  lay.pref_tile = pref_tile_for(lay.low_bits);
   lay.free_initial = h->basis_pending && !(flags & SV_UNBLOCKED);
   std::vector<int> sigma0;
   Status s = make_plan(gates, n_gates, h->n, h->c, h->g, pi, sigma, flags, steps, ctr, lay, &sigma0);
@@ -1048,6 +1049,7 @@ extern "C" int sv_compile_circuit(const sv_gate* gates, size_t n_gates, int n, i
   PlanCounters ctr;
   PlanLayout lay;
   lay.low_bits = prec == SV_FP64 ? 3 : 4;
+  lay.pref_tile = pref_tile_for(lay.low_bits);
   lay.free_initial = (flags & SV_FREE_LAYOUT) && !(flags & SV_UNBLOCKED);
   Status s = make_plan(gates, n_gates, n, c, world_log2, pi, sigma, flags, steps, ctr, lay);
   if (!s.good()) return fail(nullptr, s);
@@ -1111,6 +1113,7 @@ extern "C" int sv_jit_compile_circuit(const sv_gate* gates, size_t n_gates, int 
   PlanCounters ctr;
   PlanLayout lay;
   lay.low_bits = prec == SV_FP64 ? 3 : 4;
+  lay.pref_tile = pref_tile_for(lay.low_bits);
   lay.free_initial = (flags & SV_FREE_LAYOUT) && !(flags & SV_UNBLOCKED);
   Status s = make_plan(gates, n_gates, n, c, world_log2, pi, sigma, flags, steps, ctr, lay);
   if (!s.good()) return fail(nullptr, s);

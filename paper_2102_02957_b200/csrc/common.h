@@ -1,6 +1,7 @@
 // common.h — internal helpers shared by the host C++ and CUDA sources of libsv.so.
 #pragma once
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 #include <utility>
 #include <vector>
@@ -64,8 +65,16 @@ struct PlanLayout {
   int low_bits = 3;    // memory bits every section tile should contain (3: 128-byte fp64 runs)
   int max_tile = 13;   // largest tile (bits) one CTA holds
   int tile_default = 12;
+  int pref_tile = 13;  // largest tile worth its coalescing bits (fp64: a T=13 tile is 128 KiB of
+                      // smem, one CTA per SM, slower than a T=12 tile with 64-byte runs)
   bool free_initial = false;  // the state is a basis state: choose the initial sigma freely (NEXT-2)
 };
+
+// Preferred largest tile for swizzle width G (3: fp64, 4: fp32); SV_PREF_TILE overrides.
+inline int pref_tile_for(int G) {
+  if (const char* e = std::getenv("SV_PREF_TILE")) return std::atoi(e);
+  return G == 3 ? 12 : 13;
+}
 
 // The tile a section runs on (memory-bit mask), shared by the planner and the compiler: the
 // active bits, plus the lowest `low_bits` memory bits when that still fits max_tile, padded with
@@ -73,7 +82,12 @@ struct PlanLayout {
 inline uint64_t choose_tile(uint64_t active, int nL, const PlanLayout& L) {
   const int nlow = L.low_bits < nL ? L.low_bits : nL;
   uint64_t want = active | ((1ull << nlow) - 1);
-  if (__builtin_popcountll(want) > L.max_tile) want = active;
+  if (__builtin_popcountll(want) > L.max_tile) {
+    want = active;
+  } else if (__builtin_popcountll(want) > L.pref_tile && __builtin_popcountll(active) <= L.pref_tile) {
+    want = active;  // fewer coalescing bits (shorter runs) instead of the next tile size
+    for (int b = 0; b < nlow && __builtin_popcountll(want) < L.pref_tile; b++) want |= 1ull << b;
+  }
   const int td = L.tile_default < nL ? L.tile_default : nL;
   for (int b = 0; b < nL && __builtin_popcountll(want) < td; b++) want |= 1ull << b;
   return want;

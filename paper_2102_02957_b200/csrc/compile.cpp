@@ -97,6 +97,7 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
   PlanLayout lay;
   lay.low_bits = swizzle_bits;
   lay.max_tile = kMaxTile;
+  lay.pref_tile = pref_tile_for(swizzle_bits);
   lay.tile_default = T_default;
   const uint64_t tile = choose_tile(active, nL, lay);
   const int T = __builtin_popcountll(tile);

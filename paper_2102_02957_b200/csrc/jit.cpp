@@ -102,6 +102,15 @@ bool pipelined(const Launch& L, bool dbl) {
   return on && L.T >= 9 && L.T <= 12 && 3 * (amp << L.T) + kPipeSetsBytes * amp + 64 <= 227 * 1024;
 }
 
+// Persistent grid + L2 prefetch of each CTA's next tile for the plain generated kernel (SV_L2PF=1)
+bool l2_prefetch(const Launch& L, bool dbl) {
+  static const bool on = [] {
+    const char* e = std::getenv("SV_L2PF");
+    return e && e[0] == '1';
+  }();
+  return on && !pipelined(L, dbl) && L.T >= SV_R_BITS;
+}
+
 size_t smem_bytes(const Launch& L, bool dbl) {
   const size_t amp = dbl ? 16 : 8;
   if (pipelined(L, dbl)) return 3 * (amp << L.T) + kPipeSetsBytes * amp + 64;
@@ -164,6 +173,7 @@ std::string gen_source(const int* p, const Launch& L, bool dbl) {
   const int nt = 1 << g.ntl;
   const bool first = H->flags & SV_FLAG_FIRST_DIRECT, last = H->flags & SV_FLAG_LAST_DIRECT;
   const int nph = H->n_phases;
+  const bool persist = l2_prefetch(L, dbl);
   auto& o = g.o;
   o << "#include \"section_dev.cuh\"\nusing namespace sv;\ntypedef " << (dbl ? "double2" : "float2") << " V;\n";
   o << "extern \"C\" __global__ void __launch_bounds__(" << nt << ", " << (H->T <= 12 ? 2 : 1)
@@ -172,14 +182,43 @@ std::string gen_source(const int* p, const Launch& L, bool dbl) {
     << "  V* sm = reinterpret_cast<V*>(smem_raw);\n"
     << "  V* ctaf = reinterpret_cast<V*>(smem_raw + (sizeof(V) << " << H->T << "));\n"
     << "  (void)sm; (void)ctaf; (void)aux;\n"
-    << "  const int tid = threadIdx.x;\n"
-    << "  const uint64_t bid = blockIdx.x;\n"
-    << "  uint64_t tile_off = 0;\n";
-  {
-    o << "  {\n";
-    g.arr("int", "OB", H->out_bits, H->n_out);
-    o << "#pragma unroll\n    for (int j = 0; j < " << H->n_out << "; j++) tile_off |= ((bid >> j) & 1ull) << OB[j];\n";
-    o << "  }\n";
+    << "  const int tid = threadIdx.x;\n";
+  g.arr("int", "OB", H->out_bits, H->n_out);
+  o << "  auto tile_of = [&](uint64_t t) {\n    uint64_t r = 0;\n#pragma unroll\n    for (int j = 0; j < "
+    << H->n_out << "; j++) r |= ((t >> j) & 1ull) << OB[j];\n    return r;\n  };\n";
+  if (persist) {
+    // L2 prefetch of the CTA's next tile: one request per 128-byte line (lanes / registers whose
+    // memory bits below G are zero), through the map the tile is read with
+    const SvMap& m0 = first ? H->din : H->load;
+    const int G = dbl ? 3 : 4;
+    uint32_t lead_mask = 0;
+    int rskip = 0;
+    for (int j = 0; j < g.ntl; j++)
+      if (m0.tmb[j] < G) lead_mask |= 1u << j;
+    for (int s2 = 0; s2 < SV_R_BITS; s2++)
+      if (m0.rmb[s2] < G) rskip |= 1 << s2;
+    g.arr("int", "PTMB", m0.tmb, g.ntl);
+    long long ro[16];
+    for (int k = 0; k < 16; k++) {
+      ro[k] = 0;
+      for (int s2 = 0; s2 < SV_R_BITS; s2++)
+        if ((k >> s2) & 1) ro[k] |= 1ll << m0.rmb[s2];
+    }
+    g.arr("long long", "PRO", ro, 16);
+    o << "  const bool lead = (tid & " << lead_mask << ") == 0;\n"
+      << "  uint64_t pb = 0;\n#pragma unroll\n  for (int j = 0; j < " << g.ntl
+      << "; j++) pb |= (uint64_t)((tid >> j) & 1) << PTMB[j];\n"
+      << "  constexpr unsigned long long NTILES = 1ull << " << H->n_out << ";\n"
+      << "#pragma unroll 1\n"
+      << "  for (uint64_t bid = blockIdx.x; bid < NTILES; bid += gridDim.x) {\n"
+      << "  const uint64_t tile_off = tile_of(bid);\n"
+      << "  if (lead && bid + gridDim.x < NTILES) {\n"
+      << "    const V* q = psi + (tile_of(bid + gridDim.x) | pb);\n#pragma unroll\n"
+      << "    for (int k = 0; k < 16; k++)\n"
+      << "      if (!(k & " << rskip << ")) asm volatile(\"prefetch.global.L2 [%0];\" ::\"l\"(q + PRO[k]));\n"
+      << "  }\n";
+  } else {
+    o << "  {\n  const uint64_t tile_off = tile_of(blockIdx.x);\n";
   }
   if (H->n_sets > 0) {
     o << "  for (int f = tid; f < " << 5 * H->n_sets << "; f += " << nt << ") {\n"
@@ -231,7 +270,8 @@ std::string gen_source(const int* p, const Launch& L, bool dbl) {
     g.stg();
     o << "  }\n";
   }
-  o << "}\n";
+  if (persist) o << "  __syncthreads();  // the next tile reuses shared memory\n";
+  o << "  }\n}\n";
   (void)L;
   return o.str();
 }
@@ -632,7 +672,7 @@ bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const Launch& 
   void* args[] = {&a0, &a1};
   const unsigned threads = (pipelined(L, dbl) ? 2u : 1u) << (L.T - SV_R_BITS);
   unsigned grid = (unsigned)(1ull << L.n_out);
-  if (pipelined(L, dbl)) {  // persistent: one wave of resident CTAs
+  if (pipelined(L, dbl) || l2_prefetch(L, dbl)) {  // persistent: one wave of resident CTAs
     if (e->occ == 0) {
       int sms = 0, nb = 0;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -642,7 +682,7 @@ bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const Launch& 
       cudaGetLastError();
       e->occ = (uint64_t)nb * (uint64_t)sms;
     }
-    const uint64_t pairs = ((1ull << L.n_out) + 1) / 2;  // each CTA runs two groups
+    const uint64_t pairs = pipelined(L, dbl) ? ((1ull << L.n_out) + 1) / 2 : (1ull << L.n_out);  // two groups per CTA
     grid = (unsigned)std::min<uint64_t>(e->occ, std::max<uint64_t>(1, pairs));
   }
   *err = cudaLaunchKernel(reinterpret_cast<const void*>(e->kern), dim3(grid), dim3(threads), args,
