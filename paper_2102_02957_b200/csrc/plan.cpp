@@ -88,10 +88,33 @@ struct Planner {
     if (!rank_bits.empty()) {
       Step ex;
       ex.type = Step::EXCHANGE;
+      // Victim local bits, Belady-style (the paper's MPI-level blocking, NEXT-1): a relabel never
+      // moves a qubit's memory bit, so walking the later blocks' relabels gives the next section
+      // that needs each memory bit; evict the local bits needed furthest ahead (never: best),
+      // among bits >= low_bits (the tile coalescing bits stay), higher bits first on ties.
+      std::vector<size_t> next_use(nL, blocks.size());
+      {
+        std::vector<int> v = sigma;
+        uint64_t seen = 0;
+        for (size_t j = i + 1; j < blocks.size() && __builtin_popcountll(seen) < nL; j++) {
+          for (const auto& rl : blocks[j].relabels) std::swap(v[rl.first], v[rl.second]);
+          const uint64_t nj = needed(blocks[j], v, nL, nullptr);
+          for (int m = 0; m < nL; m++)
+            if (((nj >> m) & 1) && !((seen >> m) & 1)) {
+              next_use[m] = j;
+              seen |= 1ull << m;
+            }
+        }
+      }
+      const int nlow = std::min(L.low_bits, nL);
       uint64_t taken = need;
       for (int b : rank_bits) {
-        int m = nL - 1;
-        while (m >= 0 && ((taken >> m) & 1)) m--;
+        int m = -1;
+        for (int pass = 0; pass < 2 && m < 0; pass++)  // pass 1 may use the low bits if it must
+          for (int cand = nL - 1; cand >= (pass ? 0 : nlow); cand--) {
+            if ((taken >> cand) & 1) continue;
+            if (m < 0 || next_use[cand] > next_use[m]) m = cand;
+          }
         // m >= 0 is guaranteed: the section needs at most c <= nL local bits in total
         taken |= 1ull << m;
         ex.ex.push_back({m, b});
