@@ -88,6 +88,8 @@ struct sv_state {
   std::vector<void*> peers;       // peer shard pointers mapped in this process (self = sv)
   std::vector<void*> ipc_opened;  // to close
   bool p2p = false;
+  cudaStream_t st_x = nullptr;  // exchange stream of the pipelined exchange + section (lazy)
+  cudaEvent_t ev_x[5] = {};
 
   Program prog;
   sv_stats stats{};
@@ -175,9 +177,9 @@ BitPerm mu_inv_of(const sv_state* h) {
   return p;
 }
 
-int barrier(sv_state* h) {
+int barrier(sv_state* h, cudaStream_t st = nullptr) {
   if (h->world == 1) return SV_OK;
-  NCCL_TRY(h, h->nc->AllReduce(h->d_small.p, h->d_small.p, 1, Nccl::F32, 0, h->comm, h->st));
+  NCCL_TRY(h, h->nc->AllReduce(h->d_small.p, h->d_small.p, 1, Nccl::F32, 0, h->comm, st ? st : h->st));
   return SV_OK;
 }
 
@@ -342,6 +344,118 @@ void tend(sv_state* h, cudaEvent_t a, int kind, double bytes, double flops) {
   cudaEvent_t b = ev_get(h);
   cudaEventRecord(b, h->st);
   h->trecs.push_back({a, b, kind, bytes, flops});
+}
+
+// One section launch (generated kernel, else the interpreter), optionally restricted to the tiles
+// whose out bits match split_a / split_b (kernels.cuh).
+int launch_one(sv_state* h, const Launch& L, int split_a = 0, int split_b = 0) {
+  const int* pdev = (const int*)h->d_prog.p + L.int_off;
+  const char* cdev = (const char*)h->d_coef.p + L.coef_off * h->amp;
+  const char* adev = (const char*)h->d_aux.p + L.aux_off * h->amp;
+  cudaError_t je = cudaSuccess;
+  if (jit_launch_section(h->dbl, h->sv, h->prog.ints.data() + L.int_off, L, pdev, cdev, adev, h->st, &je, split_a,
+                         split_b)) {
+    CUDA_TRY(h, je);
+    h->stats.jit_launches++;
+  } else {
+    CUDA_TRY(h, launch_section(h->dbl, h->sv, pdev, L.int_count, cdev, L.coef_count, adev, L.T, L.n_out, L.n_phases,
+                               L.flags, L.n_sets, h->st, split_a, split_b));
+    h->stats.interp_launches++;
+  }
+  h->stats.kernel_launches++;
+  return SV_OK;
+}
+
+// Pipelined exchange + first launch of the next section (§8(e): the paper's buffer pipeline,
+// P:156-166, with the section instead of a copy as the consumer).  The exchanged pairs and the
+// section's tiles are both split by up to two local bits that are out-of-tile for the section and
+// not exchanged; piece p's exchange kernel + a cross-GPU barrier run on an exchange stream, and the
+// section's tiles of piece p start on the compute stream as soon as that piece has landed on both
+// GPUs, while piece p+1 is still on NVLink.  Returns 1 if it did the work, 0 if not applicable.
+int exchange_pipelined(sv_state* h, const std::vector<ExPair>& pairs_in, const Launch& L0, int* done) {
+  *done = 0;
+  static const int pieces_env = [] {
+    const char* e = std::getenv("SV_XPIPE");  // opt-in: measured no gain at 2 GPUs (the swap kernel
+    return e ? std::atoi(e) : 0;               // and the section compete for SMs and HBM)
+  }();
+  if (pieces_env < 2 || L0.T < SV_R_BITS) return SV_OK;
+  std::vector<ExPair> pairs = pairs_in;
+  std::sort(pairs.begin(), pairs.end(), [](const ExPair& a, const ExPair& b) { return a.m < b.m; });
+  ExchangeArgs a{};
+  a.k = (int)pairs.size();
+  if (a.k > 8) return SV_OK;
+  uint64_t mmask = 0;
+  for (int i = 0; i < a.k; i++) {
+    a.m[i] = pairs[i].m;
+    a.bsel[i] = pairs[i].b - h->nL;
+    mmask |= 1ull << pairs[i].m;
+  }
+  a.h = h->nL - 1;
+  while (a.h >= 0 && ((mmask >> a.h) & 1)) a.h--;
+  if (a.h < 0) return SV_OK;
+  // split bits: the section's highest out bits that are neither exchanged nor the work-split bit
+  const SvSecHeader* H = reinterpret_cast<const SvSecHeader*>(h->prog.ints.data() + L0.int_off);
+  const int want = pieces_env >= 4 ? 2 : 1;
+  int sidx[2], sbit[2], ns = 0;
+  for (int j = H->n_out - 1; j >= 0 && ns < want; j--) {
+    const int b = H->out_bits[j];
+    if (((mmask >> b) & 1) || b == a.h) continue;
+    sidx[ns] = j;
+    sbit[ns] = b;
+    ns++;
+  }
+  if (ns == 0) return SV_OK;
+  if (ns == 2) {  // ascending out-bit index for expand_tile
+    std::swap(sidx[0], sidx[1]);
+    std::swap(sbit[0], sbit[1]);
+  }
+  if (!h->st_x) {
+    CUDA_TRY(h, cudaStreamCreateWithFlags(&h->st_x, cudaStreamNonBlocking));
+    for (auto& e : h->ev_x) CUDA_TRY(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  const uint64_t block = 1ull << (h->nL - a.k);
+  h->stats.bytes_sent += (uint64_t)((1ull << a.k) - 1) * block * h->amp;
+  h->stats.exchanges += a.k;
+  h->stats.exchange_batches++;
+  // the exchange stream starts after everything queued so far on the compute stream
+  CUDA_TRY(h, cudaEventRecord(h->ev_x[4], h->st));
+  CUDA_TRY(h, cudaStreamWaitEvent(h->st_x, h->ev_x[4], 0));
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  if (h->timing) {
+    t0 = ev_get(h);
+    CUDA_TRY(h, cudaEventRecord(t0, h->st_x));
+  }
+  if (int rc = barrier(h, h->st_x)) return rc;
+  const int P = 1 << ns;
+  for (int p = 0; p < P; p++) {
+    a.nfix = ns;
+    for (int i = 0; i < ns; i++) {
+      a.fix_pos[i] = sbit[i];
+      a.fix_val[i] = (p >> i) & 1;
+    }
+    int launches = 0;
+    CUDA_TRY(h, launch_exchange_peer(h->dbl, h->sv, h->peers.data(), h->rank, h->nL, a, h->st_x, &launches));
+    h->stats.kernel_launches += launches;
+    if (int rc = barrier(h, h->st_x)) return rc;
+    CUDA_TRY(h, cudaEventRecord(h->ev_x[p], h->st_x));
+  }
+  if (h->timing) {
+    t1 = ev_get(h);
+    CUDA_TRY(h, cudaEventRecord(t1, h->st_x));
+    h->trecs.push_back({t0, t1, 1, 0.0, 0.0});
+  }
+  const double amps = (double)(1ull << h->nL) / P;
+  for (int p = 0; p < P; p++) {
+    CUDA_TRY(h, cudaStreamWaitEvent(h->st, h->ev_x[p], 0));
+    int sp[2] = {0, 0};
+    for (int i = 0; i < ns; i++) sp[i] = (1 << 16) | (((p >> i) & 1) << 8) | sidx[i];
+    cudaEvent_t t = tstart(h);
+    if (int rc = launch_one(h, L0, sp[0], sp[1])) return rc;
+    tend(h, t, 0, 2.0 * amps * (double)h->amp, L0.flops_per_amp * amps);
+  }
+  h->stats.sections++;
+  *done = 1;
+  return SV_OK;
 }
 
 int drain_timing(sv_state* h) {
@@ -562,6 +676,9 @@ int sv_destroy(sv_handle h) {
     cudaEventDestroy(r.b);
   }
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
+  for (cudaEvent_t e : h->ev_x)
+    if (e) cudaEventDestroy(e);
+  if (h->st_x) cudaStreamDestroy(h->st_x);
   if (h->own_stream && h->st) cudaStreamDestroy(h->st);
   cudaGetLastError();
   delete h;
@@ -599,6 +716,8 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
   lay.low_bits = h->dbl ? 3 : 4;  // 128-byte runs
   lay.pref_tile = pref_tile_for(lay.low_bits);
   lay.free_initial = h->basis_pending && !(flags & SV_UNBLOCKED);
+  // the NCCL exchange sends contiguous runs of 2^m amplitudes: keep its victims among the top bits
+  if ((flags & SV_EXCHANGE_NCCL) || !h->p2p) lay.min_victim = std::max(0, h->nL - 6);
   std::vector<int> sigma0;
   Status s = make_plan(gates, n_gates, h->n, h->c, h->g, pi, sigma, flags, steps, ctr, lay, &sigma0);
   if (!s.good()) return fail(h, s);
@@ -637,6 +756,15 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
     const Step& st = steps[i];
     switch (st.type) {
       case Step::EXCHANGE: {
+        if (h->p2p && !(flags & SV_EXCHANGE_NCCL) && i + 1 < steps.size() && steps[i + 1].type == Step::SECTION &&
+            h->nL >= SV_R_BITS && si < launch_end[i + 1]) {
+          int done = 0;
+          if (int rc = exchange_pipelined(h, st.ex, h->prog.launches[si], &done)) return rc;
+          if (done) {
+            si++;  // the next section's first launch already ran, piece by piece
+            break;
+          }
+        }
         cudaEvent_t t = tstart(h);
         if (int rc = do_exchange(h, st.ex, flags)) return rc;
         tend(h, t, 1, 0.0, 0.0);
@@ -653,21 +781,9 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
         for (; si < launch_end[i]; si++) {
           const Launch& L = h->prog.launches[si];
           cudaEvent_t t = tstart(h);
-          const int* pdev = (const int*)h->d_prog.p + L.int_off;
-          const char* cdev = (const char*)h->d_coef.p + L.coef_off * h->amp;
-          const char* adev = (const char*)h->d_aux.p + L.aux_off * h->amp;
-          cudaError_t je = cudaSuccess;
-          if (jit_launch_section(h->dbl, h->sv, h->prog.ints.data() + L.int_off, L, pdev, cdev, adev, h->st, &je)) {
-            CUDA_TRY(h, je);
-            h->stats.jit_launches++;
-          } else {
-            CUDA_TRY(h, launch_section(h->dbl, h->sv, pdev, L.int_count, cdev, L.coef_count, adev, L.T, L.n_out,
-                                       L.n_phases, L.flags, L.n_sets, h->st));
-            h->stats.interp_launches++;
-          }
+          if (int rc = launch_one(h, L)) return rc;
           const double amps = (double)(1ull << h->nL);
           tend(h, t, 0, 2.0 * amps * (double)h->amp, L.flops_per_amp * amps);
-          h->stats.kernel_launches++;
           h->stats.sections++;
         }
         break;

@@ -68,6 +68,7 @@ struct PlanLayout {
   int pref_tile = 13;  // largest tile worth its coalescing bits (fp64: a T=13 tile is 128 KiB of
                       // smem, one CTA per SM, slower than a T=12 tile with 64-byte runs)
   bool free_initial = false;  // the state is a basis state: choose the initial sigma freely (NEXT-2)
+  int min_victim = 0;         // lowest local bit an exchange may evict (NCCL path: contiguous runs)
 };
 
 // Preferred largest tile for swizzle width G (3: fp64, 4: fp32); SV_PREF_TILE overrides.

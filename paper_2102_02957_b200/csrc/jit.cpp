@@ -177,7 +177,7 @@ std::string gen_source(const int* p, const Launch& L, bool dbl) {
   auto& o = g.o;
   o << "#include \"section_dev.cuh\"\nusing namespace sv;\ntypedef " << (dbl ? "double2" : "float2") << " V;\n";
   o << "extern \"C\" __global__ void __launch_bounds__(" << nt << ", " << (H->T <= 12 ? 2 : 1)
-    << ") sv_sec(V* __restrict__ psi, const V* __restrict__ aux) {\n";
+    << ") sv_sec(V* __restrict__ psi, const V* __restrict__ aux, int split_a, int split_b) {\n";
   o << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n"
     << "  V* sm = reinterpret_cast<V*>(smem_raw);\n"
     << "  V* ctaf = reinterpret_cast<V*>(smem_raw + (sizeof(V) << " << H->T << "));\n"
@@ -218,7 +218,7 @@ std::string gen_source(const int* p, const Launch& L, bool dbl) {
       << "      if (!(k & " << rskip << ")) asm volatile(\"prefetch.global.L2 [%0];\" ::\"l\"(q + PRO[k]));\n"
       << "  }\n";
   } else {
-    o << "  {\n  const uint64_t tile_off = tile_of(blockIdx.x);\n";
+    o << "  {\n  const uint64_t tile_off = tile_of(expand_tile(blockIdx.x, split_a, split_b));\n";
   }
   if (H->n_sets > 0) {
     o << "  for (int f = tid; f < " << 5 * H->n_sets << "; f += " << nt << ") {\n"
@@ -296,7 +296,7 @@ std::string gen_source_pipelined(const int* p, const Launch& L, bool dbl) {
   o << "#include \"section_dev.cuh\"\nusing namespace sv;\ntypedef " << (dbl ? "double2" : "float2") << " V;\n";
   o << "constexpr int NTG = " << nt << ", TILE = " << (1 << H->T) << ";\n";
   o << "extern \"C\" __global__ void __launch_bounds__(" << 2 * nt
-    << ", 1) sv_sec(V* __restrict__ psi, const V* __restrict__ aux) {\n";
+    << ", 1) sv_sec(V* __restrict__ psi, const V* __restrict__ aux, int split_a, int split_b) {\n";
   o << "  extern __shared__ __align__(128) unsigned char smem_raw[];\n"
     << "  V* const bufs = reinterpret_cast<V*>(smem_raw);\n"
     << "  V* const ctaf_all = bufs + 3 * TILE;\n"
@@ -625,10 +625,12 @@ void jit_prepare(const Program& prog, bool dbl) {
 }
 
 bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const Launch& L, const int* prog_dev,
-                        const void* coef_dev, const void* aux_dev, cudaStream_t st, cudaError_t* err) {
+                        const void* coef_dev, const void* aux_dev, cudaStream_t st, cudaError_t* err, int split_a,
+                        int split_b) {
   *err = cudaSuccess;
   const Mode m = mode();
   if (m == kOff || L.T < SV_R_BITS) return false;
+  if ((split_a || split_b) && (pipelined(L, dbl) || l2_prefetch(L, dbl))) return false;  // persistent variants
   int dev = 0;
   cudaGetDevice(&dev);
   std::string key = make_key(prog_host, L, dbl, dev);
@@ -669,9 +671,10 @@ bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const Launch& 
   }
   void* a0 = sv;
   void* a1 = const_cast<void*>(aux_dev);
-  void* args[] = {&a0, &a1};
+  int a2 = split_a, a3 = split_b;
+  void* args[] = {&a0, &a1, &a2, &a3};
   const unsigned threads = (pipelined(L, dbl) ? 2u : 1u) << (L.T - SV_R_BITS);
-  unsigned grid = (unsigned)(1ull << L.n_out);
+  unsigned grid = (unsigned)(1ull << (L.n_out - (split_a ? 1 : 0) - (split_b ? 1 : 0)));
   if (pipelined(L, dbl) || l2_prefetch(L, dbl)) {  // persistent: one wave of resident CTAs
     if (e->occ == 0) {
       int sms = 0, nb = 0;

@@ -275,10 +275,10 @@ __global__ void k_sample_resolve(const V* __restrict__ sv, int B, const int64_t*
 
 // ------------------------------------------------------------------ exchange over peer memory
 struct ExDev {
-  int nins;        // number of inserted bits (k m-bits + the split bit h)
-  int pos[9];      // insertion positions, ascending
-  int val_my[9];   // bit values on the local side
-  int val_peer[9]; // bit values on the partner side
+  int nins;         // number of inserted bits (k m-bits + the split bit h + fixed piece bits)
+  int pos[11];      // insertion positions, ascending
+  int val_my[11];   // bit values on the local side
+  int val_peer[11]; // bit values on the partner side
 };
 
 __device__ __forceinline__ uint64_t insert_bit(uint64_t x, int p, int v) {
@@ -479,7 +479,7 @@ cudaError_t launch_exchange_peer(bool dbl, void* local, void* const* peer_bases,
   // rank bits of this rank at the exchanged positions
   int mine = 0;
   for (int i = 0; i < a.k; i++) mine |= ((rank >> a.bsel[i]) & 1) << i;
-  const uint64_t count = 1ull << (nL - a.k - 1);
+  const uint64_t count = 1ull << (nL - a.k - 1 - a.nfix);
   for (int mu = 0; mu < (1 << a.k); mu++) {
     if (mu == mine) continue;
     int partner = rank;
@@ -488,11 +488,12 @@ cudaError_t launch_exchange_peer(bool dbl, void* local, void* const* peer_bases,
     ExDev e{};
     struct PV {
       int p, vm, vp;
-    } ins[9];
+    } ins[11];
     int n = 0;
     for (int i = 0; i < a.k; i++) ins[n++] = {a.m[i], (mu >> i) & 1, (mine >> i) & 1};
     const int hv = rank < partner ? 0 : 1;
     ins[n++] = {a.h, hv, hv};
+    for (int i = 0; i < a.nfix; i++) ins[n++] = {a.fix_pos[i], a.fix_val[i], a.fix_val[i]};
     for (int i = 1; i < n; i++)  // ascending positions
       for (int j = i; j > 0 && ins[j].p < ins[j - 1].p; j--) {
         PV t = ins[j];

@@ -9,9 +9,11 @@ namespace sv {
 // K1: one launch per section.  Copies the section's program (int_count ints at prog_dev) and
 // coefficients (coef_count complex numbers in amp dtype at coef_dev) into __constant__ memory on
 // `st`, then launches 2^n_out CTAs.  dbl selects fp64 (double2 amplitudes) vs fp32 (float2).
+// split_a / split_b: 0, or (1 << 16) | (value << 8) | index into the section's out bits: the
+// launch covers only the tiles whose out bit has that value (pipelined exchange + section)
 cudaError_t launch_section(bool dbl, void* sv, const int* prog_dev, size_t int_count, const void* coef_dev,
                            size_t coef_count, const void* aux_dev, int T, int n_out, int n_phases, int flags,
-                           int n_sets, cudaStream_t st);
+                           int n_sets, cudaStream_t st, int split_a = 0, int split_b = 0);
 
 // K2: per-gate baseline, one pass over the shard per gate.  q0/q1 are memory bits;
 // diag codes follow program.h (rank bits pre-folded to constants).
@@ -50,6 +52,9 @@ struct ExchangeArgs {
   int m[8];       // local memory bits, ascending
   int bsel[8];    // rank-bit index (0..g-1) paired with m[i]
   int h;          // local bit (not in m) that splits each pair's work between the two ranks
+  int nfix = 0;   // pipelined exchange: only the pairs whose local bits fix_pos[i] equal fix_val[i]
+  int fix_pos[2] = {0, 0};
+  int fix_val[2] = {0, 0};
 };
 cudaError_t launch_exchange_peer(bool dbl, void* local, void* const* peer_bases /*host array [world]*/, int rank,
                                  int nL, const ExchangeArgs& a, cudaStream_t st, int* launches);

@@ -106,7 +106,7 @@ struct Planner {
             }
         }
       }
-      const int nlow = std::min(L.low_bits, nL);
+      const int nlow = std::min(std::max(L.low_bits, L.min_victim), nL);
       uint64_t taken = need;
       for (int b : rank_bits) {
         int m = -1;

@@ -101,7 +101,8 @@ __device__ __forceinline__ void run_op(V (&v)[16], int oi, int tid, uint64_t til
 }
 
 template <typename V, int G, int NT, int MINB, bool FIRST, bool LAST>
-__global__ void __launch_bounds__(NT, MINB) k_section(V* __restrict__ sv, const V* __restrict__ aux, int prefetch) {
+__global__ void __launch_bounds__(NT, MINB) k_section(V* __restrict__ sv, const V* __restrict__ aux, int prefetch,
+                                                     int split_a, int split_b) {
   using R = decltype(V().x);
   constexpr int RB = SV_R_BITS;  // the host guarantees T >= RB, so every phase has RB register slots
   constexpr int M0 = FIRST ? kH_DIN : kH_LOAD;  // the map the tile is read with
@@ -111,7 +112,7 @@ __global__ void __launch_bounds__(NT, MINB) k_section(V* __restrict__ sv, const 
   const int phoff = c_prog[kH_PHOFF], opoff = c_prog[kH_OPOFF];
   const int nt_log = T - RB;
   const int tid = threadIdx.x;
-  const uint64_t n_tiles = 1ull << n_out;
+  const uint64_t n_tiles = 1ull << (n_out - (split_a ? 1 : 0) - (split_b ? 1 : 0));
   V* ctaf = reinterpret_cast<V*>(smem_raw + (sizeof(V) << T));
   const int n_sets = c_prog[kH_NSETS];
 
@@ -128,9 +129,10 @@ __global__ void __launch_bounds__(NT, MINB) k_section(V* __restrict__ sv, const 
   // Persistent CTAs: tile blk, blk + gridDim.x, ... (the grid is sized to the resident capacity)
   for (uint64_t blk = blockIdx.x; blk < n_tiles; blk += gridDim.x) {
     uint64_t tile_off = 0;
-    for (int j = 0; j < n_out; j++) tile_off |= ((blk >> j) & 1ull) << c_prog[kH_OUT + j];
+    const uint64_t tb = expand_tile(blk, split_a, split_b);
+    for (int j = 0; j < n_out; j++) tile_off |= ((tb >> j) & 1ull) << c_prog[kH_OUT + j];
     if (lead && blk + gridDim.x < n_tiles) {
-      const uint64_t nb = blk + gridDim.x;
+      const uint64_t nb = expand_tile(blk + gridDim.x, split_a, split_b);
       uint64_t noff = 0;
       for (int j = 0; j < n_out; j++) noff |= ((nb >> j) & 1ull) << c_prog[kH_OUT + j];
       const V* p = sv + hbm_base(M0, nt_log, tid, noff);
@@ -219,7 +221,7 @@ inline bool env_set(const char* name) {
 }
 
 template <typename V, int G, int NT, int MINB, bool FIRST, bool LAST>
-cudaError_t launch_v(V* sv, const V* aux, int T, int n_out, size_t smem, cudaStream_t st) {
+cudaError_t launch_v(V* sv, const V* aux, int T, int n_out, size_t smem, cudaStream_t st, int split_a, int split_b) {
   static bool attr_set = false;
   static int sms = 0, occ_smem = -1, occ = 1;
   static const bool persist = env_set("SV_PERSIST"), prefetch = env_on("SV_PREFETCH");
@@ -241,10 +243,10 @@ cudaError_t launch_v(V* sv, const V* aux, int T, int n_out, size_t smem, cudaStr
     occ = nb > 0 ? nb : 1;
     occ_smem = (int)smem;
   }
-  const uint64_t tiles = 1ull << n_out;
+  const uint64_t tiles = 1ull << (n_out - (split_a ? 1 : 0) - (split_b ? 1 : 0));
   const uint64_t cap = (uint64_t)occ * (uint64_t)sms;
   const unsigned grid = (unsigned)(persist && tiles > cap ? cap : tiles);
-  kern<<<grid, threads, smem, st>>>(sv, aux, prefetch && grid < tiles ? 1 : 0);
+  kern<<<grid, threads, smem, st>>>(sv, aux, prefetch && grid < tiles ? 1 : 0, split_a, split_b);
   return cudaGetLastError();
 }
 
@@ -252,18 +254,18 @@ cudaError_t launch_v(V* sv, const V* aux, int T, int n_out, size_t smem, cudaStr
 // the all-smem variant: ptxas keeps the coefficient loads on the uniform datapath in the other
 // three shapes only (checked by tests/test_sass.py).
 template <typename V, int G, int NT, int MINB>
-cudaError_t launch_t(V* sv, const V* aux, int T, int n_out, int flags, size_t smem, cudaStream_t st) {
+cudaError_t launch_t(V* sv, const V* aux, int T, int n_out, int flags, size_t smem, cudaStream_t st, int sa, int sb) {
   const bool f = flags & SV_FLAG_FIRST_DIRECT, l = flags & SV_FLAG_LAST_DIRECT;
-  if (f && l) return launch_v<V, G, NT, MINB, true, true>(sv, aux, T, n_out, smem, st);
-  if (l) return launch_v<V, G, NT, MINB, false, true>(sv, aux, T, n_out, smem, st);
-  return launch_v<V, G, NT, MINB, false, false>(sv, aux, T, n_out, smem, st);
+  if (f && l) return launch_v<V, G, NT, MINB, true, true>(sv, aux, T, n_out, smem, st, sa, sb);
+  if (l) return launch_v<V, G, NT, MINB, false, true>(sv, aux, T, n_out, smem, st, sa, sb);
+  return launch_v<V, G, NT, MINB, false, false>(sv, aux, T, n_out, smem, st, sa, sb);
 }
 
 }  // namespace
 
 cudaError_t launch_section(bool dbl, void* sv, const int* prog_dev, size_t int_count, const void* coef_dev,
                            size_t coef_count, const void* aux_dev, int T, int n_out, int n_phases, int flags,
-                           int n_sets, cudaStream_t st) {
+                           int n_sets, cudaStream_t st, int split_a, int split_b) {
   if (int_count > SV_CONST_INTS) return cudaErrorInvalidValue;
   cudaError_t e = cudaMemcpyToSymbolAsync(c_prog, prog_dev, int_count * sizeof(int), 0, cudaMemcpyDeviceToDevice, st);
   if (e != cudaSuccess) return e;
@@ -282,14 +284,14 @@ cudaError_t launch_section(bool dbl, void* sv, const int* prog_dev, size_t int_c
   if (dbl) {
     const size_t smem = n_sets ? (sizeof(double2) << T) + 5 * SV_MAX_SETS * sizeof(double2)
                                : (no_smem ? 0 : sizeof(double2) << T);
-    if (T <= 12) return launch_t<double2, 3, 256, 2>((double2*)sv, (const double2*)aux_dev, T, n_out, flags, smem, st);
-    if (T == 13) return launch_t<double2, 3, 512, 1>((double2*)sv, (const double2*)aux_dev, T, n_out, flags, smem, st);
+    if (T <= 12) return launch_t<double2, 3, 256, 2>((double2*)sv, (const double2*)aux_dev, T, n_out, flags, smem, st, split_a, split_b);
+    if (T == 13) return launch_t<double2, 3, 512, 1>((double2*)sv, (const double2*)aux_dev, T, n_out, flags, smem, st, split_a, split_b);
     return cudaErrorInvalidValue;
   }
   const size_t smem = n_sets ? (sizeof(float2) << T) + 5 * SV_MAX_SETS * sizeof(float2)
                              : (no_smem ? 0 : sizeof(float2) << T);
-  if (T <= 12) return launch_t<float2, 4, 256, 2>((float2*)sv, (const float2*)aux_dev, T, n_out, flags, smem, st);
-  if (T == 13) return launch_t<float2, 4, 512, 1>((float2*)sv, (const float2*)aux_dev, T, n_out, flags, smem, st);
+  if (T <= 12) return launch_t<float2, 4, 256, 2>((float2*)sv, (const float2*)aux_dev, T, n_out, flags, smem, st, split_a, split_b);
+  if (T == 13) return launch_t<float2, 4, 512, 1>((float2*)sv, (const float2*)aux_dev, T, n_out, flags, smem, st, split_a, split_b);
   return cudaErrorInvalidValue;
 }
 

@@ -345,6 +345,22 @@ __device__ __forceinline__ void st_release(int* p, int x) {
   *(volatile int*)p = x;
 }
 
+// Tile index of launch block b when the launch covers only the tiles whose out-bit indices
+// (split & 255) have the value ((split >> 8) & 1); split = 0: all tiles.  Lower index first.
+__device__ __forceinline__ uint64_t expand_tile(uint64_t b, int split_a, int split_b) {
+  if (split_a) {
+    const int p = split_a & 255;
+    const uint64_t lo = b & ((1ull << p) - 1);
+    b = ((b - lo) << 1) | ((uint64_t)((split_a >> 8) & 1) << p) | lo;
+  }
+  if (split_b) {
+    const int p = split_b & 255;
+    const uint64_t lo = b & ((1ull << p) - 1);
+    b = ((b - lo) << 1) | ((uint64_t)((split_b >> 8) & 1) << p) | lo;
+  }
+  return b;
+}
+
 // Compile-time op (generated kernels): the same gate code as the interpreter's run_op, with the
 // op fields as template arguments, so slots and coefficient offsets are immediates.
 template <int TYPE, int A, int B, int CB, int X, typename V>
