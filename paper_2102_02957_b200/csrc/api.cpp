@@ -227,7 +227,9 @@ int do_exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags) {
     for (int i = 0; i < a.k; i++) p = (p & ~(1 << a.bsel[i])) | (((mu >> i) & 1) << a.bsel[i]);
     partners.push_back({p, mu});
   }
-  std::sort(partners.begin(), partners.end());
+  // XOR schedule (as the peer kernel): round t pairs ranks whose subcube bits differ by t
+  std::sort(partners.begin(), partners.end(),
+            [&](const std::pair<int, int>& x, const std::pair<int, int>& y) { return (x.second ^ mine) < (y.second ^ mine); });
   // insert the m-bits (value mu) into a run index: positions above mlow that are not m-bits
   auto run_start = [&](uint64_t rix, int mu) {
     uint64_t x = rix << mlow;  // compact index of the run's first element (bits >= mlow)

@@ -480,8 +480,10 @@ cudaError_t launch_exchange_peer(bool dbl, void* local, void* const* peer_bases,
   int mine = 0;
   for (int i = 0; i < a.k; i++) mine |= ((rank >> a.bsel[i]) & 1) << i;
   const uint64_t count = 1ull << (nL - a.k - 1 - a.nfix);
-  for (int mu = 0; mu < (1 << a.k); mu++) {
-    if (mu == mine) continue;
+  // round t pairs every rank with the one whose subcube bits differ by t (XOR schedule): each
+  // round is a perfect matching, so no GPU serves two peers at once
+  for (int t = 1; t < (1 << a.k); t++) {
+    const int mu = mine ^ t;
     int partner = rank;
     for (int i = 0; i < a.k; i++) partner = (partner & ~(1 << a.bsel[i])) | (((mu >> i) & 1) << a.bsel[i]);
     // my block mu (local bits m = mu) <-> partner's block `mine`; pairs split by bit h
