@@ -567,7 +567,14 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
           set_idx = H()->n_sets++;
           H()->set_desc[set_idx] = (int)desc;
         }
-        prog.ints.push_back((has_lam ? 1 : 0) | (set_idx << 8));
+        int tab_mask = 0;  // subsets whose per-thread table is not all ones (generated kernels skip the rest)
+        for (int si = 0; si < 5; si++)
+          for (int tid = 0; tid < nthr; tid++)
+            if (tab[si][tid] != cd(1.0, 0.0)) {
+              tab_mask |= 1 << si;
+              break;
+            }
+        prog.ints.push_back((has_lam ? 1 : 0) | (set_idx << 8) | (tab_mask << 16));
         prog.ints.push_back(aux0);
         const size_t off = prog.ints.size();
         prog.ints.resize(prog.ints.size() + 8, 0);

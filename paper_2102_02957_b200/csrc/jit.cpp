@@ -156,6 +156,19 @@ struct Gen {
     o << "    int x = 0;\n#pragma unroll\n    for (int j = 0; j < " << ntl
       << "; j++) x ^= ((tid >> j) & 1) ? TW[j] : 0;\n";
   }
+  // DIAGSET op with its structure specialised (section_dev.cuh diagset_c); false: not applicable
+  bool diagset_c(const int* p, const SvOp& op, const std::string& nthr) {
+    if (op.type != SV_OP_DIAGSET) return false;
+    const int d = op.a, flags = p[d];
+    const int set = (flags >> 8) & 255, tabm = (flags >> 16) & 31;
+    if (set == 255 || p[d + 9] != p[d + 8]) return false;  // per-warp CTA terms or mixed terms
+    int ctam = 0;
+    for (int i = 0; i < 5; i++)
+      if (p[d + 3 + i] > p[d + 2 + i]) ctam |= 1 << i;
+    o << "    diagset_c<" << (flags & 1) << ", " << set << ", " << tabm << ", " << ctam << ">(v, " << d << ", "
+      << op.coef << ", tid, " << nthr << ", aux, ctaf);\n";
+    return true;
+  }
   void lds() { o << "#pragma unroll\n    for (int k = 0; k < 16; k++) v[k] = sm[x ^ W[k]];\n"; }
   void sts() { o << "#pragma unroll\n    for (int k = 0; k < 16; k++) sm[x ^ W[k]] = v[k];\n"; }
   void ldg() { o << "#pragma unroll\n    for (int k = 0; k < 16; k++) v[k] = psi[b + RO[k]];\n"; }
@@ -248,8 +261,9 @@ std::string gen_source(const int* p, const Launch& L, bool dbl) {
     if (!din) g.lds();
     for (int i = 0; i < ph[k].op_count; i++) {
       const SvOp& op = ops[ph[k].op_begin + i];
-      o << "    op_c<" << op.type << ", " << op.a << ", " << op.b << ", " << op.coef << ", " << op.extra
-        << ">(v, tid, " << nt << ", tile_off, aux, ctaf);\n";
+      if (!g.diagset_c(p, op, std::to_string(nt)))
+        o << "    op_c<" << op.type << ", " << op.a << ", " << op.b << ", " << op.coef << ", " << op.extra
+          << ">(v, tid, " << nt << ", tile_off, aux, ctaf);\n";
     }
     if (dout) {
       o << "    {\n";
@@ -356,8 +370,9 @@ std::string gen_source_pipelined(const int* p, const Launch& L, bool dbl) {
     g.lds();
     for (int i = 0; i < ph[k].op_count; i++) {
       const SvOp& op = ops[ph[k].op_begin + i];
-      o << "    op_c<" << op.type << ", " << op.a << ", " << op.b << ", " << op.coef << ", " << op.extra
-        << ">(v, tid, NTG, tile_off, aux, ctaf);\n";
+      if (!g.diagset_c(p, op, "NTG"))
+        o << "    op_c<" << op.type << ", " << op.a << ", " << op.b << ", " << op.coef << ", " << op.extra
+          << ">(v, tid, NTG, tile_off, aux, ctaf);\n";
     }
     if (dout) {
       o << "    {\n";

@@ -36,7 +36,9 @@
 #define SV_OP_DIAG_CP 6 // like DIAG with d0 = d1 = d2 = 1: only s == 3 is multiplied (coef -> d3)
 #define SV_OP_DIAGSET 7 // fused run of diagonal gates: a = descriptor offset (ints from the header),
                         // coef -> LAMBDA[16] (if flag bit 0); descriptor:
-                        //   [0] flags (bit 0: LAMBDA present)   [1] aux offset of 5 thread tables
+                        //   [0] flags (bit 0: LAMBDA present; bits 8..15 prologue factor set or
+                        //       255; bits 16..20: subset i's thread table is not all ones)
+                        //   [1] aux offset of 5 thread tables
                         //   [2+i] / [7] per-CTA terms of subset i (i = 0: empty set, 1+s: slot s),
                         //               3 ints each: out-bit mask lo, hi, coef (apply if set)
                         //   [8] / [9]   per-thread mixed terms, 5 ints: i, thread mask, out lo, hi, coef

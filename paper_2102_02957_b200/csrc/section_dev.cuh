@@ -361,6 +361,49 @@ __device__ __forceinline__ uint64_t expand_tile(uint64_t b, int split_a, int spl
   return b;
 }
 
+// DIAGSET with its structure as template arguments (generated kernels): subsets without a
+// thread table (TABM) or per-CTA terms (CTAM) are identically one and cost nothing; the register
+// factors are products of the non-trivial subset factors (the compiler shares common prefixes).
+// Requires the per-CTA factors in smem (SET != 255) and no mixed terms.
+template <int LAM, int SET, int TABM, int CTAM, typename V>
+__device__ __forceinline__ void diagset_c(V (&v)[16], int desc, int cb, int tid, int nthr, const V* __restrict__ aux,
+                                          const V* ctaf) {
+  const V* tab = aux + c_prog[desc + 1];
+  V F[5];
+#pragma unroll
+  for (int i = 0; i < 5; i++) {
+    if ((TABM >> i) & 1) {
+      F[i] = tab[i * nthr + tid];
+      if ((CTAM >> i) & 1) F[i] = cmul(F[i], ctaf[5 * SET + i]);
+    } else if ((CTAM >> i) & 1) {
+      F[i] = ctaf[5 * SET + i];
+    } else {
+      F[i] = cone<V>();
+    }
+  }
+  constexpr int NT = TABM | CTAM;
+#pragma unroll
+  for (int k = 0; k < 16; k++) {
+    V f = cone<V>();
+    bool one = true;
+    if (NT & 1) {
+      f = F[0];
+      one = false;
+    }
+#pragma unroll
+    for (int s = 0; s < 4; s++)
+      if (((k >> s) & 1) && ((NT >> (1 + s)) & 1)) {
+        f = one ? F[1 + s] : cmul(f, F[1 + s]);
+        one = false;
+      }
+    if (LAM) {
+      f = one ? cc<V>(cb + k) : cmul(f, cc<V>(cb + k));
+      one = false;
+    }
+    if (!one) cmul_ip(v[k], f);
+  }
+}
+
 // Compile-time op (generated kernels): the same gate code as the interpreter's run_op, with the
 // op fields as template arguments, so slots and coefficient offsets are immediates.
 template <int TYPE, int A, int B, int CB, int X, typename V>

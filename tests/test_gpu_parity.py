@@ -183,3 +183,35 @@ def test_qv28_full_size_parity():
         got = s.state()
     ref = O.apply_circuit(circ, n)
     check(got, ref, "fp64")
+
+
+@pytest.mark.parametrize("mode", [0, 2])
+def test_interpreter_and_async_modes(mode):
+    # mode 0: every section runs the program interpreter (k_section); mode 2: the first apply of a
+    # shape runs the interpreter while its kernels compile, later applies the generated kernels
+    prev = sv.jit_mode(mode)
+    try:
+        for n, c, circ in [(14, 10, C.quantum_volume(14, 6, 5)), (16, 12, C.qft(16)),
+                           (13, 9, C.random_circuit(13, 150, 77))]:
+            for prec in ("fp64", "fp32"):
+                for rep in range(2):
+                    with sv.StateVector(n, c, prec) as s:
+                        s.reset(C.basis_index(3, n))
+                        s.apply(circ)
+                        got = s.state()
+                        st = s.stats()
+                    check(got, O.apply_circuit(circ, n, basis=C.basis_index(3, n)), prec)
+                    if mode == 0:
+                        assert st["jit_launches"] == 0 and st["interp_launches"] > 0
+                if mode == 2:
+                    sv.jit_wait()
+    finally:
+        sv.jit_mode(prev)
+
+
+def test_generated_kernels_run():
+    # default mode: the generated kernels are the ones that run
+    with sv.StateVector(14, 10, "fp64") as s:
+        s.apply(C.quantum_volume(14, 4, 9))
+        st = s.stats()
+    assert st["jit_launches"] > 0 and st["interp_launches"] == 0

@@ -1,1 +1,4 @@
-ncu --metrics gpu__time_duration.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,smsp__inst_executed.sum,sm__warps_active.avg.pct_of_peak_sustained_active,dram__bytes_read.sum,dram__bytes_write.sum,l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum,l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum,launch__registers_per_thread,smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,smsp__sass_thread_inst_executed_op_dadd_pred_on.sum --clock-control none -k regex:sv_sec -s 57 -c 19 --csv --log-file gpurun_out/qv28_launches.csv python bench.py --workload qv28 --chunk-bits 11 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_q.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/gputests.log 2>&1; echo tests=$?
+for W in qft30 qv28; do
+  timeout 600 python bench.py --workload $W --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/c_${W}.json 2> gpurun_out/c_${W}.err
+done
