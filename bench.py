@@ -6,7 +6,7 @@
 One STEP = one pass of the whole hot path over the workload: the host blocking
 pass + plan + program upload (a1-a3), every section kernel (a4, a7), every cross-GPU exchange
 (a5/a6), and a readout of marginal probabilities (a8), all through the C ABI of libsv.so.
-The default workload is BASELINE configs[3]: QV(33, depth 10, seed 1), fp64, chunk_bits 11,
+The default workload is BASELINE configs[3]: QV(33, depth 10, seed 1), fp64, chunk_bits 9,
 strong scaling over N GPUs (2^33 amplitudes = 128 GiB in total; it fits one B200).  The state
 (>= 4 GiB) is far larger than L2, so no flush is needed between steps.
 
@@ -45,21 +45,21 @@ def workload(name: str, world: int):
     if name == "qv33":
         n = 33
         return dict(name="qv33", desc="QV(33, depth 10, seed 1) fp64, strong scaling", n=n,
-                    gates=C.quantum_volume(n, 10, 1), basis=0, scaling="strong", chunk_bits=11)
+                    gates=C.quantum_volume(n, 10, 1), basis=0, scaling="strong", chunk_bits=9)
     if name == "qv28":
         return dict(name="qv28", desc="QV(28, depth 10, seed 1) fp64", n=28,
-                    gates=C.quantum_volume(28, 10, 1), basis=0, scaling="strong", chunk_bits=11)
+                    gates=C.quantum_volume(28, 10, 1), basis=0, scaling="strong", chunk_bits=9)
     if name == "qft30":
         return dict(name="qft30", desc="QFT(30) fp64 on |splitmix64(1) mod 2^30>", n=30, gates=C.qft(30),
-                    basis=C.basis_index(1, 30), scaling="strong", chunk_bits=10)
+                    basis=C.basis_index(1, 30), scaling="strong", chunk_bits=8)
     if name == "qft_weak":
         n = 33 + g
         return dict(name="qft_weak", desc=f"QFT({n}) fp64, 2^33 amplitudes per GPU (weak)", n=n, gates=C.qft(n),
-                    basis=C.basis_index(1, n), scaling="weak", chunk_bits=10)
+                    basis=C.basis_index(1, n), scaling="weak", chunk_bits=8)
     if name == "qv_weak":
         n = 30 + g
         return dict(name="qv_weak", desc=f"QV({n}, 10, 1) fp64, 2^30 amplitudes per GPU (weak)", n=n,
-                    gates=C.quantum_volume(n, 10, 1), basis=0, scaling="weak", chunk_bits=11)
+                    gates=C.quantum_volume(n, 10, 1), basis=0, scaling="weak", chunk_bits=9)
     raise SystemExit(f"unknown workload {name}")
 
 

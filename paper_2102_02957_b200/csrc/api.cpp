@@ -716,7 +716,7 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
   PlanCounters ctr;
   PlanLayout lay;
   lay.low_bits = h->dbl ? 3 : 4;  // 128-byte runs
-  lay.pref_tile = pref_tile_for(lay.low_bits);
+  apply_tile_prefs(lay);
   lay.free_initial = h->basis_pending && !(flags & SV_UNBLOCKED);
   // the NCCL exchange sends contiguous runs of 2^m amplitudes: keep its victims among the top bits
   if ((flags & SV_EXCHANGE_NCCL) || !h->p2p) lay.min_victim = std::max(0, h->nL - 6);
@@ -1089,6 +1089,7 @@ int sv_plan_circuit(const sv_gate* gates, size_t n_gates, int n, int c, int worl
   std::vector<Step> steps;
   PlanCounters ctr;
   PlanLayout lay;
+  apply_tile_prefs(lay);  // fp64 tile policy (as sv_apply_circuit on an fp64 state)
   lay.free_initial = (flags & SV_FREE_LAYOUT) && !(flags & SV_UNBLOCKED);
   Status s = make_plan(gates, n_gates, n, c, world_log2, pi, sigma, flags, steps, ctr, lay);
   if (!s.good()) return fail(nullptr, s);
@@ -1167,7 +1168,7 @@ extern "C" int sv_compile_circuit(const sv_gate* gates, size_t n_gates, int n, i
   PlanCounters ctr;
   PlanLayout lay;
   lay.low_bits = prec == SV_FP64 ? 3 : 4;
-  lay.pref_tile = pref_tile_for(lay.low_bits);
+  apply_tile_prefs(lay);
   lay.free_initial = (flags & SV_FREE_LAYOUT) && !(flags & SV_UNBLOCKED);
   Status s = make_plan(gates, n_gates, n, c, world_log2, pi, sigma, flags, steps, ctr, lay);
   if (!s.good()) return fail(nullptr, s);
@@ -1231,7 +1232,7 @@ extern "C" int sv_jit_compile_circuit(const sv_gate* gates, size_t n_gates, int 
   PlanCounters ctr;
   PlanLayout lay;
   lay.low_bits = prec == SV_FP64 ? 3 : 4;
-  lay.pref_tile = pref_tile_for(lay.low_bits);
+  apply_tile_prefs(lay);
   lay.free_initial = (flags & SV_FREE_LAYOUT) && !(flags & SV_UNBLOCKED);
   Status s = make_plan(gates, n_gates, n, c, world_log2, pi, sigma, flags, steps, ctr, lay);
   if (!s.good()) return fail(nullptr, s);

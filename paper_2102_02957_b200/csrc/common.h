@@ -64,7 +64,8 @@ struct PlanCounters {
 struct PlanLayout {
   int low_bits = 3;    // memory bits every section tile should contain (3: 128-byte fp64 runs)
   int max_tile = 13;   // largest tile (bits) one CTA holds
-  int tile_default = 12;
+  int tile_default = 11;  // small sections pad to 11 bits: 32 KiB fp64 tiles, 4 CTAs per SM (measured
+                          // faster than 12-bit tiles at 2 CTAs per SM: QFT30 c=8 35.6 vs 40.2 ms)
   int pref_tile = 13;  // largest tile worth its coalescing bits (fp64: a T=13 tile is 128 KiB of
                       // smem, one CTA per SM, slower than a T=12 tile with 64-byte runs)
   bool free_initial = false;  // the state is a basis state: choose the initial sigma freely (NEXT-2)
@@ -75,6 +76,11 @@ struct PlanLayout {
 inline int pref_tile_for(int G) {
   if (const char* e = std::getenv("SV_PREF_TILE")) return std::atoi(e);
   return G == 3 ? 12 : 13;
+}
+// Tile policy of a layout whose low_bits is set: preferred maximum and default size.
+inline void apply_tile_prefs(PlanLayout& L) {
+  L.pref_tile = pref_tile_for(L.low_bits);
+  if (L.tile_default > L.pref_tile) L.tile_default = L.pref_tile;
 }
 
 // The tile a section runs on (memory-bit mask), shared by the planner and the compiler: the
