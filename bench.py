@@ -34,6 +34,11 @@ sys.path.insert(0, ROOT)
 import circuits as C  # noqa: E402
 
 METRIC = "QV/QFT circuit gates/s (fp64 state vector, cache-blocked)"
+APPLY_FLAGS = 0  # SV_UNBLOCKED with --unblocked (the comparator), else the blocked path
+
+
+def sv_flags_unblocked():
+    return 1  # include/sv.h SV_UNBLOCKED
 FALLBACK_HBM_GBS = 6650.0
 # FP64 FMA pipe: 64 DFMA/clk/SM (measured 63.6 in tools/microbench.cu) x 148 SMs x 1.965 GHz x 2 flops
 FP64_PEAK_TFLOPS = 2 * 64 * 148 * 1.965e9 / 1e12
@@ -217,7 +222,7 @@ def run_ours(args):
 
     def step():  # simulate the circuit from its basis state, then read out
         s.reset(wl["basis"])
-        s.apply(gates)
+        s.apply(gates, flags=APPLY_FLAGS)
         s.probabilities(Q)
 
     s.reset(wl["basis"])
@@ -298,7 +303,7 @@ def run_ours(args):
             barrier()
             t0 = time.perf_counter()
             s.reset(wl["basis"])
-            s.apply(gates)
+            s.apply(gates, flags=APPLY_FLAGS)
             s.probabilities(Q)
             s.amplitudes(idx)
             dt = time.perf_counter() - t0
@@ -333,7 +338,8 @@ def run_ours(args):
             "config": {"workload": wl["desc"], "n_qubits": n, "gates": int(len(gates)), "chunk_bits": c,
                        "precision": args.precision, "parallelism": f"state sharded over {world} GPU(s)",
                        "l2": "state >= 4 GiB per GPU >> 126 MB L2 (no flush needed)",
-                       "step": "sv_reset(basis) + sv_apply_circuit (pass+plan+upload+sections+exchanges) + sv_probabilities(10 qubits)"},
+                       "step": "sv_reset(basis) + sv_apply_circuit (pass+plan+upload+sections+exchanges) + sv_probabilities(10 qubits)",
+                       "path": "unblocked per-gate baseline (SV_UNBLOCKED)" if APPLY_FLAGS else "cache-blocked"},
             "amp_updates_per_s": value * (1 << n),
             "sections_per_step": st["sections"] / args.steps, "exchanges_per_step": st["exchanges"] / args.steps,
             "exchange_bytes_per_rank_per_step": st["bytes_sent"] / args.steps,
@@ -362,6 +368,8 @@ def main():
     ap.add_argument("--workload", default="qv33")
     ap.add_argument("--chunk-bits", type=int, default=0, help="0: the workload's measured best (DESIGN.md)")
     ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"])
+    ap.add_argument("--unblocked", action="store_true",
+                    help="the paper's per-gate baseline (SV_UNBLOCKED): one pass per gate, exchanges per global gate")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -370,6 +378,8 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # contract: W >= 3
+    global APPLY_FLAGS
+    APPLY_FLAGS = sv_flags_unblocked() if args.unblocked else 0
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -236,19 +236,57 @@ Status make_plan(const sv_gate* g, size_t count, int n, int c, int world_log2, s
 
   if (sigma_initial) *sigma_initial = sigma;
   if (flags & SV_UNBLOCKED) {
-    // Per-gate baseline: each gate is one step on memory bits mu(q) = sigma[pi[q]].
+    // Per-gate baseline: each gate is one step on memory bits mu(q) = sigma[pi[q]].  On
+    // several GPUs a non-diagonal gate on a global qubit is the paper's unblocked multi-GPU
+    // baseline (NEXT-3): its rank bit is exchanged with a local bit the gate does not
+    // use, the gate runs there, and a second exchange writes the halves back.  A SWAP of a local
+    // and a global qubit is itself one exchange.
     for (size_t i = 0; i < count; i++) {
       sv_gate m = g[i];
       m.q0 = sigma[pi[g[i].q0]];
       m.q1 = is_two(g[i].kind) ? sigma[pi[g[i].q1]] : -1;
       m.pad = (int32_t)i;
-      if (!is_diag(m.kind) && (m.q0 >= nL || (is_two(m.kind) && m.q1 >= nL)))
-        return Status::err(SV_EINFEASIBLE,
-                           "unblocked mode: gate " + std::to_string(i) + " acts on a global qubit (needs the pass)");
-      Step s;
-      s.type = Step::GATE;
-      s.gates.push_back(m);
-      steps.push_back(std::move(s));
+      const bool r0 = m.q0 >= nL, r1 = is_two(m.kind) && m.q1 >= nL;
+      if (is_diag(m.kind) || (!r0 && !r1)) {
+        Step s;
+        s.type = Step::GATE;
+        s.gates.push_back(m);
+        steps.push_back(std::move(s));
+        continue;
+      }
+      if (m.kind == SV_SWAP && r0 != r1) {
+        Step ex;
+        ex.type = Step::EXCHANGE;
+        ex.ex.push_back({r0 ? m.q1 : m.q0, r0 ? m.q0 : m.q1});
+        ctr.exchanges++;
+        ctr.exchange_batches++;
+        steps.push_back(std::move(ex));
+        continue;
+      }
+      Step in;
+      in.type = Step::EXCHANGE;
+      uint64_t used = 0;
+      if (!r0) used |= 1ull << m.q0;
+      if (is_two(m.kind) && !r1) used |= 1ull << m.q1;
+      int* qs[2] = {&m.q0, &m.q1};
+      for (int k = 0; k < 2; k++) {
+        if (!(k == 0 ? r0 : r1)) continue;
+        int v = nL - 1;
+        while (v >= 0 && ((used >> v) & 1)) v--;
+        if (v < 0) return Status::err(SV_EINFEASIBLE, "unblocked mode: no local bit to exchange into");
+        used |= 1ull << v;
+        in.ex.push_back({v, *qs[k]});
+        *qs[k] = v;
+      }
+      ctr.exchanges += 2 * in.ex.size();
+      ctr.exchange_batches += 2;
+      Step gs;
+      gs.type = Step::GATE;
+      gs.gates.push_back(m);
+      Step out = in;  // the same exchange again restores the layout (write back)
+      steps.push_back(std::move(in));
+      steps.push_back(std::move(gs));
+      steps.push_back(std::move(out));
     }
     return Status::ok();
   }

@@ -34,6 +34,8 @@ def main():
         ("rand", C.random_circuit(18, 300, 5), 18, 8, 0),
         ("qv-restore", C.quantum_volume(16, 8, 3), 16, 6, sv.SV_RESTORE_ORDER),
         ("ghz", C.ghz(21), 21, 5, 0),
+        # the paper's unblocked multi-GPU baseline (NEXT-3): per-gate exchanges of global qubits
+        ("qv-unblocked", C.quantum_volume(16, 3, 4), 16, 6, sv.SV_UNBLOCKED),
     ]
     for name, recs, n, c, flags in cases:
         s = sv.create_distributed(n, c, "fp64")

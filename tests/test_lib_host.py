@@ -154,8 +154,23 @@ def test_plan_unblocked_matches():
     recs = C.random_circuit(8, 50, 5)
     plan = run_plan_dense(recs, 8, 4, 0, flags=sv.SV_UNBLOCKED)
     assert sum(1 for r in plan if int(r["kind"]) == C.BEGIN) == 50
-    with pytest.raises(sv.SvError, match="EINFEASIBLE"):
-        sv.plan_circuit(C.records([C.gate(C.U1, 7, mat=C.H_MATRIX)]), 8, 4, 1, flags=sv.SV_UNBLOCKED)
+
+    # several GPUs: the paper's unblocked multi-GPU baseline (NEXT-3) - a non-diagonal gate on a
+    # global qubit is bracketed by two exchanges of its rank bit with a free local bit
+    for g in (1, 2):
+        recs = C.random_circuit(9, 60, 17 + g, kinds=("u3", "su4", "cx", "cp", "swap"))
+        plan = run_plan_dense(recs, 9, 4, g, flags=sv.SV_UNBLOCKED)
+        glob = set(range(9 - g, 9))
+        want = 0
+        for r in recs:
+            k, qs = int(r["kind"]), {int(r["q0"])} | ({int(r["q1"])} if int(r["kind"]) in (C.U2, C.D2, C.SWAP) else set())
+            if k in (C.D1, C.D2) or not (qs & glob):
+                continue
+            if k == C.SWAP and len(qs & glob) == 1:
+                want += 1
+            else:
+                want += 2 * len(qs & glob)
+        assert sum(1 for r in plan if int(r["kind"]) == 9) == want
 
 
 def test_plan_splits_wide_sections():
