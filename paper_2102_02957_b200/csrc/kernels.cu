@@ -159,11 +159,17 @@ struct MargPlan {
 template <typename V>
 __global__ void k_marginal_tasks(const V* __restrict__ sv, MargPlan p, double* __restrict__ dst, int use_smem) {
   extern __shared__ double hist[];
+  __shared__ uint64_t offs[64];  // memory offset of each iteration index (deposit into it_b)
   const int bins = 1 << p.nq;
-  if (use_smem) {
-    for (int i = threadIdx.x; i < bins; i += blockDim.x) hist[i] = 0.0;
-    __syncthreads();
+  const int niter = 1 << p.nit;
+  for (int it = threadIdx.x; it < niter; it += blockDim.x) {
+    uint64_t x = 0;
+    for (int j = 0; j < p.nit; j++) x |= (uint64_t)((it >> j) & 1) << p.it_b[j];
+    offs[it] = x;
   }
+  if (use_smem)
+    for (int i = threadIdx.x; i < bins; i += blockDim.x) hist[i] = 0.0;
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   int y_lane = 0;
   for (int i = 0; i < p.nq; i++)
@@ -171,20 +177,20 @@ __global__ void k_marginal_tasks(const V* __restrict__ sv, MargPlan p, double* _
   const uint32_t nonq = ~p.lane_q & 31u;
   const uint64_t ntasks = 1ull << p.ntb;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  const int niter = 1 << p.nit;
   for (uint64_t t = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ntasks; t += nwarps) {
     uint64_t x0 = (uint64_t)lane;
     for (int j = 0; j < p.ntb; j++) x0 |= ((t >> j) & 1ull) << p.task_b[j];
     int y = y_lane;
     for (int i = 0; i < p.nq; i++)
       if (p.qb[i] >= 5) y |= (int)((x0 >> p.qb[i]) & 1ull) << i;
-    double acc = 0.0;
+    double acc0 = 0.0, acc1 = 0.0;
+    const V* base = sv + x0;
 #pragma unroll 8
-    for (int it = 0; it < niter; it++) {
-      uint64_t x = x0;
-      for (int j = 0; j < p.nit; j++) x |= (uint64_t)((it >> j) & 1) << p.it_b[j];
-      acc += abs2(sv[x]);
+    for (int it = 0; it < niter; it += 2) {  // niter is a power of two >= 2 here
+      acc0 += abs2(base[offs[it]]);
+      acc1 += abs2(base[offs[it + 1]]);
     }
+    double acc = acc0 + acc1;
 #pragma unroll
     for (int j = 0; j < 5; j++)
       if ((nonq >> j) & 1) acc += __shfl_xor_sync(0xffffffffu, acc, 1 << j);
@@ -399,7 +405,13 @@ cudaError_t launch_marginal(bool dbl, const void* sv, int nL, const int* qbits, 
   if (nq > 24) return cudaErrorInvalidValue;
   const uint64_t N = 1ull << nL;
   const int bins = 1 << nq;
-  if (nL < 11) {  // tiny shards: one atomic per amplitude
+  int nit_avail = 0;  // non-marginal bits >= 5 (the task form needs at least one)
+  for (int b = 5; b < nL; b++) {
+    bool q = false;
+    for (int i = 0; i < nq; i++) q |= qbits[i] == b;
+    nit_avail += q ? 0 : 1;
+  }
+  if (nL < 11 || nit_avail == 0) {  // tiny shards: one atomic per amplitude
     QBits q;
     for (int i = 0; i < nq; i++) q.b[i] = qbits[i];
     cudaError_t e = cudaMemsetAsync(out_dev, 0, sizeof(double) * bins, st);

@@ -1,7 +1,3 @@
-for C in 9 10 11; do
-  timeout 900 python bench.py --workload qv33 --chunk-bits $C --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/t_qv33_$C.json 2> gpurun_out/t_qv33_$C.err
-  timeout 600 python bench.py --workload qv28 --chunk-bits $C --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/t_qv28_$C.json 2> gpurun_out/t_qv28_$C.err
-done
-for C in 8 9 10; do
-  timeout 600 python bench.py --workload qft30 --chunk-bits $C --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/t_qft30_$C.json 2> gpurun_out/t_qft30_$C.err
-done
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "prob or marg or qft10 or mid" > gpurun_out/gputests.log 2>&1; echo tests=$?
+timeout 600 python bench.py --workload qft30 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/c_qft30.json 2> gpurun_out/c_qft30.err
+./tools/prof.sh qv28 66 2
