@@ -293,15 +293,40 @@ __device__ __forceinline__ uint64_t insert_bit(uint64_t x, int p, int v) {
 }
 
 // Swap local[x] <-> remote[x'] for every compact index j (2^(nL - k - 1) of them).
+// Four pairs per thread per iteration (j, j + stride, ...): four remote loads in flight per
+// thread keep more NVLink requests outstanding than one.
 template <typename V>
 __global__ void k_exchange_peer(V* __restrict__ local, V* __restrict__ remote, uint64_t count, ExDev e) {
+  constexpr int U = 4;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < count; j += stride) {
-    uint64_t x = j, y = j;
+  auto idx = [&](uint64_t j, uint64_t& x, uint64_t& y) {
+    x = j;
+    y = j;
     for (int i = 0; i < e.nins; i++) {
       x = insert_bit(x, e.pos[i], e.val_my[i]);
       y = insert_bit(y, e.pos[i], e.val_peer[i]);
     }
+  };
+  uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  for (; j + (U - 1) * stride < count; j += U * stride) {
+    uint64_t x[U], y[U];
+    V a[U], b[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) idx(j + u * stride, x[u], y[u]);
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      a[u] = local[x[u]];
+      b[u] = remote[y[u]];
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      local[x[u]] = b[u];
+      remote[y[u]] = a[u];
+    }
+  }
+  for (; j < count; j += stride) {
+    uint64_t x, y;
+    idx(j, x, y);
     const V a = local[x];
     const V b = remote[y];
     local[x] = b;

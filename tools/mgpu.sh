@@ -4,5 +4,5 @@ timeout 1200 python -m pytest tests/test_multi_gpu.py -q -x > gpurun_out/mgpu_te
 R="python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1"
 timeout 1500 $R --master-port 29533 bench.py --gpus $N --steps 3 --warmup 3 > gpurun_out/bench_n$N.json 2> gpurun_out/bench_n$N.err; echo bench=$?
 timeout 1500 $R --master-port 29534 bench.py --gpus $N --steps 3 --warmup 3 --workload qft_weak --no-e2e > gpurun_out/bench_qftweak_n$N.json 2> gpurun_out/bench_qftweak_n$N.err; echo benchw=$?
-timeout 1500 $R --master-port 29535 bench.py --gpus $N --steps 1 --warmup 3 --workload qv28 --unblocked --no-e2e > gpurun_out/bench_unbl_qv28_n$N.json 2> gpurun_out/bench_unbl_qv28_n$N.err; echo benchu=$?
-timeout 1500 $R --master-port 29536 bench.py --gpus $N --steps 3 --warmup 3 --workload qv28 --no-e2e > gpurun_out/bench_qv28_n$N.json 2> gpurun_out/bench_qv28_n$N.err; echo bench28=$?
+
+
