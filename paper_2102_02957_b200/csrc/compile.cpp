@@ -630,6 +630,14 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
             op.a = sa;
             op.b = sb;
             op.coef = push(m, 16);
+            {  // Gauss form for the kernel: (-(re + im), im - re) per entry (section_dev.cuh u2_slots)
+              double gm[32];
+              for (int e = 0; e < 16; e++) {
+                gm[2 * e] = -(m[2 * e] + m[2 * e + 1]);
+                gm[2 * e + 1] = m[2 * e + 1] - m[2 * e];
+              }
+              push(gm, 16);
+            }
             fpa += 32.0;
             break;
           }

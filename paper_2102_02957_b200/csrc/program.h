@@ -26,7 +26,8 @@
 #define SV_CONST_COEF32 1024  // 8 KiB of fp32 complex coefficients
 
 // op types
-#define SV_OP_U2 1      // a = slot0 < b = slot1, coef -> 16 complex (row-major, s = bit(a) + 2 bit(b))
+#define SV_OP_U2 1      // a = slot0 < b = slot1, coef -> 16 complex (row-major, s = bit(a) + 2 bit(b)),
+                        // then 16 more: (-(re + im), im - re) of each entry (3-multiply form)
 #define SV_OP_U1 2      // a = slot, coef -> 4 complex (row-major)
 #define SV_OP_H1 3      // a = slot, coef -> 1 complex (scale s, real):  (x, y) -> (s(x+y), s(x-y))
 #define SV_OP_H1U 8     // a = slot: unscaled butterfly (x, y) -> (x+y, x-y); the section's product of

@@ -48,20 +48,36 @@ __device__ __forceinline__ int swz(int i) {
 }
 
 // ---------------------------------------------------------------- gates on register slots
+// 4x4 complex matrix on the register pairs of slots S0 < S1, three real products per complex
+// multiply-add: with s = x + y of each input, out.re = T + R and out.im = T + I where
+// T = sum m.re s, R = sum -(m.re + m.im) y, I = sum (m.im - m.re) x (the host stores the two
+// derived coefficients after the matrix): 60 instead of 64 FP64 operations per 4 amplitudes.
 template <int S0, int S1, typename V>
 __device__ __forceinline__ void u2_slots(V (&v)[16], int cb) {
+  using R = decltype(V().x);
 #pragma unroll
   for (int q = 0; q < 16; q++) {
     if (((q >> S0) & 1) || ((q >> S1) & 1)) continue;
     const int i0 = q, i1 = q | (1 << S0), i2 = q | (1 << S1), i3 = q | (1 << S0) | (1 << S1);
-    const V a0 = v[i0], a1 = v[i1], a2 = v[i2], a3 = v[i3];
+    const V a[4] = {v[i0], v[i1], v[i2], v[i3]};
+    R s[4];
+#pragma unroll
+    for (int c = 0; c < 4; c++) s[c] = a[c].x + a[c].y;
 #pragma unroll
     for (int rr = 0; rr < 4; rr++) {
-      V acc = cmul(cc<V>(cb + 4 * rr + 0), a0);
-      acc = cfma(cc<V>(cb + 4 * rr + 1), a1, acc);
-      acc = cfma(cc<V>(cb + 4 * rr + 2), a2, acc);
-      acc = cfma(cc<V>(cb + 4 * rr + 3), a3, acc);
-      v[rr == 0 ? i0 : (rr == 1 ? i1 : (rr == 2 ? i2 : i3))] = acc;
+      R t = cc<V>(cb + 4 * rr).x * s[0];
+      R re = cc<V>(cb + 16 + 4 * rr).x * a[0].y;
+      R im = cc<V>(cb + 16 + 4 * rr).y * a[0].x;
+#pragma unroll
+      for (int c = 1; c < 4; c++) {
+        t = fma(cc<V>(cb + 4 * rr + c).x, s[c], t);
+        re = fma(cc<V>(cb + 16 + 4 * rr + c).x, a[c].y, re);
+        im = fma(cc<V>(cb + 16 + 4 * rr + c).y, a[c].x, im);
+      }
+      V o;
+      o.x = t + re;
+      o.y = t + im;
+      v[rr == 0 ? i0 : (rr == 1 ? i1 : (rr == 2 ? i2 : i3))] = o;
     }
   }
 }
