@@ -323,6 +323,13 @@ def run_ours(args):
         cpu = {"value": m / dt, "unit": "gates/s", "cores": cores(), "kind": "oracle",
                "sample": f"gates 2..{m + 1} of {wl['desc']} from its basis state ({m} gates, {dt:.1f} s; dense C oracle, OpenMP)"}
 
+    if roof and roof["bound"] == "alu" and clocks.get("sm_mhz"):
+        # FP64 peak scales with the SM clock; under sustained FP64 load the B200 runs below its
+        # 1965 MHz maximum (sw_power_cap): the fraction at the clock it actually ran is context
+        f = clocks["sm_mhz"] / 1965.0
+        roof["peak_at_load_clock"] = round(roof["peak"] * f, 2)
+        roof["frac_at_load_clock"] = round(roof["frac"] / f, 4)
+
     # ---- cross-GPU exchanges against NVLink 5 (900 GB/s per direction per GPU)
     nvl = None
     if world > 1 and st["exchange_ms"] > 0:
