@@ -355,8 +355,8 @@ int launch_one(sv_state* h, const Launch& L, int split_a = 0, int split_b = 0) {
   const char* cdev = (const char*)h->d_coef.p + L.coef_off * h->amp;
   const char* adev = (const char*)h->d_aux.p + L.aux_off * h->amp;
   cudaError_t je = cudaSuccess;
-  if (jit_launch_section(h->dbl, h->sv, h->prog.ints.data() + L.int_off, L, pdev, cdev, adev, h->st, &je, split_a,
-                         split_b)) {
+  if (jit_launch_section(h->dbl, h->sv, h->prog.ints.data() + L.int_off, h->prog.coefs.data() + 2 * L.coef_off, L,
+                         pdev, cdev, adev, h->st, &je, split_a, split_b)) {
     CUDA_TRY(h, je);
     h->stats.jit_launches++;
   } else {

@@ -119,6 +119,16 @@ size_t smem_bytes(const Launch& L, bool dbl) {
   return no_smem ? 0 : amp << L.T;
 }
 
+// Coefficients as a __grid_constant__ kernel parameter when they fit the 32 KiB parameter space
+// (FMAs then read them from the parameter bank); else from the module's __constant__ bank.
+constexpr size_t kParamCoefMax = 31 * 1024;
+bool coef_in_param(const Launch& L, bool dbl) { return L.coef_count * (dbl ? 16 : 8) <= kParamCoefMax; }
+std::string coef_param_decl_impl(const Launch& L, bool dbl) {
+  if (coef_in_param(L, dbl))
+    return "const __grid_constant__ CoefParam<V, " + std::to_string(L.coef_count ? L.coef_count : 1) + "> P";
+  return "const CoefBank<V> P";
+}
+
 struct Gen {
   std::ostringstream o;
   int T = 0, ntl = 0;
@@ -166,7 +176,7 @@ struct Gen {
     for (int i = 0; i < 5; i++)
       if (p[d + 3 + i] > p[d + 2 + i]) ctam |= 1 << i;
     o << "    diagset_c<" << (flags & 1) << ", " << set << ", " << tabm << ", " << ctam << ">(v, " << d << ", "
-      << op.coef << ", tid, " << nthr << ", aux, ctaf);\n";
+      << op.coef << ", tid, " << nthr << ", aux, ctaf, P);\n";
     return true;
   }
   void lds() { o << "#pragma unroll\n    for (int k = 0; k < 16; k++) v[k] = sm[x ^ W[k]];\n"; }
@@ -190,7 +200,8 @@ std::string gen_source(const int* p, const Launch& L, bool dbl) {
   auto& o = g.o;
   o << "#include \"section_dev.cuh\"\nusing namespace sv;\ntypedef " << (dbl ? "double2" : "float2") << " V;\n";
   o << "extern \"C\" __global__ void __launch_bounds__(" << nt << ", " << (H->T <= 11 ? 4 : H->T == 12 ? 2 : 1)
-    << ") sv_sec(V* __restrict__ psi, const V* __restrict__ aux, int split_a, int split_b) {\n";
+    << ") sv_sec(V* __restrict__ psi, const V* __restrict__ aux, int split_a, int split_b, "
+    << coef_param_decl_impl(L, dbl) << ") {\n";
   o << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n"
     << "  V* sm = reinterpret_cast<V*>(smem_raw);\n"
     << "  V* ctaf = reinterpret_cast<V*>(smem_raw + (sizeof(V) << " << H->T << "));\n"
@@ -236,7 +247,7 @@ std::string gen_source(const int* p, const Launch& L, bool dbl) {
   if (H->n_sets > 0) {
     o << "  for (int f = tid; f < " << 5 * H->n_sets << "; f += " << nt << ") {\n"
       << "    const int d = c_prog[kH_SETS + f / 5], i = f % 5;\n"
-      << "    ctaf[f] = cta_factor<V>(c_prog[d + 2 + i], c_prog[d + 3 + i], tile_off);\n  }\n"
+      << "    ctaf[f] = cta_factor<V>(c_prog[d + 2 + i], c_prog[d + 3 + i], tile_off, P);\n  }\n"
       << "  __syncthreads();\n";
   }
   o << "  V v[16];\n";
@@ -263,7 +274,7 @@ std::string gen_source(const int* p, const Launch& L, bool dbl) {
       const SvOp& op = ops[ph[k].op_begin + i];
       if (!g.diagset_c(p, op, std::to_string(nt)))
         o << "    op_c<" << op.type << ", " << op.a << ", " << op.b << ", " << op.coef << ", " << op.extra
-          << ">(v, tid, " << nt << ", tile_off, aux, ctaf);\n";
+          << ">(v, tid, " << nt << ", tile_off, aux, ctaf, P);\n";
     }
     if (dout) {
       o << "    {\n";
@@ -310,7 +321,8 @@ std::string gen_source_pipelined(const int* p, const Launch& L, bool dbl) {
   o << "#include \"section_dev.cuh\"\nusing namespace sv;\ntypedef " << (dbl ? "double2" : "float2") << " V;\n";
   o << "constexpr int NTG = " << nt << ", TILE = " << (1 << H->T) << ";\n";
   o << "extern \"C\" __global__ void __launch_bounds__(" << 2 * nt
-    << ", 1) sv_sec(V* __restrict__ psi, const V* __restrict__ aux, int split_a, int split_b) {\n";
+    << ", 1) sv_sec(V* __restrict__ psi, const V* __restrict__ aux, int split_a, int split_b, "
+    << coef_param_decl_impl(L, dbl) << ") {\n";
   o << "  extern __shared__ __align__(128) unsigned char smem_raw[];\n"
     << "  V* const bufs = reinterpret_cast<V*>(smem_raw);\n"
     << "  V* const ctaf_all = bufs + 3 * TILE;\n"
@@ -358,7 +370,7 @@ std::string gen_source_pipelined(const int* p, const Launch& L, bool dbl) {
   if (H->n_sets > 0) {
     o << "    for (int f = tid; f < " << 5 * H->n_sets << "; f += NTG) {\n"
       << "      const int d = c_prog[kH_SETS + f / 5], i = f % 5;\n"
-      << "      ctaf[f] = cta_factor<V>(c_prog[d + 2 + i], c_prog[d + 3 + i], tile_off);\n    }\n";
+      << "      ctaf[f] = cta_factor<V>(c_prog[d + 2 + i], c_prog[d + 3 + i], tile_off, P);\n    }\n";
   }
   o << "    cp_async_wait<0>();\n    group_sync<NTG>(bar);\n    V v[16];\n";
   const SvPhase* ph = reinterpret_cast<const SvPhase*>(p + H->phase_off);
@@ -372,7 +384,7 @@ std::string gen_source_pipelined(const int* p, const Launch& L, bool dbl) {
       const SvOp& op = ops[ph[k].op_begin + i];
       if (!g.diagset_c(p, op, "NTG"))
         o << "    op_c<" << op.type << ", " << op.a << ", " << op.b << ", " << op.coef << ", " << op.extra
-          << ">(v, tid, NTG, tile_off, aux, ctaf);\n";
+          << ">(v, tid, NTG, tile_off, aux, ctaf, P);\n";
     }
     if (dout) {
       o << "    {\n";
@@ -639,9 +651,9 @@ void jit_prepare(const Program& prog, bool dbl) {
   for (auto& t : th) t.join();
 }
 
-bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const Launch& L, const int* prog_dev,
-                        const void* coef_dev, const void* aux_dev, cudaStream_t st, cudaError_t* err, int split_a,
-                        int split_b) {
+bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const double* coef_host, const Launch& L,
+                        const int* prog_dev, const void* coef_dev, const void* aux_dev, cudaStream_t st,
+                        cudaError_t* err, int split_a, int split_b) {
   *err = cudaSuccess;
   const Mode m = mode();
   if (m == kOff || L.T < SV_R_BITS) return false;
@@ -679,7 +691,7 @@ bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const Launch& 
     *err = cudaMemcpyAsync(e->c_prog, prog_dev, L.int_count * sizeof(int), cudaMemcpyDeviceToDevice, st);
     if (*err != cudaSuccess) return true;
   }
-  if (e->c_coef && L.coef_count) {
+  if (e->c_coef && L.coef_count && !coef_in_param(L, dbl)) {
     if (L.coef_count * amp > e->c_coef_bytes) return false;
     *err = cudaMemcpyAsync(e->c_coef, coef_dev, L.coef_count * amp, cudaMemcpyDeviceToDevice, st);
     if (*err != cudaSuccess) return true;
@@ -687,7 +699,22 @@ bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const Launch& 
   void* a0 = sv;
   void* a1 = const_cast<void*>(aux_dev);
   int a2 = split_a, a3 = split_b;
-  void* args[] = {&a0, &a1, &a2, &a3};
+  // the coefficient parameter: the section's coefficients (fp64 on the host) in the state's precision
+  thread_local std::vector<char> pbuf;
+  const size_t nc = L.coef_count ? L.coef_count : 1;
+  char empty_bank = 0;
+  void* a4 = &empty_bank;  // CoefBank<V>: an empty struct parameter
+  if (coef_in_param(L, dbl)) {
+    pbuf.assign(nc * amp, 0);
+    if (dbl) {
+      std::memcpy(pbuf.data(), coef_host, L.coef_count * 16);
+    } else {
+      float* f = reinterpret_cast<float*>(pbuf.data());
+      for (size_t i = 0; i < 2 * L.coef_count; i++) f[i] = (float)coef_host[i];
+    }
+    a4 = pbuf.data();
+  }
+  void* args[] = {&a0, &a1, &a2, &a3, a4};
   const unsigned threads = (pipelined(L, dbl) ? 2u : 1u) << (L.T - SV_R_BITS);
   unsigned grid = (unsigned)(1ull << (L.n_out - (split_a ? 1 : 0) - (split_b ? 1 : 0)));
   if (pipelined(L, dbl) || l2_prefetch(L, dbl)) {  // persistent: one wave of resident CTAs

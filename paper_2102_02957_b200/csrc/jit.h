@@ -31,9 +31,10 @@ struct JitCounters {
 // Launch one section with its generated kernel.  Returns false if the caller must run the
 // interpreter instead (mode, compile pending or NVRTC unavailable); *err is the launch status.
 // split_a / split_b: restrict the launch to half / a quarter of the tiles (kernels.cuh launch_section).
-bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const Launch& L, const int* prog_dev,
-                        const void* coef_dev, const void* aux_dev, cudaStream_t st, cudaError_t* err, int split_a = 0,
-                        int split_b = 0);
+// coef_host: the launch's coefficients (fp64 complex) on the host, passed as a kernel parameter.
+bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const double* coef_host, const Launch& L,
+                        const int* prog_dev, const void* coef_dev, const void* aux_dev, cudaStream_t st,
+                        cudaError_t* err, int split_a = 0, int split_b = 0);
 
 // Make sure every launch of the program has its kernel: mode sync compiles the missing ones in
 // parallel now, mode async queues them.

@@ -34,6 +34,19 @@ __device__ __forceinline__ float2 cc<float2>(int i) {
   return c_coef32[i];
 }
 
+// Coefficient accessors: the interpreter reads the section's coefficients from the __constant__
+// bank (CoefBank); the generated kernels get them as a __grid_constant__ kernel parameter
+// (CoefParam), so every FMA takes its matrix element straight from the parameter bank.
+template <typename V>
+struct CoefBank {
+  __device__ __forceinline__ V operator()(int i) const { return cc<V>(i); }
+};
+template <typename V, int N>
+struct CoefParam {
+  V c[N];
+  __device__ __forceinline__ V operator()(int i) const { return c[i]; }
+};
+
 // XOR-fold swizzle of a tile element index: the low G bits are XORed with every higher G-bit
 // group.  GF(2)-linear, so swz(a | b) = swz(a) ^ swz(b) for disjoint a, b.
 template <int G>
@@ -52,8 +65,8 @@ __device__ __forceinline__ int swz(int i) {
 // multiply-add: with s = x + y of each input, out.re = T + R and out.im = T + I where
 // T = sum m.re s, R = sum -(m.re + m.im) y, I = sum (m.im - m.re) x (the host stores the two
 // derived coefficients after the matrix): 60 instead of 64 FP64 operations per 4 amplitudes.
-template <int S0, int S1, typename V>
-__device__ __forceinline__ void u2_slots(V (&v)[16], int cb) {
+template <int S0, int S1, typename V, typename CF = CoefBank<V>>
+__device__ __forceinline__ void u2_slots(V (&v)[16], int cb, const CF& cf = CF()) {
   using R = decltype(V().x);
 #pragma unroll
   for (int q = 0; q < 16; q++) {
@@ -65,14 +78,14 @@ __device__ __forceinline__ void u2_slots(V (&v)[16], int cb) {
     for (int c = 0; c < 4; c++) s[c] = a[c].x + a[c].y;
 #pragma unroll
     for (int rr = 0; rr < 4; rr++) {
-      R t = cc<V>(cb + 4 * rr).x * s[0];
-      R re = cc<V>(cb + 16 + 4 * rr).x * a[0].y;
-      R im = cc<V>(cb + 16 + 4 * rr).y * a[0].x;
+      R t = cf(cb + 4 * rr).x * s[0];
+      R re = cf(cb + 16 + 4 * rr).x * a[0].y;
+      R im = cf(cb + 16 + 4 * rr).y * a[0].x;
 #pragma unroll
       for (int c = 1; c < 4; c++) {
-        t = fma(cc<V>(cb + 4 * rr + c).x, s[c], t);
-        re = fma(cc<V>(cb + 16 + 4 * rr + c).x, a[c].y, re);
-        im = fma(cc<V>(cb + 16 + 4 * rr + c).y, a[c].x, im);
+        t = fma(cf(cb + 4 * rr + c).x, s[c], t);
+        re = fma(cf(cb + 16 + 4 * rr + c).x, a[c].y, re);
+        im = fma(cf(cb + 16 + 4 * rr + c).y, a[c].x, im);
       }
       V o;
       o.x = t + re;
@@ -82,14 +95,14 @@ __device__ __forceinline__ void u2_slots(V (&v)[16], int cb) {
   }
 }
 
-template <int S, typename V>
-__device__ __forceinline__ void u1_slot(V (&v)[16], int cb) {
+template <int S, typename V, typename CF = CoefBank<V>>
+__device__ __forceinline__ void u1_slot(V (&v)[16], int cb, const CF& cf = CF()) {
 #pragma unroll
   for (int q = 0; q < 16; q++) {
     if ((q >> S) & 1) continue;
     const V a0 = v[q], a1 = v[q | (1 << S)];
-    v[q] = cfma(cc<V>(cb + 1), a1, cmul(cc<V>(cb), a0));
-    v[q | (1 << S)] = cfma(cc<V>(cb + 3), a1, cmul(cc<V>(cb + 2), a0));
+    v[q] = cfma(cf(cb + 1), a1, cmul(cf(cb), a0));
+    v[q | (1 << S)] = cfma(cf(cb + 3), a1, cmul(cf(cb + 2), a0));
   }
 }
 
@@ -196,20 +209,20 @@ __device__ __forceinline__ uint64_t mask64(int lo, int hi) { return (uint64_t)(u
 // four register slots) are: per-CTA out-bit terms (lanes 0..4 of each warp, broadcast by shuffle)
 // x the host-built per-thread table x rare mixed terms; the 16 register factors are products of
 // them built as A[k & 3] * B[k >> 2] with no branches, so v stays in place.
-template <typename V>
-__device__ __forceinline__ V cta_factor(int b, int e, uint64_t tile_off) {
+template <typename V, typename CF = CoefBank<V>>
+__device__ __forceinline__ V cta_factor(int b, int e, uint64_t tile_off, const CF& cf = CF()) {
   V f = cone<V>();
   for (int t = b; t < e; t += 3) {
     const uint64_t O = mask64(c_prog[t], c_prog[t + 1]);
-    const V c = cc<V>(c_prog[t + 2]);
+    const V c = cf(c_prog[t + 2]);
     if ((tile_off & O) == O) f = cmul(f, c);
   }
   return f;
 }
 
-template <typename V>
+template <typename V, typename CF = CoefBank<V>>
 __device__ __forceinline__ void diagset(V (&v)[16], int desc, int cb, int tid, int nthr, uint64_t tile_off,
-                                        const V* __restrict__ aux, const V* ctaf) {
+                                        const V* __restrict__ aux, const V* ctaf, const CF& cf = CF()) {
   const int flags = c_prog[desc];
   const V* tab = aux + c_prog[desc + 1];
   const int lane = tid & 31;
@@ -220,19 +233,19 @@ __device__ __forceinline__ void diagset(V (&v)[16], int desc, int cb, int tid, i
     for (int i = 0; i < 5; i++) F[i] = cmul(ctaf[5 * set + i], tab[i * nthr + tid]);
   } else if (nthr >= 32) {
     V mine = cone<V>();
-    if (lane < 5) mine = cta_factor<V>(c_prog[desc + 2 + lane], c_prog[desc + 3 + lane], tile_off);
+    if (lane < 5) mine = cta_factor<V>(c_prog[desc + 2 + lane], c_prog[desc + 3 + lane], tile_off, cf);
 #pragma unroll
     for (int i = 0; i < 5; i++) F[i] = cmul(shfl_c(mine, i), tab[i * nthr + tid]);
   } else {  // tiny tiles (T < 9): fewer than 32 threads, every thread walks the terms itself
 #pragma unroll
     for (int i = 0; i < 5; i++)
-      F[i] = cmul(cta_factor<V>(c_prog[desc + 2 + i], c_prog[desc + 3 + i], tile_off), tab[i * nthr + tid]);
+      F[i] = cmul(cta_factor<V>(c_prog[desc + 2 + i], c_prog[desc + 3 + i], tile_off, cf), tab[i * nthr + tid]);
   }
   const int me = c_prog[desc + 9];
   for (int t = c_prog[desc + 8]; t < me; t += 5) {
     const int si = c_prog[t], J = c_prog[t + 1];
     const uint64_t O = mask64(c_prog[t + 2], c_prog[t + 3]);
-    const V c = cc<V>(c_prog[t + 4]);
+    const V c = cf(c_prog[t + 4]);
     if ((tid & J) == J && (tile_off & O) == O) {
 #pragma unroll
       for (int i = 0; i < 5; i++)
@@ -247,7 +260,7 @@ __device__ __forceinline__ void diagset(V (&v)[16], int desc, int cb, int tid, i
     for (int k = 0; k < 16; k++) {
       const V a = (k & 3) == 0 ? A0 : (k & 3) == 1 ? A1 : (k & 3) == 2 ? A2 : A3;
       const V f = (k >> 2) == 0 ? a : cmul(a, (k >> 2) == 1 ? B1 : (k >> 2) == 2 ? B2 : B3);
-      cmul_ip(v[k], cmul(f, cc<V>(cb + k)));
+      cmul_ip(v[k], cmul(f, cf(cb + k)));
     }
   } else {
 #pragma unroll
@@ -381,9 +394,9 @@ __device__ __forceinline__ uint64_t expand_tile(uint64_t b, int split_a, int spl
 // thread table (TABM) or per-CTA terms (CTAM) are identically one and cost nothing; the register
 // factors are products of the non-trivial subset factors (the compiler shares common prefixes).
 // Requires the per-CTA factors in smem (SET != 255) and no mixed terms.
-template <int LAM, int SET, int TABM, int CTAM, typename V>
+template <int LAM, int SET, int TABM, int CTAM, typename V, typename CF>
 __device__ __forceinline__ void diagset_c(V (&v)[16], int desc, int cb, int tid, int nthr, const V* __restrict__ aux,
-                                          const V* ctaf) {
+                                          const V* ctaf, const CF& cf) {
   const V* tab = aux + c_prog[desc + 1];
   V F[5];
 #pragma unroll
@@ -413,7 +426,7 @@ __device__ __forceinline__ void diagset_c(V (&v)[16], int desc, int cb, int tid,
         one = false;
       }
     if (LAM) {
-      f = one ? cc<V>(cb + k) : cmul(f, cc<V>(cb + k));
+      f = one ? cf(cb + k) : cmul(f, cf(cb + k));
       one = false;
     }
     if (!one) cmul_ip(v[k], f);
@@ -422,39 +435,39 @@ __device__ __forceinline__ void diagset_c(V (&v)[16], int desc, int cb, int tid,
 
 // Compile-time op (generated kernels): the same gate code as the interpreter's run_op, with the
 // op fields as template arguments, so slots and coefficient offsets are immediates.
-template <int TYPE, int A, int B, int CB, int X, typename V>
+template <int TYPE, int A, int B, int CB, int X, typename V, typename CF>
 __device__ __forceinline__ void op_c(V (&v)[16], int tid, int nthr, uint64_t tile_off, const V* __restrict__ aux,
-                                     const V* ctaf) {
+                                     const V* ctaf, const CF& cf) {
   if constexpr (TYPE == SV_OP_U2) {
-    u2_slots<A, B>(v, CB);
+    u2_slots<A, B>(v, CB, cf);
   } else if constexpr (TYPE == SV_OP_U1) {
-    u1_slot<A>(v, CB);
+    u1_slot<A>(v, CB, cf);
   } else if constexpr (TYPE == SV_OP_H1) {
-    h1_slot<A>(v, cc<V>(CB).x);
+    h1_slot<A>(v, cf(CB).x);
   } else if constexpr (TYPE == SV_OP_H1U) {
     hu_slot<A>(v);
   } else if constexpr (TYPE == SV_OP_PERM2) {
     perm_slots<A, B>(v, X);
   } else if constexpr (TYPE == SV_OP_DIAG) {
     if constexpr (A < 4 && B < 4) {
-      d2_slots<A, B>(v, cc<V>(CB), cc<V>(CB + 1), cc<V>(CB + 2), cc<V>(CB + 3));
+      d2_slots<A, B>(v, cf(CB), cf(CB + 1), cf(CB + 2), cf(CB + 3));
     } else if constexpr (A < 4) {
       const int tb = code_val(B, tid, tile_off);
-      d1_slot<A>(v, tb ? cc<V>(CB + 2) : cc<V>(CB), tb ? cc<V>(CB + 3) : cc<V>(CB + 1));
+      d1_slot<A>(v, tb ? cf(CB + 2) : cf(CB), tb ? cf(CB + 3) : cf(CB + 1));
     } else {
       const int s = code_val(A, tid, tile_off) | (code_val(B, tid, tile_off) << 1);
-      scale_all(v, sel4(s, cc<V>(CB), cc<V>(CB + 1), cc<V>(CB + 2), cc<V>(CB + 3)));
+      scale_all(v, sel4(s, cf(CB), cf(CB + 1), cf(CB + 2), cf(CB + 3)));
     }
   } else if constexpr (TYPE == SV_OP_DIAG_CP) {
     if constexpr (A < 4 && B < 4) {
-      cp_slots<A, B>(v, cc<V>(CB));
+      cp_slots<A, B>(v, cf(CB));
     } else if constexpr (A < 4) {
-      if (code_val(B, tid, tile_off)) cp_slot<A>(v, cc<V>(CB));
+      if (code_val(B, tid, tile_off)) cp_slot<A>(v, cf(CB));
     } else {
-      if (code_val(A, tid, tile_off) & code_val(B, tid, tile_off)) scale_all(v, cc<V>(CB));
+      if (code_val(A, tid, tile_off) & code_val(B, tid, tile_off)) scale_all(v, cf(CB));
     }
   } else if constexpr (TYPE == SV_OP_DIAGSET) {
-    diagset(v, A, CB, tid, nthr, tile_off, aux, ctaf);
+    diagset(v, A, CB, tid, nthr, tile_off, aux, ctaf, cf);
   }
 }
 

@@ -51,8 +51,8 @@ def test_generated_qv_kernels_are_pure_fp64_streams(tools, tmp_path):
         body = subprocess.run(["cuobjdump", "-sass", cub], capture_output=True, text=True, check=True).stdout
         u2 = open(tmp_path / f"section_{i}.cu").read().count("op_c<1,")
         dfma = len(re.findall(r"\bDFMA\b", body))
-        ldc_thread = len(re.findall(r"\bLDC(\.64)? R\d+, c\[0x3\]\[R\d+", body))  # per-lane indexed
-        uni = len(re.findall(r"\bLDCU(\.64|\.128)? UR\d+, c\[0x3\]", body))
+        ldc_thread = len(re.findall(r"\bLDC(\.64)? R\d+, c\[0x[03]\]\[R\d+", body))  # per-lane indexed
+        uni = len(re.findall(r"\bLDCU(\.64|\.128)? UR\d+, c\[0x[03]\]", body))  # parameter or constant bank
         spill = len(re.findall(r"\bSTL\b", body))
         # three-multiply U2: 4 groups x 4 outputs x 9 DFMA per thread
         assert dfma >= 144 * u2, (i, dfma, u2)
