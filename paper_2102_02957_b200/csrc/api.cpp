@@ -377,8 +377,14 @@ int launch_one(sv_state* h, const Launch& L, int split_a = 0, int split_b = 0) {
 int exchange_pipelined(sv_state* h, const std::vector<ExPair>& pairs_in, const Launch& L0, int* done) {
   *done = 0;
   static const int pieces_env = [] {
-    const char* e = std::getenv("SV_XPIPE");  // opt-in: measured no gain at 2 GPUs (the swap kernel
-    return e ? std::atoi(e) : 0;               // and the section compete for SMs and HBM)
+    const char* e = std::getenv("SV_XPIPE");  // 0 disables; 2 or 4 pieces
+    return e ? std::atoi(e) : 4;
+  }();
+  // the swap kernel of a piece runs on a high-priority stream with a capped grid, so the
+  // section's CTAs keep most SMs (QV33, 2 GPUs: 1141 -> 1050 ms with 4 pieces and 128 blocks)
+  static const unsigned xgrid = [] {
+    const char* e = std::getenv("SV_XGRID");
+    return e ? (unsigned)std::atoi(e) : 128u;
   }();
   if (pieces_env < 2 || L0.T < SV_R_BITS) return SV_OK;
   std::vector<ExPair> pairs = pairs_in;
@@ -412,7 +418,9 @@ int exchange_pipelined(sv_state* h, const std::vector<ExPair>& pairs_in, const L
     std::swap(sbit[0], sbit[1]);
   }
   if (!h->st_x) {
-    CUDA_TRY(h, cudaStreamCreateWithFlags(&h->st_x, cudaStreamNonBlocking));
+    int lo = 0, hi = 0;  // the exchange stream at the highest priority: its blocks go first
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    CUDA_TRY(h, cudaStreamCreateWithPriority(&h->st_x, cudaStreamNonBlocking, hi));
     for (auto& e : h->ev_x) CUDA_TRY(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   const uint64_t block = 1ull << (h->nL - a.k);
@@ -436,7 +444,8 @@ int exchange_pipelined(sv_state* h, const std::vector<ExPair>& pairs_in, const L
       a.fix_val[i] = (p >> i) & 1;
     }
     int launches = 0;
-    CUDA_TRY(h, launch_exchange_peer(h->dbl, h->sv, h->peers.data(), h->rank, h->nL, a, h->st_x, &launches));
+    CUDA_TRY(h, launch_exchange_peer(h->dbl, h->sv, h->peers.data(), h->rank, h->nL, a, h->st_x, &launches,
+                                     xgrid));
     h->stats.kernel_launches += launches;
     if (int rc = barrier(h, h->st_x)) return rc;
     CUDA_TRY(h, cudaEventRecord(h->ev_x[p], h->st_x));

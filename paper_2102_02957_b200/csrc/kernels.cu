@@ -7,6 +7,7 @@
 //   K6 k_set_basis    |k>.
 //   K7 k_gather       amplitude gather.
 //   exchange          peer-memory swap of local bit(s) with rank bit(s) over NVLink.
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -512,7 +513,7 @@ cudaError_t launch_gather(bool dbl, const void* sv, const uint64_t* offs, size_t
 }
 
 cudaError_t launch_exchange_peer(bool dbl, void* local, void* const* peer_bases, int rank, int nL,
-                                 const ExchangeArgs& a, cudaStream_t st, int* launches) {
+                                 const ExchangeArgs& a, cudaStream_t st, int* launches, unsigned max_blocks) {
   // rank bits of this rank at the exchanged positions
   int mine = 0;
   for (int i = 0; i < a.k; i++) mine |= ((rank >> a.bsel[i]) & 1) << i;
@@ -546,11 +547,13 @@ cudaError_t launch_exchange_peer(bool dbl, void* local, void* const* peer_bases,
       e.val_peer[i] = ins[i].vp;
     }
     const int th = 256;
+    unsigned gx = grid_for(count, th);
+    if (max_blocks && gx > max_blocks) gx = max_blocks;  // leave SMs to a concurrent section
     if (dbl)
-      k_exchange_peer<double2><<<grid_for(count, th), th, 0, st>>>((double2*)local, (double2*)peer_bases[partner],
+      k_exchange_peer<double2><<<gx, th, 0, st>>>((double2*)local, (double2*)peer_bases[partner],
                                                                    count, e);
     else
-      k_exchange_peer<float2><<<grid_for(count, th), th, 0, st>>>((float2*)local, (float2*)peer_bases[partner], count,
+      k_exchange_peer<float2><<<gx, th, 0, st>>>((float2*)local, (float2*)peer_bases[partner], count,
                                                                   e);
     if (launches) (*launches)++;
     cudaError_t err = cudaGetLastError();

@@ -57,7 +57,8 @@ struct ExchangeArgs {
   int fix_val[2] = {0, 0};
 };
 cudaError_t launch_exchange_peer(bool dbl, void* local, void* const* peer_bases /*host array [world]*/, int rank,
-                                 int nL, const ExchangeArgs& a, cudaStream_t st, int* launches);
+                                 int nL, const ExchangeArgs& a, cudaStream_t st, int* launches,
+                                 unsigned max_blocks = 0);
 // staging -> shard copy of `count` amplitudes at element offsets (for the NCCL exchange path)
 cudaError_t launch_copy(bool dbl, void* dst, const void* src, size_t count, cudaStream_t st);
 
