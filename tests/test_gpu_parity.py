@@ -175,8 +175,8 @@ def test_mirror_returns_to_basis_large():
 
 @pytest.mark.slow
 def test_qv28_full_size_parity():
-    # BASELINE configs[1] at full size in the bench's launch configuration (c = 12), full compare.
-    n, c = 28, 12
+    # BASELINE configs[1] at full size in the bench's launch configuration (c = 9), full compare.
+    n, c = 28, 9
     circ = C.quantum_volume(n, 10, 1)
     with sv.StateVector(n, c) as s:
         s.apply(circ)
@@ -215,3 +215,45 @@ def test_generated_kernels_run():
         s.apply(C.quantum_volume(14, 4, 9))
         st = s.stats()
     assert st["jit_launches"] > 0 and st["interp_launches"] == 0
+
+
+@pytest.mark.slow
+def test_qft30_full_size_closed_form():
+    # BASELINE configs[2] at full size in the bench's configuration (c = 8, from its seeded basis
+    # state): sampled amplitudes against QFT|k>_j = e^{2 pi i jk / 2^n} / 2^{n/2} (the closed form
+    # the oracle is pinned to, tests/test_oracle.py), uniform marginals, unit norm.
+    n, c = 30, 8
+    N = 1 << n
+    k = C.basis_index(1, n)
+    rng = np.random.default_rng(30)
+    idx = np.unique(np.concatenate([np.arange(64), rng.integers(0, N, 4096), [N - 1]])).astype(np.uint64)
+    with sv.StateVector(n, c) as s:
+        s.reset(k)
+        s.apply(C.qft(n))
+        a = s.amplitudes(idx)
+        p = s.probabilities(list(range(10)))
+        nrm = s.norm()
+    j = idx.astype(np.int64)
+    ref = np.exp(2j * np.pi * ((j * k) % N) / N) / math.sqrt(N)
+    assert np.max(np.abs(a - ref)) <= 1e-10
+    assert np.max(np.abs(p - 1.0 / 1024)) <= 1e-12
+    assert abs(nrm - 1.0) <= 1e-12
+
+
+@pytest.mark.slow
+def test_qv33_full_size_mirror():
+    # BASELINE configs[3] at full size (2^33 fp64 amplitudes, 128 GiB) in the bench's configuration
+    # (c = 9): the mirror circuit C C^dagger returns the seeded basis state exactly; the forward
+    # circuit keeps the norm and its marginals sum to one.
+    n, c = 33, 9
+    k = C.basis_index(6, n)
+    circ = C.quantum_volume(n, 10, 1)
+    with sv.StateVector(n, c) as s:
+        s.reset(k)
+        s.apply(C.mirror(circ))
+        a = s.amplitudes(np.array([k, (k + 1) % (1 << n)], dtype=np.uint64))
+        assert abs(a[0] - 1.0) <= 1e-10 and abs(a[1]) <= 1e-10
+        s.reset(0)
+        s.apply(circ)
+        assert abs(s.norm() - 1.0) <= 1e-12
+        assert abs(s.probabilities([0, 16, 32]).sum() - 1.0) <= 1e-12
