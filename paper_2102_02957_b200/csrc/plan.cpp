@@ -13,6 +13,7 @@
 //     (COMPACT step).  A physical swap of memory bits plus the matching relabel of sigma leaves
 //     the logical state unchanged, so none of this changes what the circuit computes.
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 
 #include "common.h"
@@ -225,6 +226,215 @@ struct Planner {
 
 }  // namespace
 
+// One-level executor mapping: the pass at chunk c, sections mapped onto memory bits, exchanges
+// when a section needs a rank bit (Belady victims, Planner::section).
+Status plan_one_level(const sv_gate* g, size_t count, int n, int c, int world_log2, std::vector<int>& pi,
+                      std::vector<int>& sigma, uint32_t flags, std::vector<Step>& steps, PlanCounters& ctr,
+                      const PlanLayout& layout, std::vector<int>* sigma_initial) {
+  const int nL = n - world_log2;
+  std::vector<sv_gate> tokens;
+  tokens.reserve(count * 2 + 16);
+  if (Status s = block_pass(g, count, n, c, pi, flags, tokens); !s.good()) return s;
+
+  std::vector<Block> blocks;
+  Block cur;
+  bool inside = false;
+  std::vector<std::pair<int, int>> trailing;  // chunk_swaps after the last section
+  for (const sv_gate& t : tokens) {
+    switch (t.kind) {
+      case SV_CHUNK_SWAP:
+        cur.relabels.push_back({t.q0, t.q1});
+        ctr.chunk_swaps++;
+        break;
+      case SV_BEGIN:
+        inside = true;
+        break;
+      case SV_END:
+        if (!inside) return Status::err(SV_EMALFORMED, "END without BEGIN");
+        blocks.push_back(std::move(cur));
+        cur = Block();
+        inside = false;
+        break;
+      default:
+        cur.gates.push_back(t);
+    }
+  }
+  if (layout.free_initial && !blocks.empty()) {
+    // NEXT-2 "free initial layout" (the paper's bit reordering, P:287-289): the state is a basis
+    // state, so sigma can be chosen freely at no data cost.  Put the first section's qubits on
+    // the lowest memory bits (its tile is then coalesced and no exchange is needed), keep every
+    // other qubit's relative order, then undo the first block's chunk_swap relabels.
+    std::vector<int> after = sigma;
+    for (const auto& rl : blocks[0].relabels) std::swap(after[rl.first], after[rl.second]);
+    const uint64_t need = Planner::needed(blocks[0], after, n, nullptr);
+    std::vector<int> order(n);  // paper qubits: needed first, each group by current memory bit
+    for (int p = 0; p < n; p++) order[p] = p;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+      const bool na = (need >> after[a]) & 1, nb = (need >> after[b]) & 1;
+      if (na != nb) return na;
+      return after[a] < after[b];
+    });
+    for (int i = 0; i < n; i++) after[order[i]] = i;
+    for (auto it = blocks[0].relabels.rbegin(); it != blocks[0].relabels.rend(); ++it)
+      std::swap(after[it->first], after[it->second]);
+    sigma = after;
+  }
+  if (sigma_initial) *sigma_initial = sigma;
+  Planner planner(n, nL, layout, sigma, steps, ctr);
+  planner.run(blocks);
+  for (const auto& rl : cur.relabels) planner.relabel(rl.first, rl.second);  // trailing chunk_swaps
+  return Status::ok();
+}
+
+double exchange_volume(const std::vector<Step>& steps) {  // shard-equivalents sent per GPU
+  double v = 0.0;
+  for (const Step& st : steps)
+    if (st.type == Step::EXCHANGE) v += 1.0 - std::ldexp(1.0, -(int)st.ex.size());
+  return v;
+}
+
+// Two-level blocking (NEXT-1; the paper's own MPI-level use of the pass): an outer
+// pass with chunk = the GPU shard (nL qubits) decides which qubits are global; its chunk_swaps are
+// the cross-GPU exchanges (batched), and every outer block — whose non-diagonal gates are all on
+// local qubits — is planned by the one-level mapping with the inner chunk c, which then never
+// exchanges.  Outer positions are memory bits; tau tracks where the inner plans' physical moves
+// (store swaps, compactions) put each of them.
+Status plan_two_level(const sv_gate* g, size_t count, int n, int c, int world_log2, std::vector<int>& pi,
+                      std::vector<int>& sigma, uint32_t flags, std::vector<Step>& steps, PlanCounters& ctr,
+                      const PlanLayout& layout, std::vector<int>* sigma_initial) {
+  const int nL = n - world_log2;
+  std::vector<int> mem(n);  // logical -> memory bit at entry
+  for (int q = 0; q < n; q++) mem[q] = sigma[pi[q]];
+  std::vector<int> piO = mem;
+  std::vector<sv_gate> tokens;
+  tokens.reserve(count * 2 + 16);
+  if (layout.free_initial) {
+    // basis state: the first outer block's qubits start local (no exchange before it)
+    std::vector<int> probe = piO;
+    if (Status s = block_pass(g, count, n, nL, probe, 0, tokens); !s.good()) return s;
+    std::vector<int> inv(n);
+    for (int q = 0; q < n; q++) inv[piO[q]] = q;
+    uint64_t first = 0;  // logical qubits of the first outer block's non-diagonal gates
+    bool inside = false;
+    std::vector<int> cur = piO, curinv = inv;
+    for (const sv_gate& t : tokens) {
+      if (t.kind == SV_CHUNK_SWAP) {  // the pass's relabel in outer positions
+        const int a = curinv[t.q0], b = curinv[t.q1];
+        std::swap(cur[a], cur[b]);
+        curinv[cur[a]] = a;
+        curinv[cur[b]] = b;
+      } else if (t.kind == SV_BEGIN) {
+        inside = true;
+      } else if (t.kind == SV_END) {
+        break;
+      } else if (inside && !is_diag(t.kind)) {
+        first |= 1ull << curinv[t.q0];
+        if (is_two(t.kind)) first |= 1ull << curinv[t.q1];
+      }
+    }
+    std::vector<int> order(n);
+    for (int q = 0; q < n; q++) order[q] = q;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+      const bool fa = (first >> a) & 1, fb = (first >> b) & 1;
+      if (fa != fb) return fa;
+      return piO[a] < piO[b];
+    });
+    for (int i = 0; i < n; i++) piO[order[i]] = i;
+    tokens.clear();
+  }
+  const std::vector<int> piO0 = piO;
+  if (Status s = block_pass(g, count, n, nL, piO, 0, tokens); !s.good()) return s;
+
+  std::vector<int> tau(n), init_tau(n);
+  for (int p = 0; p < n; p++) tau[p] = init_tau[p] = p;
+  bool first_block = true;
+  Step batch;
+  batch.type = Step::EXCHANGE;
+  auto flush = [&]() {
+    if (batch.ex.empty()) return;
+    ctr.exchanges += batch.ex.size();
+    ctr.exchange_batches++;
+    steps.push_back(std::move(batch));
+    batch = Step();
+    batch.type = Step::EXCHANGE;
+  };
+  std::vector<sv_gate> blk;
+  bool inside = false;
+  for (const sv_gate& t : tokens) {
+    if (t.kind == SV_CHUNK_SWAP) {
+      if (t.q1 < nL || t.q0 >= nL) return Status::err(SV_EMALFORMED, "internal: outer chunk_swap not local/global");
+      batch.ex.push_back({tau[t.q0], tau[t.q1]});
+      ctr.chunk_swaps++;
+    } else if (t.kind == SV_BEGIN) {
+      flush();
+      blk.clear();
+      inside = true;
+    } else if (t.kind == SV_END) {
+      if (!inside) return Status::err(SV_EMALFORMED, "END without BEGIN");
+      inside = false;
+      for (sv_gate& x : blk) {
+        x.q0 = tau[x.q0];
+        if (is_two(x.kind)) x.q1 = tau[x.q1];
+      }
+      std::vector<int> pin(n), sin(n), sinit;
+      for (int p = 0; p < n; p++) pin[p] = sin[p] = p;
+      PlanLayout L2 = layout;
+      L2.free_initial = layout.free_initial && first_block;
+      if (Status s = plan_one_level(blk.data(), blk.size(), n, c, world_log2, pin, sin, flags & ~(uint32_t)SV_RESTORE_ORDER,
+                                    steps, ctr, L2, &sinit);
+          !s.good())
+        return s;
+      if (first_block && layout.free_initial) init_tau = sinit;  // block-start bit p lives at sinit[p]
+      std::vector<int> rho(n);
+      for (int x = 0; x < n; x++) rho[x] = sin[pin[x]];
+      for (int p = 0; p < n; p++) tau[p] = rho[first_block && layout.free_initial ? p : tau[p]];
+      first_block = false;
+    } else {
+      blk.push_back(t);
+    }
+  }
+  flush();
+  // logical q: outer position piO[q] -> memory bit tau[piO[q]]
+  if (sigma_initial) {
+    std::vector<int> s0(n);
+    for (int q = 0; q < n; q++) s0[pi[q]] = init_tau[piO0[q]];
+    *sigma_initial = s0;
+  }
+  pi = piO;
+  sigma = tau;
+  return Status::ok();
+}
+
+// Blocked plan: one-level, or — on several GPUs — the two-level plan when it moves fewer bytes
+// across GPUs (SV_TWO_LEVEL=0 disables it).
+Status plan_blocked(const sv_gate* g, size_t count, int n, int c, int world_log2, std::vector<int>& pi,
+                    std::vector<int>& sigma, uint32_t flags, std::vector<Step>& steps, PlanCounters& ctr,
+                    const PlanLayout& layout, std::vector<int>* sigma_initial) {
+  static const bool two = [] {
+    const char* e = std::getenv("SV_TWO_LEVEL");
+    return !(e && e[0] == '0');
+  }();
+  if (!two || world_log2 == 0 || (flags & SV_RESTORE_ORDER))
+    return plan_one_level(g, count, n, c, world_log2, pi, sigma, flags, steps, ctr, layout, sigma_initial);
+  std::vector<int> pi1 = pi, s1 = sigma, pi2 = pi, s2 = sigma, init1, init2;
+  std::vector<Step> st1, st2;
+  PlanCounters c1, c2;
+  if (Status s = plan_one_level(g, count, n, c, world_log2, pi1, s1, flags, st1, c1, layout, &init1); !s.good())
+    return s;
+  Status s = plan_two_level(g, count, n, c, world_log2, pi2, s2, flags, st2, c2, layout, &init2);
+  const bool use2 = s.good() && exchange_volume(st2) < exchange_volume(st1);
+  if (use2) {
+    pi = pi2, sigma = s2, ctr = c2;
+    steps.insert(steps.end(), st2.begin(), st2.end());
+    if (sigma_initial) *sigma_initial = init2;
+  } else {
+    pi = pi1, sigma = s1, ctr = c1;
+    steps.insert(steps.end(), st1.begin(), st1.end());
+    if (sigma_initial) *sigma_initial = init1;
+  }
+  return Status::ok();
+}
+
 Status make_plan(const sv_gate* g, size_t count, int n, int c, int world_log2, std::vector<int>& pi,
                  std::vector<int>& sigma, uint32_t flags, std::vector<Step>& steps, PlanCounters& ctr,
                  const PlanLayout& layout, std::vector<int>* sigma_initial) {
@@ -291,58 +501,7 @@ Status make_plan(const sv_gate* g, size_t count, int n, int c, int world_log2, s
     return Status::ok();
   }
 
-  std::vector<sv_gate> tokens;
-  tokens.reserve(count * 2 + 16);
-  if (Status s = block_pass(g, count, n, c, pi, flags, tokens); !s.good()) return s;
-
-  std::vector<Block> blocks;
-  Block cur;
-  bool inside = false;
-  std::vector<std::pair<int, int>> trailing;  // chunk_swaps after the last section
-  for (const sv_gate& t : tokens) {
-    switch (t.kind) {
-      case SV_CHUNK_SWAP:
-        cur.relabels.push_back({t.q0, t.q1});
-        ctr.chunk_swaps++;
-        break;
-      case SV_BEGIN:
-        inside = true;
-        break;
-      case SV_END:
-        if (!inside) return Status::err(SV_EMALFORMED, "END without BEGIN");
-        blocks.push_back(std::move(cur));
-        cur = Block();
-        inside = false;
-        break;
-      default:
-        cur.gates.push_back(t);
-    }
-  }
-  if (layout.free_initial && !blocks.empty()) {
-    // NEXT-2 "free initial layout" (the paper's bit reordering, P:287-289): the state is a basis
-    // state, so sigma can be chosen freely at no data cost.  Put the first section's qubits on
-    // the lowest memory bits (its tile is then coalesced and no exchange is needed), keep every
-    // other qubit's relative order, then undo the first block's chunk_swap relabels.
-    std::vector<int> after = sigma;
-    for (const auto& rl : blocks[0].relabels) std::swap(after[rl.first], after[rl.second]);
-    const uint64_t need = Planner::needed(blocks[0], after, n, nullptr);
-    std::vector<int> order(n);  // paper qubits: needed first, each group by current memory bit
-    for (int p = 0; p < n; p++) order[p] = p;
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-      const bool na = (need >> after[a]) & 1, nb = (need >> after[b]) & 1;
-      if (na != nb) return na;
-      return after[a] < after[b];
-    });
-    for (int i = 0; i < n; i++) after[order[i]] = i;
-    for (auto it = blocks[0].relabels.rbegin(); it != blocks[0].relabels.rend(); ++it)
-      std::swap(after[it->first], after[it->second]);
-    sigma = after;
-  }
-  if (sigma_initial) *sigma_initial = sigma;
-  Planner planner(n, nL, layout, sigma, steps, ctr);
-  planner.run(blocks);
-  for (const auto& rl : cur.relabels) planner.relabel(rl.first, rl.second);  // trailing chunk_swaps
-  return Status::ok();
+  return plan_blocked(g, count, n, c, world_log2, pi, sigma, flags, steps, ctr, layout, sigma_initial);
 }
 
 }  // namespace sv

@@ -97,7 +97,7 @@ def test_pass_errors():
         sv.block_circuit(bad, 4, 2)
 
 
-def run_plan_dense(recs, n, c, g, flags=0, seed=0):
+def run_plan_dense(recs, n, c, g, flags=0, seed=0, basis_zero=False):
     """Execute the library's plan densely (exchange = SWAP of memory bits) and compare with the
     oracle on the original circuit, un-permuting through mu(q) = sigma[pi[q]]."""
     plan, pi, sigma = sv.plan_circuit(recs, n, c, g, flags=flags)
@@ -125,6 +125,9 @@ def run_plan_dense(recs, n, c, g, flags=0, seed=0):
     rng = np.random.default_rng(seed)
     psi = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
     psi /= np.linalg.norm(psi)
+    if basis_zero:  # SV_FREE_LAYOUT plans assume a basis state; |0> sits at 0 under any layout
+        psi = np.zeros(1 << n, dtype=np.complex128)
+        psi[0] = 1
     ref = O.apply_circuit(recs, n, psi)
     mem = O.apply_circuit(plan_to_dense_records(plan), n, psi)
     got = O.unpermute(mem, memory_perm(pi, sigma))
@@ -201,3 +204,28 @@ def test_jit_sources_compile_for_sm100a(prec, tmp_path):
     srcs = [open(p).read() for p in sorted(tmp_path.glob("section_*.cu"))]
     assert len(srcs) == k and len(list(tmp_path.glob("section_*.cubin"))) == k
     assert all("op_c<" in s for s in srcs)
+
+
+@pytest.mark.parametrize("g", [1, 2, 3])
+def test_two_level_and_free_layout_plans(g):
+    # multi-GPU plans take the two-level form (outer pass at the shard size, NEXT-1) when it moves
+    # fewer bytes; with SV_FREE_LAYOUT the first outer block starts local.  Dense semantics hold.
+    for recs, n, c in [(C.quantum_volume(12, 8, 2), 12, 5), (C.qft(12), 12, 4),
+                       (C.random_circuit(11, 150, 40 + g), 11, 4)]:
+        run_plan_dense(recs, n, c, g, flags=sv.SV_FREE_LAYOUT, basis_zero=True)
+        run_plan_dense(recs, n, c, g)
+
+
+def test_two_level_exchange_volume_qv33():
+    # QV(33, 10, 1), c = 9: cross-GPU exchanges per GPU in shard-equivalents (SURVEY §8(f) NEXT-1
+    # predicted 1.5 / 2.25 / 2.62 for the two-level pass; the one-level Belady mapping needs
+    # 2.5 / 4.5 / 6.1)
+    circ = C.quantum_volume(33, 10, 1)
+    for g, most in [(1, 1.0), (2, 1.5), (3, 2.5)]:
+        plan, _, _ = sv.plan_circuit(circ, 33, 9, g, flags=sv.SV_FREE_LAYOUT)
+        ex = plan[plan["kind"] == 9]
+        batches = {}
+        for r in ex:
+            batches[int(r["pad"])] = batches.get(int(r["pad"]), 0) + 1
+        vol = sum(1 - 2.0 ** -k for k in batches.values())
+        assert vol <= most + 1e-9, (g, vol)
