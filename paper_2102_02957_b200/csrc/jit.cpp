@@ -199,7 +199,7 @@ std::string gen_source(const int* p, const Launch& L, bool dbl) {
   const bool persist = l2_prefetch(L, dbl);
   auto& o = g.o;
   o << "#include \"section_dev.cuh\"\nusing namespace sv;\ntypedef " << (dbl ? "double2" : "float2") << " V;\n";
-  o << "extern \"C\" __global__ void __launch_bounds__(" << nt << ", " << (H->T <= 11 ? 4 : H->T == 12 ? 2 : 1)
+  o << "extern \"C\" __global__ void __launch_bounds__(" << nt << ", " << (H->T <= 12 ? std::min(16, 512 / nt) : 1)
     << ") sv_sec(V* __restrict__ psi, const V* __restrict__ aux, int split_a, int split_b, "
     << coef_param_decl_impl(L, dbl) << ") {\n";
   o << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n"
