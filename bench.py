@@ -207,6 +207,7 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     wl = workload(args.workload, world)
+    wl["desc"] = wl["desc"].replace("fp64", args.precision)
     n, gates = wl["n"], wl["gates"]
     c = args.chunk_bits if args.chunk_bits else wl["chunk_bits"]
     stream = torch.cuda.Stream()

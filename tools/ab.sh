@@ -1,5 +1,4 @@
-for C in 6 7; do
-  SV_PREF_TILE=10 timeout 600 python bench.py --workload qft30 --chunk-bits $C --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/t10_qft30_$C.json 2> gpurun_out/t10_qft30_$C.err
-done
-SV_PREF_TILE=10 timeout 600 python bench.py --workload qv28 --chunk-bits 7 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/t10_qv28_7.json 2> gpurun_out/t10_qv28_7.err
-timeout 600 python bench.py --workload qft30 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/t11_qft30_8.json 2> gpurun_out/t11_qft30_8.err
+timeout 900 python bench.py --workload qft_weak --precision fp32 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/f32_qft33.json 2> gpurun_out/f32_qft33.err
+timeout 900 python bench.py --workload qft_weak --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/f64_qft33.json 2> gpurun_out/f64_qft33.err
+timeout 900 python bench.py --workload qv_weak --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/f64_qv30.json 2> gpurun_out/f64_qv30.err
+timeout 900 python bench.py --workload qv28 --precision fp32 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/f32_qv28.json 2> gpurun_out/f32_qv28.err
