@@ -320,8 +320,8 @@ std::string gen_source_pipelined(const int* p, const Launch& L, bool dbl) {
   auto& o = g.o;
   o << "#include \"section_dev.cuh\"\nusing namespace sv;\ntypedef " << (dbl ? "double2" : "float2") << " V;\n";
   o << "constexpr int NTG = " << nt << ", TILE = " << (1 << H->T) << ";\n";
-  o << "extern \"C\" __global__ void __launch_bounds__(" << 2 * nt
-    << ", 1) sv_sec(V* __restrict__ psi, const V* __restrict__ aux, int split_a, int split_b, "
+  o << "extern \"C\" __global__ void __launch_bounds__(" << 2 * nt << ", " << std::max(1, 512 / (2 * nt))
+    << ") sv_sec(V* __restrict__ psi, const V* __restrict__ aux, int split_a, int split_b, "
     << coef_param_decl_impl(L, dbl) << ") {\n";
   o << "  extern __shared__ __align__(128) unsigned char smem_raw[];\n"
     << "  V* const bufs = reinterpret_cast<V*>(smem_raw);\n"
