@@ -314,6 +314,10 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
     std::vector<int> cand;
     for (int pos = 0; pos < T; pos++)
       if (po.slot_of[pos] < 0) cand.push_back(pos);
+    // the last phase of a multi-phase section walks the lowest STORE memory bits first (they
+    // differ from the load order after fused store swaps): its store can then go straight to HBM
+    if (pi + 1 == phases.size() && phases.size() > 1)
+      std::stable_sort(cand.begin(), cand.end(), [&](int a, int b) { return store_bits[a] < store_bits[b]; });
     std::vector<bool> taken(cand.size(), false);
     uint32_t span = 1;  // bit v set: vector v is an XOR of chosen vectors (v = 0 always)
     for (size_t i = 0; i < cand.size() && (int)po.chosen.size() < G; i++) {

@@ -22,6 +22,8 @@ namespace sv {
 
 namespace {
 
+constexpr int SV_R_BITS_PLAN = 4;  // register qubits per phase (program.h SV_R_BITS)
+
 sv_gate to_memory(const sv_gate& t, const std::vector<int>& sigma) {
   sv_gate r = t;
   r.q0 = sigma[t.q0];
@@ -169,9 +171,28 @@ struct Planner {
       const uint64_t nxt = needed(blocks[i + 1], v, nL, nullptr) & ((nL >= 64) ? ~0ull : ((1ull << nL) - 1));
       if (__builtin_popcountll(nxt) <= L.max_tile) {
         uint64_t cand = nxt & tile & ~low;  // next-section bits we can pull down now
+        // qubits of the next section's first gates (about its first register phase): leave them
+        // off the low bits when others can go there, so that phase's lanes can walk the low bits
+        // and read HBM directly
+        uint64_t early = 0;
+        {
+          std::vector<int> w = v;
+          for (const sv_gate& t : blocks[i + 1].gates) {
+            if (t.kind == SV_SWAP) {
+              std::swap(w[t.q0], w[t.q1]);
+              continue;
+            }
+            if (is_diag(t.kind)) continue;
+            uint64_t m = 1ull << w[t.q0];
+            if (is_two(t.kind)) m |= 1ull << w[t.q1];
+            if (__builtin_popcountll(early | m) > SV_R_BITS_PLAN) break;
+            early |= m;
+          }
+        }
         for (int l = 0; l < nlow && cand; l++) {
           if (((nxt >> l) & 1) || !((tile >> l) & 1)) continue;
-          const int x = 63 - __builtin_clzll(cand);  // highest candidate
+          const uint64_t pref = (cand & ~early) ? (cand & ~early) : cand;
+          const int x = 63 - __builtin_clzll(pref);  // highest (late-used) candidate
           cand &= ~(1ull << x);
           sw.push_back({l, x});
         }
