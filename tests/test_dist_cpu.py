@@ -1,4 +1,4 @@
-"""The N > 1 path on CPU: world_size 2 and 4 over gloo.
+"""The N > 1 path on CPU: world_size 2, 4 and 8 over gloo.
 
 Each process is one rank: it compiles its own section programs (sv_compile_circuit with its rank,
 so rank bits fold into constants exactly as on the GPU), runs them on its shard with the kernel
@@ -102,7 +102,7 @@ def _worker(rank, world, port, cases, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_distributed_plan_over_gloo(world):
     import torch.multiprocessing as mp
     from paper_2102_02957_b200 import build
