@@ -67,6 +67,10 @@ typedef struct {
 #define SV_RESTORE_ORDER (1u << 1) /* append swaps returning the paper-physical order to logical */
 #define SV_EXCHANGE_NCCL (1u << 2) /* cross-GPU exchange by NCCL send/recv through a staging ring */
                                    /* instead of the peer-memory swap kernel                    */
+#define SV_FUSE_EXCHANGE (1u << 4) /* sv_compile_circuit: fuse one-bit exchanges into the next  */
+                                   /* section's load (as sv_apply_circuit does on GPUs with peer */
+                                   /* access); the exchange record gets [4] = 1, the launch      */
+                                   /* record [10], [11] = the exchanged local / rank bit         */
 #define SV_FREE_LAYOUT   (1u << 3) /* sv_plan_circuit / sv_compile_circuit: plan as sv_apply_   */
                                    /* circuit does right after sv_reset (the state is a basis   */
                                    /* state, so the planner chooses the initial memory layout; */

@@ -355,10 +355,23 @@ int launch_one(sv_state* h, const Launch& L, int split_a = 0, int split_b = 0) {
   const char* cdev = (const char*)h->d_coef.p + L.coef_off * h->amp;
   const char* adev = (const char*)h->d_aux.p + L.aux_off * h->amp;
   cudaError_t je = cudaSuccess;
-  if (jit_launch_section(h->dbl, h->sv, h->prog.ints.data() + L.int_off, h->prog.coefs.data() + 2 * L.coef_off, L,
-                         pdev, cdev, adev, h->st, &je, split_a, split_b)) {
+  void* lo = h->sv;
+  void* hi = nullptr;
+  if (L.flags & SV_FLAG_XRANK) {
+    // fused exchange + section: the tiles span this GPU and its partner across rank bit xb; each
+    // GPU takes the tiles whose highest out bit equals its own value of that rank bit
+    const int rb = L.xb - h->nL, mine = (h->rank >> rb) & 1, partner = h->rank ^ (1 << rb);
+    lo = mine ? h->peers[partner] : h->sv;
+    hi = mine ? h->sv : h->peers[partner];
+    split_a = (1 << 16) | (mine << 8) | (L.n_out - 1);
+    split_b = 0;
+  }
+  if (jit_launch_section(h->dbl, lo, h->prog.ints.data() + L.int_off, h->prog.coefs.data() + 2 * L.coef_off, L,
+                         pdev, cdev, adev, h->st, &je, split_a, split_b, hi)) {
     CUDA_TRY(h, je);
     h->stats.jit_launches++;
+  } else if (L.flags & SV_FLAG_XRANK) {
+    return fail(h, SV_ECUDA, "internal: fused exchange section without its generated kernel");
   } else {
     CUDA_TRY(h, launch_section(h->dbl, h->sv, pdev, L.int_count, cdev, L.coef_count, adev, L.T, L.n_out, L.n_phases,
                                L.flags, L.n_sets, h->st, split_a, split_b));
@@ -749,10 +762,27 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
   h->prog.clear();
   const int T_default = lay.tile_default;
   std::vector<size_t> launch_end(steps.size(), 0);  // one past the last launch of each step
+  // Fused exchange + section (one kernel over peer memory, §8(e)): a one-bit exchange directly
+  // followed by a section whose tile can also hold the two exchanged bits becomes that section's
+  // load (needs the peer mapping and generated kernels; SV_FUSE=0 disables)
+  static const bool fuse_env = [] {
+    const char* e = std::getenv("SV_FUSE");
+    return !(e && e[0] == '0');
+  }();
+  const bool can_fuse = fuse_env && h->world > 1 && h->p2p && !(flags & SV_EXCHANGE_NCCL) && jit_set_mode(-1) == 1 &&
+                        h->nL >= SV_R_BITS;
+  std::vector<char> fused(steps.size(), 0);
   for (size_t i = 0; i < steps.size(); i++) {
     const Step& st = steps[i];
     if (st.type == Step::SECTION && h->nL >= SV_R_BITS) {
-      Status cs = compile_section_split(st.gates, h->nL, h->rank, h->g, T_default, lay.low_bits, st.swaps, h->prog);
+      Status cs = Status::err(kNoFuse, "");
+      if (can_fuse && i > 0 && steps[i - 1].type == Step::EXCHANGE && steps[i - 1].ex.size() == 1) {
+        cs = compile_section_split(st.gates, h->nL, h->rank, h->g, T_default, lay.low_bits, st.swaps, h->prog,
+                                   &steps[i - 1].ex[0]);
+        if (cs.good()) fused[i - 1] = 1;
+      }
+      if (cs.code == kNoFuse)
+        cs = compile_section_split(st.gates, h->nL, h->rank, h->g, T_default, lay.low_bits, st.swaps, h->prog);
       if (!cs.good()) return fail(h, cs);
       if (h->prog.launches.back().T > 13)
         return fail(h, SV_ECAPACITY, "a section needs a tile larger than shared memory (lower chunk_bits)");
@@ -767,6 +797,12 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
     const Step& st = steps[i];
     switch (st.type) {
       case Step::EXCHANGE: {
+        if (fused[i]) {  // carried out by the next section's load (kernel sv_sec with SV_FLAG_XRANK)
+          h->stats.bytes_sent += (uint64_t)(1ull << (h->nL - 1)) * h->amp;
+          h->stats.exchanges += 1;
+          h->stats.exchange_batches++;
+          break;
+        }
         if (h->p2p && !(flags & SV_EXCHANGE_NCCL) && i + 1 < steps.size() && steps[i + 1].type == Step::SECTION &&
             h->nL >= SV_R_BITS && si < launch_end[i + 1]) {
           int done = 0;
@@ -791,10 +827,15 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
         }
         for (; si < launch_end[i]; si++) {
           const Launch& L = h->prog.launches[si];
+          const bool x = L.flags & SV_FLAG_XRANK;
+          if (x)  // the partner is done with every earlier kernel touching its shard
+            if (int rc = barrier(h)) return rc;
           cudaEvent_t t = tstart(h);
           if (int rc = launch_one(h, L)) return rc;
           const double amps = (double)(1ull << h->nL);
           tend(h, t, 0, 2.0 * amps * (double)h->amp, L.flops_per_amp * amps);
+          if (x)  // both GPUs' halves written before anything reads them
+            if (int rc = barrier(h)) return rc;
           h->stats.sections++;
         }
         break;
@@ -1200,12 +1241,20 @@ extern "C" int sv_compile_circuit(const sv_gate* gates, size_t n_gates, int n, i
       for (const auto& sw : st.swaps) put({3, sw.first, sw.second});
     } else {
       const size_t first = prog.launches.size();
-      Status cs = compile_section_split(st.gates, nL, rank, world_log2, lay.tile_default, lay.low_bits, st.swaps, prog);
+      Status cs = Status::err(kNoFuse, "");
+      if ((flags & SV_FUSE_EXCHANGE) && world_log2 > 0 && i > 0 && steps[i - 1].type == Step::EXCHANGE &&
+          steps[i - 1].ex.size() == 1) {
+        cs = compile_section_split(st.gates, nL, rank, world_log2, lay.tile_default, lay.low_bits, st.swaps, prog,
+                                   &steps[i - 1].ex[0]);
+        if (cs.good()) rec[rec.size() - 12 + 4] = 1;  // the exchange record: fused into this section
+      }
+      if (cs.code == kNoFuse)
+        cs = compile_section_split(st.gates, nL, rank, world_log2, lay.tile_default, lay.low_bits, st.swaps, prog);
       if (!cs.good()) return fail(nullptr, cs);
       for (size_t k = first; k < prog.launches.size(); k++) {
         const Launch& L = prog.launches[k];
         put({1, (int64_t)L.int_off, (int64_t)L.int_count, (int64_t)L.coef_off, (int64_t)L.coef_count, L.T, L.n_out,
-             L.flags, (int64_t)L.aux_off, (int64_t)L.aux_count});
+             L.flags, (int64_t)L.aux_off, (int64_t)L.aux_count, L.xm, L.xb});
       }
     }
   }

@@ -99,7 +99,8 @@ bool pipelined(const Launch& L, bool dbl) {
     return e && e[0] == '1';
   }();
   const size_t amp = dbl ? 16 : 8;
-  return on && L.T >= 9 && L.T <= 12 && 3 * (amp << L.T) + kPipeSetsBytes * amp + 64 <= 227 * 1024;
+  return on && !(L.flags & SV_FLAG_XRANK) && L.T >= 9 && L.T <= 12 &&
+         3 * (amp << L.T) + kPipeSetsBytes * amp + 64 <= 227 * 1024;
 }
 
 // Persistent grid + L2 prefetch of each CTA's next tile for the plain generated kernel (SV_L2PF=1)
@@ -108,7 +109,7 @@ bool l2_prefetch(const Launch& L, bool dbl) {
     const char* e = std::getenv("SV_L2PF");
     return e && e[0] == '1';
   }();
-  return on && !pipelined(L, dbl) && L.T >= SV_R_BITS;
+  return on && !pipelined(L, dbl) && !(L.flags & SV_FLAG_XRANK) && L.T >= SV_R_BITS;
 }
 
 size_t smem_bytes(const Launch& L, bool dbl) {
@@ -141,17 +142,35 @@ struct Gen {
     o << "};\n";
   }
   // HBM element offset of register 0 (b) and of every register k (RO[k]) under map m
+  int nl = 64;  // memory bits >= nl are rank bits (fused exchange, SV_FLAG_XRANK)
+  bool xrank = false;
   void hbm(const SvMap& m) {
     long long ro[16];
+    int gk[16], tmb[16];
+    uint32_t trank = 0;  // thread bits on the rank bit
     for (int k = 0; k < 16; k++) {
       ro[k] = 0;
+      gk[k] = 0;
       for (int s = 0; s < SV_R_BITS; s++)
-        if ((k >> s) & 1) ro[k] |= 1ll << m.rmb[s];
+        if ((k >> s) & 1) {
+          if (m.rmb[s] >= nl)
+            gk[k] = 1;
+          else
+            ro[k] |= 1ll << m.rmb[s];
+        }
     }
-    arr("int", "TMB", m.tmb, ntl);
+    for (int j = 0; j < ntl; j++) {
+      tmb[j] = m.tmb[j] >= nl ? 63 : m.tmb[j];  // 63: contributes nothing below (masked)
+      if (m.tmb[j] >= nl) trank |= 1u << j;
+    }
+    arr("int", "TMB", tmb, ntl);
     arr("long long", "RO", ro, 16);
     o << "    uint64_t b = tile_off;\n"
-      << "#pragma unroll\n    for (int j = 0; j < " << ntl << "; j++) b |= (uint64_t)((tid >> j) & 1) << TMB[j];\n";
+      << "#pragma unroll\n    for (int j = 0; j < " << ntl << "; j++) if (TMB[j] != 63) b |= (uint64_t)((tid >> j) & 1) << TMB[j];\n";
+    if (xrank) {  // which GPU's shard each register lives on (the rank bit's value)
+      arr("int", "GK", gk, 16);
+      o << "    const int gs = (tid & " << trank << ") ? 1 : 0;\n";
+    }
   }
   // swizzled smem offset of register 0 (x) and XOR offsets W[k] for thread-bit words tw, slot words rw
   void smem(const int* tw, const int* rw) {
@@ -181,8 +200,18 @@ struct Gen {
   }
   void lds() { o << "#pragma unroll\n    for (int k = 0; k < 16; k++) v[k] = sm[x ^ W[k]];\n"; }
   void sts() { o << "#pragma unroll\n    for (int k = 0; k < 16; k++) sm[x ^ W[k]] = v[k];\n"; }
-  void ldg() { o << "#pragma unroll\n    for (int k = 0; k < 16; k++) v[k] = psi[b + RO[k]];\n"; }
-  void stg() { o << "#pragma unroll\n    for (int k = 0; k < 16; k++) psi[b + RO[k]] = v[k];\n"; }
+  void ldg() {
+    if (xrank)
+      o << "#pragma unroll\n    for (int k = 0; k < 16; k++) v[k] = ((gs ^ GK[k]) ? psi_hi : psi)[b + RO[k]];\n";
+    else
+      o << "#pragma unroll\n    for (int k = 0; k < 16; k++) v[k] = psi[b + RO[k]];\n";
+  }
+  void stg() {
+    if (xrank)
+      o << "#pragma unroll\n    for (int k = 0; k < 16; k++) ((gs ^ GK[k]) ? psi_hi : psi)[b + RO[k]] = v[k];\n";
+    else
+      o << "#pragma unroll\n    for (int k = 0; k < 16; k++) psi[b + RO[k]] = v[k];\n";
+  }
 };
 
 std::string gen_source_pipelined(const int* p, const Launch& L, bool dbl);
@@ -191,6 +220,8 @@ std::string gen_source(const int* p, const Launch& L, bool dbl) {
   if (pipelined(L, dbl)) return gen_source_pipelined(p, L, dbl);
   const SvSecHeader* H = reinterpret_cast<const SvSecHeader*>(p);
   Gen g;
+  g.xrank = (H->flags & SV_FLAG_XRANK) != 0;
+  g.nl = g.xrank ? H->nl : 64;
   g.T = H->T;
   g.ntl = H->T - SV_R_BITS;
   const int nt = 1 << g.ntl;
@@ -200,7 +231,7 @@ std::string gen_source(const int* p, const Launch& L, bool dbl) {
   auto& o = g.o;
   o << "#include \"section_dev.cuh\"\nusing namespace sv;\ntypedef " << (dbl ? "double2" : "float2") << " V;\n";
   o << "extern \"C\" __global__ void __launch_bounds__(" << nt << ", " << (H->T <= 12 ? std::min(16, 512 / nt) : 1)
-    << ") sv_sec(V* __restrict__ psi, const V* __restrict__ aux, int split_a, int split_b, "
+    << ") sv_sec(V* __restrict__ psi, V* __restrict__ psi_hi, const V* __restrict__ aux, int split_a, int split_b, "
     << coef_param_decl_impl(L, dbl) << ") {\n";
   o << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n"
     << "  V* sm = reinterpret_cast<V*>(smem_raw);\n"
@@ -321,7 +352,7 @@ std::string gen_source_pipelined(const int* p, const Launch& L, bool dbl) {
   o << "#include \"section_dev.cuh\"\nusing namespace sv;\ntypedef " << (dbl ? "double2" : "float2") << " V;\n";
   o << "constexpr int NTG = " << nt << ", TILE = " << (1 << H->T) << ";\n";
   o << "extern \"C\" __global__ void __launch_bounds__(" << 2 * nt << ", " << std::max(1, 512 / (2 * nt))
-    << ") sv_sec(V* __restrict__ psi, const V* __restrict__ aux, int split_a, int split_b, "
+    << ") sv_sec(V* __restrict__ psi, V* __restrict__ psi_hi, const V* __restrict__ aux, int split_a, int split_b, "
     << coef_param_decl_impl(L, dbl) << ") {\n";
   o << "  extern __shared__ __align__(128) unsigned char smem_raw[];\n"
     << "  V* const bufs = reinterpret_cast<V*>(smem_raw);\n"
@@ -653,7 +684,7 @@ void jit_prepare(const Program& prog, bool dbl) {
 
 bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const double* coef_host, const Launch& L,
                         const int* prog_dev, const void* coef_dev, const void* aux_dev, cudaStream_t st,
-                        cudaError_t* err, int split_a, int split_b) {
+                        cudaError_t* err, int split_a, int split_b, void* sv_hi) {
   *err = cudaSuccess;
   const Mode m = mode();
   if (m == kOff || L.T < SV_R_BITS) return false;
@@ -697,6 +728,7 @@ bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const double* 
     if (*err != cudaSuccess) return true;
   }
   void* a0 = sv;
+  void* a0h = sv_hi ? sv_hi : sv;
   void* a1 = const_cast<void*>(aux_dev);
   int a2 = split_a, a3 = split_b;
   // the coefficient parameter: the section's coefficients (fp64 on the host) in the state's precision
@@ -714,7 +746,7 @@ bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const double* 
     }
     a4 = pbuf.data();
   }
-  void* args[] = {&a0, &a1, &a2, &a3, a4};
+  void* args[] = {&a0, &a0h, &a1, &a2, &a3, a4};
   const unsigned threads = (pipelined(L, dbl) ? 2u : 1u) << (L.T - SV_R_BITS);
   unsigned grid = (unsigned)(1ull << (L.n_out - (split_a ? 1 : 0) - (split_b ? 1 : 0)));
   if (pipelined(L, dbl) || l2_prefetch(L, dbl)) {  // persistent: one wave of resident CTAs

@@ -34,7 +34,9 @@ struct JitCounters {
 // coef_host: the launch's coefficients (fp64 complex) on the host, passed as a kernel parameter.
 bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const double* coef_host, const Launch& L,
                         const int* prog_dev, const void* coef_dev, const void* aux_dev, cudaStream_t st,
-                        cudaError_t* err, int split_a = 0, int split_b = 0);
+                        cudaError_t* err, int split_a = 0, int split_b = 0, void* sv_hi = nullptr);
+// sv_hi: for a fused exchange (SV_FLAG_XRANK) sv / sv_hi are the shards whose exchanged rank bit
+// is 0 / 1 (one of them this GPU's, the other its partner's, mapped over NVLink).
 
 // Make sure every launch of the program has its kernel: mode sync compiles the missing ones in
 // parallel now, mode async queues them.

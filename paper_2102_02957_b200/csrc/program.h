@@ -55,6 +55,8 @@
 
 #define SV_FLAG_FIRST_DIRECT 1        // first phase loads straight from HBM
 #define SV_FLAG_LAST_DIRECT 2         // last phase stores straight to HBM
+#define SV_FLAG_XRANK 4               // fused exchange: one tile position is a rank bit (memory bit
+                                      // >= nl): its loads / stores address the partner GPU's shard
 
 // A thread/register <-> tile mapping used at a tile boundary: smem offsets (swizzled) and the
 // HBM memory bit of every thread bit j and register slot s.
@@ -83,7 +85,7 @@ struct SvSecHeader {
   SvMap dout;               // direct last phase: last-phase mapping, store memory bits
   int n_sets;               // DIAGSETs whose per-CTA factors the CTA prologue computes (<= SV_MAX_SETS)
   int set_desc[SV_MAX_SETS];  // their descriptor offsets; factors go to smem after the tile
-  int pad_sets[1];
+  int nl;                   // local memory bits (memory bits >= nl in the maps are rank bits)
 };
 
 #ifndef __CUDACC_RTC__
