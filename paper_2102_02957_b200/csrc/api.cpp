@@ -485,9 +485,11 @@ int exchange_pipelined(sv_state* h, const std::vector<ExPair>& pairs_in, const L
 int drain_timing(sv_state* h) {
   if (h->trecs.empty()) return SV_OK;
   CUDA_TRY(h, cudaEventSynchronize(h->trecs.back().b));
+  static const bool dbg = std::getenv("SV_DEBUG_TIMING") != nullptr;  // per-launch times (analysis aid)
   for (auto& r : h->trecs) {
     float ms = 0.f;
     CUDA_TRY(h, cudaEventElapsedTime(&ms, r.a, r.b));
+    if (dbg) std::fprintf(stderr, "[sv] rank %d kind %d %.3f ms\n", h->rank, r.kind, ms);
     if (r.kind == 0) {
       h->stats.timed_sections++;
       h->stats.section_ms += ms;
@@ -764,10 +766,12 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
   std::vector<size_t> launch_end(steps.size(), 0);  // one past the last launch of each step
   // Fused exchange + section (one kernel over peer memory, §8(e)): a one-bit exchange directly
   // followed by a section whose tile can also hold the two exchanged bits becomes that section's
-  // load (needs the peer mapping and generated kernels; SV_FUSE=0 disables)
+  // load (needs the peer mapping and generated kernels).  Opt-in (SV_FUSE=1): correct, but the
+  // tile's scattered peer accesses ran at ~140 GB/s over NVLink (QFT34 on 2 GPUs: the fused
+  // section 489 ms vs 112 ms exchange + ~104 ms section pipelined), so the swap kernel wins.
   static const bool fuse_env = [] {
     const char* e = std::getenv("SV_FUSE");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   const bool can_fuse = fuse_env && h->world > 1 && h->p2p && !(flags & SV_EXCHANGE_NCCL) && jit_set_mode(-1) == 1 &&
                         h->nL >= SV_R_BITS;
