@@ -61,6 +61,10 @@ def workload(name: str, world: int):
         n = 33 + g
         return dict(name="qft_weak", desc=f"QFT({n}) fp64, 2^33 amplitudes per GPU (weak)", n=n, gates=C.qft(n),
                     basis=C.basis_index(1, n), scaling="weak", chunk_bits=8)
+    if name == "qft_weak_fp32":  # BASELINE configs[4]'s fp32 variant: 2^34 fp32 amplitudes per GPU (37q at 8)
+        n = 34 + g
+        return dict(name="qft_weak_fp32", desc=f"QFT({n}) fp32, 2^34 amplitudes per GPU (weak)", n=n, gates=C.qft(n),
+                    basis=C.basis_index(1, n), scaling="weak", chunk_bits=8, precision="fp32")
     if name == "qv_weak":
         n = 30 + g
         return dict(name="qv_weak", desc=f"QV({n}, 10, 1) fp64, 2^30 amplitudes per GPU (weak)", n=n,
@@ -207,6 +211,8 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     wl = workload(args.workload, world)
+    if wl.get("precision"):
+        args.precision = wl["precision"]
     wl["desc"] = wl["desc"].replace("fp64", args.precision)
     n, gates = wl["n"], wl["gates"]
     c = args.chunk_bits if args.chunk_bits else wl["chunk_bits"]
