@@ -8,6 +8,8 @@
 #include "jit.h"
 
 #include <dlfcn.h>
+#include <sys/stat.h>
+#include <unistd.h>
 #include <nvrtc.h>
 
 #include <algorithm>
@@ -19,6 +21,7 @@
 #include <fstream>
 #include <cstring>
 #include <deque>
+#include <iterator>
 #include <memory>
 #include <mutex>
 #include <sstream>
@@ -513,11 +516,82 @@ bool compile_cubin(const std::string& src, bool dbl, std::vector<char>& cubin, s
   return true;
 }
 
+// On-disk cubin cache (SV_JIT_CACHE=<dir>, default $HOME/.cache/sv_jit; "0" disables): a kernel
+// compiled once is reused by later processes.  Key: FNV-1a of the source, the embedded headers
+// and the NVRTC options; file: [u32 len][name_prog][u32 len][name_coef][cubin].
+std::string cache_dir() {
+  static const std::string d = [] {
+    const char* e = std::getenv("SV_JIT_CACHE");
+    if (e) return std::string(e[0] == '0' && e[1] == '\0' ? "" : e);
+    const char* home = std::getenv("HOME");
+    return home ? std::string(home) + "/.cache/sv_jit" : std::string();
+  }();
+  return d;
+}
+std::string cache_path(const std::string& src, bool dbl) {
+  const std::string dir = cache_dir();
+  if (dir.empty()) return {};
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](const char* p, size_t n) {
+    for (size_t i = 0; i < n; i++) h = (h ^ (unsigned char)p[i]) * 1099511628211ull;
+  };
+  mix(src.data(), src.size());
+  for (int i = 0; i < kJitHeaderCount; i++) mix(kJitHeaderTexts[i], std::strlen(kJitHeaderTexts[i]));
+  const char* tag = dbl ? "sm_100a/fp64/v1" : "sm_100a/fp32/v1";
+  mix(tag, std::strlen(tag));
+  char name[40];
+  std::snprintf(name, sizeof(name), "/sv_%016llx.bin", (unsigned long long)h);
+  return dir + name;
+}
+bool cache_load(const std::string& path, std::vector<char>& cubin, std::string& np, std::string& nc) {
+  if (path.empty()) return false;
+  std::ifstream f(path, std::ios::binary);
+  if (!f) return false;
+  std::vector<char> all((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+  size_t at = 0;
+  auto str = [&](std::string& out) {
+    uint32_t n = 0;
+    if (at + 4 > all.size()) return false;
+    std::memcpy(&n, all.data() + at, 4);
+    at += 4;
+    if (at + n > all.size()) return false;
+    out.assign(all.data() + at, n);
+    at += n;
+    return true;
+  };
+  if (!str(np) || !str(nc) || at >= all.size()) return false;
+  cubin.assign(all.begin() + (long)at, all.end());
+  return true;
+}
+void cache_store(const std::string& path, const std::vector<char>& cubin, const std::string& np,
+                 const std::string& nc) {
+  if (path.empty()) return;
+  const std::string dir = cache_dir();
+  std::string cmd_dir = dir;  // create the directory (one level below an existing parent)
+  ::mkdir(cmd_dir.c_str(), 0755);
+  const std::string tmp = path + ".tmp" + std::to_string((long long)::getpid());
+  {
+    std::ofstream f(tmp, std::ios::binary);
+    if (!f) return;
+    const uint32_t a = (uint32_t)np.size(), b = (uint32_t)nc.size();
+    f.write(reinterpret_cast<const char*>(&a), 4);
+    f.write(np.data(), a);
+    f.write(reinterpret_cast<const char*>(&b), 4);
+    f.write(nc.data(), b);
+    f.write(cubin.data(), (std::streamsize)cubin.size());
+    if (!f) return;
+  }
+  std::rename(tmp.c_str(), path.c_str());
+}
+
 void build_entry(Entry& e, const std::string& src, int dev, bool dbl) {
   const auto t0 = std::chrono::steady_clock::now();
   std::vector<char> cubin;
   std::string name_prog, name_coef;
-  if (!compile_cubin(src, dbl, cubin, name_prog, name_coef, e.err)) {
+  const std::string cpath = cache_path(src, dbl);
+  const bool hit = cache_load(cpath, cubin, name_prog, name_coef);
+  if (!hit && compile_cubin(src, dbl, cubin, name_prog, name_coef, e.err)) cache_store(cpath, cubin, name_prog, name_coef);
+  if (!hit && cubin.empty()) {
     static std::once_flag once;
     std::call_once(once, [&] { std::fprintf(stderr, "[sv] JIT disabled for this kernel: %s\n", e.err.c_str()); });
     e.state = 2;
@@ -525,6 +599,15 @@ void build_entry(Entry& e, const std::string& src, int dev, bool dbl) {
   }
   cudaSetDevice(dev);
   cudaError_t ce = cudaLibraryLoadData(&e.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+  if (ce != cudaSuccess && hit) {  // a damaged cache entry: drop it and compile
+    cudaGetLastError();
+    std::remove(cpath.c_str());
+    cubin.clear();
+    if (compile_cubin(src, dbl, cubin, name_prog, name_coef, e.err)) {
+      cache_store(cpath, cubin, name_prog, name_coef);
+      ce = cudaLibraryLoadData(&e.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+    }
+  }
   if (ce == cudaSuccess) ce = cudaLibraryGetKernel(&e.kern, e.lib, "sv_sec");
   if (ce != cudaSuccess) {
     e.err = std::string("module load failed: ") + cudaGetErrorString(ce);

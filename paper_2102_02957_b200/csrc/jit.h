@@ -10,6 +10,8 @@
 //   "sync"  (default) compile on first use, then launch the generated kernel;
 //   "async" launch the interpreter while a background thread compiles;
 //   "0"     interpreter only.
+// Compiled cubins are also kept on disk (SV_JIT_CACHE=<dir>, default $HOME/.cache/sv_jit, "0"
+// disables), keyed by the source and the embedded headers, so later processes skip NVRTC.
 #pragma once
 #include <cuda_runtime.h>
 
