@@ -96,6 +96,7 @@ struct sv_state {
   std::string err;
   bool basis_pending = false;  // state is exactly |basis_index> (set by sv_reset)
   uint64_t basis_index = 0;
+  bool virt = false;  // ... and not written yet: the next circuit's first section generates it
 
   // optional per-launch device timing (sv_set_timing)
   struct TRec {
@@ -348,9 +349,11 @@ void tend(sv_state* h, cudaEvent_t a, int kind, double bytes, double flops) {
   h->trecs.push_back({a, b, kind, bytes, flops});
 }
 
+int materialize_at(sv_state* h, int64_t vidx);
+
 // One section launch (generated kernel, else the interpreter), optionally restricted to the tiles
 // whose out bits match split_a / split_b (kernels.cuh).
-int launch_one(sv_state* h, const Launch& L, int split_a = 0, int split_b = 0) {
+int launch_one(sv_state* h, const Launch& L, int split_a = 0, int split_b = 0, int64_t vidx = -1) {
   const int* pdev = (const int*)h->d_prog.p + L.int_off;
   const char* cdev = (const char*)h->d_coef.p + L.coef_off * h->amp;
   const char* adev = (const char*)h->d_aux.p + L.aux_off * h->amp;
@@ -367,9 +370,14 @@ int launch_one(sv_state* h, const Launch& L, int split_a = 0, int split_b = 0) {
     split_b = 0;
   }
   if (jit_launch_section(h->dbl, lo, h->prog.ints.data() + L.int_off, h->prog.coefs.data() + 2 * L.coef_off, L,
-                         pdev, cdev, adev, h->st, &je, split_a, split_b, hi)) {
+                         pdev, cdev, adev, h->st, &je, split_a, split_b, hi, vidx)) {
     CUDA_TRY(h, je);
     h->stats.jit_launches++;
+    h->stats.kernel_launches++;
+    return SV_OK;
+  } else if (vidx != -1) {  // no generated kernel after all: write the basis state, then run normally
+    if (int rc = materialize_at(h, vidx)) return rc;
+    return launch_one(h, L, split_a, split_b, -1);
   } else if (L.flags & SV_FLAG_XRANK) {
     return fail(h, SV_ECUDA, "internal: fused exchange section without its generated kernel");
   } else {
@@ -522,6 +530,36 @@ int check_handle(sv_state* h) {
   if (!h) return fail(nullptr, SV_EINVAL, "null handle");
   CUDA_TRY(h, cudaSetDevice(h->device));
   return SV_OK;
+}
+
+// Memory index of logical basis index k under the layout (pi, sigma).
+uint64_t basis_memory_index(const sv_state* h, uint64_t k, const std::vector<int>& sigma) {
+  uint64_t x = 0;
+  for (int q = 0; q < h->n; q++) x |= ((k >> q) & 1ull) << sigma[h->pi[q]];
+  return x;
+}
+
+// Write the pending basis state |basis_index> (sv_reset defers it) at its memory index under sigma.
+int materialize(sv_state* h, const std::vector<int>& sigma) {
+  if (!h->virt) return SV_OK;
+  const uint64_t x = basis_memory_index(h, h->basis_index, sigma);
+  const int64_t off = (int)(x >> h->nL) == h->rank ? (int64_t)(x & ((1ull << h->nL) - 1)) : -1;
+  CUDA_TRY(h, launch_set_basis(h->dbl, h->sv, h->nL, off, h->st));
+  h->stats.kernel_launches += off >= 0 ? 1 : 0;
+  h->virt = false;
+  return SV_OK;
+}
+
+int materialize_at(sv_state* h, int64_t vidx) {  // shard offset (or -2: the amplitude is elsewhere)
+  CUDA_TRY(h, launch_set_basis(h->dbl, h->sv, h->nL, vidx >= 0 ? vidx : -1, h->st));
+  h->stats.kernel_launches += vidx >= 0 ? 1 : 0;
+  h->virt = false;
+  return SV_OK;
+}
+
+int ready(sv_state* h) {  // a call that reads the state: valid handle, state written
+  if (int rc = check_handle(h)) return rc;
+  return materialize(h, h->sigma);
 }
 
 // Sum `count` values of dtype over all ranks in place (device buffer).
@@ -716,12 +754,11 @@ int sv_reset(sv_handle h, uint64_t k) {
   if (h->n < 64 && (k >> h->n)) return fail(h, SV_EINVAL, "basis index out of range");
   std::iota(h->pi.begin(), h->pi.end(), 0);
   std::iota(h->sigma.begin(), h->sigma.end(), 0);
-  const int owner = (int)(k >> h->nL);
-  const int64_t off = owner == h->rank ? (int64_t)(k & ((1ull << h->nL) - 1)) : -1;
-  CUDA_TRY(h, launch_set_basis(h->dbl, h->sv, h->nL, off, h->st));
-  h->stats.kernel_launches += off >= 0 ? 1 : 0;
+  // Deferred: the next circuit's first section generates |k> in its load (no memset pass, no read
+  // pass), or the first call that reads the state writes it (materialize).
   h->basis_pending = true;  // the next circuit may choose its memory layout freely (NEXT-2)
   h->basis_index = k;
+  h->virt = true;
   return SV_OK;
 }
 
@@ -747,14 +784,11 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
   std::vector<int> sigma0;
   Status s = make_plan(gates, n_gates, h->n, h->c, h->g, pi, sigma, flags, steps, ctr, lay, &sigma0);
   if (!s.good()) return fail(h, s);
-  if (lay.free_initial && sigma0 != h->sigma) {
+  if (!lay.free_initial) sigma0 = h->sigma;
+  if (!h->virt && lay.free_initial && sigma0 != h->sigma) {
     // relocate the single nonzero amplitude of |k> to its place under the chosen layout
-    uint64_t from = 0, to = 0;
-    for (int q = 0; q < h->n; q++) {
-      const uint64_t b = (h->basis_index >> q) & 1;
-      from |= b << h->sigma[h->pi[q]];
-      to |= b << sigma0[h->pi[q]];
-    }
+    const uint64_t from = basis_memory_index(h, h->basis_index, h->sigma);
+    const uint64_t to = basis_memory_index(h, h->basis_index, sigma0);
     const uint64_t lm = (1ull << h->nL) - 1;
     if ((int)(from >> h->nL) == h->rank) CUDA_TRY(h, launch_set_amp(h->dbl, h->sv, (int64_t)(from & lm), 0.0, h->st));
     if ((int)(to >> h->nL) == h->rank) CUDA_TRY(h, launch_set_amp(h->dbl, h->sv, (int64_t)(to & lm), 1.0, h->st));
@@ -794,7 +828,20 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
     launch_end[i] = h->prog.launches.size();
   }
   h->stats.pass_ms = now_ms() - t0;
-  jit_prepare(h->prog, h->dbl);  // run-time specialised kernels (jit.h): compile what is missing
+  // A deferred basis state (sv_reset) is generated by the first section's load when the plan
+  // starts with a section run by a generated kernel; else it is written now.
+  int64_t vidx = -1;  // -1: read the state; >= 0 the shard offset of the one amplitude; -2 none here
+  if (h->virt) {
+    if (!steps.empty() && steps[0].type == Step::SECTION && !h->prog.launches.empty() &&
+        jit_virtual_input_ok(h->prog.launches[0], h->dbl)) {
+      const uint64_t x = basis_memory_index(h, h->basis_index, sigma0);
+      vidx = (int)(x >> h->nL) == h->rank ? (int64_t)(x & ((1ull << h->nL) - 1)) : -2;
+      h->virt = false;
+    } else if (int rc = materialize(h, sigma0)) {
+      return rc;
+    }
+  }
+  jit_prepare(h->prog, h->dbl, vidx != -1);  // run-time specialised kernels (jit.h): compile what is missing
   if (int rc = upload_program(h)) return rc;
   size_t si = 0;
   for (size_t i = 0; i < steps.size(); i++) {
@@ -835,7 +882,7 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
           if (x)  // the partner is done with every earlier kernel touching its shard
             if (int rc = barrier(h)) return rc;
           cudaEvent_t t = tstart(h);
-          if (int rc = launch_one(h, L)) return rc;
+          if (int rc = launch_one(h, L, 0, 0, si == 0 ? vidx : -1)) return rc;
           const double amps = (double)(1ull << h->nL);
           tend(h, t, 0, 2.0 * amps * (double)h->amp, L.flops_per_amp * amps);
           if (x)  // both GPUs' halves written before anything reads them
@@ -900,7 +947,7 @@ int sv_set_timing(sv_handle h, int enable) {
 }
 
 int sv_norm(sv_handle h, double* out) {
-  if (int rc = check_handle(h)) return rc;
+  if (int rc = ready(h)) return rc;
   if (!out) return fail(h, SV_EINVAL, "null output");
   if (int rc = ensure_dev(h, h->d_scratch, norm_scratch_doubles() * sizeof(double))) return rc;
   CUDA_TRY(h, launch_norm(h->dbl, h->sv, h->nL, (double*)h->d_scratch.p, (double*)h->d_small.p + 8, h->st));
@@ -912,7 +959,7 @@ int sv_norm(sv_handle h, double* out) {
 }
 
 int sv_probabilities(sv_handle h, const int32_t* qubits, int nq, double* host_out) {
-  if (int rc = check_handle(h)) return rc;
+  if (int rc = ready(h)) return rc;
   if (nq < 0 || nq > 24 || (nq && (!qubits || !host_out))) return fail(h, SV_EINVAL, "bad qubit list (nq <= 24)");
   uint64_t seen = 0;
   std::vector<int> loc_bits, loc_pos;
@@ -957,7 +1004,7 @@ int sv_probabilities(sv_handle h, const int32_t* qubits, int nq, double* host_ou
 }
 
 int sv_get_amplitudes(sv_handle h, const uint64_t* idx, size_t cnt, void* host_out) {
-  if (int rc = check_handle(h)) return rc;
+  if (int rc = ready(h)) return rc;
   if (cnt == 0) return SV_OK;
   if (!idx || !host_out) return fail(h, SV_EINVAL, "null argument");
   const BitPerm mu = mu_of(h);
@@ -987,7 +1034,7 @@ int sv_get_amplitudes(sv_handle h, const uint64_t* idx, size_t cnt, void* host_o
 }
 
 int sv_get_state(sv_handle h, void* host_out) {
-  if (int rc = check_handle(h)) return rc;
+  if (int rc = ready(h)) return rc;
   if (h->rank == 0 && !host_out) return fail(h, SV_EINVAL, "null output");
   const BitPerm inv = mu_inv_of(h);
   const size_t piece = std::min<size_t>(size_t(1) << h->nL, (size_t(256) << 20) / h->amp);
@@ -1029,7 +1076,7 @@ static uint64_t splitmix64(uint64_t x) {
 }
 
 int sv_sample(sv_handle h, size_t shots, uint64_t seed, uint64_t* host_out) {
-  if (int rc = check_handle(h)) return rc;
+  if (int rc = ready(h)) return rc;
   if (shots == 0) return SV_OK;
   if (!host_out) return fail(h, SV_EINVAL, "null output");
   const int B = std::min(12, h->nL);

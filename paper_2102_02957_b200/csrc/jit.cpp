@@ -147,6 +147,7 @@ struct Gen {
   // HBM element offset of register 0 (b) and of every register k (RO[k]) under map m
   int nl = 64;  // memory bits >= nl are rank bits (fused exchange, SV_FLAG_XRANK)
   bool xrank = false;
+  bool virt = false;  // the tile's input is generated: 1 at shard offset vidx, 0 elsewhere
   void hbm(const SvMap& m) {
     long long ro[16];
     int gk[16], tmb[16];
@@ -204,6 +205,10 @@ struct Gen {
   void lds() { o << "#pragma unroll\n    for (int k = 0; k < 16; k++) v[k] = sm[x ^ W[k]];\n"; }
   void sts() { o << "#pragma unroll\n    for (int k = 0; k < 16; k++) sm[x ^ W[k]] = v[k];\n"; }
   void ldg() {
+    if (virt) {
+      o << "#pragma unroll\n    for (int k = 0; k < 16; k++) { v[k].x = (long long)(b + RO[k]) == vidx ? 1 : 0; v[k].y = 0; }\n";
+      return;
+    }
     if (xrank)
       o << "#pragma unroll\n    for (int k = 0; k < 16; k++) v[k] = ((gs ^ GK[k]) ? psi_hi : psi)[b + RO[k]];\n";
     else
@@ -219,10 +224,11 @@ struct Gen {
 
 std::string gen_source_pipelined(const int* p, const Launch& L, bool dbl);
 
-std::string gen_source(const int* p, const Launch& L, bool dbl) {
+std::string gen_source(const int* p, const Launch& L, bool dbl, bool virt = false) {
   if (pipelined(L, dbl)) return gen_source_pipelined(p, L, dbl);
   const SvSecHeader* H = reinterpret_cast<const SvSecHeader*>(p);
   Gen g;
+  g.virt = virt;
   g.xrank = (H->flags & SV_FLAG_XRANK) != 0;
   g.nl = g.xrank ? H->nl : 64;
   g.T = H->T;
@@ -235,11 +241,12 @@ std::string gen_source(const int* p, const Launch& L, bool dbl) {
   o << "#include \"section_dev.cuh\"\nusing namespace sv;\ntypedef " << (dbl ? "double2" : "float2") << " V;\n";
   o << "extern \"C\" __global__ void __launch_bounds__(" << nt << ", " << (H->T <= 12 ? std::min(16, 512 / nt) : 1)
     << ") sv_sec(V* __restrict__ psi, V* __restrict__ psi_hi, const V* __restrict__ aux, int split_a, int split_b, "
+    << "long long vidx, "
     << coef_param_decl_impl(L, dbl) << ") {\n";
   o << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n"
     << "  V* sm = reinterpret_cast<V*>(smem_raw);\n"
     << "  V* ctaf = reinterpret_cast<V*>(smem_raw + (sizeof(V) << " << H->T << "));\n"
-    << "  (void)sm; (void)ctaf; (void)aux;\n"
+    << "  (void)sm; (void)ctaf; (void)aux; (void)vidx; (void)psi_hi;\n"
     << "  const int tid = threadIdx.x;\n";
   g.arr("int", "OB", H->out_bits, H->n_out);
   o << "  auto tile_of = [&](uint64_t t) {\n    uint64_t r = 0;\n#pragma unroll\n    for (int j = 0; j < "
@@ -356,6 +363,7 @@ std::string gen_source_pipelined(const int* p, const Launch& L, bool dbl) {
   o << "constexpr int NTG = " << nt << ", TILE = " << (1 << H->T) << ";\n";
   o << "extern \"C\" __global__ void __launch_bounds__(" << 2 * nt << ", " << std::max(1, 512 / (2 * nt))
     << ") sv_sec(V* __restrict__ psi, V* __restrict__ psi_hi, const V* __restrict__ aux, int split_a, int split_b, "
+    << "long long vidx, "
     << coef_param_decl_impl(L, dbl) << ") {\n";
   o << "  extern __shared__ __align__(128) unsigned char smem_raw[];\n"
     << "  V* const bufs = reinterpret_cast<V*>(smem_raw);\n"
@@ -363,7 +371,7 @@ std::string gen_source_pipelined(const int* p, const Launch& L, bool dbl) {
     << "  int* const done = reinterpret_cast<int*>(ctaf_all + " << kPipeSetsBytes << ");\n"
     << "  const int grp = threadIdx.x / NTG, tid = threadIdx.x % NTG, bar = 1 + grp;\n"
     << "  V* const ctaf = ctaf_all + grp * " << 5 * SV_MAX_SETS << ";\n"
-    << "  (void)ctaf; (void)aux;\n"
+    << "  (void)ctaf; (void)aux; (void)vidx; (void)psi_hi;\n"
     << "  constexpr unsigned long long NTILES = 1ull << " << H->n_out << ";\n";
   g.arr("int", "OB", H->out_bits, H->n_out);
   o << "  auto tile_of = [&](uint64_t t) {\n    uint64_t r = 0;\n#pragma unroll\n    for (int j = 0; j < "
@@ -714,9 +722,10 @@ Status jit_compile_only(const int* prog_host, const Launch& L, bool dbl, const c
 }
 
 namespace {
-std::string make_key(const int* prog_host, const Launch& L, bool dbl, int dev) {
+std::string make_key(const int* prog_host, const Launch& L, bool dbl, int dev, bool virt = false) {
   std::string key(reinterpret_cast<const char*>(prog_host), L.int_count * sizeof(int));
   key.push_back(dbl ? 'd' : 'f');
+  if (virt) key.push_back('v');
   key.append(reinterpret_cast<const char*>(&dev), sizeof(dev));
   return key;
 }
@@ -728,16 +737,23 @@ int jit_set_mode(int m) {
   return prev;
 }
 
-void jit_prepare(const Program& prog, bool dbl) {
+bool jit_virtual_input_ok(const Launch& L, bool dbl) {
+  return mode() == kSync && L.T >= SV_R_BITS && !pipelined(L, dbl) && !l2_prefetch(L, dbl) &&
+         !(L.flags & SV_FLAG_XRANK);
+}
+
+void jit_prepare(const Program& prog, bool dbl, bool virt_first) {
   const Mode m = mode();
   if (m == kOff) return;
   int dev = 0;
   cudaGetDevice(&dev);
   std::vector<std::pair<std::shared_ptr<Entry>, std::string>> todo;
-  for (const Launch& L : prog.launches) {
+  for (size_t li = 0; li < prog.launches.size(); li++) {
+    const Launch& L = prog.launches[li];
     if (L.T < SV_R_BITS) continue;
+    const bool virt = virt_first && li == 0;
     const int* p = prog.ints.data() + L.int_off;
-    std::string key = make_key(p, L, dbl, dev);
+    std::string key = make_key(p, L, dbl, dev, virt);
     std::shared_ptr<Entry> e;
     {
       std::lock_guard<std::mutex> lk(g_mu);
@@ -745,7 +761,7 @@ void jit_prepare(const Program& prog, bool dbl) {
       e = std::make_shared<Entry>();
       g_cache.emplace(std::move(key), e);
     }
-    todo.emplace_back(e, gen_source(p, L, dbl));
+    todo.emplace_back(e, gen_source(p, L, dbl, virt));
   }
   if (todo.empty()) return;
   if (m == kAsync) {
@@ -767,14 +783,16 @@ void jit_prepare(const Program& prog, bool dbl) {
 
 bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const double* coef_host, const Launch& L,
                         const int* prog_dev, const void* coef_dev, const void* aux_dev, cudaStream_t st,
-                        cudaError_t* err, int split_a, int split_b, void* sv_hi) {
+                        cudaError_t* err, int split_a, int split_b, void* sv_hi, int64_t vidx) {
   *err = cudaSuccess;
   const Mode m = mode();
   if (m == kOff || L.T < SV_R_BITS) return false;
   if ((split_a || split_b) && (pipelined(L, dbl) || l2_prefetch(L, dbl))) return false;  // persistent variants
   int dev = 0;
   cudaGetDevice(&dev);
-  std::string key = make_key(prog_host, L, dbl, dev);
+  const bool virt = vidx != -1;
+  if (virt && !jit_virtual_input_ok(L, dbl)) return false;
+  std::string key = make_key(prog_host, L, dbl, dev, virt);
   std::shared_ptr<Entry> e;
   bool fresh = false;
   {
@@ -790,9 +808,9 @@ bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const double* 
   }
   if (fresh) {
     if (m == kSync)
-      build_entry(*e, gen_source(prog_host, L, dbl), dev, dbl);
+      build_entry(*e, gen_source(prog_host, L, dbl, virt), dev, dbl);
     else
-      worker().push(Job{e, gen_source(prog_host, L, dbl), dev, dbl});
+      worker().push(Job{e, gen_source(prog_host, L, dbl, virt), dev, dbl});
   }
   if (e->state.load() != 1) {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -829,7 +847,8 @@ bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const double* 
     }
     a4 = pbuf.data();
   }
-  void* args[] = {&a0, &a0h, &a1, &a2, &a3, a4};
+  long long av = (long long)vidx;
+  void* args[] = {&a0, &a0h, &a1, &a2, &a3, &av, a4};
   const unsigned threads = (pipelined(L, dbl) ? 2u : 1u) << (L.T - SV_R_BITS);
   unsigned grid = (unsigned)(1ull << (L.n_out - (split_a ? 1 : 0) - (split_b ? 1 : 0)));
   if (pipelined(L, dbl) || l2_prefetch(L, dbl)) {  // persistent: one wave of resident CTAs

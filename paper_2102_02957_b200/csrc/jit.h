@@ -36,13 +36,19 @@ struct JitCounters {
 // coef_host: the launch's coefficients (fp64 complex) on the host, passed as a kernel parameter.
 bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const double* coef_host, const Launch& L,
                         const int* prog_dev, const void* coef_dev, const void* aux_dev, cudaStream_t st,
-                        cudaError_t* err, int split_a = 0, int split_b = 0, void* sv_hi = nullptr);
+                        cudaError_t* err, int split_a = 0, int split_b = 0, void* sv_hi = nullptr,
+                        int64_t vidx = -1);
+// vidx != -1: the launch does not read the state; its input is the basis state whose single
+// amplitude (1) sits at shard offset vidx (-2: on another GPU, all zeros here).
 // sv_hi: for a fused exchange (SV_FLAG_XRANK) sv / sv_hi are the shards whose exchanged rank bit
 // is 0 / 1 (one of them this GPU's, the other its partner's, mapped over NVLink).
 
 // Make sure every launch of the program has its kernel: mode sync compiles the missing ones in
 // parallel now, mode async queues them.
-void jit_prepare(const Program& prog, bool dbl);
+// virt_first: the first launch reads a deferred basis state (jit_launch_section vidx).
+void jit_prepare(const Program& prog, bool dbl, bool virt_first = false);
+// Whether the generated kernel of this launch can generate its input (a deferred basis state).
+bool jit_virtual_input_ok(const Launch& L, bool dbl);
 // Process-wide mode: 0 off, 1 sync, 2 async, -1 query; returns the previous mode.
 int jit_set_mode(int mode);
 // Block until background compiles have finished (mode async).
