@@ -352,7 +352,7 @@ def run_ours(args):
             "config": {"workload": wl["desc"], "n_qubits": n, "gates": int(len(gates)), "chunk_bits": c,
                        "precision": args.precision, "parallelism": f"state sharded over {world} GPU(s)",
                        "l2": "state >= 4 GiB per GPU >> 126 MB L2 (no flush needed)",
-                       "step": "sv_reset(basis) + sv_apply_circuit (pass+plan+upload+sections+exchanges) + sv_probabilities(10 qubits)",
+                       "step": "sv_reset(basis; generated inside the first section's load) + sv_apply_circuit (pass+plan+upload+sections+exchanges) + sv_probabilities(10 qubits)",
                        "path": "unblocked per-gate baseline (SV_UNBLOCKED)" if APPLY_FLAGS else "cache-blocked"},
             "amp_updates_per_s": value * (1 << n),
             "sections_per_step": st["sections"] / args.steps, "exchanges_per_step": st["exchanges"] / args.steps,
