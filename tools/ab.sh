@@ -1,5 +1,7 @@
-timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/gputests.log 2>&1; echo tests=$?
-for W in qft30 qv28; do
-timeout 600 python bench.py --workload $W --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/c_$W.json 2> gpurun_out/c_$W.err
+for C in 8 9 10; do
+  timeout 900 python bench.py --workload qv33 --chunk-bits $C --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/s_qv33_$C.json 2> gpurun_out/s_qv33_$C.err
+  timeout 600 python bench.py --workload qv28 --chunk-bits $C --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/s_qv28_$C.json 2> gpurun_out/s_qv28_$C.err
 done
-timeout 900 python bench.py --workload qv33 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/c_qv33.json 2> gpurun_out/c_qv33.err
+for C in 7 8 9; do
+  timeout 600 python bench.py --workload qft30 --chunk-bits $C --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/s_qft30_$C.json 2> gpurun_out/s_qft30_$C.err
+done
