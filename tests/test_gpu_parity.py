@@ -257,3 +257,34 @@ def test_qv33_full_size_mirror():
         s.apply(circ)
         assert abs(s.norm() - 1.0) <= 1e-12
         assert abs(s.probabilities([0, 16, 32]).sum() - 1.0) <= 1e-12
+
+
+def test_deferred_basis_state_readers():
+    # sv_reset defers writing |k> to the next circuit's first section; every reader, an empty
+    # circuit, the unblocked path and a plan not starting with a section must still see |k>
+    n, c = 12, 6
+    k = C.basis_index(9, n)
+    ref = np.zeros(1 << n, dtype=np.complex128)
+    ref[k] = 1
+    with sv.StateVector(n, c) as s:
+        s.reset(k)
+        check(s.state(), ref, "fp64")
+        s.reset(k)
+        assert abs(s.norm() - 1) <= 1e-15
+        s.reset(k)
+        assert abs(s.amplitudes(np.array([k], dtype=np.uint64))[0] - 1) <= 1e-15
+        s.reset(k)
+        s.apply(C.records([]))
+        check(s.state(), ref, "fp64")
+        s.reset(k)
+        p = s.probabilities([0, 1, 2])
+        assert abs(p[k & 7] - 1) <= 1e-15
+        circ = C.random_circuit(n, 40, 3)
+        for flags in (0, sv.SV_UNBLOCKED):
+            s.reset(k)
+            s.apply(circ, flags=flags)
+            check(s.state(), O.apply_circuit(circ, n, basis=k), "fp64")
+        s.reset(k)
+        s.reset(k ^ 5)  # two resets in a row: the last one wins
+        s.apply(circ)
+        check(s.state(), O.apply_circuit(circ, n, basis=k ^ 5), "fp64")
