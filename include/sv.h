@@ -163,6 +163,26 @@ int sv_stats_reset(sv_handle h);
 int sv_set_timing(sv_handle h, int enable);
 const char* sv_last_error(sv_handle h);
 
+/* ---- host-memory tier (NEXT-4) -------------------------
+ * The state lives in pinned host memory (2^n amplitudes) and the GPU caches 2^device_bits-
+ * amplitude chunks: every blocked section is one streaming pass of all chunks through the current
+ * device (H2D, section kernel, D2H overlapped); the top n - device_bits qubits index chunks like
+ * rank bits index GPUs, so an exchange with them is a bit permutation of the host array.  For
+ * states beyond HBM (PCIe-bound: expect ~2 x state bytes / PCIe bandwidth per section).
+ * Requires 4 <= device_bits < n <= 40, 1 <= chunk_bits <= device_bits.  State |0..0> after
+ * create.  Blocked path only (flags SV_UNBLOCKED / SV_EXCHANGE_NCCL: SV_EINVAL).  Outputs: the
+ * full state in logical order (2^n amplitudes of the precision), the norm, marginals as
+ * sv_probabilities.  Errors: sv_host_last_error. */
+typedef struct sv_host_state* sv_host_handle;
+int sv_host_create(int n_qubits, int chunk_bits, sv_precision prec, int device_bits, sv_host_handle* out);
+int sv_host_destroy(sv_host_handle h);
+int sv_host_reset(sv_host_handle h, uint64_t basis_index);
+int sv_host_apply_circuit(sv_host_handle h, const sv_gate* gates, size_t n_gates, uint32_t flags);
+int sv_host_get_state(sv_host_handle h, void* host_out);
+int sv_host_norm(sv_host_handle h, double* out);
+int sv_host_probabilities(sv_host_handle h, const int32_t* qubits, int nq, double* host_out);
+const char* sv_host_last_error(sv_host_handle h);
+
 /* ---- host-only (no GPU needed; used for parity of the pass and the plan) -------------- */
 /* The cache-blocking pass (Listing 3, DESIGN R2-R6) on logical gates.  *out receives the
  * token stream (SV_CHUNK_SWAP / SV_BEGIN / SV_END and gates on physical qubits, pad = input

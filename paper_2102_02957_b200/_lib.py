@@ -43,7 +43,9 @@ class Stats(ctypes.Structure):
 EXPORTS = ["sv_create", "sv_create_dist", "sv_destroy", "sv_nccl_unique_id", "sv_reset", "sv_apply_circuit",
            "sv_synchronize", "sv_get_amplitudes", "sv_get_state", "sv_norm", "sv_probabilities", "sv_sample",
            "sv_get_permutation", "sv_stats_get", "sv_stats_reset", "sv_set_timing", "sv_last_error", "sv_block_circuit", "sv_plan_circuit",
-           "sv_compile_circuit", "sv_jit_compile_circuit", "sv_jit_mode", "sv_jit_wait", "sv_free",
+           "sv_compile_circuit", "sv_jit_compile_circuit", "sv_jit_mode", "sv_jit_wait", "sv_host_create", "sv_host_destroy", "sv_host_reset",
+           "sv_host_apply_circuit", "sv_host_get_state", "sv_host_norm", "sv_host_probabilities",
+           "sv_host_last_error", "sv_free",
            "sv_abi_version"]
 
 _lib = None
@@ -86,6 +88,14 @@ def lib():
         "sv_jit_compile_circuit": ([vp, sz, i32, i32, i32, i32, i32, u32, ctypes.c_char_p, ip,
                                     ctypes.POINTER(ctypes.c_double)], i32),
         "sv_jit_mode": ([i32], i32),
+        "sv_host_create": ([i32, i32, i32, i32, ctypes.POINTER(vp)], i32),
+        "sv_host_destroy": ([vp], i32),
+        "sv_host_reset": ([vp, ctypes.c_uint64], i32),
+        "sv_host_apply_circuit": ([vp, vp, sz, u32], i32),
+        "sv_host_get_state": ([vp, vp], i32),
+        "sv_host_norm": ([vp, ctypes.POINTER(ctypes.c_double)], i32),
+        "sv_host_probabilities": ([vp, ip, i32, ctypes.POINTER(ctypes.c_double)], i32),
+        "sv_host_last_error": ([vp], ctypes.c_char_p),
         "sv_jit_wait": ([], i32),
         "sv_free": ([vp], None),
         "sv_abi_version": ([], i32),
@@ -312,3 +322,65 @@ class StateVector:
         s = Stats()
         self._check(lib().sv_stats_get(self._h, ctypes.byref(s)))
         return {k: getattr(s, k) for k, _ in Stats._fields_}
+
+
+class HostStateVector:
+    """Host-memory tier (NEXT-4, sv_host_*): the state in pinned host memory, the current GPU
+    caching 2^device_bits-amplitude chunks; every section streams all chunks through the GPU."""
+
+    def __init__(self, n_qubits: int, chunk_bits: int, device_bits: int, precision: str = "fp64"):
+        self.n = n_qubits
+        self.precision = precision
+        h = ctypes.c_void_p()
+        prec = {"fp64": SV_FP64, "fp32": SV_FP32}[precision]
+        rc = lib().sv_host_create(n_qubits, chunk_bits, prec, device_bits, ctypes.byref(h))
+        if rc != 0:
+            msg = lib().sv_host_last_error(None)
+            raise SvError(rc, msg.decode() if msg else "")
+        self._h = h
+
+    def _check(self, rc):
+        if rc != 0:
+            msg = lib().sv_host_last_error(self._h)
+            raise SvError(rc, msg.decode() if msg else "")
+
+    def reset(self, basis_index: int = 0):
+        self._check(lib().sv_host_reset(self._h, int(basis_index)))
+
+    def apply(self, gates, flags: int = 0):
+        g = as_gates(gates)
+        self._check(lib().sv_host_apply_circuit(self._h, g.ctypes.data if len(g) else None, len(g), flags))
+
+    def state(self) -> np.ndarray:
+        out = np.empty(1 << self.n, dtype=np.complex128 if self.precision == "fp64" else np.complex64)
+        self._check(lib().sv_host_get_state(self._h, out.ctypes.data))
+        return out
+
+    def norm(self) -> float:
+        v = ctypes.c_double()
+        self._check(lib().sv_host_norm(self._h, ctypes.byref(v)))
+        return v.value
+
+    def probabilities(self, qubits) -> np.ndarray:
+        q = np.ascontiguousarray(qubits, dtype=np.int32)
+        out = np.empty(1 << len(q), dtype=np.float64)
+        self._check(lib().sv_host_probabilities(self._h, _ip(q), len(q),
+                                                out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().sv_host_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -288,3 +288,23 @@ def test_deferred_basis_state_readers():
         s.reset(k ^ 5)  # two resets in a row: the last one wins
         s.apply(circ)
         check(s.state(), O.apply_circuit(circ, n, basis=k ^ 5), "fp64")
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_host_memory_tier(prec):
+    # NEXT-4: state in host memory, the GPU streaming 2^d-amplitude chunks through every section
+    for n, c, d, circ, basis in [(14, 6, 11, C.quantum_volume(14, 8, 2), 0), (15, 5, 11, C.qft(15), C.basis_index(3, 15)),
+                                 (13, 5, 10, C.random_circuit(13, 200, 21), 5)]:
+        with sv.HostStateVector(n, c, d, prec) as s:
+            s.reset(basis)
+            s.apply(circ)
+            ref = O.apply_circuit(circ, n, basis=basis)
+            check(s.state(), ref, prec)
+            tol = 1e-12 if prec == "fp64" else 1e-5
+            assert abs(s.norm() - 1) <= tol
+            Q = [0, n - 1, n // 2]
+            assert np.max(np.abs(s.probabilities(Q) - O.marginal(ref, Q))) <= tol
+            s.apply(C.mirror(circ))  # the layout carries over to the next circuit
+            back = np.zeros(1 << n, dtype=np.complex128)
+            back[:] = O.apply_circuit(C.mirror(circ), n, ref)
+            check(s.state(), back, prec)
