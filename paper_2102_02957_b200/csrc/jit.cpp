@@ -123,6 +123,18 @@ size_t smem_bytes(const Launch& L, bool dbl) {
   return no_smem ? 0 : amp << L.T;
 }
 
+// Resident CTAs per SM the generated kernel is register-budgeted for (launch bounds): 512 threads
+// per SM at 128 registers (SV_JIT_THREADS_SM overrides the target for tiles below 12 bits).
+int resident_ctas(int T, int nt) {
+  static const int target = [] {
+    const char* e = std::getenv("SV_JIT_THREADS_SM");
+    return e ? std::max(32, std::atoi(e)) : 512;
+  }();
+  if (T > 12) return 1;
+  if (T == 12) return 2;
+  return std::max(1, std::min(16, target / nt));
+}
+
 // Coefficients as a __grid_constant__ kernel parameter when they fit the 32 KiB parameter space
 // (FMAs then read them from the parameter bank); else from the module's __constant__ bank.
 constexpr size_t kParamCoefMax = 31 * 1024;
@@ -239,7 +251,7 @@ std::string gen_source(const int* p, const Launch& L, bool dbl, bool virt = fals
   const bool persist = l2_prefetch(L, dbl);
   auto& o = g.o;
   o << "#include \"section_dev.cuh\"\nusing namespace sv;\ntypedef " << (dbl ? "double2" : "float2") << " V;\n";
-  o << "extern \"C\" __global__ void __launch_bounds__(" << nt << ", " << (H->T <= 12 ? std::min(16, 512 / nt) : 1)
+  o << "extern \"C\" __global__ void __launch_bounds__(" << nt << ", " << resident_ctas(H->T, nt)
     << ") sv_sec(V* __restrict__ psi, V* __restrict__ psi_hi, const V* __restrict__ aux, int split_a, int split_b, "
     << "long long vidx, "
     << coef_param_decl_impl(L, dbl) << ") {\n";

@@ -1,7 +1,4 @@
-for C in 8 9 10; do
-  timeout 900 python bench.py --workload qv33 --chunk-bits $C --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/s_qv33_$C.json 2> gpurun_out/s_qv33_$C.err
-  timeout 600 python bench.py --workload qv28 --chunk-bits $C --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/s_qv28_$C.json 2> gpurun_out/s_qv28_$C.err
-done
-for C in 7 8 9; do
-  timeout 600 python bench.py --workload qft30 --chunk-bits $C --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/s_qft30_$C.json 2> gpurun_out/s_qft30_$C.err
+for TS in 384 512; do
+  SV_JIT_CACHE=0 SV_JIT_THREADS_SM=$TS timeout 600 python bench.py --workload qv28 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ts_qv28_$TS.json 2> gpurun_out/ts_qv28_$TS.err
+  SV_JIT_CACHE=0 SV_JIT_THREADS_SM=$TS timeout 600 python bench.py --workload qft30 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ts_qft30_$TS.json 2> gpurun_out/ts_qft30_$TS.err
 done
