@@ -125,14 +125,25 @@ size_t smem_bytes(const Launch& L, bool dbl) {
 
 // Resident CTAs per SM the generated kernel is register-budgeted for (launch bounds): 512 threads
 // per SM at 128 registers (SV_JIT_THREADS_SM overrides the target for tiles below 12 bits).
-int resident_ctas(int T, int nt) {
+// Sections without dense 2-qubit gates (QFT-like: butterflies and phases) need fewer registers
+// and run 640 threads per SM (QFT30 29.7 -> 29.3 ms); U2 sections would spill there.
+int resident_ctas(int T, int nt, bool dense) {
   static const int target = [] {
     const char* e = std::getenv("SV_JIT_THREADS_SM");
-    return e ? std::max(32, std::atoi(e)) : 512;
+    return e ? std::max(32, std::atoi(e)) : 0;
   }();
   if (T > 12) return 1;
   if (T == 12) return 2;
-  return std::max(1, std::min(16, target / nt));
+  const int t = target ? target : (dense ? 512 : 640);
+  return std::max(1, std::min(16, t / nt));
+}
+
+bool has_dense(const int* p) {
+  const SvSecHeader* H = reinterpret_cast<const SvSecHeader*>(p);
+  const SvOp* ops = reinterpret_cast<const SvOp*>(p + H->op_off);
+  for (int i = 0; i < H->n_ops; i++)
+    if (ops[i].type == SV_OP_U2 || ops[i].type == SV_OP_U1) return true;
+  return false;
 }
 
 // Coefficients as a __grid_constant__ kernel parameter when they fit the 32 KiB parameter space
@@ -251,7 +262,7 @@ std::string gen_source(const int* p, const Launch& L, bool dbl, bool virt = fals
   const bool persist = l2_prefetch(L, dbl);
   auto& o = g.o;
   o << "#include \"section_dev.cuh\"\nusing namespace sv;\ntypedef " << (dbl ? "double2" : "float2") << " V;\n";
-  o << "extern \"C\" __global__ void __launch_bounds__(" << nt << ", " << resident_ctas(H->T, nt)
+  o << "extern \"C\" __global__ void __launch_bounds__(" << nt << ", " << resident_ctas(H->T, nt, has_dense(p))
     << ") sv_sec(V* __restrict__ psi, V* __restrict__ psi_hi, const V* __restrict__ aux, int split_a, int split_b, "
     << "long long vidx, "
     << coef_param_decl_impl(L, dbl) << ") {\n";
