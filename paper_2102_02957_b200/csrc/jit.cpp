@@ -598,8 +598,8 @@ void cache_store(const std::string& path, const std::vector<char>& cubin, const 
                  const std::string& nc) {
   if (path.empty()) return;
   const std::string dir = cache_dir();
-  std::string cmd_dir = dir;  // create the directory (one level below an existing parent)
-  ::mkdir(cmd_dir.c_str(), 0755);
+  for (size_t at = 1; at <= dir.size(); at++)  // mkdir -p
+    if (at == dir.size() || dir[at] == '/') ::mkdir(dir.substr(0, at).c_str(), 0755);
   const std::string tmp = path + ".tmp" + std::to_string((long long)::getpid());
   {
     std::ofstream f(tmp, std::ios::binary);
