@@ -294,11 +294,14 @@ __device__ __forceinline__ uint64_t insert_bit(uint64_t x, int p, int v) {
 }
 
 // Swap local[x] <-> remote[x'] for every compact index j (2^(nL - k - 1) of them).
-// Four pairs per thread per iteration (j, j + stride, ...): four remote loads in flight per
+#ifndef SV_XU
+#define SV_XU 8
+#endif
+// Eight pairs per thread per iteration (j, j + stride, ...): eight remote loads in flight per
 // thread keep more NVLink requests outstanding than one.
 template <typename V>
 __global__ void k_exchange_peer(V* __restrict__ local, V* __restrict__ remote, uint64_t count, ExDev e) {
-  constexpr int U = 4;
+  constexpr int U = SV_XU;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   auto idx = [&](uint64_t j, uint64_t& x, uint64_t& y) {
     x = j;
