@@ -64,8 +64,10 @@ struct PlanCounters {
 struct PlanLayout {
   int low_bits = 3;    // memory bits every section tile should contain (3: 128-byte fp64 runs)
   int max_tile = 13;   // largest tile (bits) one CTA holds
-  int tile_default = 11;  // small sections pad to 11 bits: 32 KiB fp64 tiles, 4 CTAs per SM (measured
-                          // faster than 12-bit tiles at 2 CTAs per SM: QFT30 c=8 35.6 vs 40.2 ms)
+  int tile_default = 11;  // small sections pad to 11 bits (32 KiB fp64 tiles, 4 CTAs per SM): more
+                          // independent CTAs overlap HBM phases and barriers better than 12-bit tiles
+                          // (QFT30 c=8 35.6 vs 40.2 ms; QV33 c=9 1724 vs 1842 ms); 10 bits gains
+                          // ~1-2% on QV but loses 15% on QFT (SV_TILE_DEFAULT)
   int pref_tile = 13;  // largest tile worth its coalescing bits (fp64: a T=13 tile is 128 KiB of
                       // smem, one CTA per SM, slower than a T=12 tile with 64-byte runs)
   bool free_initial = false;  // the state is a basis state: choose the initial sigma freely (NEXT-2)
@@ -80,6 +82,7 @@ inline int pref_tile_for(int G) {
 // Tile policy of a layout whose low_bits is set: preferred maximum and default size.
 inline void apply_tile_prefs(PlanLayout& L) {
   L.pref_tile = pref_tile_for(L.low_bits);
+  if (const char* e = std::getenv("SV_TILE_DEFAULT")) L.tile_default = std::atoi(e);  // measurements
   if (L.tile_default > L.pref_tile) L.tile_default = L.pref_tile;
 }
 

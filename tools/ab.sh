@@ -1,5 +1,4 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "qft or mid or random" > gpurun_out/gt.log 2>&1; echo t=$?
-for i in 1 2; do
-timeout 600 python bench.py --workload qft30 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/q$i.json 2> gpurun_out/q$i.err
-done
-timeout 600 python bench.py --workload qv28 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/v.json 2> gpurun_out/v.err
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/gputests.log 2>&1; echo tests=$?
+timeout 600 python tools/stress.py 5 120 > gpurun_out/stress.log 2>&1; echo stress=$?
+for W in qft30 qv28; do timeout 600 python bench.py --workload $W --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/f_$W.json 2> gpurun_out/f_$W.err; done
+timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/f_qv33.json 2> gpurun_out/f_qv33.err
