@@ -152,6 +152,20 @@ def oracle_sample(wl, target_s: float = 15.0, max_gates: int = None):
     return m, dt, per
 
 
+def oracle_fits(wl):
+    """The oracle holds the whole 2^n-amplitude complex128 state in host RAM; return None if it fits
+    in MemAvailable (with 10% headroom), else a one-line reason."""
+    need = 16 << wl["n"]
+    try:
+        with open("/proc/meminfo") as f:
+            avail = next(int(l.split()[1]) * 1024 for l in f if l.startswith("MemAvailable:"))
+    except (OSError, StopIteration):
+        return None
+    if need * 1.1 > avail:
+        return f"oracle state for {wl['n']} qubits needs {need / 2**30:.0f} GiB of host RAM, {avail / 2**30:.0f} GiB available"
+    return None
+
+
 def cores():
     v = os.environ.get("OMP_NUM_THREADS")
     return int(v) if v else (len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count())
@@ -164,6 +178,10 @@ def run_reference(args):
     if rank != 0:
         return 0
     wl = workload(args.workload, args.gpus)
+    why = oracle_fits(wl)
+    if why:
+        print(json.dumps({"impl": "reference", "unavailable": why}), flush=True)
+        return 0
     import oracle as O
     n, gates = wl["n"], wl["gates"]
     a = O.basis_state(n, wl["basis"])
@@ -325,7 +343,9 @@ def run_ours(args):
 
     # ---- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and oracle_fits(wl):
+        cpu = {"value": None, "unit": "gates/s", "cores": cores(), "kind": "oracle", "sample": oracle_fits(wl)}
+    elif rank == 0 and world == 1 and not args.no_cpu_baseline:
         m, dt, per = oracle_sample(wl, target_s=args.cpu_target_s)
         cpu = {"value": m / dt, "unit": "gates/s", "cores": cores(), "kind": "oracle",
                "sample": f"gates 2..{m + 1} of {wl['desc']} from its basis state ({m} gates, {dt:.1f} s; dense C oracle, OpenMP)"}
