@@ -295,7 +295,7 @@ def run_ours(args):
         t_alu = flops_l / (FP64_PEAK_TFLOPS * 1e12) if args.precision == "fp64" else flops_l / (2 * FP64_PEAK_TFLOPS * 1e12)
         traffic = None
         prof = os.path.join(ROOT, "profiles", "section_traffic.json")
-        if os.path.exists(prof):
+        if os.path.exists(prof) and world == 1:  # captured on one GPU: the N = 1 launch shape only
             try:
                 traffic = json.load(open(prof)).get(wl["name"])
             except Exception:
