@@ -67,10 +67,6 @@ typedef struct {
 #define SV_RESTORE_ORDER (1u << 1) /* append swaps returning the paper-physical order to logical */
 #define SV_EXCHANGE_NCCL (1u << 2) /* cross-GPU exchange by NCCL send/recv through a staging ring */
                                    /* instead of the peer-memory swap kernel                    */
-#define SV_FUSE_EXCHANGE (1u << 4) /* sv_compile_circuit: fuse one-bit exchanges into the next  */
-                                   /* section's load (as sv_apply_circuit does on GPUs with peer */
-                                   /* access); the exchange record gets [4] = 1, the launch      */
-                                   /* record [10], [11] = the exchanged local / rank bit         */
 #define SV_FREE_LAYOUT   (1u << 3) /* sv_plan_circuit / sv_compile_circuit: plan as sv_apply_   */
                                    /* circuit does right after sv_reset (the state is a basis   */
                                    /* state, so the planner chooses the initial memory layout; */
@@ -84,7 +80,9 @@ typedef struct {
                           /* per-gate (unblocked) non-diagonal gate on a global qubit          */
 #define SV_EMALFORMED  -4 /* malformed record / marker sequence                               */
 #define SV_ECUDA       -5 /* CUDA runtime failure                                              */
-#define SV_ENCCL       -6 /* NCCL failure or NCCL library not loadable                         */
+#define SV_ENCCL       -6 /* NCCL failure or NCCL library not loadable; a collective that did  */
+                          /* not complete within SV_COMM_TIMEOUT_S (default 600 s; the        */
+                          /* communicator is then aborted) or reported an asynchronous error   */
 #define SV_EUNAVAILABLE -7 /* optional run-time component missing (NVRTC for sv_jit_compile_*) */
 
 typedef struct sv_stats {
@@ -130,6 +128,25 @@ int sv_destroy(sv_handle h);
 /* Write ncclGetUniqueId() into out (128 bytes). */
 int sv_nccl_unique_id(void* out128);
 
+/* ---- in-process virtual world (testing the multi-GPU path on one device) ----------------
+ * The paper distributes 2^(n - log2 G)-amplitude shards over G processes and
+ * exchanges them only at chunk_swaps on global qubits.  A virtual world runs the
+ * same G ranks inside ONE process on the caller's current device: sv_world_create(G) makes the
+ * world, sv_create_local(..., w, r, ...) creates rank r's handle (its shard on the current device,
+ * cuda_stream nullable as in sv_create_dist).  Each rank's handle must be driven by its own host
+ * thread, every rank calling the same collective sequence as under NCCL; exchanges run the same
+ * peer-memory swap kernels and plans, barriers are CUDA events passed through a host barrier (no
+ * device-side waiting), reductions are summed on the host in rank order, send/recv are
+ * device-to-device copies.  A rank that does not reach a collective within SV_COMM_TIMEOUT_S
+ * seconds (default 600) makes the others fail with SV_ENCCL.  The world is reference counted:
+ * sv_world_destroy may be called right after the last sv_create_local.  Errors: SV_EINVAL
+ * (world not a power of two <= 64, bad rank), as sv_create_dist otherwise. */
+typedef struct sv_world_s* sv_world;
+int sv_world_create(int world, sv_world* out);
+int sv_world_destroy(sv_world w);
+int sv_create_local(int n_qubits, int chunk_bits, sv_precision prec, sv_world w, int rank, void* cuda_stream,
+                    sv_handle* out);
+
 /* ---- evolution ------------------------------------------------------------------------ */
 /* |k> for LOGICAL basis index k; resets the tracked permutations to identity. */
 int sv_reset(sv_handle h, uint64_t basis_index);
@@ -137,7 +154,8 @@ int sv_reset(sv_handle h, uint64_t basis_index);
  * blocked (Listing 3 pass, then one section kernel per section and exchanges only for
  * global qubits).  Returns after all work is enqueued on the handle's stream. */
 int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t flags);
-/* Block until the handle's stream is idle. */
+/* Block until the handle's stream is idle (with world > 1: polling the communicator for
+ * asynchronous errors, SV_ENCCL after SV_COMM_TIMEOUT_S seconds). */
 int sv_synchronize(sv_handle h);
 
 /* ---- readout (all collective; results on every rank) --------------------------------- */

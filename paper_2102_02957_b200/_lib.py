@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libsv.so")
 GATE_DTYPE = np.dtype([("kind", "<i4"), ("q0", "<i4"), ("q1", "<i4"), ("pad", "<i4"), ("m", "<f8", (32,))])
 SV_U1, SV_U2, SV_D1, SV_D2, SV_SWAP, SV_CHUNK_SWAP, SV_BEGIN, SV_END, SV_EXCHANGE = range(1, 10)
 SV_FP32, SV_FP64 = 0, 1
-SV_UNBLOCKED, SV_RESTORE_ORDER, SV_EXCHANGE_NCCL, SV_FREE_LAYOUT, SV_FUSE_EXCHANGE = 1, 2, 4, 8, 16
+SV_UNBLOCKED, SV_RESTORE_ORDER, SV_EXCHANGE_NCCL, SV_FREE_LAYOUT = 1, 2, 4, 8
 ERRORS = {-1: "SV_EINVAL", -2: "SV_ECAPACITY", -3: "SV_EINFEASIBLE", -4: "SV_EMALFORMED", -5: "SV_ECUDA", -6: "SV_ENCCL"}
 
 
@@ -40,7 +40,7 @@ class Stats(ctypes.Structure):
                 ("jit_compiled", ctypes.c_uint64), ("jit_compile_ms", ctypes.c_double)]
 
 
-EXPORTS = ["sv_create", "sv_create_dist", "sv_destroy", "sv_nccl_unique_id", "sv_reset", "sv_apply_circuit",
+EXPORTS = ["sv_create", "sv_create_dist", "sv_world_create", "sv_world_destroy", "sv_create_local", "sv_destroy", "sv_nccl_unique_id", "sv_reset", "sv_apply_circuit",
            "sv_synchronize", "sv_get_amplitudes", "sv_get_state", "sv_norm", "sv_probabilities", "sv_sample",
            "sv_get_permutation", "sv_stats_get", "sv_stats_reset", "sv_set_timing", "sv_last_error", "sv_block_circuit", "sv_plan_circuit",
            "sv_compile_circuit", "sv_jit_compile_circuit", "sv_jit_mode", "sv_jit_wait", "sv_host_create", "sv_host_destroy", "sv_host_reset",
@@ -66,6 +66,9 @@ def lib():
     sig = {
         "sv_create": ([i32, i32, i32, hp], i32),
         "sv_create_dist": ([i32, i32, i32, i32, i32, vp, vp, sz, vp, hp], i32),
+        "sv_world_create": ([i32, hp], i32),
+        "sv_world_destroy": ([vp], i32),
+        "sv_create_local": ([i32, i32, i32, vp, i32, vp, hp], i32),
         "sv_destroy": ([vp], i32),
         "sv_nccl_unique_id": ([vp], i32),
         "sv_reset": ([vp, u64], i32),
@@ -226,18 +229,74 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+class LocalWorld:
+    """In-process virtual world of `world` ranks on the current device (sv_world_create): the
+    multi-GPU path (exchange kernels, plans, collectives) with every shard on one GPU.  Each rank's
+    StateVector(..., rank=r, local_world=w) must be driven by its own thread: run(fn) calls fn(rank)
+    on `world` threads and returns the per-rank results (re-raising the first exception)."""
+
+    def __init__(self, world: int):
+        h = ctypes.c_void_p()
+        check(lib().sv_world_create(world, ctypes.byref(h)))
+        self._h = h
+        self.world = world
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().sv_world_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def run(self, fn):
+        import threading
+        out = [None] * self.world
+        errs = [None] * self.world
+
+        def body(r):
+            try:
+                out[r] = fn(r)
+            except BaseException as e:  # noqa: BLE001 - re-raised in the caller
+                errs[r] = e
+
+        th = [threading.Thread(target=body, args=(r,)) for r in range(self.world)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        for e in errs:
+            if e is not None:
+                raise e
+        return out
+
+
 class StateVector:
-    """One rank's handle on a chunk-sharded n-qubit state (sv_create / sv_create_dist)."""
+    """One rank's handle on a chunk-sharded n-qubit state (sv_create / sv_create_dist /
+    sv_create_local)."""
 
     def __init__(self, n_qubits: int, chunk_bits: int, precision: str = "fp64", *, rank: int = 0, world: int = 1,
-                 nccl_id: bytes = None, stream: int = None, buffer_ptr: int = None, buffer_bytes: int = 0):
+                 nccl_id: bytes = None, stream: int = None, buffer_ptr: int = None, buffer_bytes: int = 0,
+                 local_world: "LocalWorld" = None):
         self.n, self.c = n_qubits, chunk_bits
         self.precision = precision
         self.rank, self.world = rank, world
         prec = {"fp64": SV_FP64, "fp32": SV_FP32}[precision]
         self.cdtype = np.complex128 if prec == SV_FP64 else np.complex64
         h = ctypes.c_void_p()
-        if world == 1 and buffer_ptr is None and stream is None:
+        if local_world is not None:
+            self.world = local_world.world
+            rc = lib().sv_create_local(n_qubits, chunk_bits, prec, local_world._h, rank, stream, ctypes.byref(h))
+        elif world == 1 and buffer_ptr is None and stream is None:
             rc = lib().sv_create(n_qubits, chunk_bits, prec, ctypes.byref(h))
         else:
             uid = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None

@@ -83,8 +83,7 @@ struct sv_state {
   cudaEvent_t ev_upload = nullptr;
   bool upload_pending = false;
 
-  Nccl* nc = nullptr;
-  Nccl::Comm comm = nullptr;
+  Comm* comm = nullptr;            // NCCL (one process per GPU) or an in-process local world
   std::vector<void*> peers;       // peer shard pointers mapped in this process (self = sv)
   std::vector<void*> ipc_opened;  // to close
   bool p2p = false;
@@ -125,11 +124,10 @@ int fail(sv_state* h, const Status& s) { return fail(h, s.code, s.msg); }
       return fail(h, SV_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));              \
   } while (0)
 
-#define NCCL_TRY(h, expr)                                                                        \
+#define COMM_TRY(h, expr)                                                                        \
   do {                                                                                           \
     int _r = (expr);                                                                             \
-    if (_r != 0)                                                                                 \
-      return fail(h, SV_ENCCL, std::string(#expr) + ": " + (h)->nc->GetErrorString(_r));        \
+    if (_r != 0) return fail(h, _r, (h)->comm->err());                                           \
   } while (0)
 
 int ensure_dev(sv_state* h, DevBuf& b, size_t bytes) {
@@ -180,7 +178,18 @@ BitPerm mu_inv_of(const sv_state* h) {
 
 int barrier(sv_state* h, cudaStream_t st = nullptr) {
   if (h->world == 1) return SV_OK;
-  NCCL_TRY(h, h->nc->AllReduce(h->d_small.p, h->d_small.p, 1, Nccl::F32, 0, h->comm, st ? st : h->st));
+  COMM_TRY(h, h->comm->barrier(st ? st : h->st));
+  return SV_OK;
+}
+
+// Block until the handle's stream is idle; on several ranks through the communicator, which fails
+// (SV_ENCCL) instead of hanging when a peer is gone (comm.h).
+int sync_stream(sv_state* h) {
+  if (h->world == 1 || !h->comm) {
+    CUDA_TRY(h, cudaStreamSynchronize(h->st));
+    return SV_OK;
+  }
+  COMM_TRY(h, h->comm->wait(h->st));
   return SV_OK;
 }
 
@@ -212,15 +221,16 @@ int do_exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags) {
     return barrier(h);
   }
 
-  // NCCL path: my block mu (local m-bits = mu) goes to the partner whose rank bits are mu; its
-  // block `mine` comes back into the same place, through a staging buffer, run by run.
+  // NCCL send/recv path (P:420's MPI send/recv pairs): my block mu (local m-bits = mu) goes to the
+  // partner whose rank bits are mu and its block `mine` comes back into the same places.  The
+  // blocks are strided whenever an m-bit is not a top bit, so each piece is packed into a
+  // contiguous staging buffer, sent / received in one grouped call, and unpacked in place.
   int mine = 0;
   for (int i = 0; i < a.k; i++) mine |= ((h->rank >> a.bsel[i]) & 1) << i;
-  const int mlow = a.m[0];
-  const uint64_t run = 1ull << mlow;  // contiguous amplitudes per run
-  const uint64_t runs = 1ull << (h->nL - mlow - a.k);
-  const size_t piece_amps = std::min<uint64_t>(run, (64ull << 20) / h->amp);
-  if (int rc = ensure_dev(h, h->d_stage, piece_amps * h->amp)) return rc;
+  const uint64_t piece = std::min<uint64_t>(block, (256ull << 20) / h->amp);
+  if (int rc = ensure_dev(h, h->d_stage, 2 * piece * h->amp)) return rc;
+  char* send_buf = (char*)h->d_stage.p;
+  char* recv_buf = send_buf + piece * h->amp;
   std::vector<std::pair<int, int>> partners;  // (partner rank, mu)
   for (int mu = 0; mu < (1 << a.k); mu++) {
     if (mu == mine) continue;
@@ -231,29 +241,18 @@ int do_exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags) {
   // XOR schedule (as the peer kernel): round t pairs ranks whose subcube bits differ by t
   std::sort(partners.begin(), partners.end(),
             [&](const std::pair<int, int>& x, const std::pair<int, int>& y) { return (x.second ^ mine) < (y.second ^ mine); });
-  // insert the m-bits (value mu) into a run index: positions above mlow that are not m-bits
-  auto run_start = [&](uint64_t rix, int mu) {
-    uint64_t x = rix << mlow;  // compact index of the run's first element (bits >= mlow)
-    for (int i = 0; i < a.k; i++) {
-      const int p = a.m[i];
-      const uint64_t lo = x & ((1ull << p) - 1);
-      x = ((x - lo) << 1) | ((uint64_t)((mu >> i) & 1) << p) | lo;
-    }
-    return x;
-  };
-  char* base = (char*)h->sv;
+  int val[8];
   for (auto& pm : partners) {
-    for (uint64_t rix = 0; rix < runs; rix++) {
-      const uint64_t start = run_start(rix, pm.second);
-      for (uint64_t off = 0; off < run; off += piece_amps) {
-        const size_t cnt = (size_t)std::min<uint64_t>(piece_amps, run - off);
-        char* p = base + (start + off) * h->amp;
-        NCCL_TRY(h, h->nc->GroupStart());
-        NCCL_TRY(h, h->nc->Send(p, cnt * h->amp, Nccl::Uint8, pm.first, h->comm, h->st));
-        NCCL_TRY(h, h->nc->Recv(h->d_stage.p, cnt * h->amp, Nccl::Uint8, pm.first, h->comm, h->st));
-        NCCL_TRY(h, h->nc->GroupEnd());
-        CUDA_TRY(h, cudaMemcpyAsync(p, h->d_stage.p, cnt * h->amp, cudaMemcpyDeviceToDevice, h->st));
-      }
+    for (int i = 0; i < a.k; i++) val[i] = (pm.second >> i) & 1;
+    for (uint64_t off = 0; off < block; off += piece) {
+      const uint64_t cnt = std::min<uint64_t>(piece, block - off);
+      CUDA_TRY(h, launch_pack_bits(h->dbl, true, h->sv, send_buf, off, cnt, a.k, a.m, val, h->st));
+      COMM_TRY(h, h->comm->group_start());
+      COMM_TRY(h, h->comm->send(send_buf, cnt * h->amp, pm.first, h->st));
+      COMM_TRY(h, h->comm->recv(recv_buf, cnt * h->amp, pm.first, h->st));
+      COMM_TRY(h, h->comm->group_end());
+      CUDA_TRY(h, launch_pack_bits(h->dbl, false, h->sv, recv_buf, off, cnt, a.k, a.m, val, h->st));
+      h->stats.kernel_launches += 2;
     }
   }
   return SV_OK;
@@ -358,19 +357,8 @@ int launch_one(sv_state* h, const Launch& L, int split_a = 0, int split_b = 0, i
   const char* cdev = (const char*)h->d_coef.p + L.coef_off * h->amp;
   const char* adev = (const char*)h->d_aux.p + L.aux_off * h->amp;
   cudaError_t je = cudaSuccess;
-  void* lo = h->sv;
-  void* hi = nullptr;
-  if (L.flags & SV_FLAG_XRANK) {
-    // fused exchange + section: the tiles span this GPU and its partner across rank bit xb; each
-    // GPU takes the tiles whose highest out bit equals its own value of that rank bit
-    const int rb = L.xb - h->nL, mine = (h->rank >> rb) & 1, partner = h->rank ^ (1 << rb);
-    lo = mine ? h->peers[partner] : h->sv;
-    hi = mine ? h->sv : h->peers[partner];
-    split_a = (1 << 16) | (mine << 8) | (L.n_out - 1);
-    split_b = 0;
-  }
-  if (jit_launch_section(h->dbl, lo, h->prog.ints.data() + L.int_off, h->prog.coefs.data() + 2 * L.coef_off, L,
-                         pdev, cdev, adev, h->st, &je, split_a, split_b, hi, vidx)) {
+  if (jit_launch_section(h->dbl, h->sv, h->prog.ints.data() + L.int_off, h->prog.coefs.data() + 2 * L.coef_off, L,
+                         cdev, adev, h->st, &je, split_a, split_b, vidx)) {
     CUDA_TRY(h, je);
     h->stats.jit_launches++;
     h->stats.kernel_launches++;
@@ -378,8 +366,6 @@ int launch_one(sv_state* h, const Launch& L, int split_a = 0, int split_b = 0, i
   } else if (vidx != -1) {  // no generated kernel after all: write the basis state, then run normally
     if (int rc = materialize_at(h, vidx)) return rc;
     return launch_one(h, L, split_a, split_b, -1);
-  } else if (L.flags & SV_FLAG_XRANK) {
-    return fail(h, SV_ECUDA, "internal: fused exchange section without its generated kernel");
   } else {
     CUDA_TRY(h, launch_section(h->dbl, h->sv, pdev, L.int_count, cdev, L.coef_count, adev, L.T, L.n_out, L.n_phases,
                                L.flags, L.n_sets, h->st, split_a, split_b));
@@ -563,13 +549,19 @@ int ready(sv_state* h) {  // a call that reads the state: valid handle, state wr
 }
 
 // Sum `count` values of dtype over all ranks in place (device buffer).
-int allreduce(sv_state* h, void* buf, size_t count, int dtype) {
+int allreduce(sv_state* h, void* buf, size_t count, CommType type) {
   if (h->world == 1) return SV_OK;
-  NCCL_TRY(h, h->nc->AllReduce(buf, buf, count, dtype, 0, h->comm, h->st));
+  COMM_TRY(h, h->comm->allreduce_sum(buf, count, type, h->st));
   return SV_OK;
 }
 
 int setup_p2p(sv_state* h, void* base_alloc, size_t base_off) {
+  if (h->comm->local()) {  // one process, one device: the other ranks' shards are plain pointers
+    h->peers.assign(h->world, nullptr);
+    COMM_TRY(h, h->comm->share_pointers(h->sv, h->peers.data()));
+    h->p2p = true;
+    return SV_OK;
+  }
   // Exchange CUDA IPC handles of every rank's shard allocation (NCCL all-gather).
   struct Rec {
     cudaIpcMemHandle_t hd;
@@ -584,10 +576,10 @@ int setup_p2p(sv_state* h, void* base_alloc, size_t base_off) {
   mine.off = base_off;
   if (int rc = ensure_dev(h, h->d_tmp, sizeof(Rec) * (h->world + 1))) return rc;
   CUDA_TRY(h, cudaMemcpyAsync((char*)h->d_tmp.p + sizeof(Rec) * h->world, &mine, sizeof(Rec), cudaMemcpyHostToDevice, h->st));
-  NCCL_TRY(h, h->nc->AllGather((char*)h->d_tmp.p + sizeof(Rec) * h->world, h->d_tmp.p, sizeof(Rec), Nccl::Uint8, h->comm, h->st));
+  COMM_TRY(h, h->comm->allgather((char*)h->d_tmp.p + sizeof(Rec) * h->world, h->d_tmp.p, sizeof(Rec), h->st));
   std::vector<Rec> all(h->world);
   CUDA_TRY(h, cudaMemcpyAsync(all.data(), h->d_tmp.p, sizeof(Rec) * h->world, cudaMemcpyDeviceToHost, h->st));
-  CUDA_TRY(h, cudaStreamSynchronize(h->st));
+  if (int rc_ = sync_stream(h)) return rc_;
   int ok = 1;
   for (auto& r : all) ok &= r.ok;
   h->peers.assign(h->world, nullptr);
@@ -606,9 +598,9 @@ int setup_p2p(sv_state* h, void* base_alloc, size_t base_off) {
   // agree across ranks
   float f = ok ? 0.f : 1.f;
   CUDA_TRY(h, cudaMemcpyAsync(h->d_small.p, &f, sizeof(float), cudaMemcpyHostToDevice, h->st));
-  if (int rc = allreduce(h, h->d_small.p, 1, Nccl::F32)) return rc;
+  if (int rc = allreduce(h, h->d_small.p, 1, kF32)) return rc;
   CUDA_TRY(h, cudaMemcpyAsync(&f, h->d_small.p, sizeof(float), cudaMemcpyDeviceToHost, h->st));
-  CUDA_TRY(h, cudaStreamSynchronize(h->st));
+  if (int rc_ = sync_stream(h)) return rc_;
   h->p2p = (f == 0.f);
   return SV_OK;
 }
@@ -638,8 +630,11 @@ int sv_create(int n_qubits, int chunk_bits, sv_precision prec, sv_handle* out) {
   return sv_create_dist(n_qubits, chunk_bits, prec, 0, 1, nullptr, nullptr, 0, nullptr, out);
 }
 
-int sv_create_dist(int n_qubits, int chunk_bits, sv_precision prec, int rank, int world, const void* uid,
-                   void* ext_dev_buf, size_t ext_bytes, void* cuda_stream, sv_handle* out) {
+namespace {
+// Shared by sv_create_dist (NCCL world, one process per GPU) and sv_create_local (in-process world
+// on one device): `local` non-null selects the latter.
+int create_common(int n_qubits, int chunk_bits, sv_precision prec, int rank, int world, const void* uid,
+                  LocalWorld* local, void* ext_dev_buf, size_t ext_bytes, void* cuda_stream, sv_handle* out) {
   if (!out) return fail(nullptr, SV_EINVAL, "null output handle");
   *out = nullptr;
   if (world < 1 || (world & (world - 1))) return fail(nullptr, SV_EINVAL, "world must be a power of two");
@@ -650,7 +645,7 @@ int sv_create_dist(int n_qubits, int chunk_bits, sv_precision prec, int rank, in
   if (n_qubits - g < 1) return fail(nullptr, SV_EINVAL, "more GPUs than amplitudes");
   if (chunk_bits < 1 || chunk_bits > n_qubits - g)
     return fail(nullptr, SV_EINVAL, "chunk_bits must satisfy 1 <= c <= n - log2(world)");
-  if (world > 1 && !uid) return fail(nullptr, SV_EINVAL, "world > 1 needs an NCCL unique id");
+  if (world > 1 && !uid && !local) return fail(nullptr, SV_EINVAL, "world > 1 needs an NCCL unique id");
 
   auto* h = new sv_state();
   h->n = n_qubits;
@@ -698,14 +693,12 @@ int sv_create_dist(int n_qubits, int chunk_bits, sv_precision prec, int rank, in
   if (cudaMemsetAsync(h->d_small.p, 0, 4096, h->st) != cudaSuccess) return bail(fail(nullptr, SV_ECUDA, "memset"));
   if (world > 1) {
     std::string er;
-    h->nc = nccl(er);
-    if (!h->nc) return bail(fail(nullptr, SV_ENCCL, er));
-    int r = nccl_comm_init(h->nc, &h->comm, world, uid, rank);
-    if (r != 0) return bail(fail(nullptr, SV_ENCCL, std::string("ncclCommInitRank: ") + h->nc->GetErrorString(r)));
+    h->comm = local ? make_local_comm(local, rank, er) : make_nccl_comm(world, rank, uid, h->d_small.p, er);
+    if (!h->comm) return bail(fail(nullptr, SV_ENCCL, er));
     // allocation base of the shard for CUDA IPC
     void* base = h->sv;
     size_t off = 0;
-    if (!h->own_sv) {
+    if (!h->own_sv && !local) {
       typedef int (*GetRange)(unsigned long long*, size_t*, unsigned long long);
       void* lib = dlopen("libcuda.so.1", RTLD_NOW | RTLD_NOLOAD);
       GetRange fn = lib ? (GetRange)dlsym(lib, "cuMemGetAddressRange_v2") : nullptr;
@@ -722,13 +715,40 @@ int sv_create_dist(int n_qubits, int chunk_bits, sv_precision prec, int rank, in
   *out = h;
   return SV_OK;
 }
+}  // namespace
+
+int sv_create_dist(int n_qubits, int chunk_bits, sv_precision prec, int rank, int world, const void* uid,
+                   void* ext_dev_buf, size_t ext_bytes, void* cuda_stream, sv_handle* out) {
+  return create_common(n_qubits, chunk_bits, prec, rank, world, uid, nullptr, ext_dev_buf, ext_bytes, cuda_stream, out);
+}
+
+int sv_world_create(int world, sv_world* out) {
+  if (!out) return fail(nullptr, SV_EINVAL, "null output");
+  *out = nullptr;
+  if (world < 1 || world > 64 || (world & (world - 1))) return fail(nullptr, SV_EINVAL, "world must be a power of two <= 64");
+  *out = reinterpret_cast<sv_world>(local_world_create(world));
+  return SV_OK;
+}
+
+int sv_world_destroy(sv_world w) {
+  local_world_release(reinterpret_cast<LocalWorld*>(w));
+  return SV_OK;
+}
+
+int sv_create_local(int n_qubits, int chunk_bits, sv_precision prec, sv_world w, int rank, void* cuda_stream,
+                    sv_handle* out) {
+  if (!w) return fail(nullptr, SV_EINVAL, "null world");
+  LocalWorld* lw = reinterpret_cast<LocalWorld*>(w);
+  return create_common(n_qubits, chunk_bits, prec, rank, local_world_size(lw), nullptr, lw, nullptr, 0, cuda_stream,
+                       out);
+}
 
 int sv_destroy(sv_handle h) {
   if (!h) return SV_OK;
   cudaSetDevice(h->device);
   if (h->st) cudaStreamSynchronize(h->st);
   for (void* p : h->ipc_opened) cudaIpcCloseMemHandle(p);
-  if (h->comm && h->nc) h->nc->CommDestroy(h->comm);
+  delete h->comm;
   for (DevBuf* b : {&h->d_prog, &h->d_coef, &h->d_aux, &h->d_scratch, &h->d_small, &h->d_tmp, &h->d_tmp2, &h->d_stage})
     if (b->p) cudaFree(b->p);
   for (PinBuf* b : {&h->h_stage, &h->h_stage2})
@@ -764,7 +784,7 @@ int sv_reset(sv_handle h, uint64_t k) {
 
 int sv_synchronize(sv_handle h) {
   if (int rc = check_handle(h)) return rc;
-  CUDA_TRY(h, cudaStreamSynchronize(h->st));
+  if (int rc_ = sync_stream(h)) return rc_;
   return SV_OK;
 }
 
@@ -779,8 +799,6 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
   lay.low_bits = h->dbl ? 3 : 4;  // 128-byte runs
   apply_tile_prefs(lay);
   lay.free_initial = h->basis_pending && !(flags & SV_UNBLOCKED);
-  // the NCCL exchange sends contiguous runs of 2^m amplitudes: keep its victims among the top bits
-  if ((flags & SV_EXCHANGE_NCCL) || !h->p2p) lay.min_victim = std::max(0, h->nL - 6);
   std::vector<int> sigma0;
   Status s = make_plan(gates, n_gates, h->n, h->c, h->g, pi, sigma, flags, steps, ctr, lay, &sigma0);
   if (!s.good()) return fail(h, s);
@@ -798,29 +816,11 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
   h->prog.clear();
   const int T_default = lay.tile_default;
   std::vector<size_t> launch_end(steps.size(), 0);  // one past the last launch of each step
-  // Fused exchange + section (one kernel over peer memory, §8(e)): a one-bit exchange directly
-  // followed by a section whose tile can also hold the two exchanged bits becomes that section's
-  // load (needs the peer mapping and generated kernels).  Opt-in (SV_FUSE=1): correct, but the
-  // tile's scattered peer accesses ran at ~140 GB/s over NVLink (QFT34 on 2 GPUs: the fused
-  // section 489 ms vs 112 ms exchange + ~104 ms section pipelined), so the swap kernel wins.
-  static const bool fuse_env = [] {
-    const char* e = std::getenv("SV_FUSE");
-    return e && e[0] == '1';
-  }();
-  const bool can_fuse = fuse_env && h->world > 1 && h->p2p && !(flags & SV_EXCHANGE_NCCL) && jit_set_mode(-1) == 1 &&
-                        h->nL >= SV_R_BITS;
-  std::vector<char> fused(steps.size(), 0);
   for (size_t i = 0; i < steps.size(); i++) {
     const Step& st = steps[i];
     if (st.type == Step::SECTION && h->nL >= SV_R_BITS) {
-      Status cs = Status::err(kNoFuse, "");
-      if (can_fuse && i > 0 && steps[i - 1].type == Step::EXCHANGE && steps[i - 1].ex.size() == 1) {
-        cs = compile_section_split(st.gates, h->nL, h->rank, h->g, T_default, lay.low_bits, st.swaps, h->prog,
-                                   &steps[i - 1].ex[0]);
-        if (cs.good()) fused[i - 1] = 1;
-      }
-      if (cs.code == kNoFuse)
-        cs = compile_section_split(st.gates, h->nL, h->rank, h->g, T_default, lay.low_bits, st.swaps, h->prog);
+      const Status cs =
+          compile_section_split(st.gates, h->nL, h->rank, h->g, T_default, lay.low_bits, st.swaps, h->prog);
       if (!cs.good()) return fail(h, cs);
       if (h->prog.launches.back().T > 13)
         return fail(h, SV_ECAPACITY, "a section needs a tile larger than shared memory (lower chunk_bits)");
@@ -848,12 +848,6 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
     const Step& st = steps[i];
     switch (st.type) {
       case Step::EXCHANGE: {
-        if (fused[i]) {  // carried out by the next section's load (kernel sv_sec with SV_FLAG_XRANK)
-          h->stats.bytes_sent += (uint64_t)(1ull << (h->nL - 1)) * h->amp;
-          h->stats.exchanges += 1;
-          h->stats.exchange_batches++;
-          break;
-        }
         if (h->p2p && !(flags & SV_EXCHANGE_NCCL) && i + 1 < steps.size() && steps[i + 1].type == Step::SECTION &&
             h->nL >= SV_R_BITS && si < launch_end[i + 1]) {
           int done = 0;
@@ -878,15 +872,11 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
         }
         for (; si < launch_end[i]; si++) {
           const Launch& L = h->prog.launches[si];
-          const bool x = L.flags & SV_FLAG_XRANK;
-          if (x)  // the partner is done with every earlier kernel touching its shard
-            if (int rc = barrier(h)) return rc;
           cudaEvent_t t = tstart(h);
+          const bool gen_input = si == 0 && vidx != -1;  // the deferred basis state: a write-only pass
           if (int rc = launch_one(h, L, 0, 0, si == 0 ? vidx : -1)) return rc;
           const double amps = (double)(1ull << h->nL);
-          tend(h, t, 0, 2.0 * amps * (double)h->amp, L.flops_per_amp * amps);
-          if (x)  // both GPUs' halves written before anything reads them
-            if (int rc = barrier(h)) return rc;
+          tend(h, t, 0, (gen_input ? 1.0 : 2.0) * amps * (double)h->amp, L.flops_per_amp * amps);
           h->stats.sections++;
         }
         break;
@@ -952,9 +942,9 @@ int sv_norm(sv_handle h, double* out) {
   if (int rc = ensure_dev(h, h->d_scratch, norm_scratch_doubles() * sizeof(double))) return rc;
   CUDA_TRY(h, launch_norm(h->dbl, h->sv, h->nL, (double*)h->d_scratch.p, (double*)h->d_small.p + 8, h->st));
   h->stats.kernel_launches += 2;
-  if (int rc = allreduce(h, (double*)h->d_small.p + 8, 1, Nccl::F64)) return rc;
+  if (int rc = allreduce(h, (double*)h->d_small.p + 8, 1, kF64)) return rc;
   CUDA_TRY(h, cudaMemcpyAsync(out, (double*)h->d_small.p + 8, sizeof(double), cudaMemcpyDeviceToHost, h->st));
-  CUDA_TRY(h, cudaStreamSynchronize(h->st));
+  if (int rc_ = sync_stream(h)) return rc_;
   return SV_OK;
 }
 
@@ -984,12 +974,12 @@ int sv_probabilities(sv_handle h, const int32_t* qubits, int nq, double* host_ou
   h->stats.kernel_launches += 2;
   if (h->world == 1) {
     CUDA_TRY(h, cudaMemcpyAsync(host_out, h->d_tmp.p, bins * sizeof(double), cudaMemcpyDeviceToHost, h->st));
-    CUDA_TRY(h, cudaStreamSynchronize(h->st));
+    if (int rc_ = sync_stream(h)) return rc_;
     return SV_OK;
   }
   std::vector<double> loc(bins_l);
   CUDA_TRY(h, cudaMemcpyAsync(loc.data(), h->d_tmp.p, bins_l * sizeof(double), cudaMemcpyDeviceToHost, h->st));
-  CUDA_TRY(h, cudaStreamSynchronize(h->st));
+  if (int rc_ = sync_stream(h)) return rc_;
   std::vector<double> full(bins, 0.0);
   for (size_t y = 0; y < bins_l; y++) {
     size_t o = rank_part;
@@ -997,9 +987,9 @@ int sv_probabilities(sv_handle h, const int32_t* qubits, int nq, double* host_ou
     full[o] = loc[y];
   }
   CUDA_TRY(h, cudaMemcpyAsync(h->d_tmp.p, full.data(), bins * sizeof(double), cudaMemcpyHostToDevice, h->st));
-  if (int rc = allreduce(h, h->d_tmp.p, bins, Nccl::F64)) return rc;
+  if (int rc = allreduce(h, h->d_tmp.p, bins, kF64)) return rc;
   CUDA_TRY(h, cudaMemcpyAsync(host_out, h->d_tmp.p, bins * sizeof(double), cudaMemcpyDeviceToHost, h->st));
-  CUDA_TRY(h, cudaStreamSynchronize(h->st));
+  if (int rc_ = sync_stream(h)) return rc_;
   return SV_OK;
 }
 
@@ -1015,7 +1005,7 @@ int sv_get_amplitudes(sv_handle h, const uint64_t* idx, size_t cnt, void* host_o
   if (int rc = ensure_dev(h, h->d_tmp2, chunk * h->amp)) return rc;
   for (size_t b = 0; b < cnt; b += chunk) {
     const size_t m = std::min(chunk, cnt - b);
-    CUDA_TRY(h, cudaStreamSynchronize(h->st));  // staging reuse
+    if (int rc_ = sync_stream(h)) return rc_;  // staging reuse
     uint64_t* offs = (uint64_t*)h->h_stage2.p;
     for (size_t i = 0; i < m; i++) {
       const uint64_t x = idx[b + i];
@@ -1026,10 +1016,10 @@ int sv_get_amplitudes(sv_handle h, const uint64_t* idx, size_t cnt, void* host_o
     CUDA_TRY(h, cudaMemcpyAsync(h->d_tmp.p, offs, m * sizeof(uint64_t), cudaMemcpyHostToDevice, h->st));
     CUDA_TRY(h, launch_gather(h->dbl, h->sv, (const uint64_t*)h->d_tmp.p, m, h->d_tmp2.p, h->st));
     h->stats.kernel_launches++;
-    if (int rc = allreduce(h, h->d_tmp2.p, 2 * m, h->dbl ? Nccl::F64 : Nccl::F32)) return rc;
+    if (int rc = allreduce(h, h->d_tmp2.p, 2 * m, h->dbl ? kF64 : kF32)) return rc;
     CUDA_TRY(h, cudaMemcpyAsync((char*)host_out + b * h->amp, h->d_tmp2.p, m * h->amp, cudaMemcpyDeviceToHost, h->st));
   }
-  CUDA_TRY(h, cudaStreamSynchronize(h->st));
+  if (int rc_ = sync_stream(h)) return rc_;
   return SV_OK;
 }
 
@@ -1048,22 +1038,22 @@ int sv_get_state(sv_handle h, void* host_out) {
       const void* dev = (char*)h->sv + off * h->amp;
       if (src != 0) {
         if (h->rank == src) {
-          NCCL_TRY(h, h->nc->Send(dev, cnt * h->amp, Nccl::Uint8, 0, h->comm, h->st));
+          COMM_TRY(h, h->comm->send(dev, cnt * h->amp, 0, h->st));
         } else if (h->rank == 0) {
-          NCCL_TRY(h, h->nc->Recv(h->d_stage.p, cnt * h->amp, Nccl::Uint8, src, h->comm, h->st));
+          COMM_TRY(h, h->comm->recv(h->d_stage.p, cnt * h->amp, src, h->st));
           dev = h->d_stage.p;
         }
       }
       if (h->rank != 0) continue;
       CUDA_TRY(h, cudaMemcpyAsync(h->h_stage2.p, dev, cnt * h->amp, cudaMemcpyDeviceToHost, h->st));
-      CUDA_TRY(h, cudaStreamSynchronize(h->st));
+      if (int rc_ = sync_stream(h)) return rc_;
       const uint64_t mbase = ((uint64_t)src << h->nL) + off;
       const char* in = (const char*)h->h_stage2.p;
       char* o = (char*)host_out;
       for (size_t i = 0; i < cnt; i++) std::memcpy(o + inv(mbase + i) * h->amp, in + i * h->amp, h->amp);
     }
   }
-  CUDA_TRY(h, cudaStreamSynchronize(h->st));
+  if (int rc_ = sync_stream(h)) return rc_;
   return SV_OK;
 }
 
@@ -1086,7 +1076,7 @@ int sv_sample(sv_handle h, size_t shots, uint64_t seed, uint64_t* host_out) {
   h->stats.kernel_launches++;
   std::vector<double> bs(nblk);
   CUDA_TRY(h, cudaMemcpyAsync(bs.data(), h->d_tmp.p, nblk * sizeof(double), cudaMemcpyDeviceToHost, h->st));
-  CUDA_TRY(h, cudaStreamSynchronize(h->st));
+  if (int rc_ = sync_stream(h)) return rc_;
   std::vector<double> cum(nblk);
   double tot = 0.0;
   for (size_t i = 0; i < nblk; i++) {
@@ -1097,9 +1087,9 @@ int sv_sample(sv_handle h, size_t shots, uint64_t seed, uint64_t* host_out) {
   totals[h->rank] = tot;
   if (h->world > 1) {
     CUDA_TRY(h, cudaMemcpyAsync(h->d_tmp.p, totals.data(), h->world * sizeof(double), cudaMemcpyHostToDevice, h->st));
-    if (int rc = allreduce(h, h->d_tmp.p, h->world, Nccl::F64)) return rc;
+    if (int rc = allreduce(h, h->d_tmp.p, h->world, kF64)) return rc;
     CUDA_TRY(h, cudaMemcpyAsync(totals.data(), h->d_tmp.p, h->world * sizeof(double), cudaMemcpyDeviceToHost, h->st));
-    CUDA_TRY(h, cudaStreamSynchronize(h->st));
+    if (int rc_ = sync_stream(h)) return rc_;
   }
   double before = 0.0;
   for (int r = 0; r < h->rank; r++) before += totals[r];
@@ -1143,16 +1133,16 @@ int sv_sample(sv_handle h, size_t shots, uint64_t seed, uint64_t* host_out) {
     h->stats.kernel_launches++;
     std::vector<uint64_t> offs(nsh);
     CUDA_TRY(h, cudaMemcpyAsync(offs.data(), d_off, nsh * 8, cudaMemcpyDeviceToHost, h->st));
-    CUDA_TRY(h, cudaStreamSynchronize(h->st));
+    if (int rc_ = sync_stream(h)) return rc_;
     const BitPerm inv = mu_inv_of(h);
     for (size_t i = 0; i < nsh; i++) res[who[i]] = inv(((uint64_t)h->rank << h->nL) | offs[i]);
   }
   if (h->world > 1) {
     if (int rc = ensure_dev(h, h->d_tmp, shots * 8)) return rc;
     CUDA_TRY(h, cudaMemcpyAsync(h->d_tmp.p, res.data(), shots * 8, cudaMemcpyHostToDevice, h->st));
-    if (int rc = allreduce(h, h->d_tmp.p, shots, Nccl::Uint64)) return rc;
+    if (int rc = allreduce(h, h->d_tmp.p, shots, kU64)) return rc;
     CUDA_TRY(h, cudaMemcpyAsync(res.data(), h->d_tmp.p, shots * 8, cudaMemcpyDeviceToHost, h->st));
-    CUDA_TRY(h, cudaStreamSynchronize(h->st));
+    if (int rc_ = sync_stream(h)) return rc_;
   }
   std::memcpy(host_out, res.data(), shots * 8);
   return SV_OK;
@@ -1292,20 +1282,13 @@ extern "C" int sv_compile_circuit(const sv_gate* gates, size_t n_gates, int n, i
       for (const auto& sw : st.swaps) put({3, sw.first, sw.second});
     } else {
       const size_t first = prog.launches.size();
-      Status cs = Status::err(kNoFuse, "");
-      if ((flags & SV_FUSE_EXCHANGE) && world_log2 > 0 && i > 0 && steps[i - 1].type == Step::EXCHANGE &&
-          steps[i - 1].ex.size() == 1) {
-        cs = compile_section_split(st.gates, nL, rank, world_log2, lay.tile_default, lay.low_bits, st.swaps, prog,
-                                   &steps[i - 1].ex[0]);
-        if (cs.good()) rec[rec.size() - 12 + 4] = 1;  // the exchange record: fused into this section
-      }
-      if (cs.code == kNoFuse)
-        cs = compile_section_split(st.gates, nL, rank, world_log2, lay.tile_default, lay.low_bits, st.swaps, prog);
+      const Status cs =
+          compile_section_split(st.gates, nL, rank, world_log2, lay.tile_default, lay.low_bits, st.swaps, prog);
       if (!cs.good()) return fail(nullptr, cs);
       for (size_t k = first; k < prog.launches.size(); k++) {
         const Launch& L = prog.launches[k];
         put({1, (int64_t)L.int_off, (int64_t)L.int_count, (int64_t)L.coef_off, (int64_t)L.coef_count, L.T, L.n_out,
-             L.flags, (int64_t)L.aux_off, (int64_t)L.aux_count, L.xm, L.xb});
+             L.flags, (int64_t)L.aux_off, (int64_t)L.aux_count});
       }
     }
   }

@@ -67,22 +67,17 @@ struct PlanLayout {
   int tile_default = 11;  // small sections pad to 11 bits (32 KiB fp64 tiles, 4 CTAs per SM): more
                           // independent CTAs overlap HBM phases and barriers better than 12-bit tiles
                           // (QFT30 c=8 35.6 vs 40.2 ms; QV33 c=9 1724 vs 1842 ms); 10 bits gains
-                          // ~1-2% on QV but loses 15% on QFT (SV_TILE_DEFAULT)
+                          // ~1-2% on QV but loses 15% on QFT (round-1 measurements)
   int pref_tile = 13;  // largest tile worth its coalescing bits (fp64: a T=13 tile is 128 KiB of
                       // smem, one CTA per SM, slower than a T=12 tile with 64-byte runs)
   bool free_initial = false;  // the state is a basis state: choose the initial sigma freely (NEXT-2)
-  int min_victim = 0;         // lowest local bit an exchange may evict (NCCL path: contiguous runs)
 };
 
-// Preferred largest tile for swizzle width G (3: fp64, 4: fp32); SV_PREF_TILE overrides.
-inline int pref_tile_for(int G) {
-  if (const char* e = std::getenv("SV_PREF_TILE")) return std::atoi(e);
-  return G == 3 ? 12 : 13;
-}
+// Preferred largest tile for swizzle width G (3: fp64, 4: fp32).
+inline int pref_tile_for(int G) { return G == 3 ? 12 : 13; }
 // Tile policy of a layout whose low_bits is set: preferred maximum and default size.
 inline void apply_tile_prefs(PlanLayout& L) {
   L.pref_tile = pref_tile_for(L.low_bits);
-  if (const char* e = std::getenv("SV_TILE_DEFAULT")) L.tile_default = std::atoi(e);  // measurements
   if (L.tile_default > L.pref_tile) L.tile_default = L.pref_tile;
 }
 

@@ -81,8 +81,7 @@ struct TermKey {
 }  // namespace
 
 Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int world_log2, int T_default,
-                       int swizzle_bits, const std::vector<std::pair<int, int>>& store_swaps, Program& prog,
-                       const ExPair* xload) {
+                       int swizzle_bits, const std::vector<std::pair<int, int>>& store_swaps, Program& prog) {
   (void)world_log2;
   // ---- tile bits
   uint64_t active = 0;
@@ -100,12 +99,7 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
   lay.max_tile = kMaxTile;
   lay.pref_tile = pref_tile_for(swizzle_bits);
   lay.tile_default = T_default;
-  uint64_t tile = choose_tile(active | (xload ? 1ull << xload->m : 0ull), nL, lay);
-  if (xload) {
-    tile |= 1ull << xload->b;  // the rank bit is a tile position (loads / stores reach the partner)
-    if (__builtin_popcountll(tile) > lay.pref_tile)
-      return Status::err(kNoFuse, "fused exchange does not fit the tile");
-  }
+  const uint64_t tile = choose_tile(active, nL, lay);
   const int T = __builtin_popcountll(tile);
   if (T > kMaxTile) return Status::err(SV_ECAPACITY, "section needs more tile bits than shared memory holds");
   int tile_bits[16], pos_of[64];
@@ -116,19 +110,14 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
       pos_of[b] = t;
       tile_bits[t++] = b;
     }
-  // load-side memory bits: the fused exchange swaps m and b on the load (the section computes in
-  // the post-exchange frame and stores there)
-  int load_bits[16];
+  int load_bits[16];  // tile position -> memory bit on the load (the store side may differ)
   for (int j = 0; j < T; j++) load_bits[j] = tile_bits[j];
-  if (xload) std::swap(load_bits[pos_of[xload->m]], load_bits[pos_of[xload->b]]);
   int out_bits[SV_MAX_OUT], n_out = 0;
   for (int b = 0; b < nL; b++)
     if (!((tile >> b) & 1)) {
       if (n_out >= SV_MAX_OUT) return Status::err(SV_ECAPACITY, "too many local bits");
       out_bits[n_out++] = b;
     }
-  // a fused exchange splits the tiles between the two GPUs by the highest out bit
-  if (xload && n_out == 0) return Status::err(kNoFuse, "fused exchange needs an out-of-tile bit");
   const int r = std::min(SV_R_BITS, T);
 
   // ---- gates on positions
@@ -161,8 +150,8 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
       case SV_D2: {
         p.diag = true;
         auto operand = [&](int mb) {
-          if (mb >= nL && !((tile >> mb) & 1)) return ((rank >> (mb - nL)) & 1) ? SV_CODE_ONE : SV_CODE_ZERO;
-          return kDiagLocal - mb;  // a local bit, or the fused exchange's rank bit (a tile position)
+          if (mb >= nL) return ((rank >> (mb - nL)) & 1) ? SV_CODE_ONE : SV_CODE_ZERO;  // rank bit: a constant
+          return kDiagLocal - mb;
         };
         p.a = operand(g.q0);
         p.b = g.kind == SV_D2 ? operand(g.q1) : SV_CODE_ZERO;
@@ -720,8 +709,7 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
       op_cursor++;
     }
   }
-  H()->flags = (lanes_contiguous_first ? SV_FLAG_FIRST_DIRECT : 0) | (lanes_contiguous_last ? SV_FLAG_LAST_DIRECT : 0) |
-               (xload ? SV_FLAG_XRANK : 0);
+  H()->flags = (lanes_contiguous_first ? SV_FLAG_FIRST_DIRECT : 0) | (lanes_contiguous_last ? SV_FLAG_LAST_DIRECT : 0);
   H()->nl = nL;
   const size_t total_ints = prog.ints.size() - base;
   const size_t ncoef = prog.coefs.size() / 2 - cbase;
@@ -755,10 +743,6 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
   L.n_ops = (int)n_items;
   L.flags = H()->flags;
   L.n_sets = H()->n_sets;
-  if (xload) {
-    L.xm = xload->m;
-    L.xb = xload->b;
-  }
   prog.launches.push_back(L);
   // keep every section 16-byte aligned
   while (prog.ints.size() % 4) prog.ints.push_back(0);
@@ -766,10 +750,9 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
 }
 
 Status compile_section_split(const std::vector<sv_gate>& gates, int nL, int rank, int world_log2, int T_default,
-                             int swizzle_bits, const std::vector<std::pair<int, int>>& store_swaps, Program& prog,
-                             const ExPair* xload) {
+                             int swizzle_bits, const std::vector<std::pair<int, int>>& store_swaps, Program& prog) {
   const size_t ni = prog.ints.size(), nc = prog.coefs.size(), na = prog.aux.size();
-  Status s = compile_section(gates, nL, rank, world_log2, T_default, swizzle_bits, store_swaps, prog, xload);
+  Status s = compile_section(gates, nL, rank, world_log2, T_default, swizzle_bits, store_swaps, prog);
   if (s.code != kTooBig) return s;
   prog.ints.resize(ni);
   prog.coefs.resize(nc);
@@ -778,7 +761,7 @@ Status compile_section_split(const std::vector<sv_gate>& gates, int nL, int rank
   // Consecutive halves of the in-order gate list: each half is a valid section on its own.
   const size_t h = gates.size() / 2;
   std::vector<sv_gate> a(gates.begin(), gates.begin() + h), b(gates.begin() + h, gates.end());
-  if (Status sa = compile_section_split(a, nL, rank, world_log2, T_default, swizzle_bits, {}, prog, xload); !sa.good())
+  if (Status sa = compile_section_split(a, nL, rank, world_log2, T_default, swizzle_bits, {}, prog); !sa.good())
     return sa;
   return compile_section_split(b, nL, rank, world_log2, T_default, swizzle_bits, store_swaps, prog);
 }

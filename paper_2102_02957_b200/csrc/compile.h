@@ -9,7 +9,6 @@
 namespace sv {
 
 constexpr int kTooBig = -100;  // internal: section exceeds the __constant__ budget (split it)
-constexpr int kNoFuse = -101;  // internal: a fused exchange does not fit the tile
 
 struct Launch {
   size_t int_off;     // start of the section's SvSecHeader in Program::ints
@@ -19,7 +18,6 @@ struct Launch {
   size_t aux_off;     // first complex of the section's DIAGSET factor tables in Program::aux
   size_t aux_count;
   int T, r, n_out, n_phases, n_ops, flags, n_sets;
-  int xm = -1, xb = -1;  // fused exchange (SV_FLAG_XRANK): local bit xm <-> rank bit xb on the load
   double flops_per_amp;  // algorithmic flops per amplitude of the section (DESIGN "Roofline")
 };
 
@@ -41,13 +39,9 @@ struct Program {
 // compile_section_split splits sections whose program or coefficients exceed the __constant__
 // budget into consecutive in-order pieces (each its own launch).
 // store_swaps: memory-bit transpositions (both bits in the tile) fused into the final store.
-// xload (nullable): fuse the preceding one-bit exchange {m, b} into the section's load — the tile
-// then holds local bit m and rank bit b, and loads them swapped (kNoFuse if that does not fit).
 Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int world_log2, int T_default,
-                       int swizzle_bits, const std::vector<std::pair<int, int>>& store_swaps, Program& prog,
-                       const ExPair* xload = nullptr);
+                       int swizzle_bits, const std::vector<std::pair<int, int>>& store_swaps, Program& prog);
 Status compile_section_split(const std::vector<sv_gate>& gates, int nL, int rank, int world_log2, int T_default,
-                             int swizzle_bits, const std::vector<std::pair<int, int>>& store_swaps, Program& prog,
-                             const ExPair* xload = nullptr);
+                             int swizzle_bits, const std::vector<std::pair<int, int>>& store_swaps, Program& prog);
 
 }  // namespace sv

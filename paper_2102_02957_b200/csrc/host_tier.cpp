@@ -303,7 +303,7 @@ extern "C" int sv_host_apply_circuit(sv_host_handle h, const sv_gate* gates, siz
           const char* adev = (const char*)rp.d_aux + L.aux_off * h->amp;
           cudaError_t je = cudaSuccess;
           if (!jit_launch_section(h->dbl, buf, rp.prog.ints.data() + L.int_off, rp.prog.coefs.data() + 2 * L.coef_off,
-                                  L, pdev, cdev, adev, stm, &je))
+                                  L, cdev, adev, stm, &je))
             je = launch_section(h->dbl, buf, pdev, L.int_count, cdev, L.coef_count, adev, L.T, L.n_out, L.n_phases,
                                 L.flags, L.n_sets, stm);
           HCUDA(h, je);

@@ -92,50 +92,20 @@ Mode mode() {
 }
 
 // ------------------------------------------------------------------------------------ source
-// Pipelined variant (gen_source_pipelined): two warp groups per CTA work on alternate tiles of
-// a persistent CTA with three tile buffers in shared memory, each group loading its next tile
-// with cp.async while it computes the current one.
-constexpr int kPipeSetsBytes = 2 * 5 * SV_MAX_SETS;  // per-CTA factor slots (both groups), in amplitudes
-bool pipelined(const Launch& L, bool dbl) {
-  static const bool on = [] {
-    const char* e = std::getenv("SV_PIPE");  // opt-in: measured slower than two CTAs per SM
-    return e && e[0] == '1';
-  }();
-  const size_t amp = dbl ? 16 : 8;
-  return on && !(L.flags & SV_FLAG_XRANK) && L.T >= 9 && L.T <= 12 &&
-         3 * (amp << L.T) + kPipeSetsBytes * amp + 64 <= 227 * 1024;
-}
-
-// Persistent grid + L2 prefetch of each CTA's next tile for the plain generated kernel (SV_L2PF=1)
-bool l2_prefetch(const Launch& L, bool dbl) {
-  static const bool on = [] {
-    const char* e = std::getenv("SV_L2PF");
-    return e && e[0] == '1';
-  }();
-  return on && !pipelined(L, dbl) && !(L.flags & SV_FLAG_XRANK) && L.T >= SV_R_BITS;
-}
-
 size_t smem_bytes(const Launch& L, bool dbl) {
   const size_t amp = dbl ? 16 : 8;
-  if (pipelined(L, dbl)) return 3 * (amp << L.T) + kPipeSetsBytes * amp + 64;
   const bool no_smem = L.n_phases == 1 && (L.flags & SV_FLAG_FIRST_DIRECT) && (L.flags & SV_FLAG_LAST_DIRECT);
   if (L.n_sets) return (amp << L.T) + 5 * SV_MAX_SETS * amp;
   return no_smem ? 0 : amp << L.T;
 }
 
 // Resident CTAs per SM the generated kernel is register-budgeted for (launch bounds): 512 threads
-// per SM at 128 registers (SV_JIT_THREADS_SM overrides the target for tiles below 12 bits).
-// Sections without dense 2-qubit gates (QFT-like: butterflies and phases) need fewer registers
-// and run 640 threads per SM (QFT30 29.7 -> 29.3 ms); U2 sections would spill there.
+// per SM at 128 registers.  Sections without dense gates (QFT-like: butterflies and phases) need
+// fewer registers and run 640 threads per SM (QFT30 29.7 -> 29.3 ms); U2 sections would spill there.
 int resident_ctas(int T, int nt, bool dense) {
-  static const int target = [] {
-    const char* e = std::getenv("SV_JIT_THREADS_SM");
-    return e ? std::max(32, std::atoi(e)) : 0;
-  }();
   if (T > 12) return 1;
   if (T == 12) return 2;
-  const int t = target ? target : (dense ? 512 : 640);
-  return std::max(1, std::min(16, t / nt));
+  return std::max(1, std::min(16, (dense ? 512 : 640) / nt));
 }
 
 bool has_dense(const int* p) {
@@ -147,13 +117,14 @@ bool has_dense(const int* p) {
 }
 
 // Coefficients as a __grid_constant__ kernel parameter when they fit the 32 KiB parameter space
-// (FMAs then read them from the parameter bank); else from the module's __constant__ bank.
+// (FMAs then read them from the parameter bank); else through a pointer to the handle's device
+// copy of the section's coefficients (CoefPtr).
 constexpr size_t kParamCoefMax = 31 * 1024;
 bool coef_in_param(const Launch& L, bool dbl) { return L.coef_count * (dbl ? 16 : 8) <= kParamCoefMax; }
 std::string coef_param_decl_impl(const Launch& L, bool dbl) {
   if (coef_in_param(L, dbl))
     return "const __grid_constant__ CoefParam<V, " + std::to_string(L.coef_count ? L.coef_count : 1) + "> P";
-  return "const CoefBank<V> P";
+  return "const CoefPtr<V> P";
 }
 
 struct Gen {
@@ -168,36 +139,18 @@ struct Gen {
     o << "};\n";
   }
   // HBM element offset of register 0 (b) and of every register k (RO[k]) under map m
-  int nl = 64;  // memory bits >= nl are rank bits (fused exchange, SV_FLAG_XRANK)
-  bool xrank = false;
   bool virt = false;  // the tile's input is generated: 1 at shard offset vidx, 0 elsewhere
   void hbm(const SvMap& m) {
     long long ro[16];
-    int gk[16], tmb[16];
-    uint32_t trank = 0;  // thread bits on the rank bit
     for (int k = 0; k < 16; k++) {
       ro[k] = 0;
-      gk[k] = 0;
       for (int s = 0; s < SV_R_BITS; s++)
-        if ((k >> s) & 1) {
-          if (m.rmb[s] >= nl)
-            gk[k] = 1;
-          else
-            ro[k] |= 1ll << m.rmb[s];
-        }
+        if ((k >> s) & 1) ro[k] |= 1ll << m.rmb[s];
     }
-    for (int j = 0; j < ntl; j++) {
-      tmb[j] = m.tmb[j] >= nl ? 63 : m.tmb[j];  // 63: contributes nothing below (masked)
-      if (m.tmb[j] >= nl) trank |= 1u << j;
-    }
-    arr("int", "TMB", tmb, ntl);
+    arr("int", "TMB", m.tmb, ntl);
     arr("long long", "RO", ro, 16);
     o << "    uint64_t b = tile_off;\n"
-      << "#pragma unroll\n    for (int j = 0; j < " << ntl << "; j++) if (TMB[j] != 63) b |= (uint64_t)((tid >> j) & 1) << TMB[j];\n";
-    if (xrank) {  // which GPU's shard each register lives on (the rank bit's value)
-      arr("int", "GK", gk, 16);
-      o << "    const int gs = (tid & " << trank << ") ? 1 : 0;\n";
-    }
+      << "#pragma unroll\n    for (int j = 0; j < " << ntl << "; j++) b |= (uint64_t)((tid >> j) & 1) << TMB[j];\n";
   }
   // swizzled smem offset of register 0 (x) and XOR offsets W[k] for thread-bit words tw, slot words rw
   void smem(const int* tw, const int* rw) {
@@ -232,82 +185,37 @@ struct Gen {
       o << "#pragma unroll\n    for (int k = 0; k < 16; k++) { v[k].x = (long long)(b + RO[k]) == vidx ? 1 : 0; v[k].y = 0; }\n";
       return;
     }
-    if (xrank)
-      o << "#pragma unroll\n    for (int k = 0; k < 16; k++) v[k] = ((gs ^ GK[k]) ? psi_hi : psi)[b + RO[k]];\n";
-    else
-      o << "#pragma unroll\n    for (int k = 0; k < 16; k++) v[k] = psi[b + RO[k]];\n";
+    o << "#pragma unroll\n    for (int k = 0; k < 16; k++) v[k] = psi[b + RO[k]];\n";
   }
-  void stg() {
-    if (xrank)
-      o << "#pragma unroll\n    for (int k = 0; k < 16; k++) ((gs ^ GK[k]) ? psi_hi : psi)[b + RO[k]] = v[k];\n";
-    else
-      o << "#pragma unroll\n    for (int k = 0; k < 16; k++) psi[b + RO[k]] = v[k];\n";
-  }
+  void stg() { o << "#pragma unroll\n    for (int k = 0; k < 16; k++) psi[b + RO[k]] = v[k];\n"; }
 };
 
-std::string gen_source_pipelined(const int* p, const Launch& L, bool dbl);
-
 std::string gen_source(const int* p, const Launch& L, bool dbl, bool virt = false) {
-  if (pipelined(L, dbl)) return gen_source_pipelined(p, L, dbl);
   const SvSecHeader* H = reinterpret_cast<const SvSecHeader*>(p);
   Gen g;
   g.virt = virt;
-  g.xrank = (H->flags & SV_FLAG_XRANK) != 0;
-  g.nl = g.xrank ? H->nl : 64;
   g.T = H->T;
   g.ntl = H->T - SV_R_BITS;
   const int nt = 1 << g.ntl;
   const bool first = H->flags & SV_FLAG_FIRST_DIRECT, last = H->flags & SV_FLAG_LAST_DIRECT;
   const int nph = H->n_phases;
-  const bool persist = l2_prefetch(L, dbl);
   auto& o = g.o;
-  o << "#include \"section_dev.cuh\"\nusing namespace sv;\ntypedef " << (dbl ? "double2" : "float2") << " V;\n";
+  // the program itself goes into the module's constant bank (section_dev.cuh SV_JIT_PROG)
+  o << "#define SV_JIT_PROG ";
+  for (size_t i = 0; i < L.int_count; i++) o << (i ? "," : "") << p[i];
+  o << "\n#include \"section_dev.cuh\"\nusing namespace sv;\ntypedef " << (dbl ? "double2" : "float2") << " V;\n";
   o << "extern \"C\" __global__ void __launch_bounds__(" << nt << ", " << resident_ctas(H->T, nt, has_dense(p))
-    << ") sv_sec(V* __restrict__ psi, V* __restrict__ psi_hi, const V* __restrict__ aux, int split_a, int split_b, "
-    << "long long vidx, "
+    << ") sv_sec(V* __restrict__ psi, const V* __restrict__ aux, int split_a, int split_b, long long vidx, "
     << coef_param_decl_impl(L, dbl) << ") {\n";
   o << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n"
     << "  V* sm = reinterpret_cast<V*>(smem_raw);\n"
     << "  V* ctaf = reinterpret_cast<V*>(smem_raw + (sizeof(V) << " << H->T << "));\n"
-    << "  (void)sm; (void)ctaf; (void)aux; (void)vidx; (void)psi_hi;\n"
+    << "  (void)sm; (void)ctaf; (void)aux; (void)vidx;\n"
     << "  const int tid = threadIdx.x;\n";
   g.arr("int", "OB", H->out_bits, H->n_out);
   o << "  auto tile_of = [&](uint64_t t) {\n    uint64_t r = 0;\n#pragma unroll\n    for (int j = 0; j < "
     << H->n_out << "; j++) r |= ((t >> j) & 1ull) << OB[j];\n    return r;\n  };\n";
-  if (persist) {
-    // L2 prefetch of the CTA's next tile: one request per 128-byte line (lanes / registers whose
-    // memory bits below G are zero), through the map the tile is read with
-    const SvMap& m0 = first ? H->din : H->load;
-    const int G = dbl ? 3 : 4;
-    uint32_t lead_mask = 0;
-    int rskip = 0;
-    for (int j = 0; j < g.ntl; j++)
-      if (m0.tmb[j] < G) lead_mask |= 1u << j;
-    for (int s2 = 0; s2 < SV_R_BITS; s2++)
-      if (m0.rmb[s2] < G) rskip |= 1 << s2;
-    g.arr("int", "PTMB", m0.tmb, g.ntl);
-    long long ro[16];
-    for (int k = 0; k < 16; k++) {
-      ro[k] = 0;
-      for (int s2 = 0; s2 < SV_R_BITS; s2++)
-        if ((k >> s2) & 1) ro[k] |= 1ll << m0.rmb[s2];
-    }
-    g.arr("long long", "PRO", ro, 16);
-    o << "  const bool lead = (tid & " << lead_mask << ") == 0;\n"
-      << "  uint64_t pb = 0;\n#pragma unroll\n  for (int j = 0; j < " << g.ntl
-      << "; j++) pb |= (uint64_t)((tid >> j) & 1) << PTMB[j];\n"
-      << "  constexpr unsigned long long NTILES = 1ull << " << H->n_out << ";\n"
-      << "#pragma unroll 1\n"
-      << "  for (uint64_t bid = blockIdx.x; bid < NTILES; bid += gridDim.x) {\n"
-      << "  const uint64_t tile_off = tile_of(bid);\n"
-      << "  if (lead && bid + gridDim.x < NTILES) {\n"
-      << "    const V* q = psi + (tile_of(bid + gridDim.x) | pb);\n#pragma unroll\n"
-      << "    for (int k = 0; k < 16; k++)\n"
-      << "      if (!(k & " << rskip << ")) asm volatile(\"prefetch.global.L2 [%0];\" ::\"l\"(q + PRO[k]));\n"
-      << "  }\n";
-  } else {
-    o << "  {\n  const uint64_t tile_off = tile_of(expand_tile(blockIdx.x, split_a, split_b));\n";
-  }
+  o << "  const uint64_t tile_off = tile_of(expand_tile(blockIdx.x, split_a, split_b));\n";
   if (H->n_sets > 0) {
     o << "  for (int f = tid; f < " << 5 * H->n_sets << "; f += " << nt << ") {\n"
       << "    const int d = c_prog[kH_SETS + f / 5], i = f % 5;\n"
@@ -359,126 +267,7 @@ std::string gen_source(const int* p, const Launch& L, bool dbl, bool virt = fals
     g.stg();
     o << "  }\n";
   }
-  if (persist) o << "  __syncthreads();  // the next tile reuses shared memory\n";
-  o << "  }\n}\n";
-  (void)L;
-  return o.str();
-}
-
-// Persistent CTA, two warp groups of 2^(T-4) threads, three tile buffers.  The CTA's tiles
-// j = 0, 1, 2, ... (tile blockIdx.x + j * gridDim.x) alternate between the groups and tile j
-// lives in buffer j % 3.  Buffer (j + 2) % 3 is released when the other group finishes tile
-// j - 1 (done[] in shared memory), and the group computing tile j then issues the cp.async
-// loads of its next tile j + 2 there: at the first phase boundary that sees the release, or at
-// the end of tile j.  Phase barriers are named barriers of the group, so the two groups drift
-// freely and one group's loads / shared-memory traffic overlap the other's arithmetic.
-std::string gen_source_pipelined(const int* p, const Launch& L, bool dbl) {
-  (void)L;
-  const SvSecHeader* H = reinterpret_cast<const SvSecHeader*>(p);
-  Gen g;
-  g.T = H->T;
-  g.ntl = H->T - SV_R_BITS;
-  const int nt = 1 << g.ntl;
-  const bool last = H->flags & SV_FLAG_LAST_DIRECT;
-  const int nph = H->n_phases;
-  auto& o = g.o;
-  o << "#include \"section_dev.cuh\"\nusing namespace sv;\ntypedef " << (dbl ? "double2" : "float2") << " V;\n";
-  o << "constexpr int NTG = " << nt << ", TILE = " << (1 << H->T) << ";\n";
-  o << "extern \"C\" __global__ void __launch_bounds__(" << 2 * nt << ", " << std::max(1, 512 / (2 * nt))
-    << ") sv_sec(V* __restrict__ psi, V* __restrict__ psi_hi, const V* __restrict__ aux, int split_a, int split_b, "
-    << "long long vidx, "
-    << coef_param_decl_impl(L, dbl) << ") {\n";
-  o << "  extern __shared__ __align__(128) unsigned char smem_raw[];\n"
-    << "  V* const bufs = reinterpret_cast<V*>(smem_raw);\n"
-    << "  V* const ctaf_all = bufs + 3 * TILE;\n"
-    << "  int* const done = reinterpret_cast<int*>(ctaf_all + " << kPipeSetsBytes << ");\n"
-    << "  const int grp = threadIdx.x / NTG, tid = threadIdx.x % NTG, bar = 1 + grp;\n"
-    << "  V* const ctaf = ctaf_all + grp * " << 5 * SV_MAX_SETS << ";\n"
-    << "  (void)ctaf; (void)aux; (void)vidx; (void)psi_hi;\n"
-    << "  constexpr unsigned long long NTILES = 1ull << " << H->n_out << ";\n";
-  g.arr("int", "OB", H->out_bits, H->n_out);
-  o << "  auto tile_of = [&](uint64_t t) {\n    uint64_t r = 0;\n#pragma unroll\n    for (int j = 0; j < "
-    << H->n_out << "; j++) r |= ((t >> j) & 1ull) << OB[j];\n    return r;\n  };\n"
-    << "  auto blk_of = [&](long long j) { return (uint64_t)blockIdx.x + (uint64_t)j * gridDim.x; };\n";
-  {  // load map: thread part of the HBM offset and of the swizzled smem offset (tile-invariant)
-    long long ro[16];
-    int w[16];
-    for (int k = 0; k < 16; k++) {
-      ro[k] = 0;
-      w[k] = 0;
-      for (int s = 0; s < SV_R_BITS; s++)
-        if ((k >> s) & 1) {
-          ro[k] |= 1ll << H->load.rmb[s];
-          w[k] ^= H->load.rw[s];
-        }
-    }
-    g.arr("int", "LTMB", H->load.tmb, g.ntl);
-    g.arr("int", "LTW", H->load.tw, g.ntl);
-    g.arr("long long", "LRO", ro, 16);
-    g.arr("int", "LW", w, 16);
-  }
-  o << "  uint64_t lb = 0;\n  int lx = 0;\n#pragma unroll\n  for (int j = 0; j < " << g.ntl
-    << "; j++) {\n    lb |= (uint64_t)((tid >> j) & 1) << LTMB[j];\n    lx ^= ((tid >> j) & 1) ? LTW[j] : 0;\n  }\n";
-  o << "  auto issue = [&](long long j) {\n    V* dst = bufs + (int)(j % 3) * TILE;\n"
-    << "    const V* src = psi + (tile_of(blk_of(j)) | lb);\n#pragma unroll\n"
-    << "    for (int k = 0; k < 16; k++) cp_async_v(dst + (lx ^ LW[k]), src + LRO[k]);\n    cp_async_commit();\n  };\n";
-  o << "  if (threadIdx.x < 3) done[threadIdx.x] = (int)threadIdx.x - 3;  // tile -3 + b 'finished' in buffer b\n"
-    << "  __syncthreads();\n"
-    << "  long long j = grp;\n  if (blk_of(j) < NTILES) issue(j);\n"
-    << "#pragma unroll 1\n"  // keep the tile body single: unrolling it doubles compile time and code
-    << "  for (; blk_of(j) < NTILES; j += 2) {\n"
-    << "    V* const sm = bufs + (int)(j % 3) * TILE;\n"
-    << "    const bool want = blk_of(j + 2) < NTILES;\n"
-    << "    int* const nxt_done = done + (int)((j + 2) % 3);\n"
-    << "    bool issued = false;\n"
-    << "    const uint64_t tile_off = tile_of(blk_of(j));\n";
-  if (H->n_sets > 0) {
-    o << "    for (int f = tid; f < " << 5 * H->n_sets << "; f += NTG) {\n"
-      << "      const int d = c_prog[kH_SETS + f / 5], i = f % 5;\n"
-      << "      ctaf[f] = cta_factor<V>(c_prog[d + 2 + i], c_prog[d + 3 + i], tile_off, P);\n    }\n";
-  }
-  o << "    cp_async_wait<0>();\n    group_sync<NTG>(bar);\n    V v[16];\n";
-  const SvPhase* ph = reinterpret_cast<const SvPhase*>(p + H->phase_off);
-  const SvOp* ops = reinterpret_cast<const SvOp*>(p + H->op_off);
-  for (int k = 0; k < nph; k++) {
-    const bool dout = last && k == nph - 1;
-    o << "  {  // phase " << k << "\n";
-    g.smem(ph[k].tw, ph[k].rw);
-    g.lds();
-    for (int i = 0; i < ph[k].op_count; i++) {
-      const SvOp& op = ops[ph[k].op_begin + i];
-      if (!g.diagset_c(p, op, "NTG"))
-        o << "    op_c<" << op.type << ", " << op.a << ", " << op.b << ", " << op.coef << ", " << op.extra
-          << ">(v, tid, NTG, tile_off, aux, ctaf, P);\n";
-    }
-    if (dout) {
-      o << "    {\n";
-      g.hbm(H->dout);
-      g.stg();
-      o << "    }\n";
-    } else {
-      g.sts();
-      o << "    if (want && !issued) {\n"
-        << "      if (group_sync_or<NTG>(bar, ld_volatile(nxt_done) >= j - 1)) {\n"
-        << "        issue(j + 2);\n        issued = true;\n      }\n"
-        << "    } else {\n      group_sync<NTG>(bar);\n    }\n";
-    }
-    o << "  }\n";
-  }
-  if (!last) {
-    o << "  {  // gather in store order, lanes walk the lowest store memory bits\n";
-    g.smem(H->store.tw, H->store.rw);
-    g.lds();
-    g.hbm(H->store);
-    g.stg();
-    o << "  }\n";
-  }
-  o << "    group_sync<NTG>(bar);  // every read of this buffer is done: release it\n"
-    << "    if (tid == 0) st_release(done + (int)(j % 3), (int)j);\n"
-    << "    if (want && !issued) {\n"
-    << "      while (ld_volatile(nxt_done) < j - 1) {\n      }\n"
-    << "      issue(j + 2);\n    }\n"
-    << "  }\n}\n";
+  o << "}\n";
   return o.str();
 }
 
@@ -487,11 +276,6 @@ struct Entry {
   std::atomic<int> state{0};  // 0 pending, 1 ready, 2 failed
   cudaLibrary_t lib = nullptr;
   cudaKernel_t kern = nullptr;
-  void* c_prog = nullptr;
-  size_t c_prog_bytes = 0;
-  void* c_coef = nullptr;
-  size_t c_coef_bytes = 0;
-  uint64_t occ = 0;  // resident CTAs on the device (pipelined variant's grid)
   std::string err;
 };
 
@@ -506,9 +290,12 @@ std::mutex g_mu;
 std::unordered_map<std::string, std::shared_ptr<Entry>> g_cache;
 JitCounters g_ctr;
 
-// NVRTC: source -> sm_100a cubin (+ the lowered names of the __constant__ arrays)
-bool compile_cubin(const std::string& src, bool dbl, std::vector<char>& cubin, std::string& name_prog,
-                   std::string& name_coef, std::string& err) {
+const char* const kNvrtcOpts[] = {"-arch=sm_100a", "-std=c++17", "-lineinfo", "-DSV_JIT_KERNEL=1"};
+constexpr int kNvrtcNopts = 4;
+constexpr const char* kAbiTag = "sv_sec/abi-3";  // bump when the generated kernel's parameters change
+
+// NVRTC: source -> sm_100a cubin
+bool compile_cubin(const std::string& src, std::vector<char>& cubin, std::string& err) {
   Nvrtc& N = nvrtc();
   if (!N.ok) {
     err = "NVRTC (libnvrtc.so.12) not found";
@@ -520,12 +307,7 @@ bool compile_cubin(const std::string& src, bool dbl, std::vector<char>& cubin, s
     err = "nvrtcCreateProgram failed";
     return false;
   }
-  const char* sym_prog = "&sv::c_prog";
-  const char* sym_coef = dbl ? "&sv::c_coef64" : "&sv::c_coef32";
-  N.add_name(prog, sym_prog);
-  N.add_name(prog, sym_coef);
-  const char* opts[] = {"-arch=sm_100a", "-std=c++17", "-lineinfo", "-DSV_JIT_KERNEL=1"};
-  const nvrtcResult rc = N.compile(prog, 4, opts);
+  const nvrtcResult rc = N.compile(prog, kNvrtcNopts, kNvrtcOpts);
   if (rc != NVRTC_SUCCESS) {
     size_t n = 0;
     N.log_size(prog, &n);
@@ -539,17 +321,15 @@ bool compile_cubin(const std::string& src, bool dbl, std::vector<char>& cubin, s
   N.cubin_size(prog, &nc);
   cubin.resize(nc);
   N.cubin(prog, cubin.data());
-  const char* lp = nullptr;
-  const char* lc = nullptr;
-  if (N.lowered(prog, sym_prog, &lp) == NVRTC_SUCCESS && lp) name_prog = lp;
-  if (N.lowered(prog, sym_coef, &lc) == NVRTC_SUCCESS && lc) name_coef = lc;
   N.destroy(&prog);
   return true;
 }
 
 // On-disk cubin cache (SV_JIT_CACHE=<dir>, default $HOME/.cache/sv_jit; "0" disables): a kernel
-// compiled once is reused by later processes.  Key: FNV-1a of the source, the embedded headers
-// and the NVRTC options; file: [u32 len][name_prog][u32 len][name_coef][cubin].
+// compiled once is reused by later processes.  The key is a 128-bit hash (two FNV-1a streams) of
+// everything that determines the cubin: the generated source, the embedded headers, the NVRTC
+// options and version, the precision and an ABI tag.  The file stores the key again and the
+// source length, both checked on load, so a foreign or stale file is recompiled, never launched.
 std::string cache_dir() {
   static const std::string d = [] {
     const char* e = std::getenv("SV_JIT_CACHE");
@@ -559,56 +339,67 @@ std::string cache_dir() {
   }();
   return d;
 }
-std::string cache_path(const std::string& src, bool dbl) {
+struct CacheKey {
+  uint64_t h1 = 1469598103934665603ull, h2 = 0x84222325cbf29ce4ull;
+  void mix(const void* data, size_t n) {
+    const unsigned char* p = static_cast<const unsigned char*>(data);
+    for (size_t i = 0; i < n; i++) {
+      h1 = (h1 ^ p[i]) * 1099511628211ull;
+      h2 = (h2 ^ p[i]) * 0x100000001b3ull + 0x9E3779B97F4A7C15ull;
+    }
+  }
+  void mix(const char* z) { mix(z, std::strlen(z) + 1); }
+};
+CacheKey cache_key(const std::string& src, bool dbl) {
+  CacheKey k;
+  k.mix(src.data(), src.size());
+  for (int i = 0; i < kJitHeaderCount; i++) k.mix(kJitHeaderTexts[i]);
+  for (int i = 0; i < kNvrtcNopts; i++) k.mix(kNvrtcOpts[i]);
+  k.mix(kAbiTag);
+  k.mix(dbl ? "fp64" : "fp32");
+  int ver[2] = {0, 0};
+  typedef nvrtcResult (*VerFn)(int*, int*);
+  static VerFn vf = [] {
+    void* h = dlopen("libnvrtc.so.12", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("/usr/local/cuda/lib64/libnvrtc.so.12", RTLD_NOW | RTLD_NOLOAD);
+    return h ? reinterpret_cast<VerFn>(dlsym(h, "nvrtcVersion")) : nullptr;
+  }();
+  if (vf) vf(&ver[0], &ver[1]);
+  k.mix(ver, sizeof(ver));
+  return k;
+}
+std::string cache_path(const CacheKey& k) {
   const std::string dir = cache_dir();
   if (dir.empty()) return {};
-  uint64_t h = 1469598103934665603ull;
-  auto mix = [&](const char* p, size_t n) {
-    for (size_t i = 0; i < n; i++) h = (h ^ (unsigned char)p[i]) * 1099511628211ull;
-  };
-  mix(src.data(), src.size());
-  for (int i = 0; i < kJitHeaderCount; i++) mix(kJitHeaderTexts[i], std::strlen(kJitHeaderTexts[i]));
-  const char* tag = dbl ? "sm_100a/fp64/v1" : "sm_100a/fp32/v1";
-  mix(tag, std::strlen(tag));
-  char name[40];
-  std::snprintf(name, sizeof(name), "/sv_%016llx.bin", (unsigned long long)h);
+  char name[64];
+  std::snprintf(name, sizeof(name), "/sv_%016llx%016llx.bin", (unsigned long long)k.h1, (unsigned long long)k.h2);
   return dir + name;
 }
-bool cache_load(const std::string& path, std::vector<char>& cubin, std::string& np, std::string& nc) {
+// file: [u64 h1][u64 h2][u64 source length][cubin]
+bool cache_load(const std::string& path, const CacheKey& k, size_t src_len, std::vector<char>& cubin) {
   if (path.empty()) return false;
   std::ifstream f(path, std::ios::binary);
   if (!f) return false;
   std::vector<char> all((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
-  size_t at = 0;
-  auto str = [&](std::string& out) {
-    uint32_t n = 0;
-    if (at + 4 > all.size()) return false;
-    std::memcpy(&n, all.data() + at, 4);
-    at += 4;
-    if (at + n > all.size()) return false;
-    out.assign(all.data() + at, n);
-    at += n;
-    return true;
-  };
-  if (!str(np) || !str(nc) || at >= all.size()) return false;
-  cubin.assign(all.begin() + (long)at, all.end());
+  if (all.size() <= 24) return false;
+  uint64_t hdr[3];
+  std::memcpy(hdr, all.data(), 24);
+  if (hdr[0] != k.h1 || hdr[1] != k.h2 || hdr[2] != (uint64_t)src_len) return false;
+  cubin.assign(all.begin() + 24, all.end());
   return true;
 }
-void cache_store(const std::string& path, const std::vector<char>& cubin, const std::string& np,
-                 const std::string& nc) {
+void cache_store(const std::string& path, const CacheKey& k, size_t src_len, const std::vector<char>& cubin) {
   if (path.empty()) return;
   const std::string dir = cache_dir();
   for (size_t at = 1; at <= dir.size(); at++)  // mkdir -p
     if (at == dir.size() || dir[at] == '/') ::mkdir(dir.substr(0, at).c_str(), 0755);
-  const std::string tmp = path + ".tmp" + std::to_string((long long)::getpid());
+  const std::string tmp = path + ".tmp" + std::to_string((long long)::getpid()) + "_" +
+                          std::to_string((unsigned long long)std::hash<std::thread::id>()(std::this_thread::get_id()));
   {
     std::ofstream f(tmp, std::ios::binary);
     if (!f) return;
-    const uint32_t a = (uint32_t)np.size(), b = (uint32_t)nc.size();
-    f.write(reinterpret_cast<const char*>(&a), 4);
-    f.write(np.data(), a);
-    f.write(reinterpret_cast<const char*>(&b), 4);
-    f.write(nc.data(), b);
+    const uint64_t hdr[3] = {k.h1, k.h2, (uint64_t)src_len};
+    f.write(reinterpret_cast<const char*>(hdr), 24);
     f.write(cubin.data(), (std::streamsize)cubin.size());
     if (!f) return;
   }
@@ -618,10 +409,10 @@ void cache_store(const std::string& path, const std::vector<char>& cubin, const 
 void build_entry(Entry& e, const std::string& src, int dev, bool dbl) {
   const auto t0 = std::chrono::steady_clock::now();
   std::vector<char> cubin;
-  std::string name_prog, name_coef;
-  const std::string cpath = cache_path(src, dbl);
-  const bool hit = cache_load(cpath, cubin, name_prog, name_coef);
-  if (!hit && compile_cubin(src, dbl, cubin, name_prog, name_coef, e.err)) cache_store(cpath, cubin, name_prog, name_coef);
+  const CacheKey key = cache_key(src, dbl);
+  const std::string cpath = cache_path(key);
+  const bool hit = cache_load(cpath, key, src.size(), cubin);
+  if (!hit && compile_cubin(src, cubin, e.err)) cache_store(cpath, key, src.size(), cubin);
   if (!hit && cubin.empty()) {
     static std::once_flag once;
     std::call_once(once, [&] { std::fprintf(stderr, "[sv] JIT disabled for this kernel: %s\n", e.err.c_str()); });
@@ -634,8 +425,8 @@ void build_entry(Entry& e, const std::string& src, int dev, bool dbl) {
     cudaGetLastError();
     std::remove(cpath.c_str());
     cubin.clear();
-    if (compile_cubin(src, dbl, cubin, name_prog, name_coef, e.err)) {
-      cache_store(cpath, cubin, name_prog, name_coef);
+    if (compile_cubin(src, cubin, e.err)) {
+      cache_store(cpath, key, src.size(), cubin);
       ce = cudaLibraryLoadData(&e.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
     }
   }
@@ -646,12 +437,6 @@ void build_entry(Entry& e, const std::string& src, int dev, bool dbl) {
     e.state = 2;
     return;
   }
-  if (!name_prog.empty() && cudaLibraryGetGlobal(&e.c_prog, &e.c_prog_bytes, e.lib, name_prog.c_str()) != cudaSuccess)
-    e.c_prog = nullptr;
-  if (!name_coef.empty() && cudaLibraryGetGlobal(&e.c_coef, &e.c_coef_bytes, e.lib, name_coef.c_str()) != cudaSuccess)
-    e.c_coef = nullptr;
-  cudaGetLastError();
-  const size_t amp = dbl ? 16 : 8;
   ce = cudaFuncSetAttribute(reinterpret_cast<const void*>(e.kern), cudaFuncAttributeMaxDynamicSharedMemorySize,
                             227 * 1024);  // the opt-in maximum; occupancy follows the launch size
   if (ce != cudaSuccess) {
@@ -723,6 +508,12 @@ Worker& worker() {
   return w;
 }
 
+// Mode sync: another thread (another rank of a local world, jit_prepare of another handle) may be
+// compiling this entry right now; wait for it instead of falling back to the interpreter.
+void wait_ready(const Entry& e) {
+  while (e.state.load() == 0) std::this_thread::sleep_for(std::chrono::microseconds(200));
+}
+
 }  // namespace
 
 std::string jit_source(const int* prog_host, const Launch& L, bool dbl) { return gen_source(prog_host, L, dbl); }
@@ -732,8 +523,8 @@ Status jit_compile_only(const int* prog_host, const Launch& L, bool dbl, const c
   const auto t0 = std::chrono::steady_clock::now();
   const std::string src = gen_source(prog_host, L, dbl);
   std::vector<char> cubin;
-  std::string np, nc, err;
-  const bool ok = compile_cubin(src, dbl, cubin, np, nc, err);
+  std::string err;
+  const bool ok = compile_cubin(src, cubin, err);
   *ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   if (dump_dir) {
     const std::string base = std::string(dump_dir) + "/section_" + std::to_string(index);
@@ -761,8 +552,8 @@ int jit_set_mode(int m) {
 }
 
 bool jit_virtual_input_ok(const Launch& L, bool dbl) {
-  return mode() == kSync && L.T >= SV_R_BITS && !pipelined(L, dbl) && !l2_prefetch(L, dbl) &&
-         !(L.flags & SV_FLAG_XRANK);
+  (void)dbl;
+  return mode() == kSync && L.T >= SV_R_BITS;
 }
 
 void jit_prepare(const Program& prog, bool dbl, bool virt_first) {
@@ -805,12 +596,11 @@ void jit_prepare(const Program& prog, bool dbl, bool virt_first) {
 }
 
 bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const double* coef_host, const Launch& L,
-                        const int* prog_dev, const void* coef_dev, const void* aux_dev, cudaStream_t st,
-                        cudaError_t* err, int split_a, int split_b, void* sv_hi, int64_t vidx) {
+                        const void* coef_dev, const void* aux_dev, cudaStream_t st, cudaError_t* err, int split_a,
+                        int split_b, int64_t vidx) {
   *err = cudaSuccess;
   const Mode m = mode();
   if (m == kOff || L.T < SV_R_BITS) return false;
-  if ((split_a || split_b) && (pipelined(L, dbl) || l2_prefetch(L, dbl))) return false;  // persistent variants
   int dev = 0;
   cudaGetDevice(&dev);
   const bool virt = vidx != -1;
@@ -834,6 +624,8 @@ bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const double* 
       build_entry(*e, gen_source(prog_host, L, dbl, virt), dev, dbl);
     else
       worker().push(Job{e, gen_source(prog_host, L, dbl, virt), dev, dbl});
+  } else if (m == kSync) {
+    wait_ready(*e);
   }
   if (e->state.load() != 1) {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -841,25 +633,16 @@ bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const double* 
     return false;
   }
   const size_t amp = dbl ? 16 : 8;
-  if (e->c_prog) {
-    if (L.int_count * sizeof(int) > e->c_prog_bytes) return false;
-    *err = cudaMemcpyAsync(e->c_prog, prog_dev, L.int_count * sizeof(int), cudaMemcpyDeviceToDevice, st);
-    if (*err != cudaSuccess) return true;
-  }
-  if (e->c_coef && L.coef_count && !coef_in_param(L, dbl)) {
-    if (L.coef_count * amp > e->c_coef_bytes) return false;
-    *err = cudaMemcpyAsync(e->c_coef, coef_dev, L.coef_count * amp, cudaMemcpyDeviceToDevice, st);
-    if (*err != cudaSuccess) return true;
-  }
   void* a0 = sv;
-  void* a0h = sv_hi ? sv_hi : sv;
   void* a1 = const_cast<void*>(aux_dev);
   int a2 = split_a, a3 = split_b;
-  // the coefficient parameter: the section's coefficients (fp64 on the host) in the state's precision
+  long long av = (long long)vidx;
+  // the coefficient parameter: the section's coefficients (fp64 on the host) in the state's precision,
+  // or a pointer to the handle's device copy (already in the state's precision)
   thread_local std::vector<char> pbuf;
   const size_t nc = L.coef_count ? L.coef_count : 1;
-  char empty_bank = 0;
-  void* a4 = &empty_bank;  // CoefBank<V>: an empty struct parameter
+  const void* coef_ptr = coef_dev;
+  void* a4 = &coef_ptr;
   if (coef_in_param(L, dbl)) {
     pbuf.assign(nc * amp, 0);
     if (dbl) {
@@ -870,25 +653,10 @@ bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const double* 
     }
     a4 = pbuf.data();
   }
-  long long av = (long long)vidx;
-  void* args[] = {&a0, &a0h, &a1, &a2, &a3, &av, a4};
-  const unsigned threads = (pipelined(L, dbl) ? 2u : 1u) << (L.T - SV_R_BITS);
-  unsigned grid = (unsigned)(1ull << (L.n_out - (split_a ? 1 : 0) - (split_b ? 1 : 0)));
-  if (pipelined(L, dbl) || l2_prefetch(L, dbl)) {  // persistent: one wave of resident CTAs
-    if (e->occ == 0) {
-      int sms = 0, nb = 0;
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, reinterpret_cast<const void*>(e->kern), (int)threads,
-                                                        smem_bytes(L, dbl)) != cudaSuccess || nb < 1)
-        nb = 1;
-      cudaGetLastError();
-      e->occ = (uint64_t)nb * (uint64_t)sms;
-    }
-    const uint64_t pairs = pipelined(L, dbl) ? ((1ull << L.n_out) + 1) / 2 : (1ull << L.n_out);  // two groups per CTA
-    grid = (unsigned)std::min<uint64_t>(e->occ, std::max<uint64_t>(1, pairs));
-  }
-  *err = cudaLaunchKernel(reinterpret_cast<const void*>(e->kern), dim3(grid), dim3(threads), args,
-                          smem_bytes(L, dbl), st);
+  void* args[] = {&a0, &a1, &a2, &a3, &av, a4};
+  const unsigned threads = 1u << (L.T - SV_R_BITS);
+  const unsigned grid = (unsigned)(1ull << (L.n_out - (split_a ? 1 : 0) - (split_b ? 1 : 0)));
+  *err = cudaLaunchKernel(reinterpret_cast<const void*>(e->kern), dim3(grid), dim3(threads), args, smem_bytes(L, dbl), st);
   {
     std::lock_guard<std::mutex> lk(g_mu);
     g_ctr.hits++;

@@ -3,10 +3,10 @@
 // The interpreter kernel (section.cu) walks a section's program from __constant__ memory; every
 // op pays a dispatch and the register file is reshuffled at each dispatch merge point.  Here the
 // same program (compile.cpp, already checked by the emulator and the parity tests) is printed as
-// straight-line CUDA — slots, maps and coefficient offsets become immediates — and compiled
-// for sm_100a with NVRTC.  Kernels are cached by the program's structure (its ints; coefficient
-// values stay run-time data in __constant__ memory), so a circuit with the same shape reuses
-// them.  Mode (environment SV_JIT):
+// straight-line CUDA — slots, maps and coefficient offsets become immediates, the program's ints
+// are baked into the module's constant bank — and compiled for sm_100a with NVRTC.  Kernels are
+// cached by the program's structure (its ints; coefficient values stay run-time data, passed as
+// a kernel parameter), so a circuit with the same shape reuses them.  Mode (environment SV_JIT):
 //   "sync"  (default) compile on first use, then launch the generated kernel;
 //   "async" launch the interpreter while a background thread compiles;
 //   "0"     interpreter only.
@@ -34,14 +34,13 @@ struct JitCounters {
 // interpreter instead (mode, compile pending or NVRTC unavailable); *err is the launch status.
 // split_a / split_b: restrict the launch to half / a quarter of the tiles (kernels.cuh launch_section).
 // coef_host: the launch's coefficients (fp64 complex) on the host, passed as a kernel parameter.
+// coef_dev: the same coefficients on the device in the state's precision (used when they exceed
+// the kernel-parameter space).
 bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const double* coef_host, const Launch& L,
-                        const int* prog_dev, const void* coef_dev, const void* aux_dev, cudaStream_t st,
-                        cudaError_t* err, int split_a = 0, int split_b = 0, void* sv_hi = nullptr,
-                        int64_t vidx = -1);
+                        const void* coef_dev, const void* aux_dev, cudaStream_t st, cudaError_t* err,
+                        int split_a = 0, int split_b = 0, int64_t vidx = -1);
 // vidx != -1: the launch does not read the state; its input is the basis state whose single
 // amplitude (1) sits at shard offset vidx (-2: on another GPU, all zeros here).
-// sv_hi: for a fused exchange (SV_FLAG_XRANK) sv / sv_hi are the shards whose exchanged rank bit
-// is 0 / 1 (one of them this GPU's, the other its partner's, mapped over NVLink).
 
 // Make sure every launch of the program has its kernel: mode sync compiles the missing ones in
 // parallel now, mode async queues them.

@@ -12,6 +12,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <utility>
 
 #include "cplx.cuh"
 #include "kernels.cuh"
@@ -338,6 +339,27 @@ __global__ void k_exchange_peer(V* __restrict__ local, V* __restrict__ remote, u
   }
 }
 
+// Pack / unpack for the NCCL send/recv exchange: element j of a block (compact index over the
+// local bits that are not exchanged) lives at the index with the exchanged bits inserted
+// (values fixed per block); consecutive j are consecutive amplitudes below the lowest m-bit.
+struct InsDev {
+  int nins;
+  int pos[11];  // ascending
+  int val[11];
+};
+template <typename V, bool PACK>
+__global__ void k_pack_bits(V* __restrict__ sv, V* __restrict__ stage, uint64_t first, uint64_t count, InsDev e) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += stride) {
+    uint64_t x = first + i;
+    for (int k = 0; k < e.nins; k++) x = insert_bit(x, e.pos[k], e.val[k]);
+    if (PACK)
+      stage[i] = sv[x];
+    else
+      sv[x] = stage[i];
+  }
+}
+
 // ------------------------------------------------------------------ host helpers
 inline unsigned grid_for(uint64_t work, int threads) {
   uint64_t b = (work + threads - 1) / threads;
@@ -493,11 +515,16 @@ cudaError_t launch_sample_resolve(bool dbl, const void* sv, int B, const int64_t
                                   const double* resid, uint64_t* out_off, cudaStream_t st) {
   if (n_items == 0) return cudaSuccess;
   const size_t smem = sizeof(double) << B;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_sample_resolve<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-    cudaFuncSetAttribute(k_sample_resolve<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-    attr = true;
+  static bool attr[64] = {};  // cudaFuncSetAttribute applies to the current device only
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  if (!attr[dev]) {
+    if ((e = cudaFuncSetAttribute(k_sample_resolve<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024)) != cudaSuccess ||
+        (e = cudaFuncSetAttribute(k_sample_resolve<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024)) != cudaSuccess)
+      return e;
+    attr[dev] = true;
   }
   if (dbl)
     k_sample_resolve<double2><<<n_items, 256, smem, st>>>((const double2*)sv, B, items, resid, out_off);
@@ -565,8 +592,33 @@ cudaError_t launch_exchange_peer(bool dbl, void* local, void* const* peer_bases,
   return cudaSuccess;
 }
 
-cudaError_t launch_copy(bool dbl, void* dst, const void* src, size_t count, cudaStream_t st) {
-  return cudaMemcpyAsync(dst, src, count * (dbl ? 16 : 8), cudaMemcpyDeviceToDevice, st);
+cudaError_t launch_pack_bits(bool dbl, bool pack, void* sv, void* stage, uint64_t first, uint64_t count, int nins,
+                             const int* pos, const int* val, cudaStream_t st) {
+  if (nins > 11) return cudaErrorInvalidValue;
+  InsDev e{};
+  e.nins = nins;
+  for (int i = 0; i < nins; i++) {  // ascending positions (insert_bit order)
+    e.pos[i] = pos[i];
+    e.val[i] = val[i];
+  }
+  for (int i = 1; i < nins; i++)
+    for (int j = i; j > 0 && e.pos[j] < e.pos[j - 1]; j--) {
+      std::swap(e.pos[j], e.pos[j - 1]);
+      std::swap(e.val[j], e.val[j - 1]);
+    }
+  const unsigned g = grid_for(count, 256);
+  if (dbl) {
+    if (pack)
+      k_pack_bits<double2, true><<<g, 256, 0, st>>>((double2*)sv, (double2*)stage, first, count, e);
+    else
+      k_pack_bits<double2, false><<<g, 256, 0, st>>>((double2*)sv, (double2*)stage, first, count, e);
+  } else {
+    if (pack)
+      k_pack_bits<float2, true><<<g, 256, 0, st>>>((float2*)sv, (float2*)stage, first, count, e);
+    else
+      k_pack_bits<float2, false><<<g, 256, 0, st>>>((float2*)sv, (float2*)stage, first, count, e);
+  }
+  return cudaGetLastError();
 }
 
 }  // namespace sv

@@ -59,7 +59,9 @@ struct ExchangeArgs {
 cudaError_t launch_exchange_peer(bool dbl, void* local, void* const* peer_bases /*host array [world]*/, int rank,
                                  int nL, const ExchangeArgs& a, cudaStream_t st, int* launches,
                                  unsigned max_blocks = 0);
-// staging -> shard copy of `count` amplitudes at element offsets (for the NCCL exchange path)
-cudaError_t launch_copy(bool dbl, void* dst, const void* src, size_t count, cudaStream_t st);
+// NCCL exchange path: pack (stage[i] = sv[x_i]) or unpack (sv[x_i] = stage[i]) elements
+// first .. first + count - 1 of a block, x_i = (first + i) with bit val[k] inserted at pos[k].
+cudaError_t launch_pack_bits(bool dbl, bool pack, void* sv, void* stage, uint64_t first, uint64_t count, int nins,
+                             const int* pos, const int* val, cudaStream_t st);
 
 }  // namespace sv

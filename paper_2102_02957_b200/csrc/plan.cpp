@@ -109,7 +109,7 @@ struct Planner {
             }
         }
       }
-      const int nlow = std::min(std::max(L.low_bits, L.min_victim), nL);
+      const int nlow = std::min(L.low_bits, nL);
       uint64_t taken = need;
       for (int b : rank_bits) {
         int m = -1;
@@ -427,15 +427,12 @@ Status plan_two_level(const sv_gate* g, size_t count, int n, int c, int world_lo
 }
 
 // Blocked plan: one-level, or — on several GPUs — the two-level plan when it moves fewer bytes
-// across GPUs (SV_TWO_LEVEL=0 disables it).
+// across GPUs.  (Either plan's exchanges may pick any local bit: both exchange transports handle
+// strided blocks — the peer kernel element-wise, the NCCL path by packing.)
 Status plan_blocked(const sv_gate* g, size_t count, int n, int c, int world_log2, std::vector<int>& pi,
                     std::vector<int>& sigma, uint32_t flags, std::vector<Step>& steps, PlanCounters& ctr,
                     const PlanLayout& layout, std::vector<int>* sigma_initial) {
-  static const bool two = [] {
-    const char* e = std::getenv("SV_TWO_LEVEL");
-    return !(e && e[0] == '0');
-  }();
-  if (!two || world_log2 == 0 || (flags & SV_RESTORE_ORDER))
+  if (world_log2 == 0 || (flags & SV_RESTORE_ORDER))
     return plan_one_level(g, count, n, c, world_log2, pi, sigma, flags, steps, ctr, layout, sigma_initial);
   std::vector<int> pi1 = pi, s1 = sigma, pi2 = pi, s2 = sigma, init1, init2;
   std::vector<Step> st1, st2;

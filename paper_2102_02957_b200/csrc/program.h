@@ -55,8 +55,6 @@
 
 #define SV_FLAG_FIRST_DIRECT 1        // first phase loads straight from HBM
 #define SV_FLAG_LAST_DIRECT 2         // last phase stores straight to HBM
-#define SV_FLAG_XRANK 4               // fused exchange: one tile position is a rank bit (memory bit
-                                      // >= nl): its loads / stores address the partner GPU's shard
 
 // A thread/register <-> tile mapping used at a tile boundary: smem offsets (swizzled) and the
 // HBM memory bit of every thread bit j and register slot s.

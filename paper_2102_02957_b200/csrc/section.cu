@@ -12,6 +12,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <mutex>
 
 #include "kernels.cuh"
 #include "section_dev.cuh"
@@ -101,8 +102,8 @@ __device__ __forceinline__ void run_op(V (&v)[16], int oi, int tid, uint64_t til
 }
 
 template <typename V, int G, int NT, int MINB, bool FIRST, bool LAST>
-__global__ void __launch_bounds__(NT, MINB) k_section(V* __restrict__ sv, const V* __restrict__ aux, int prefetch,
-                                                     int split_a, int split_b) {
+__global__ void __launch_bounds__(NT, MINB) k_section(V* __restrict__ sv, const V* __restrict__ aux, int split_a,
+                                                     int split_b) {
   using R = decltype(V().x);
   constexpr int RB = SV_R_BITS;  // the host guarantees T >= RB, so every phase has RB register slots
   constexpr int M0 = FIRST ? kH_DIN : kH_LOAD;  // the map the tile is read with
@@ -116,36 +117,13 @@ __global__ void __launch_bounds__(NT, MINB) k_section(V* __restrict__ sv, const 
   V* ctaf = reinterpret_cast<V*>(smem_raw + (sizeof(V) << T));
   const int n_sets = c_prog[kH_NSETS];
 
-  // L2 prefetch of the CTA's next tile (persistent grid): one request per 128-byte line, issued
-  // by the thread / registers whose memory bits below G are all zero (the line's first amplitude)
-  bool lead = prefetch != 0;
-  int rskip = 0;
-  for (int j = 0; j < nt_log; j++)
-    if (c_prog[M0 + kM_TMB + j] < G && ((tid >> j) & 1)) lead = false;
-#pragma unroll
-  for (int s = 0; s < RB; s++)
-    if (c_prog[M0 + kM_RMB + s] < G) rskip |= 1 << s;
-
-  // Persistent CTAs: tile blk, blk + gridDim.x, ... (the grid is sized to the resident capacity)
+  (void)M0;
+  (void)G;
+  // one tile per CTA (a grid-stride loop only if the launch ever exceeds the grid limit)
   for (uint64_t blk = blockIdx.x; blk < n_tiles; blk += gridDim.x) {
     uint64_t tile_off = 0;
     const uint64_t tb = expand_tile(blk, split_a, split_b);
     for (int j = 0; j < n_out; j++) tile_off |= ((tb >> j) & 1ull) << c_prog[kH_OUT + j];
-    if (lead && blk + gridDim.x < n_tiles) {
-      const uint64_t nb = expand_tile(blk + gridDim.x, split_a, split_b);
-      uint64_t noff = 0;
-      for (int j = 0; j < n_out; j++) noff |= ((nb >> j) & 1ull) << c_prog[kH_OUT + j];
-      const V* p = sv + hbm_base(M0, nt_log, tid, noff);
-#pragma unroll
-      for (int k = 0; k < 16; k++) {
-        if (k & rskip) continue;
-        int64_t o = 0;
-#pragma unroll
-        for (int s = 0; s < RB; s++)
-          if ((k >> s) & 1) o |= (int64_t)1 << c_prog[M0 + kM_RMB + s];
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(p + o));
-      }
-    }
 
     // per-CTA DIAGSET factors (out-of-tile terms), computed once per tile into smem
     if (n_sets > 0) {
@@ -208,45 +186,26 @@ __global__ void __launch_bounds__(NT, MINB) k_section(V* __restrict__ sv, const 
   }
 }
 
-// Knobs for measurements only: SV_PERSIST=1 runs a persistent grid (one CTA per resident slot,
-// measured slightly slower than one CTA per tile), SV_PREFETCH=0 then drops its L2 prefetch of
-// the next tile.
-inline bool env_on(const char* name) {
-  const char* e = std::getenv(name);
-  return !(e && e[0] == '0');
-}
-inline bool env_set(const char* name) {
-  const char* e = std::getenv(name);
-  return e && e[0] == '1';
-}
+constexpr int kMaxDev = 64;
 
 template <typename V, int G, int NT, int MINB, bool FIRST, bool LAST>
 cudaError_t launch_v(V* sv, const V* aux, int T, int n_out, size_t smem, cudaStream_t st, int split_a, int split_b) {
-  static bool attr_set = false;
-  static int sms = 0, occ_smem = -1, occ = 1;
-  static const bool persist = env_set("SV_PERSIST"), prefetch = env_on("SV_PREFETCH");
+  static bool attr_set[kMaxDev] = {};  // cudaFuncSetAttribute applies to the current device only
   auto kern = k_section<V, G, NT, MINB, FIRST, LAST>;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)((sizeof(V) << 13) + 5 * SV_MAX_SETS * sizeof(V)));
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
+  if (!attr_set[dev]) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)((sizeof(V) << 13) + 5 * SV_MAX_SETS * sizeof(V)));
     if (e != cudaSuccess) return e;
-    int dev = 0;
-    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
-    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-    attr_set = true;
+    attr_set[dev] = true;
   }
   const int threads = 1 << (T - SV_R_BITS);
-  if ((int)smem != occ_smem || threads != NT) {  // resident CTAs per SM for this shape
-    int nb = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem);
-    if (e != cudaSuccess) return e;
-    occ = nb > 0 ? nb : 1;
-    occ_smem = (int)smem;
-  }
   const uint64_t tiles = 1ull << (n_out - (split_a ? 1 : 0) - (split_b ? 1 : 0));
-  const uint64_t cap = (uint64_t)occ * (uint64_t)sms;
-  const unsigned grid = (unsigned)(persist && tiles > cap ? cap : tiles);
-  kern<<<grid, threads, smem, st>>>(sv, aux, prefetch && grid < tiles ? 1 : 0, split_a, split_b);
+  const unsigned grid = (unsigned)(tiles < 0x7fffffffull ? tiles : 0x7fffffffull);
+  kern<<<grid, threads, smem, st>>>(sv, aux, split_a, split_b);
   return cudaGetLastError();
 }
 
@@ -263,10 +222,39 @@ cudaError_t launch_t(V* sv, const V* aux, int T, int n_out, int flags, size_t sm
 
 }  // namespace
 
+namespace {
+cudaError_t launch_section_locked(bool dbl, void* sv, const int* prog_dev, size_t int_count, const void* coef_dev,
+                                  size_t coef_count, const void* aux_dev, int T, int n_out, int n_phases, int flags,
+                                  int n_sets, cudaStream_t st, int split_a, int split_b);
+}  // namespace
+
 cudaError_t launch_section(bool dbl, void* sv, const int* prog_dev, size_t int_count, const void* coef_dev,
                            size_t coef_count, const void* aux_dev, int T, int n_out, int n_phases, int flags,
                            int n_sets, cudaStream_t st, int split_a, int split_b) {
   if (int_count > SV_CONST_INTS) return cudaErrorInvalidValue;
+  // The interpreter's program and coefficients live in this module's __constant__ bank, one per
+  // device and shared by every handle.  Handles on different streams (several ranks of a local
+  // world, a host-tier handle beside a device handle) are serialised: each copy + launch waits for
+  // the previous user's launch (an event chain per device, under a process-wide lock).
+  static std::mutex mu;
+  static cudaEvent_t last[kMaxDev] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
+  if (!last[dev] && (e = cudaEventCreateWithFlags(&last[dev], cudaEventDisableTiming)) != cudaSuccess) return e;
+  if ((e = cudaStreamWaitEvent(st, last[dev], 0)) != cudaSuccess) return e;
+  e = launch_section_locked(dbl, sv, prog_dev, int_count, coef_dev, coef_count, aux_dev, T, n_out, n_phases, flags,
+                            n_sets, st, split_a, split_b);
+  if (e != cudaSuccess) return e;
+  return cudaEventRecord(last[dev], st);
+}
+
+namespace {
+cudaError_t launch_section_locked(bool dbl, void* sv, const int* prog_dev, size_t int_count, const void* coef_dev,
+                                  size_t coef_count, const void* aux_dev, int T, int n_out, int n_phases, int flags,
+                                  int n_sets, cudaStream_t st, int split_a, int split_b) {
   cudaError_t e = cudaMemcpyToSymbolAsync(c_prog, prog_dev, int_count * sizeof(int), 0, cudaMemcpyDeviceToDevice, st);
   if (e != cudaSuccess) return e;
   if (coef_count) {
@@ -294,5 +282,7 @@ cudaError_t launch_section(bool dbl, void* sv, const int* prog_dev, size_t int_c
   if (T == 13) return launch_t<float2, 4, 512, 1>((float2*)sv, (const float2*)aux_dev, T, n_out, flags, smem, st, split_a, split_b);
   return cudaErrorInvalidValue;
 }
+
+}  // namespace
 
 }  // namespace sv

@@ -17,12 +17,26 @@ typedef unsigned int uint32_t;
 
 namespace sv {
 
+// The section program.  A generated kernel (jit.cpp) bakes its own program into its module's
+// constant bank (SV_JIT_PROG: the program's ints, which are also the kernel's cache key), so no
+// copy precedes its launches and handles on different streams never share mutable constants; the
+// interpreter (section.cu) copies each section's program in before its launch.
+#ifdef SV_JIT_PROG
+__constant__ int c_prog[SV_CONST_INTS] = {SV_JIT_PROG};
+#else
 __constant__ int c_prog[SV_CONST_INTS];
 __constant__ double2 c_coef64[SV_CONST_COEF64];
 __constant__ float2 c_coef32[SV_CONST_COEF32];
+#endif
 
 namespace {
 
+// Coefficient accessors: the interpreter reads the section's coefficients from the __constant__
+// bank (CoefBank); the generated kernels get them as a __grid_constant__ kernel parameter
+// (CoefParam), so every FMA takes its matrix element straight from the parameter bank, or — for
+// the rare section whose coefficients exceed the 32 KiB parameter space — through a pointer to
+// the handle's device copy (CoefPtr, read-only cached loads).
+#ifndef SV_JIT_PROG
 template <typename V>
 __device__ __forceinline__ V cc(int i);
 template <>
@@ -33,18 +47,23 @@ template <>
 __device__ __forceinline__ float2 cc<float2>(int i) {
   return c_coef32[i];
 }
-
-// Coefficient accessors: the interpreter reads the section's coefficients from the __constant__
-// bank (CoefBank); the generated kernels get them as a __grid_constant__ kernel parameter
-// (CoefParam), so every FMA takes its matrix element straight from the parameter bank.
 template <typename V>
 struct CoefBank {
   __device__ __forceinline__ V operator()(int i) const { return cc<V>(i); }
 };
+#else
+template <typename V>
+struct CoefBank;  // generated kernels have no coefficient bank
+#endif
 template <typename V, int N>
 struct CoefParam {
   V c[N];
   __device__ __forceinline__ V operator()(int i) const { return c[i]; }
+};
+template <typename V>
+struct CoefPtr {
+  const V* p;
+  __device__ __forceinline__ V operator()(int i) const { return __ldg(p + i); }
 };
 
 // XOR-fold swizzle of a tile element index: the low G bits are XORed with every higher G-bit
@@ -336,42 +355,6 @@ __device__ __forceinline__ void hbm_store(const V (&v)[16], V* __restrict__ dst,
       if ((k >> s) & 1) o |= ro[s];
     dst[o] = v[k];
   }
-}
-
-// Asynchronous global -> shared copies (cp.async, sm_80+): the pipelined generated kernels
-// (jit.cpp) load the next tile while the current one is computed.
-template <typename V>
-__device__ __forceinline__ void cp_async_v(V* smem, const V* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  if constexpr (sizeof(V) == 16)
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-  else
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-// Named barrier over the NT threads of one warp group (id 1..15; 0 is __syncthreads)
-template <int NT>
-__device__ __forceinline__ void group_sync(int id) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(NT) : "memory");
-}
-// ... that also returns whether any thread of the group passed pred != 0
-template <int NT>
-__device__ __forceinline__ bool group_sync_or(int id, bool pred) {
-  int r;
-  asm volatile("{\n\t.reg .pred p, q;\n\tsetp.ne.s32 p, %1, 0;\n\tbar.red.or.pred q, %2, %3, p;\n\tselp.s32 %0, 1, 0, q;\n\t}"
-               : "=r"(r)
-               : "r"((int)pred), "r"(id), "n"(NT)
-               : "memory");
-  return r != 0;
-}
-__device__ __forceinline__ int ld_volatile(const int* p) { return *(const volatile int*)p; }
-__device__ __forceinline__ void st_release(int* p, int x) {
-  __threadfence_block();
-  *(volatile int*)p = x;
 }
 
 // Tile index of launch block b when the launch covers only the tiles whose out-bit indices

@@ -24,9 +24,7 @@ def _bits(x, b):
     return (x >> b) & 1
 
 
-def run_section(mem, prog, coefs, n_out, T, flags, aux=None, top=None):
-    """top: run only the tiles whose highest out bit equals top (a fused-exchange launch covers
-    half the tiles on each of the two GPUs; mem is then the full two-shard state)."""
+def run_section(mem, prog, coefs, n_out, T, flags, aux=None):
     nt = 1 << (T - 4)
     tids = np.arange(nt)
     first = bool(flags & 1) and bool(flags & 2)  # launch_t runs (first direct, last smem) as smem-only
@@ -55,8 +53,6 @@ def run_section(mem, prog, coefs, n_out, T, flags, aux=None, top=None):
         return idx
 
     for b in range(1 << n_out):
-        if top is not None and ((b >> (n_out - 1)) & 1) != top:
-            continue
         tile_off = 0
         for j, ob in enumerate(out_bits):
             tile_off |= ((b >> j) & 1) << int(ob)

@@ -113,48 +113,38 @@ def test_section_smem_maps_conflict_free(prec, G):
                 assert not bad, (n, c, bad)
 
 
-def test_fused_exchange_emulated():
-    # A one-bit cross-GPU exchange fused into the next section's load (SV_FUSE_EXCHANGE, what
-    # sv_apply_circuit does with peer access): the tile holds the exchanged local and rank bits,
-    # each GPU runs half of the tiles over both shards.  Two ranks emulated on the full state.
+def test_two_rank_programs_emulated():
+    # Two ranks' section programs (rank bits folded into constants per rank) run on their halves
+    # of the full memory-ordered state, with each cross-GPU exchange emulated as a swap of the
+    # local and rank memory bits (the plan's semantics): the result equals the oracle.
     from emulator import run_section, swap_bits
-    cases_fused = 0
+    exchanged = 0
     for n, c, circ in [(14, 6, C.quantum_volume(14, 6, 1)), (13, 5, C.qft(13)),
                        (12, 5, C.random_circuit(12, 160, 9, kinds=("u3", "su4", "cp", "d2", "swap")))]:
         g, nL = 1, n - 1
-        per = [sv.compile_circuit(circ, n, c, g, r, "fp64", sv.SV_FUSE_EXCHANGE) for r in (0, 1)]
+        per = [sv.compile_circuit(circ, n, c, g, r, "fp64") for r in (0, 1)]
         steps = [p[0] for p in per]
-        assert np.array_equal(steps[0][:, [0, 5, 6, 7, 10, 11]], steps[1][:, [0, 5, 6, 7, 10, 11]])
-        fused = 0
+        assert np.array_equal(steps[0][:, [0, 5, 6, 7]], steps[1][:, [0, 5, 6, 7]])
         rng = np.random.default_rng(n)
         psi = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
         psi /= np.linalg.norm(psi)
         mem = psi.copy()
         for i, st in enumerate(steps[0]):
             kind = int(st[0])
-            if kind == 0:
-                if int(st[4]) == 1:
-                    fused += 1
-                    continue
+            if kind in (0, 3):
                 swap_bits(mem, int(st[1]), int(st[2]))
-            elif kind == 3:
-                swap_bits(mem, int(st[1]), int(st[2]))
+                exchanged += kind == 0
             elif kind == 1:
                 for r in (0, 1):
                     sr = steps[r][i]
                     _, ints, coefs, aux, _, _ = per[r]
                     off, cnt, coff, ccnt, T, n_out, flags, aoff, acnt = (int(x) for x in sr[1:10])
-                    args = (ints[off:off + cnt], coefs[coff:coff + ccnt], n_out, T, flags, aux[aoff:aoff + acnt])
-                    if flags & 4:  # SV_FLAG_XRANK
-                        run_section(mem, *args, top=(r >> (int(sr[11]) - nL)) & 1)
-                    else:
-                        view = mem[r << nL:(r + 1) << nL]
-                        run_section(view, *args)
+                    run_section(mem[r << nL:(r + 1) << nL], ints[off:off + cnt], coefs[coff:coff + ccnt], n_out, T,
+                                flags, aux[aoff:aoff + acnt])
             else:
                 raise AssertionError(kind)
-        cases_fused += fused > 0
         pi, sigma = per[0][4], per[0][5]
         got = O.unpermute(mem, [int(sigma[int(p)]) for p in pi])
         ref = O.apply_circuit(circ, n, psi)
         assert np.max(np.abs(got - ref)) <= 1e-12, (n, c)
-    assert cases_fused >= 2
+    assert exchanged >= 2

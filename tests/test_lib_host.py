@@ -229,3 +229,15 @@ def test_two_level_exchange_volume_qv33():
             batches[int(r["pad"])] = batches.get(int(r["pad"]), 0) + 1
         vol = sum(1 - 2.0 ** -k for k in batches.values())
         assert vol <= most + 1e-9, (g, vol)
+
+
+def test_nccl_exchange_plan_is_the_default_plan():
+    # The NCCL send/recv exchange packs strided blocks into a staging buffer (kernels.cu
+    # k_pack_bits), so it takes the same plan as the peer-memory exchange — the two-level plan
+    # included — whatever local bits the exchanges pick (a victim restriction to the
+    # top bits used to be ignored by the two-level plan).  QFT34 on 2 GPUs exchanges low bits.
+    for n, g, circ in [(33, 2, C.quantum_volume(33, 10, 1)), (33, 3, C.quantum_volume(33, 10, 1)), (34, 1, C.qft(34))]:
+        a, pa, sa = sv.plan_circuit(circ, n, 9, g, flags=sv.SV_EXCHANGE_NCCL | sv.SV_FREE_LAYOUT)
+        b, pb, sb = sv.plan_circuit(circ, n, 9, g, flags=sv.SV_FREE_LAYOUT)
+        assert np.array_equal(a, b) and np.array_equal(pa, pb) and np.array_equal(sa, sb)
+        assert any(int(r["kind"]) == sv.SV_EXCHANGE for r in a)

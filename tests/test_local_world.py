@@ -1,0 +1,95 @@
+"""Multi-rank parity on ONE GPU: the in-process virtual world (sv_world_create / sv_create_local).
+
+G ranks, each a host thread with its own handle and shard on the same B200, run the multi-GPU path
+end to end — the two-level plan, the peer-memory swap kernel and the pipelined exchange + section,
+the NCCL-style send/recv exchange (as device copies), the unblocked per-gate exchanges, every
+collective readout — and rank 0's results are checked against the CPU oracle and against a
+one-GPU run (tests/mgpu_cases.py).  PAPER.md P:137-166 (data distribution, pipelined exchange),
+P:407-420 (chunk_swap across processes); SURVEY §8(a) a6, §8(f) NEXT-1..NEXT-3."""
+import os
+
+import numpy as np
+import pytest
+
+os.environ.setdefault("SV_COMM_TIMEOUT_S", "300")  # a failed rank thread must not hang the suite
+
+import circuits as C  # noqa: E402
+import mgpu_cases as M  # noqa: E402
+from conftest import gpu_available  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+sv = pytest.importorskip("paper_2102_02957_b200")
+
+_REF, _ONE = {}, {}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_gpu():
+    if not gpu_available():
+        pytest.skip("no CUDA device")
+    import torch
+    torch.cuda.set_device(0)
+
+
+def run_world(world, case):
+    name, recs, n, c, flags, basis, prec, second = case
+    with sv.LocalWorld(world) as w:
+        def body(r):
+            with sv.StateVector(n, c, prec, rank=r, local_world=w) as s:
+                return M.run_rank(s, case)
+        return w.run(body)
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("case", M.cases(), ids=[c[0] for c in M.cases()])
+def test_local_world_parity(world, case):
+    name = case[0]
+    if name not in _REF:
+        _REF[name] = M.reference(case)
+        _ONE[name] = M.single_gpu(sv, case)
+    res = run_world(world, case)
+    checks, err, d1 = M.check(case, res[0], _REF[name], _ONE[name], world)
+    bad = [k for k, ok in checks.items() if not ok]
+    assert not bad, (name, world, bad, err, d1, res[0]["stats"])
+    # every rank returned the same collective readouts
+    for r in range(1, world):
+        assert res[r]["state"] is None
+        assert res[r]["norm"] == res[0]["norm"]
+        assert np.array_equal(res[r]["probs"], res[0]["probs"])
+        assert np.array_equal(res[r]["amps"], res[0]["amps"])
+        assert np.array_equal(res[r]["shots"], res[0]["shots"])
+        assert res[r]["stats"]["exchanges"] == res[0]["stats"]["exchanges"]
+
+
+def test_local_world_two_level_volume():
+    # The two-level plan (NEXT-1) moves fewer bytes than the one-level plan and the exchange byte
+    # ledger matches the plan: bytes sent per rank = sum over batches of (1 - 2^-k) * shard bytes.
+    n, c, world = 20, 8, 4
+    circ = C.quantum_volume(n, 10, 3)
+    recs, _, _ = sv.plan_circuit(circ, n, c, 2, flags=sv.SV_FREE_LAYOUT)
+    batches = {}
+    for r in recs:
+        if int(r["kind"]) == sv.SV_EXCHANGE:
+            batches.setdefault(int(r["pad"]), 0)
+            batches[int(r["pad"])] += 1
+    shard = 16 << (n - 2)
+    want = sum((1 - 2.0 ** -k) * shard for k in batches.values())
+
+    with sv.LocalWorld(world) as w:
+        def body(r):
+            with sv.StateVector(n, c, "fp64", rank=r, local_world=w) as s:
+                s.reset(0)
+                s.apply(circ)
+                return s.stats()
+        st = w.run(body)
+    assert st[0]["exchange_batches"] == len(batches)
+    assert st[0]["bytes_sent"] == int(want)
+
+
+def test_local_world_errors():
+    # a world of a non-power-of-two size, a bad rank, and a timeout when one rank never joins
+    with pytest.raises(sv.SvError):
+        sv.LocalWorld(3)
+    with sv.LocalWorld(2) as w:
+        with pytest.raises(sv.SvError):
+            sv.StateVector(12, 4, rank=2, local_world=w)
