@@ -40,7 +40,8 @@ APPLY_FLAGS = 0  # SV_UNBLOCKED with --unblocked (the comparator), else the bloc
 def sv_flags_unblocked():
     return 1  # include/sv.h SV_UNBLOCKED
 FALLBACK_HBM_GBS = 6650.0
-# FP64 FMA pipe: 64 DFMA/clk/SM (measured 63.6 in tools/microbench.cu) x 148 SMs x 1.965 GHz x 2 flops
+# FP64 FMA pipe, derived (fallback when profiles/r02_peaks.json is absent): 64 DFMA/clk/SM x 148 SMs
+# x 1.965 GHz x 2 flops
 FP64_PEAK_TFLOPS = 2 * 64 * 148 * 1.965e9 / 1e12
 
 
@@ -214,35 +215,56 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- our arm
-def run_ours(args):
-    import torch
-    import torch.distributed as dist
+def fp64_peak():
+    """Measured FP64 FMA peak (TFLOP/s) on this pool's B200 (tools/microbench.cu, 4 s of DFMA back to
+    back at the 1965 MHz it held: profiles/r02_peaks.json); the derived 64 DFMA/clk/SM x 148 SMs x
+    1.965 GHz x 2 = 37.2 TFLOP/s if that file is missing."""
+    p = os.path.join(ROOT, "profiles", "r02_peaks.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["fp64_tflops"]), float(d.get("fp32_tflops", 2 * d["fp64_tflops"])), \
+            "measured (profiles/r02_peaks.json: tools/microbench.cu DFMA 4 s at 1965 MHz)"
+    return FP64_PEAK_TFLOPS, 2 * FP64_PEAK_TFLOPS, "derived: 64 DFMA/clk/SM x 148 SMs x 1.965 GHz x 2"
 
+
+class Ctx:
+    """Per-process state shared by the workloads of one bench run."""
+
+    def __init__(self, args):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist, self.args = torch, dist, args
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+        self.torch.cuda.synchronize()
+
+    def max_over_ranks(self, x):
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64, device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+
+def measure(ctx, wl, precision, c, steps, warmup, e2e_steps, with_clocks=True):
+    """Time `steps` hot-path steps of workload wl on this rank's GPU(s); returns the raw numbers."""
     import paper_2102_02957_b200 as sv
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    wl = workload(args.workload, world)
-    if wl.get("precision"):
-        args.precision = wl["precision"]
-    wl["desc"] = wl["desc"].replace("fp64", args.precision)
+    torch, world, rank = ctx.torch, ctx.world, ctx.rank
     n, gates = wl["n"], wl["gates"]
-    c = args.chunk_bits if args.chunk_bits else wl["chunk_bits"]
     stream = torch.cuda.Stream()
     uid = None
     if world > 1:
         u = torch.zeros(128, dtype=torch.uint8, device="cuda")
         if rank == 0:
             u.copy_(torch.tensor(np.frombuffer(sv.nccl_unique_id(), dtype=np.uint8).copy()))
-        dist.broadcast(u, 0)
+        ctx.dist.broadcast(u, 0)
         uid = bytes(u.cpu().numpy().tobytes())
-    s = sv.StateVector(n, c, args.precision, rank=rank, world=world, nccl_id=uid, stream=stream.cuda_stream)
+    s = sv.StateVector(n, c, precision, rank=rank, world=world, nccl_id=uid, stream=stream.cuda_stream)
     Q = list(range(min(10, n)))
 
     def step():  # simulate the circuit from its basis state (P:77, P:374), then read out
@@ -251,95 +273,133 @@ def run_ours(args):
         s.probabilities(Q)
 
     s.reset(wl["basis"])
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
     s.synchronize()
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-
     # ---- timed region (device time, CUDA events on the library's stream)
     s.reset_stats()
     s.set_timing(True)
-    clk = ClockSampler(local)
-    clk.start()
-    barrier()
+    clk = ClockSampler(ctx.local)
+    if with_clocks:
+        clk.start()
+    ctx.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(args.steps):
+    for _ in range(steps):
         step()
     e1.record(stream)
     e1.synchronize()
-    barrier()
-    clocks = clk.stop()
-    ms = e0.elapsed_time(e1)
+    ctx.barrier()
+    clocks = clk.stop() if with_clocks else None
+    ms = ctx.max_over_ranks(e0.elapsed_time(e1))
     st = s.stats()
     s.set_timing(False)
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    ms_step = ms / args.steps
-    value = len(gates) / (ms_step / 1e3)
-
-    # ---- roofline of the dominant kernel (section kernel K1)
-    hbm_peak, hbm_src = peaks()
-    roof = None
-    if st["timed_sections"]:
-        t_launch = st["section_ms"] / st["timed_sections"] / 1e3
-        bytes_l = st["section_bytes"] / st["timed_sections"]
-        flops_l = st["section_flops"] / st["timed_sections"]
-        t_hbm = bytes_l / (hbm_peak * 1e9)
-        t_alu = flops_l / (FP64_PEAK_TFLOPS * 1e12) if args.precision == "fp64" else flops_l / (2 * FP64_PEAK_TFLOPS * 1e12)
-        traffic = None
-        prof = os.path.join(ROOT, "profiles", "section_traffic.json")
-        if os.path.exists(prof) and world == 1:  # captured on one GPU: the N = 1 launch shape only
-            try:
-                traffic = json.load(open(prof)).get(wl["name"])
-            except Exception:
-                traffic = None
-        if t_hbm >= t_alu:
-            ach = bytes_l / t_launch / 1e9
-            roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
-                    "frac": round(ach / hbm_peak, 4), "traffic": traffic, "peak_source": hbm_src}
-        else:
-            ach = flops_l / t_launch / 1e12
-            pk = FP64_PEAK_TFLOPS if args.precision == "fp64" else 2 * FP64_PEAK_TFLOPS
-            roof = {"bound": "alu", "achieved": round(ach, 3), "peak": round(pk, 2), "unit": "TFLOP/s",
-                    "frac": round(ach / pk, 4), "traffic": traffic,
-                    "peak_source": "derived: 64 DFMA/clk/SM x 148 SMs x 1.965 GHz x 2 (DESIGN.md Roofline)"}
-        roof.update({"kernel": "sv_sec (run-time specialised section kernel; k_section when interpreted)",
-                     "launches_timed": st["timed_sections"],
-                     "avg_launch_ms": round(t_launch * 1e3, 4), "alg_bytes_per_launch": bytes_l,
-                     "alg_flops_per_launch": flops_l,
-                     "hbm_frac_of_measured": round(bytes_l / t_launch / 1e9 / hbm_peak, 4),
-                     "section_share_of_step": round(st["section_ms"] / ms, 4)})
-
     # ---- e2e through the public API with host buffers
     e2e = None
-    if not args.no_e2e:
+    if e2e_steps:
         idx = np.arange(0, 1 << n, max(1, (1 << n) // 1024), dtype=np.uint64)[:1024]
         h2d = gates.nbytes + idx.nbytes
-        d2h = (8 << len(Q)) + idx.size * (16 if args.precision == "fp64" else 8)
+        d2h = (8 << len(Q)) + idx.size * (16 if precision == "fp64" else 8)
         times = []
-        for it in range(args.e2e_steps + 1):
-            barrier()
+        for it in range(e2e_steps + 1):
+            ctx.barrier()
             t0 = time.perf_counter()
             s.reset(wl["basis"])
             s.apply(gates, flags=APPLY_FLAGS)
             s.probabilities(Q)
             s.amplitudes(idx)
-            dt = time.perf_counter() - t0
-            if world > 1:
-                t = torch.tensor([dt], dtype=torch.float64, device="cuda")
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                dt = float(t.item())
+            dt = ctx.max_over_ranks(time.perf_counter() - t0)
             if it > 0:
                 times.append(dt)
         e2e = {"value": len(gates) / (sum(times) / len(times)), "unit": "gates/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "steps": len(times)}
+    s.close()
+    return dict(ms=ms, ms_step=ms / steps, value=len(gates) / (ms / steps / 1e3), st=st, clocks=clocks, e2e=e2e)
+
+
+def roofline(wl, precision, r, world):
+    """The section kernel (K1, the dominant kernel) against the roofline that binds it."""
+    st, ms = r["st"], r["ms"]
+    if not st["timed_sections"]:
+        return None
+    hbm_peak, hbm_src = peaks()
+    f64, f32, fsrc = fp64_peak()
+    fpk = f64 if precision == "fp64" else f32
+    t_launch = st["section_ms"] / st["timed_sections"] / 1e3
+    bytes_l = st["section_bytes"] / st["timed_sections"]
+    flops_l = st["section_flops"] / st["timed_sections"]
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "section_traffic.json")
+    if os.path.exists(prof) and world == 1:  # captured on one GPU: the N = 1 launch shape only
+        try:
+            traffic = json.load(open(prof)).get(wl["name"])
+        except Exception:
+            traffic = None
+    if bytes_l / (hbm_peak * 1e9) >= flops_l / (fpk * 1e12):
+        ach = bytes_l / t_launch / 1e9
+        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(ach / hbm_peak, 4), "traffic": traffic, "peak_source": hbm_src}
+    else:
+        ach = flops_l / t_launch / 1e12
+        roof = {"bound": "alu", "achieved": round(ach, 3), "peak": round(fpk, 2), "unit": "TFLOP/s",
+                "frac": round(ach / fpk, 4), "traffic": traffic, "peak_source": fsrc}
+    roof.update({"kernel": "sv_sec (run-time specialised section kernel; k_section when interpreted)",
+                 "launches_timed": st["timed_sections"], "avg_launch_ms": round(t_launch * 1e3, 4),
+                 "alg_bytes_per_launch": bytes_l, "alg_flops_per_launch": flops_l,
+                 "hbm_frac_of_measured": round(bytes_l / t_launch / 1e9 / hbm_peak, 4),
+                 "section_share_of_step": round(st["section_ms"] / ms, 4),
+                 "alg_bytes_note": "2 x shard bytes per section launch (read + write); 1 x for the first section "
+                                   "after sv_reset, whose input is generated in-kernel (write only)"})
+    clocks = r.get("clocks") or {}
+    if roof["bound"] == "alu" and clocks.get("sm_mhz"):
+        # the FP64 peak scales with the SM clock; under FP64 + HBM load the B200 runs below its
+        # 1965 MHz maximum (sw_power_cap): the fraction at the clock it actually ran is context
+        f = clocks["sm_mhz"] / 1965.0
+        roof["peak_at_load_clock"] = round(roof["peak"] * f, 2)
+        roof["frac_at_load_clock"] = round(roof["frac"] / f, 4)
+    return roof
+
+
+def nvlink(r, steps):
+    st, ms = r["st"], r["ms"]
+    if not st["exchange_ms"]:
+        return None
+    gbs = st["bytes_sent"] / (st["exchange_ms"] / 1e3) / 1e9
+    return {"achieved": round(gbs, 1), "peak": 900.0, "unit": "GB/s per direction", "frac": round(gbs / 900.0, 4),
+            "frac_of_measured_peer_copy": round(gbs / 770.0, 4), "bytes_per_rank_per_step": st["bytes_sent"] / steps,
+            "share_of_step": round(st["exchange_ms"] / ms, 4),
+            "transport": "NCCL send/recv (packed)" if APPLY_FLAGS & 4 else "peer-memory swap kernel (CUDA IPC)"}
+
+
+def run_ours(args):
+    ctx = Ctx(args)
+    torch, world, rank = ctx.torch, ctx.world, ctx.rank
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(ctx.local)
+    if world > 1:
+        ctx.dist.init_process_group("nccl", device_id=torch.device("cuda", ctx.local))
+    wl = workload(args.workload, world)
+    if wl.get("precision"):
+        args.precision = wl["precision"]
+    wl["desc"] = wl["desc"].replace("fp64", args.precision)
+    n, gates = wl["n"], wl["gates"]
+    c = args.chunk_bits if args.chunk_bits else wl["chunk_bits"]
+    r = measure(ctx, wl, args.precision, c, args.steps, args.warmup, 0 if args.no_e2e else args.e2e_steps)
+    st, ms, clocks = r["st"], r["ms"], r["clocks"]
+    roof = roofline(wl, args.precision, r, world)
+    nvl = nvlink(r, args.steps) if world > 1 else None
+
+    # ---- the HBM-bound workload beside it (BASELINE configs[2], QFT30 fp64 c = 8), same GPUs
+    sub = {}
+    if not args.no_sub and args.workload != "qft30":
+        wq = workload("qft30", world)
+        rq = measure(ctx, wq, "fp64", wq["chunk_bits"], 20, 3, 0, with_clocks=True)
+        sub["qft30"] = {"workload": wq["desc"], "value": rq["value"], "unit": "gates/s", "ms_per_step": rq["ms_step"],
+                        "steps": 20, "warmup": 3, "chunk_bits": wq["chunk_bits"],
+                        "roofline": roofline(wq, "fp64", rq, world),
+                        "nvlink": nvlink(rq, 20) if world > 1 else None, "clocks": rq["clocks"],
+                        "gpu_launches": int(rq["st"]["kernel_launches"])}
 
     # ---- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
@@ -350,46 +410,33 @@ def run_ours(args):
         cpu = {"value": m / dt, "unit": "gates/s", "cores": cores(), "kind": "oracle",
                "sample": f"gates 2..{m + 1} of {wl['desc']} from its basis state ({m} gates, {dt:.1f} s; dense C oracle, OpenMP)"}
 
-    if roof and roof["bound"] == "alu" and clocks.get("sm_mhz"):
-        # FP64 peak scales with the SM clock; under sustained FP64 load the B200 runs below its
-        # 1965 MHz maximum (sw_power_cap): the fraction at the clock it actually ran is context
-        f = clocks["sm_mhz"] / 1965.0
-        roof["peak_at_load_clock"] = round(roof["peak"] * f, 2)
-        roof["frac_at_load_clock"] = round(roof["frac"] / f, 4)
-
-    # ---- cross-GPU exchanges against NVLink 5 (900 GB/s per direction per GPU)
-    nvl = None
-    if world > 1 and st["exchange_ms"] > 0:
-        gbs = st["bytes_sent"] / (st["exchange_ms"] / 1e3) / 1e9
-        nvl = {"achieved": round(gbs, 1), "peak": 900.0, "unit": "GB/s per direction", "frac": round(gbs / 900.0, 4),
-               "bytes_per_rank_per_step": st["bytes_sent"] / args.steps,
-               "share_of_step": round(st["exchange_ms"] / ms, 4)}
-
-    line = {"metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": wl["scaling"],
+    line = {"metric": METRIC, "value": r["value"], "unit": "gates/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": r["ms_step"], "higher_is_better": True, "scaling": wl["scaling"],
             "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32",
             "data": "synthetic (seeded QV/QFT generator, circuits/gen.py)",
             "config": {"workload": wl["desc"], "n_qubits": n, "gates": int(len(gates)), "chunk_bits": c,
                        "precision": args.precision, "parallelism": f"state sharded over {world} GPU(s)",
                        "l2": "state >= 4 GiB per GPU >> 126 MB L2 (no flush needed)",
                        "step": "sv_reset(basis; generated inside the first section's load) + sv_apply_circuit (pass+plan+upload+sections+exchanges) + sv_probabilities(10 qubits)",
-                       "path": "unblocked per-gate baseline (SV_UNBLOCKED)" if APPLY_FLAGS else "cache-blocked"},
-            "amp_updates_per_s": value * (1 << n),
+                       "path": ("unblocked per-gate baseline (SV_UNBLOCKED)" if APPLY_FLAGS & 1 else "cache-blocked") +
+                               (", NCCL send/recv exchange" if APPLY_FLAGS & 4 else "")},
+            "amp_updates_per_s": r["value"] * (1 << n),
             "sections_per_step": st["sections"] / args.steps, "exchanges_per_step": st["exchanges"] / args.steps,
             "exchange_bytes_per_rank_per_step": st["bytes_sent"] / args.steps,
             "exchange_ms_per_step": st["exchange_ms"] / args.steps,
             "host_pass_ms": st["pass_ms"],
-            "roofline": roof, "nvlink": nvl, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "nvlink": nvl, "cpu_baseline": cpu, "e2e": r["e2e"],
             "section_kernels": {"generated": int(st["jit_launches"]), "interpreted": int(st["interp_launches"]),
                                 "compiled_total": int(st["jit_compiled"]),
                                 "compile_ms_total": round(st["jit_compile_ms"], 1)},
             "gpu_launches": int(st["kernel_launches"]), "clocks": clocks}
+    if sub:
+        line["workloads"] = sub
     if rank == 0:
         print(json.dumps(line), flush=True)
-    s.close()
     if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+        ctx.dist.barrier()
+        ctx.dist.destroy_process_group()
     return 0
 
 
@@ -405,6 +452,8 @@ def main():
     ap.add_argument("--unblocked", action="store_true",
                     help="the paper's per-gate baseline (SV_UNBLOCKED): one pass per gate, exchanges per global gate")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sub", action="store_true", help="skip the QFT30 (HBM-bound) sub-workload of the line")
+    ap.add_argument("--nccl", action="store_true", help="cross-GPU exchange by NCCL send/recv (SV_EXCHANGE_NCCL)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-target-s", type=float, default=15.0)
@@ -413,7 +462,7 @@ def main():
     if args.warmup < 3:
         args.warmup = 3  # contract: W >= 3
     global APPLY_FLAGS
-    APPLY_FLAGS = sv_flags_unblocked() if args.unblocked else 0
+    APPLY_FLAGS = (sv_flags_unblocked() if args.unblocked else 0) | (4 if args.nccl else 0)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -1094,8 +1094,16 @@ int sv_sample(sv_handle h, size_t shots, uint64_t seed, uint64_t* host_out) {
   double before = 0.0;
   for (int r = 0; r < h->rank; r++) before += totals[r];
   const double mine_end = before + tot;
-  const bool last = h->rank == h->world - 1;
-  // u_s, sorted; shots in [before, mine_end) (the last rank also takes u >= total)
+  // A u at or above the total mass (rounding) goes to the last nonzero outcome: the last block
+  // with mass on the last rank that has mass (never a zero-probability index).
+  int last_nz_rank = -1;
+  for (int r = 0; r < h->world; r++)
+    if (totals[r] > 0.0) last_nz_rank = r;
+  const bool tail_here = h->rank == last_nz_rank;
+  size_t tail_blk = 0;
+  for (size_t i = 0; i < nblk; i++)
+    if (bs[i] > 0.0) tail_blk = i;
+  // u_s, sorted; this rank takes the shots in [before, mine_end) (and the tail, see above)
   std::vector<std::pair<double, size_t>> us(shots);
   for (size_t s = 0; s < shots; s++) us[s] = {(double)(splitmix64(seed ^ (uint64_t)s) >> 11) * 0x1.0p-53, s};
   std::sort(us.begin(), us.end());
@@ -1105,10 +1113,15 @@ int sv_sample(sv_handle h, size_t shots, uint64_t seed, uint64_t* host_out) {
   size_t bi = 0;
   for (auto& pr : us) {
     const double u = pr.first;
-    if (u < before || (u >= mine_end && !last)) continue;
-    double r = u - before;
-    while (bi + 1 < nblk && cum[bi] <= r) bi++;
-    const double r2 = r - (bi ? cum[bi - 1] : 0.0);
+    if (u < before || (u >= mine_end && !tail_here)) continue;
+    double r = u - before, r2;
+    if (u >= mine_end) {  // the tail: past every element of the last block with mass
+      bi = std::max(bi, tail_blk);
+      r2 = bs[bi];
+    } else {
+      while (bi + 1 < nblk && cum[bi] <= r) bi++;
+      r2 = r - (bi ? cum[bi - 1] : 0.0);
+    }
     if (!items.empty() && items[items.size() - 3] == (int64_t)bi) {
       items.back()++;
     } else {

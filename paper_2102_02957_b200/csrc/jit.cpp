@@ -13,6 +13,7 @@
 #include <nvrtc.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
@@ -30,6 +31,8 @@
 #include <vector>
 
 #include "program.h"
+
+typedef int CUresult_sv;  // CUresult (driver API) without including cuda.h
 
 namespace sv {
 namespace {
@@ -190,7 +193,9 @@ struct Gen {
   void stg() { o << "#pragma unroll\n    for (int k = 0; k < 16; k++) psi[b + RO[k]] = v[k];\n"; }
 };
 
-std::string gen_source(const int* p, const Launch& L, bool dbl, bool virt = false) {
+struct TmaPlan;
+void emit_tma_coords(std::ostringstream& o, const TmaPlan& TP, const char* base, const char* call);
+std::string gen_source(const int* p, const Launch& L, bool dbl, bool virt = false, const TmaPlan* pf = nullptr) {
   const SvSecHeader* H = reinterpret_cast<const SvSecHeader*>(p);
   Gen g;
   g.virt = virt;
@@ -206,7 +211,8 @@ std::string gen_source(const int* p, const Launch& L, bool dbl, bool virt = fals
   o << "\n#include \"section_dev.cuh\"\nusing namespace sv;\ntypedef " << (dbl ? "double2" : "float2") << " V;\n";
   o << "extern \"C\" __global__ void __launch_bounds__(" << nt << ", " << resident_ctas(H->T, nt, has_dense(p))
     << ") sv_sec(V* __restrict__ psi, const V* __restrict__ aux, int split_a, int split_b, long long vidx, "
-    << coef_param_decl_impl(L, dbl) << ") {\n";
+    << (pf ? "const __grid_constant__ SvTmap tm, unsigned long long ntiles, " : "") << coef_param_decl_impl(L, dbl)
+    << ") {\n";
   o << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n"
     << "  V* sm = reinterpret_cast<V*>(smem_raw);\n"
     << "  V* ctaf = reinterpret_cast<V*>(smem_raw + (sizeof(V) << " << H->T << "));\n"
@@ -215,7 +221,17 @@ std::string gen_source(const int* p, const Launch& L, bool dbl, bool virt = fals
   g.arr("int", "OB", H->out_bits, H->n_out);
   o << "  auto tile_of = [&](uint64_t t) {\n    uint64_t r = 0;\n#pragma unroll\n    for (int j = 0; j < "
     << H->n_out << "; j++) r |= ((t >> j) & 1ull) << OB[j];\n    return r;\n  };\n";
-  o << "  const uint64_t tile_off = tile_of(expand_tile(blockIdx.x, split_a, split_b));\n";
+  if (pf) {  // persistent CTAs; the TMA stages each CTA's next tile in L2 during this one
+    o << "  auto prefetch = [&](uint64_t b) {\n";
+    emit_tma_coords(o, *pf, "tile_of(expand_tile(b, split_a, split_b))", "tma_prefetch_l2");
+    o << "  };\n"
+      << "  if (tid == 0) prefetch(blockIdx.x);\n"
+      << "#pragma unroll 1\n  for (uint64_t blk = blockIdx.x; blk < ntiles; blk += gridDim.x) {\n"
+      << "  if (tid == 0 && blk + gridDim.x < ntiles) prefetch(blk + gridDim.x);\n"
+      << "  const uint64_t tile_off = tile_of(expand_tile(blk, split_a, split_b));\n";
+  } else {
+    o << "  {\n  const uint64_t tile_off = tile_of(expand_tile(blockIdx.x, split_a, split_b));\n";
+  }
   if (H->n_sets > 0) {
     o << "  for (int f = tid; f < " << 5 * H->n_sets << "; f += " << nt << ") {\n"
       << "    const int d = c_prog[kH_SETS + f / 5], i = f % 5;\n"
@@ -267,8 +283,313 @@ std::string gen_source(const int* p, const Launch& L, bool dbl, bool virt = fals
     g.stg();
     o << "  }\n";
   }
-  o << "}\n";
+  if (pf) o << "  __syncthreads();  // the next tile reuses shared memory\n";
+  o << "  }\n}\n";
   return o.str();
+}
+
+// ------------------------------------------------------------------------------- TMA variant
+// Tile loads by the Tensor Memory Accelerator (cp.async.bulk.tensor, SASS UTMALDG): the shard is
+// described to the TMA as a tensor of up to 5 dimensions cut at the starts of the tile's runs of
+// consecutive memory bits, so one box (2^w0 x ... amplitudes, rows of >= 128 bytes) is a whole
+// tile, or 2^E boxes when more runs than dimensions remain (E "enumerated" tile bits).  A
+// persistent CTA keeps a ring of S tile slots: while it computes tile j in slot j % S, the TMA
+// fills the slots of tiles j + 1 .. j + S - 1 (mbarrier transaction counts), so HBM reads run
+// continuously instead of in the load phase of each CTA (microbench: this gather pattern reaches
+// 5.8 TB/s read + write with a 2-3 slot ring vs 5.2 TB/s for LDG at the section kernel's 7
+// resident 32 KiB tiles per SM).  The box lands in "natural" order (tile position p at smem bit
+// nat[p]); the first step reads it with lanes on the lowest memory bits (conflict-free) and, after
+// a CTA barrier, writes the swizzled layout of the phases into the same slot.
+struct TmaPlan {
+  bool ok = false;
+  int D = 0;                      // tensor dimensions (1..5)
+  int lo[5] = {}, span[5] = {}, w[5] = {};  // dim d: memory bits [lo, lo + span); box: bits [lo, lo + w)
+  int E = 0;                      // enumerated tile bits (2^E boxes per tile)
+  int ebits[8] = {};
+  int nat[16] = {};               // tile position -> smem index bit of the natural layout
+  int boxbits = 0;
+};
+
+// SV_TMA (measurement switch): 0 off; 1 / 2: TMA L2 prefetch of the next tile in the persistent plain
+// kernel for sections without dense gates / every section; 3 / 4: the shared-memory slot ring
+int tma_mode() {
+  static const int m = [] {
+    const char* e = std::getenv("SV_TMA");
+    return e ? std::atoi(e) : 1;
+  }();
+  return m;
+}
+constexpr int kTmaSlots = 2;
+
+TmaPlan tma_plan(const int* p, const Launch& L, bool dbl) {
+  TmaPlan P;
+  const SvSecHeader* H = reinterpret_cast<const SvSecHeader*>(p);
+  const int T = H->T, nL = H->T + H->n_out;
+  const int md = tma_mode();
+  if (md == 0 || T < SV_R_BITS || (md >= 3 && T > 11)) return P;
+  if ((md == 1 || md == 3) && has_dense(p)) return P;
+  if (md >= 3 && kTmaSlots * (size_t(dbl ? 16 : 8) << T) + 5 * SV_MAX_SETS * 16 + 64 > 227 * 1024) return P;
+  (void)L;
+  const int* tb = H->tile_bits;
+  const int G = dbl ? 3 : 4;  // rows of >= 128 bytes
+  if (tb[0] != 0) return P;
+  std::vector<std::pair<int, int>> runs;  // (first bit, length)
+  for (int j = 0; j < T; j++) {
+    if (j == 0 || tb[j] != tb[j - 1] + 1)
+      runs.push_back({tb[j], 1});
+    else
+      runs.back().second++;
+  }
+  if (runs[0].second < G) return P;
+  std::vector<std::pair<int, int>> pieces;  // box limit: 256 elements per dimension
+  for (size_t r = 0; r < runs.size(); r++) {
+    int st = runs[r].first, len = runs[r].second;
+    int cap = r == 0 ? 7 : 8;  // dim 0 counts 2 elements (re, im) per amplitude
+    while (len > 0) {
+      const int l = std::min(len, cap);
+      pieces.push_back({st, l});
+      st += l;
+      len -= l;
+      cap = 8;
+    }
+  }
+  std::vector<int> order(pieces.size());
+  for (size_t i = 0; i < order.size(); i++) order[i] = (int)i;
+  std::stable_sort(order.begin() + 1, order.end(), [&](int a, int b) { return pieces[a].second > pieces[b].second; });
+  std::vector<std::pair<int, int>> box;
+  for (size_t i = 0; i < order.size() && box.size() < 5; i++) box.push_back(pieces[order[i]]);
+  std::sort(box.begin(), box.end());
+  int E = 0;
+  for (size_t i = 0; i < order.size(); i++) {
+    const auto& pc = pieces[order[i]];
+    if (std::find(box.begin(), box.end(), pc) != box.end()) continue;
+    for (int b = 0; b < pc.second; b++) {
+      if (E >= 4) return P;  // at most 16 boxes per tile
+      P.ebits[E++] = pc.first + b;
+    }
+  }
+  std::sort(P.ebits, P.ebits + E);
+  // dimension spans: from each box's first bit to the next box's (the top one to nL); a span the
+  // tensor map cannot describe in one dimension (2^32 elements) gets an extra box-width-0 dimension
+  std::vector<std::array<int, 3>> dims;  // lo, span, w
+  for (size_t i = 0; i < box.size(); i++) {
+    const int lo = box[i].first, hi = i + 1 < box.size() ? box[i + 1].first : nL;
+    dims.push_back({lo, hi - lo, box[i].second});
+  }
+  for (size_t i = 0; i < dims.size(); i++) {
+    const int lim = i == 0 ? 31 : 32;
+    if (dims[i][1] > lim) {
+      if (dims.size() >= 5) return P;
+      const int cut = dims[i][0] + std::max(dims[i][2], dims[i][1] / 2);
+      const std::array<int, 3> extra = {cut, dims[i][0] + dims[i][1] - cut, 0};
+      dims[i][1] = cut - dims[i][0];
+      dims.insert(dims.begin() + i + 1, extra);
+      i = (size_t)-1;  // re-check from the start
+    }
+  }
+  P.D = (int)dims.size();
+  int acc = 0;
+  for (int d = 0; d < P.D; d++) {
+    P.lo[d] = dims[d][0];
+    P.span[d] = dims[d][1];
+    P.w[d] = dims[d][2];
+    acc += P.w[d];
+  }
+  P.boxbits = acc;
+  P.E = E;
+  // natural layout: box bits in dimension order, then the enumerated bits
+  for (int pos = 0; pos < T; pos++) {
+    const int m = tb[pos];
+    int bit = -1, base = 0;
+    for (int d = 0; d < P.D; d++) {
+      if (m >= P.lo[d] && m < P.lo[d] + P.w[d]) bit = base + (m - P.lo[d]);
+      base += P.w[d];
+    }
+    for (int i = 0; i < E; i++)
+      if (P.ebits[i] == m) bit = P.boxbits + i;
+    if (bit < 0) return TmaPlan();
+    P.nat[pos] = bit;
+  }
+  P.ok = true;
+  return P;
+}
+
+// the 2^E boxes of the tile at amplitude offset `base`, each handed to `call`<D>(&tm, c[, ...])
+void emit_tma_coords(std::ostringstream& o, const TmaPlan& TP, const char* base, const char* call) {
+  o << "    const uint64_t a0 = " << base << ";\n";
+  o << "#pragma unroll\n    for (int e = 0; e < " << (1 << TP.E) << "; e++) {\n      uint64_t a = a0;\n";
+  for (int i = 0; i < TP.E; i++) o << "      if ((e >> " << i << ") & 1) a |= 1ull << " << TP.ebits[i] << ";\n";
+  o << "      int c[5] = {0, 0, 0, 0, 0};\n";
+  for (int d = 0; d < TP.D; d++) {
+    const unsigned long long mask = (TP.span[d] >= 64) ? ~0ull : ((1ull << TP.span[d]) - 1);
+    if (d == 0)
+      o << "      c[0] = (int)(2 * (a & " << mask << "ull));\n";
+    else
+      o << "      c[" << d << "] = (int)((a >> " << TP.lo[d] << ") & " << mask << "ull);\n";
+  }
+  if (std::strcmp(call, "tma_load") == 0)
+    o << "      tma_load<" << TP.D << ">(slots + s * TILE + e * BOX, &tm, c[0], c[1], c[2], c[3], c[4], &bar[s]);\n    }\n";
+  else
+    o << "      " << call << "<" << TP.D << ">(&tm, c[0], c[1], c[2], c[3], c[4]);\n    }\n";
+}
+
+int tma_ctas_per_sm(const Launch& L, bool dbl) {
+  const size_t bytes = kTmaSlots * (size_t(dbl ? 16 : 8) << L.T) + 5 * SV_MAX_SETS * (dbl ? 16 : 8) + 64;
+  return (int)std::max<size_t>(1, std::min<size_t>(8, (228 * 1024) / (bytes + 1024)));
+}
+size_t tma_smem_bytes(const Launch& L, bool dbl) {
+  return kTmaSlots * (size_t(dbl ? 16 : 8) << L.T) + 5 * SV_MAX_SETS * (dbl ? 16 : 8) + 64;
+}
+
+std::string gen_source_tma(const int* p, const Launch& L, bool dbl, const TmaPlan& TP) {
+  const SvSecHeader* H = reinterpret_cast<const SvSecHeader*>(p);
+  Gen g;
+  g.T = H->T;
+  g.ntl = H->T - SV_R_BITS;
+  const int nt = 1 << g.ntl;
+  const bool first = H->flags & SV_FLAG_FIRST_DIRECT, last = H->flags & SV_FLAG_LAST_DIRECT;
+  const int nph = H->n_phases;
+  const int T = H->T;
+  auto& o = g.o;
+  int pos_of[64];
+  std::fill(pos_of, pos_of + 64, -1);
+  for (int j = 0; j < T; j++) pos_of[H->tile_bits[j]] = j;
+  // natural-layout words of a boundary map (thread bit j / register slot s -> 1 << nat bit)
+  auto nat_map = [&](const SvMap& m) {
+    int tw[16], rw[SV_R_BITS];
+    for (int j = 0; j < g.ntl; j++) tw[j] = 1 << TP.nat[pos_of[m.tmb[j]]];
+    for (int s2 = 0; s2 < SV_R_BITS; s2++) rw[s2] = 1 << TP.nat[pos_of[m.rmb[s2]]];
+    g.smem(tw, rw);
+  };
+  o << "#define SV_JIT_PROG ";
+  for (size_t i = 0; i < L.int_count; i++) o << (i ? "," : "") << p[i];
+  o << "\n#include \"section_dev.cuh\"\nusing namespace sv;\ntypedef " << (dbl ? "double2" : "float2") << " V;\n";
+  o << "constexpr int S = " << kTmaSlots << ", TILE = " << (1 << T) << ", BOX = " << (1 << TP.boxbits) << ";\n";
+  o << "extern \"C\" __global__ void __launch_bounds__(" << nt << ", " << tma_ctas_per_sm(L, dbl)
+    << ") sv_sec(V* __restrict__ psi, const V* __restrict__ aux, int split_a, int split_b, long long vidx, "
+    << "const __grid_constant__ SvTmap tm, unsigned long long ntiles, " << coef_param_decl_impl(L, dbl) << ") {\n";
+  o << "  extern __shared__ __align__(1024) unsigned char smem_raw[];\n"
+    << "  V* const slots = reinterpret_cast<V*>(smem_raw);\n"
+    << "  V* const ctaf = reinterpret_cast<V*>(smem_raw + S * TILE * sizeof(V));\n"
+    << "  uint64_t* const bar = reinterpret_cast<uint64_t*>(smem_raw + S * TILE * sizeof(V) + " << 5 * SV_MAX_SETS
+    << " * sizeof(V));\n"
+    << "  (void)ctaf; (void)aux; (void)vidx;\n"
+    << "  const int tid = threadIdx.x;\n";
+  g.arr("int", "OB", H->out_bits, H->n_out);
+  o << "  auto tile_of = [&](uint64_t t) {\n    uint64_t r = 0;\n#pragma unroll\n    for (int j = 0; j < "
+    << H->n_out << "; j++) r |= ((t >> j) & 1ull) << OB[j];\n    return r;\n  };\n";
+  o << "  if (tid == 0) {\n    for (int s = 0; s < S; s++) mbar_init(&bar[s], 1);\n    mbar_init_fence();\n  }\n"
+    << "  __syncthreads();\n";
+  // the issue of one tile: 2^E boxes, coordinates from the tile's amplitude offset
+  o << "  auto issue = [&](uint64_t b, int s) {\n"
+    << "    fence_proxy_async();\n"
+    << "    mbar_expect_tx(&bar[s], TILE * (uint32_t)sizeof(V));\n";
+  emit_tma_coords(o, TP, "tile_of(expand_tile(b, split_a, split_b))", "tma_load");
+  o << "  };\n";
+  o << "  if (tid == 0)\n    for (int i = 0; i < S - 1; i++) {\n"
+    << "      const uint64_t b = blockIdx.x + (uint64_t)i * gridDim.x;\n      if (b < ntiles) issue(b, i);\n    }\n";
+  o << "  uint32_t j = 0;\n#pragma unroll 1\n"
+    << "  for (uint64_t blk = blockIdx.x; blk < ntiles; blk += gridDim.x, j++) {\n"
+    << "    const int s = (int)(j % S);\n"
+    << "    if (tid == 0) {\n      const uint64_t bn = blk + (uint64_t)(S - 1) * gridDim.x;\n"
+    << "      if (bn < ntiles) issue(bn, (int)((j + S - 1) % S));\n    }\n"
+    << "    const uint64_t tile_off = tile_of(expand_tile(blk, split_a, split_b));\n"
+    << "    V* const sm = slots + s * TILE;\n";
+  if (H->n_sets > 0) {
+    o << "    for (int f = tid; f < " << 5 * H->n_sets << "; f += " << nt << ") {\n"
+      << "      const int d = c_prog[kH_SETS + f / 5], i = f % 5;\n"
+      << "      ctaf[f] = cta_factor<V>(c_prog[d + 2 + i], c_prog[d + 3 + i], tile_off, P);\n    }\n"
+      << "    __syncthreads();\n";
+  }
+  o << "    mbar_wait_parity(&bar[s], (j / S) & 1);\n";
+  o << "    V v[16];\n";
+  const SvPhase* ph = reinterpret_cast<const SvPhase*>(p + H->phase_off);
+  const SvOp* ops = reinterpret_cast<const SvOp*>(p + H->op_off);
+  if (!first) {
+    o << "    {  // the staged tile (natural order), lanes on the lowest load memory bits -> swizzled layout\n";
+    nat_map(H->load);
+    g.lds();
+    o << "    }\n    __syncthreads();\n    {\n";
+    g.smem(H->load.tw, H->load.rw);
+    g.sts();
+    o << "    __syncthreads();\n    }\n";
+  }
+  for (int k = 0; k < nph; k++) {
+    const bool din = first && k == 0, dout = last && k == nph - 1;
+    o << "    {  // phase " << k << "\n";
+    if (din) {
+      o << "    {\n";
+      nat_map(H->din);
+      g.lds();
+      o << "    }\n";
+    } else {
+      g.smem(ph[k].tw, ph[k].rw);
+      g.lds();
+    }
+    for (int i = 0; i < ph[k].op_count; i++) {
+      const SvOp& op = ops[ph[k].op_begin + i];
+      if (!g.diagset_c(p, op, std::to_string(nt)))
+        o << "    op_c<" << op.type << ", " << op.a << ", " << op.b << ", " << op.coef << ", " << op.extra
+          << ">(v, tid, " << nt << ", tile_off, aux, ctaf, P);\n";
+    }
+    if (dout) {
+      o << "    {\n";
+      g.hbm(H->dout);
+      g.stg();
+      o << "    }\n";
+    } else {
+      if (din) {  // every thread has read the natural layout before the slot is rewritten
+        o << "    __syncthreads();\n";
+        g.smem(ph[k].tw, ph[k].rw);
+      }
+      g.sts();
+      o << "    __syncthreads();\n";
+    }
+    o << "    }\n";
+  }
+  if (!last) {
+    o << "    {  // gather in store order, lanes walk the lowest store memory bits\n";
+    g.smem(H->store.tw, H->store.rw);
+    g.lds();
+    g.hbm(H->store);
+    g.stg();
+    o << "    }\n";
+  }
+  o << "    __syncthreads();  // slot s is free for the tile S - 1 ahead\n  }\n}\n";
+  return o.str();
+}
+
+// host side: encode the tensor map of a launch's tile gather over the shard at sv
+typedef CUresult_sv (*EncodeTiledFn)(void*, int, unsigned, void*, const uint64_t*, const uint64_t*, const uint32_t*,
+                                      const uint32_t*, int, int, int, int);
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    cudaGetLastError();
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
+bool encode_tmap(const TmaPlan& P, bool dbl, void* sv, unsigned char (&out)[128]) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return false;
+  uint64_t dims[5], strides[4];
+  uint32_t box[5], es[5];
+  const uint64_t amp = dbl ? 16 : 8;
+  for (int d = 0; d < P.D; d++) {
+    dims[d] = (d == 0 ? 2ull : 1ull) << P.span[d];
+    box[d] = (d == 0 ? 2u : 1u) << P.w[d];
+    es[d] = 1;
+    if (d > 0) strides[d - 1] = amp << P.lo[d];
+  }
+  // CU_TENSOR_MAP_DATA_TYPE_FLOAT64 = 8, FLOAT32 = 7; interleave none = 0, swizzle none = 0,
+  // L2 promotion 256B = 3, oob fill none = 0
+  const int r = enc(out, dbl ? 8 : 7, (unsigned)P.D, sv, dims, strides, box, es, 0, 0, 3, 0);
+  return r == 0;
 }
 
 // ------------------------------------------------------------------------------------ cache
@@ -277,7 +598,23 @@ struct Entry {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t kern = nullptr;
   std::string err;
+  bool tma = false;  // the TMA-fed persistent variant (gen_source_tma), with its tile plan
+  bool pf = false;   // the persistent plain variant with TMA L2 prefetch of the next tile
+  TmaPlan tp;
+  std::atomic<int> occ{0};  // resident CTAs on the device of the TMA variant (its persistent grid)
 };
+
+// The source of a launch's kernel; decides (once, at entry creation) between the TMA-fed
+// persistent variant and the plain one.  A launch that generates its input (vidx) reads nothing.
+std::string source_for(const int* p, const Launch& L, bool dbl, bool virt, Entry& e) {
+  if (!virt) {
+    e.tp = tma_plan(p, L, dbl);
+    e.tma = e.tp.ok && tma_mode() >= 3;
+    e.pf = e.tp.ok && tma_mode() <= 2;
+  }
+  if (e.tma) return gen_source_tma(p, L, dbl, e.tp);
+  return gen_source(p, L, dbl, virt, e.pf ? &e.tp : nullptr);
+}
 
 struct Job {
   std::shared_ptr<Entry> e;
@@ -445,6 +782,7 @@ void build_entry(Entry& e, const std::string& src, int dev, bool dbl) {
     e.state = 2;
     return;
   }
+
   const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -516,12 +854,16 @@ void wait_ready(const Entry& e) {
 
 }  // namespace
 
-std::string jit_source(const int* prog_host, const Launch& L, bool dbl) { return gen_source(prog_host, L, dbl); }
+std::string jit_source(const int* prog_host, const Launch& L, bool dbl) {
+  Entry tmp;
+  return source_for(prog_host, L, dbl, false, tmp);
+}
 
 Status jit_compile_only(const int* prog_host, const Launch& L, bool dbl, const char* dump_dir, int index,
                         double* ms) {
   const auto t0 = std::chrono::steady_clock::now();
-  const std::string src = gen_source(prog_host, L, dbl);
+  Entry tmp;
+  const std::string src = source_for(prog_host, L, dbl, false, tmp);
   std::vector<char> cubin;
   std::string err;
   const bool ok = compile_cubin(src, cubin, err);
@@ -575,7 +917,7 @@ void jit_prepare(const Program& prog, bool dbl, bool virt_first) {
       e = std::make_shared<Entry>();
       g_cache.emplace(std::move(key), e);
     }
-    todo.emplace_back(e, gen_source(p, L, dbl, virt));
+    todo.emplace_back(e, source_for(p, L, dbl, virt, *e));
   }
   if (todo.empty()) return;
   if (m == kAsync) {
@@ -620,10 +962,11 @@ bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const double* 
     }
   }
   if (fresh) {
+    std::string src = source_for(prog_host, L, dbl, virt, *e);
     if (m == kSync)
-      build_entry(*e, gen_source(prog_host, L, dbl, virt), dev, dbl);
+      build_entry(*e, src, dev, dbl);
     else
-      worker().push(Job{e, gen_source(prog_host, L, dbl, virt), dev, dbl});
+      worker().push(Job{e, std::move(src), dev, dbl});
   } else if (m == kSync) {
     wait_ready(*e);
   }
@@ -653,10 +996,35 @@ bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const double* 
     }
     a4 = pbuf.data();
   }
-  void* args[] = {&a0, &a1, &a2, &a3, &av, a4};
   const unsigned threads = 1u << (L.T - SV_R_BITS);
-  const unsigned grid = (unsigned)(1ull << (L.n_out - (split_a ? 1 : 0) - (split_b ? 1 : 0)));
-  *err = cudaLaunchKernel(reinterpret_cast<const void*>(e->kern), dim3(grid), dim3(threads), args, smem_bytes(L, dbl), st);
+  const unsigned long long ntiles = 1ull << (L.n_out - (split_a ? 1 : 0) - (split_b ? 1 : 0));
+  if (e->tma || e->pf) {
+    alignas(64) unsigned char tmap[128];
+    if (!encode_tmap(e->tp, dbl, sv, tmap)) {
+      *err = cudaErrorInvalidValue;
+      return true;
+    }
+    if (e->occ <= 0) {  // resident CTAs on the device (first launch of this kernel)
+      int nb = 0, sms = 0;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, reinterpret_cast<const void*>(e->kern), (int)threads,
+                                                        e->tma ? tma_smem_bytes(L, dbl) : smem_bytes(L, dbl)) !=
+              cudaSuccess ||
+          nb < 1)
+        nb = 1;
+      cudaGetLastError();
+      e->occ = nb * sms;
+    }
+    unsigned long long nt = ntiles;
+    void* args[] = {&a0, &a1, &a2, &a3, &av, tmap, &nt, a4};
+    const unsigned grid = (unsigned)std::min<unsigned long long>(ntiles, (unsigned long long)e->occ);
+    *err = cudaLaunchKernel(reinterpret_cast<const void*>(e->kern), dim3(grid), dim3(threads), args,
+                            e->tma ? tma_smem_bytes(L, dbl) : smem_bytes(L, dbl), st);
+  } else {
+    void* args[] = {&a0, &a1, &a2, &a3, &av, a4};
+    *err = cudaLaunchKernel(reinterpret_cast<const void*>(e->kern), dim3((unsigned)ntiles), dim3(threads), args,
+                            smem_bytes(L, dbl), st);
+  }
   {
     std::lock_guard<std::mutex> lk(g_mu);
     g_ctr.hits++;

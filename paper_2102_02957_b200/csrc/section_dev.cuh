@@ -357,6 +357,81 @@ __device__ __forceinline__ void hbm_store(const V (&v)[16], V* __restrict__ dst,
   }
 }
 
+// ---------------------------------------------------------------- TMA tile loads (sm_90+ / sm_100a)
+// The tensor-map variant of the generated kernel (jit.cpp gen_source_tma) streams each CTA's
+// next tiles into a ring of shared-memory slots with cp.async.bulk.tensor (UTMALDG), completion
+// counted on an mbarrier per slot, while the CTA computes the current tile.  SvTmap is the
+// opaque 128-byte CUtensorMap, passed as a __grid_constant__ kernel parameter.
+struct alignas(64) SvTmap {
+  unsigned long long w[16];
+};
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tSV_WAIT_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra SV_WAIT_%=;\n\t}" ::"r"(
+          smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+// generic-proxy writes of a slot (the previous tile's phases) before the async proxy refills it
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+template <int D>
+__device__ __forceinline__ void tma_load(void* dst, const SvTmap* tm, int c0, int c1, int c2, int c3, int c4, uint64_t* bar) {
+  const int c[5] = {c0, c1, c2, c3, c4};
+  const unsigned long long t = reinterpret_cast<unsigned long long>(tm);
+  if constexpr (D == 1)
+    asm volatile("cp.async.bulk.tensor.1d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2}], [%3];" ::"r"(
+                     smem_u32(dst)), "l"(t), "r"(c[0]), "r"(smem_u32(bar))
+                 : "memory");
+  else if constexpr (D == 2)
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                     smem_u32(dst)), "l"(t), "r"(c[0]), "r"(c[1]), "r"(smem_u32(bar))
+                 : "memory");
+  else if constexpr (D == 3)
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+            smem_u32(dst)), "l"(t), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(smem_u32(bar))
+        : "memory");
+  else if constexpr (D == 4)
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
+            smem_u32(dst)), "l"(t), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(smem_u32(bar))
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(
+            smem_u32(dst)), "l"(t), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// L2 prefetch of a tile through the same tensor map (no shared memory, no registers held): the
+// persistent plain kernel asks the TMA to stage its next tile in L2 while it computes this one.
+template <int D>
+__device__ __forceinline__ void tma_prefetch_l2(const SvTmap* tm, int c0, int c1, int c2, int c3, int c4) {
+  const int c[5] = {c0, c1, c2, c3, c4};
+  const unsigned long long t = reinterpret_cast<unsigned long long>(tm);
+  if constexpr (D == 1)
+    asm volatile("cp.async.bulk.prefetch.tensor.1d.L2.global.tile [%0, {%1}];" ::"l"(t), "r"(c[0]) : "memory");
+  else if constexpr (D == 2)
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(t), "r"(c[0]), "r"(c[1]) : "memory");
+  else if constexpr (D == 3)
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(t), "r"(c[0]), "r"(c[1]),
+                 "r"(c[2]) : "memory");
+  else if constexpr (D == 4)
+    asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(t), "r"(c[0]), "r"(c[1]),
+                 "r"(c[2]), "r"(c[3]) : "memory");
+  else
+    asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(t), "r"(c[0]),
+                 "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]) : "memory");
+}
+
 // Tile index of launch block b when the launch covers only the tiles whose out-bit indices
 // (split & 255) have the value ((split >> 8) & 1); split = 0: all tiles.  Lower index first.
 __device__ __forceinline__ uint64_t expand_tile(uint64_t b, int split_a, int split_b) {

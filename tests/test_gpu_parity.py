@@ -149,17 +149,26 @@ def test_sampling():
     near_edge = np.min(np.abs(cdf[None, :] - us[:, None]), axis=1) < 1e-12
     exp = O.sample(ref, us)
     assert np.array_equal(shots[~near_edge], exp[~near_edge])
-    # blocked (pi != id): distribution check (chi^2 over the 16 most likely outcomes + rest)
-    with sv.StateVector(n, c) as s:
-        s.apply(circ)
-        shots = s.sample(200000, 7)
-    p = np.abs(ref) ** 2
-    top = np.argsort(p)[::-1][:16]
-    obs = np.array([np.sum(shots == t) for t in top] + [0.0])
-    obs[-1] = len(shots) - obs[:-1].sum()
-    expv = np.concatenate([p[top], [1 - p[top].sum()]]) * len(shots)
-    chi2 = np.sum((obs - expv) ** 2 / expv)
-    assert chi2 < 45.0  # 16 dof, p ~ 1e-4
+    # blocked (pi != id, so the GPU scans in memory order): a chi^2 test over ALL outcomes
+    # (outcomes expected fewer than 5 times are pooled into one bin), every shot a nonzero outcome
+    from scipy.stats import chi2 as chi2_dist
+    for n2, c2, shots, seed in [(12, 6, 400_000, 7), (16, 8, 2_000_000, 8)]:
+        circ2 = C.quantum_volume(n2, 6, 5)
+        with sv.StateVector(n2, c2) as s:
+            s.apply(circ2)
+            assert list(s.permutation()) != list(range(n2))
+            got = s.sample(shots, seed)
+        p = np.abs(O.apply_circuit(circ2, n2)) ** 2
+        assert np.all(p[got.astype(np.int64)] > 0)
+        obs = np.bincount(got.astype(np.int64), minlength=1 << n2).astype(np.float64)
+        exp = p * shots
+        big = exp >= 5
+        o2 = np.concatenate([obs[big], [obs[~big].sum()]])
+        e2 = np.concatenate([exp[big], [exp[~big].sum()]])
+        keep = e2 > 0
+        stat = float(np.sum((o2[keep] - e2[keep]) ** 2 / e2[keep]))
+        dof = int(keep.sum()) - 1
+        assert chi2_dist.sf(stat, dof) > 1e-6, (n2, stat, dof)
 
 
 def test_mirror_returns_to_basis_large():
@@ -171,18 +180,6 @@ def test_mirror_returns_to_basis_large():
         a = s.amplitudes(np.array([k], dtype=np.uint64))
         assert abs(a[0] - 1.0) <= 1e-10
         assert abs(s.norm() - 1.0) <= 1e-12
-
-
-@pytest.mark.slow
-def test_qv28_full_size_parity():
-    # BASELINE configs[1] at full size in the bench's launch configuration (c = 9), full compare.
-    n, c = 28, 9
-    circ = C.quantum_volume(n, 10, 1)
-    with sv.StateVector(n, c) as s:
-        s.apply(circ)
-        got = s.state()
-    ref = O.apply_circuit(circ, n)
-    check(got, ref, "fp64")
 
 
 @pytest.mark.parametrize("mode", [0, 2])
@@ -215,29 +212,6 @@ def test_generated_kernels_run():
         s.apply(C.quantum_volume(14, 4, 9))
         st = s.stats()
     assert st["jit_launches"] > 0 and st["interp_launches"] == 0
-
-
-@pytest.mark.slow
-def test_qft30_full_size_closed_form():
-    # BASELINE configs[2] at full size in the bench's configuration (c = 8, from its seeded basis
-    # state): sampled amplitudes against QFT|k>_j = e^{2 pi i jk / 2^n} / 2^{n/2} (the closed form
-    # the oracle is pinned to, tests/test_oracle.py), uniform marginals, unit norm.
-    n, c = 30, 8
-    N = 1 << n
-    k = C.basis_index(1, n)
-    rng = np.random.default_rng(30)
-    idx = np.unique(np.concatenate([np.arange(64), rng.integers(0, N, 4096), [N - 1]])).astype(np.uint64)
-    with sv.StateVector(n, c) as s:
-        s.reset(k)
-        s.apply(C.qft(n))
-        a = s.amplitudes(idx)
-        p = s.probabilities(list(range(10)))
-        nrm = s.norm()
-    j = idx.astype(np.int64)
-    ref = np.exp(2j * np.pi * ((j * k) % N) / N) / math.sqrt(N)
-    assert np.max(np.abs(a - ref)) <= 1e-10
-    assert np.max(np.abs(p - 1.0 / 1024)) <= 1e-12
-    assert abs(nrm - 1.0) <= 1e-12
 
 
 @pytest.mark.slow

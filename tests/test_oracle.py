@@ -183,3 +183,32 @@ def test_sampling_against_searchsorted():
     cdf = np.cumsum(np.abs(psi) ** 2)
     ref = np.searchsorted(cdf, us, side="right")
     assert np.array_equal(got, ref.astype(np.uint64))
+
+
+def test_norm2_non_unit_vectors():
+    # or_norm2 = sum_x |a_x|^2 (the definition, not sqrt of it): a hand-computed vector and the
+    # quadratic scaling law norm2(c a) = |c|^2 norm2(a) on a random non-normalised state.
+    a = np.array([3 + 4j, 0, 1j, -2, 0.5, 0, 0, -0.5j], dtype=np.complex128)
+    assert O.norm2(a) == 25 + 0 + 1 + 4 + 0.25 + 0.25
+    rng = np.random.default_rng(5)
+    b = rng.standard_normal(1 << 10) + 1j * rng.standard_normal(1 << 10)
+    ref = float(np.sum(b.real ** 2 + b.imag ** 2))
+    assert abs(O.norm2(b) - ref) <= 1e-12 * ref
+    assert abs(O.norm2(3.0 * b) - 9.0 * ref) <= 1e-12 * 9 * ref
+    assert O.norm2(np.zeros(4, dtype=np.complex128)) == 0.0
+
+
+def test_sampling_tail_beyond_total_mass():
+    # u at or beyond the total mass (rounding, or a sub-normalised state) returns the last outcome
+    # with nonzero probability, never a zero-probability index (R16).
+    a = np.zeros(16, dtype=np.complex128)
+    a[3] = 0.6
+    a[9] = 0.8j * 0.999  # total mass 0.36 + 0.6387... < 1
+    mass = abs(a[3]) ** 2 + abs(a[9]) ** 2
+    us = np.array([0.0, 0.35, 0.37, mass - 1e-12, mass, 0.99999, 0.5])
+    got = O.sample(a, us)
+    assert list(got) == [3, 3, 9, 9, 9, 9, 9]
+    # a state whose trailing amplitudes are zero: the tail goes to the last nonzero one, not 2^n - 1
+    b = np.zeros(8, dtype=np.complex128)
+    b[0] = b[2] = np.sqrt(0.5)
+    assert list(O.sample(b, np.array([0.25, 0.75, 1.0 - 2 ** -53]))) == [0, 2, 2]
