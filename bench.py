@@ -328,6 +328,14 @@ def roofline(wl, precision, r, world):
     t_launch = st["section_ms"] / st["timed_sections"] / 1e3
     bytes_l = st["section_bytes"] / st["timed_sections"]
     flops_l = st["section_flops"] / st["timed_sections"]
+    # HBM roofline over the read + write launches; the first section after sv_reset generates its
+    # input in-kernel (write only) and is reported beside them
+    n_in = st.get("timed_input_sections", 0)
+    n_rw = st["timed_sections"] - n_in
+    rw = None
+    if n_rw > 0 and n_in > 0:
+        rw = ((st["section_bytes"] - st["input_section_bytes"]) / n_rw,
+              (st["section_ms"] - st["input_section_ms"]) / n_rw / 1e3)
     traffic = None
     prof = os.path.join(ROOT, "profiles", "section_traffic.json")
     if os.path.exists(prof) and world == 1:  # captured on one GPU: the N = 1 launch shape only
@@ -336,9 +344,11 @@ def roofline(wl, precision, r, world):
         except Exception:
             traffic = None
     if bytes_l / (hbm_peak * 1e9) >= flops_l / (fpk * 1e12):
-        ach = bytes_l / t_launch / 1e9
+        b_rw, t_rw = rw if rw else (bytes_l, t_launch)
+        ach = b_rw / t_rw / 1e9
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
-                "frac": round(ach / hbm_peak, 4), "traffic": traffic, "peak_source": hbm_src}
+                "frac": round(ach / hbm_peak, 4), "traffic": traffic, "peak_source": hbm_src,
+                "launches_rw": n_rw, "avg_launch_ms_rw": round(t_rw * 1e3, 4), "alg_bytes_per_launch_rw": b_rw}
     else:
         ach = flops_l / t_launch / 1e12
         roof = {"bound": "alu", "achieved": round(ach, 3), "peak": round(fpk, 2), "unit": "TFLOP/s",
@@ -348,6 +358,9 @@ def roofline(wl, precision, r, world):
                  "alg_bytes_per_launch": bytes_l, "alg_flops_per_launch": flops_l,
                  "hbm_frac_of_measured": round(bytes_l / t_launch / 1e9 / hbm_peak, 4),
                  "section_share_of_step": round(st["section_ms"] / ms, 4),
+                 "input_sections": ({"launches": n_in, "avg_ms": round(st["input_section_ms"] / n_in, 4),
+                                     "write_only_gbs": round(st["input_section_bytes"] / (st["input_section_ms"] / 1e3) / 1e9, 1)}
+                                    if n_in else None),
                  "alg_bytes_note": "2 x shard bytes per section launch (read + write); 1 x for the first section "
                                    "after sv_reset, whose input is generated in-kernel (write only)"})
     clocks = r.get("clocks") or {}

@@ -110,6 +110,11 @@ typedef struct sv_stats {
   uint64_t interp_launches;   /* section launches that ran the program interpreter             */
   uint64_t jit_compiled;      /* kernels compiled by this process so far (cache misses)        */
   double jit_compile_ms;      /* host time spent compiling them (process total)                */
+  /* the timed sections whose input is generated in-kernel (the first section after sv_reset:
+   * write-only, 1 x shard bytes); also counted in timed_sections / section_ms / section_bytes */
+  uint64_t timed_input_sections;
+  double input_section_ms;
+  double input_section_bytes;
 } sv_stats;
 
 /* ---- lifetime ------------------------------------------------------------------------- */

@@ -6,9 +6,11 @@
 // CUDA IPC peer memory).
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <chrono>
+#include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -27,6 +29,22 @@ using namespace sv;
 namespace {
 
 thread_local std::string g_last_error;
+
+// NVTX ranges (header-only NVTX3: free unless a tool such as Nsight Systems is attached) around
+// every circuit, section launch, exchange and readout, so a timeline shows the step structure.
+struct Nvtx {
+  explicit Nvtx(const char* fmt, ...) __attribute__((format(printf, 2, 3))) {
+    char buf[160];
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    nvtxRangePushA(buf);
+  }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
 
 double now_ms() {
   using namespace std::chrono;
@@ -87,8 +105,15 @@ struct sv_state {
   std::vector<void*> peers;       // peer shard pointers mapped in this process (self = sv)
   std::vector<void*> ipc_opened;  // to close
   bool p2p = false;
-  cudaStream_t st_x = nullptr;  // exchange stream of the pipelined exchange + section (lazy)
-  cudaEvent_t ev_x[5] = {};
+  // cross-GPU exchange engine (exchange(), lazy): receive slots mapped by every peer, a push /
+  // transport stream and an unpack stream (both high priority), and the pipeline's events
+  DevBuf d_xrecv, d_xsend;
+  std::vector<void*> peer_xrecv;  // every rank's receive slots (peer path)
+  std::vector<void*> xrecv_opened;
+  bool xrecv_shared = false;
+  uint64_t xslot = 0;             // amplitudes per slot
+  cudaStream_t st_x = nullptr, st_u = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_pushed[2] = {}, ev_unpacked[2] = {}, ev_landed[4] = {}, ev_done = nullptr;
 
   Program prog;
   sv_stats stats{};
@@ -100,7 +125,7 @@ struct sv_state {
   // optional per-launch device timing (sv_set_timing)
   struct TRec {
     cudaEvent_t a, b;
-    int kind;  // 0 section, 1 exchange, 2 gate
+    int kind;  // 0 section, 1 exchange, 2 gate, 3 section with a generated input (write only)
     double bytes, flops;
   };
   bool timing = false;
@@ -193,70 +218,7 @@ int sync_stream(sv_state* h) {
   return SV_OK;
 }
 
-// Cross-GPU exchange of local memory bits with rank bits (one grouped step, §8(e)).
-int do_exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags) {
-  std::sort(pairs.begin(), pairs.end(), [](const ExPair& a, const ExPair& b) { return a.m < b.m; });
-  ExchangeArgs a{};
-  a.k = (int)pairs.size();
-  if (a.k > 8) return fail(h, SV_EINVAL, "internal: exchange of more than 8 bits");
-  uint64_t mmask = 0;
-  for (int i = 0; i < a.k; i++) {
-    a.m[i] = pairs[i].m;
-    a.bsel[i] = pairs[i].b - h->nL;
-    mmask |= 1ull << pairs[i].m;
-  }
-  a.h = h->nL - 1;
-  while (a.h >= 0 && ((mmask >> a.h) & 1)) a.h--;
-  if (a.h < 0) return fail(h, SV_EINVAL, "internal: no split bit for the exchange");
-  const uint64_t block = 1ull << (h->nL - a.k);
-  h->stats.bytes_sent += (uint64_t)((1ull << a.k) - 1) * block * h->amp;
-  h->stats.exchanges += a.k;
-  h->stats.exchange_batches++;
-
-  if (h->p2p && !(flags & SV_EXCHANGE_NCCL)) {
-    if (int rc = barrier(h)) return rc;
-    int launches = 0;
-    CUDA_TRY(h, launch_exchange_peer(h->dbl, h->sv, h->peers.data(), h->rank, h->nL, a, h->st, &launches));
-    h->stats.kernel_launches += launches;
-    return barrier(h);
-  }
-
-  // NCCL send/recv path (P:420's MPI send/recv pairs): my block mu (local m-bits = mu) goes to the
-  // partner whose rank bits are mu and its block `mine` comes back into the same places.  The
-  // blocks are strided whenever an m-bit is not a top bit, so each piece is packed into a
-  // contiguous staging buffer, sent / received in one grouped call, and unpacked in place.
-  int mine = 0;
-  for (int i = 0; i < a.k; i++) mine |= ((h->rank >> a.bsel[i]) & 1) << i;
-  const uint64_t piece = std::min<uint64_t>(block, (256ull << 20) / h->amp);
-  if (int rc = ensure_dev(h, h->d_stage, 2 * piece * h->amp)) return rc;
-  char* send_buf = (char*)h->d_stage.p;
-  char* recv_buf = send_buf + piece * h->amp;
-  std::vector<std::pair<int, int>> partners;  // (partner rank, mu)
-  for (int mu = 0; mu < (1 << a.k); mu++) {
-    if (mu == mine) continue;
-    int p = h->rank;
-    for (int i = 0; i < a.k; i++) p = (p & ~(1 << a.bsel[i])) | (((mu >> i) & 1) << a.bsel[i]);
-    partners.push_back({p, mu});
-  }
-  // XOR schedule (as the peer kernel): round t pairs ranks whose subcube bits differ by t
-  std::sort(partners.begin(), partners.end(),
-            [&](const std::pair<int, int>& x, const std::pair<int, int>& y) { return (x.second ^ mine) < (y.second ^ mine); });
-  int val[8];
-  for (auto& pm : partners) {
-    for (int i = 0; i < a.k; i++) val[i] = (pm.second >> i) & 1;
-    for (uint64_t off = 0; off < block; off += piece) {
-      const uint64_t cnt = std::min<uint64_t>(piece, block - off);
-      CUDA_TRY(h, launch_pack_bits(h->dbl, true, h->sv, send_buf, off, cnt, a.k, a.m, val, h->st));
-      COMM_TRY(h, h->comm->group_start());
-      COMM_TRY(h, h->comm->send(send_buf, cnt * h->amp, pm.first, h->st));
-      COMM_TRY(h, h->comm->recv(recv_buf, cnt * h->amp, pm.first, h->st));
-      COMM_TRY(h, h->comm->group_end());
-      CUDA_TRY(h, launch_pack_bits(h->dbl, false, h->sv, recv_buf, off, cnt, a.k, a.m, val, h->st));
-      h->stats.kernel_launches += 2;
-    }
-  }
-  return SV_OK;
-}
+int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launch* L0, int* done);
 
 int upload_program(sv_state* h) {
   const size_t ib = h->prog.ints.size() * sizeof(int);
@@ -353,6 +315,7 @@ int materialize_at(sv_state* h, int64_t vidx);
 // One section launch (generated kernel, else the interpreter), optionally restricted to the tiles
 // whose out bits match split_a / split_b (kernels.cuh).
 int launch_one(sv_state* h, const Launch& L, int split_a = 0, int split_b = 0, int64_t vidx = -1) {
+  Nvtx r("sv section T=%d phases=%d ops=%d%s", L.T, L.n_phases, L.n_ops, split_a ? " (quarter)" : "");
   const int* pdev = (const int*)h->d_prog.p + L.int_off;
   const char* cdev = (const char*)h->d_coef.p + L.coef_off * h->amp;
   const char* adev = (const char*)h->d_aux.p + L.aux_off * h->amp;
@@ -375,107 +338,6 @@ int launch_one(sv_state* h, const Launch& L, int split_a = 0, int split_b = 0, i
   return SV_OK;
 }
 
-// Pipelined exchange + first launch of the next section (§8(e): the paper's buffer pipeline,
-// P:156-166, with the section instead of a copy as the consumer).  The exchanged pairs and the
-// section's tiles are both split by up to two local bits that are out-of-tile for the section and
-// not exchanged; piece p's exchange kernel + a cross-GPU barrier run on an exchange stream, and the
-// section's tiles of piece p start on the compute stream as soon as that piece has landed on both
-// GPUs, while piece p+1 is still on NVLink.  Returns 1 if it did the work, 0 if not applicable.
-int exchange_pipelined(sv_state* h, const std::vector<ExPair>& pairs_in, const Launch& L0, int* done) {
-  *done = 0;
-  static const int pieces_env = [] {
-    const char* e = std::getenv("SV_XPIPE");  // 0 disables; 2 or 4 pieces
-    return e ? std::atoi(e) : 4;
-  }();
-  // the swap kernel of a piece runs on a high-priority stream with a capped grid, so the
-  // section's CTAs keep most SMs (QV33, 2 GPUs: 1141 -> 1050 ms with 4 pieces and 128 blocks)
-  static const unsigned xgrid = [] {
-    const char* e = std::getenv("SV_XGRID");
-    return e ? (unsigned)std::atoi(e) : 128u;
-  }();
-  if (pieces_env < 2 || L0.T < SV_R_BITS) return SV_OK;
-  std::vector<ExPair> pairs = pairs_in;
-  std::sort(pairs.begin(), pairs.end(), [](const ExPair& a, const ExPair& b) { return a.m < b.m; });
-  ExchangeArgs a{};
-  a.k = (int)pairs.size();
-  if (a.k > 8) return SV_OK;
-  uint64_t mmask = 0;
-  for (int i = 0; i < a.k; i++) {
-    a.m[i] = pairs[i].m;
-    a.bsel[i] = pairs[i].b - h->nL;
-    mmask |= 1ull << pairs[i].m;
-  }
-  a.h = h->nL - 1;
-  while (a.h >= 0 && ((mmask >> a.h) & 1)) a.h--;
-  if (a.h < 0) return SV_OK;
-  // split bits: the section's highest out bits that are neither exchanged nor the work-split bit
-  const SvSecHeader* H = reinterpret_cast<const SvSecHeader*>(h->prog.ints.data() + L0.int_off);
-  const int want = pieces_env >= 4 ? 2 : 1;
-  int sidx[2], sbit[2], ns = 0;
-  for (int j = H->n_out - 1; j >= 0 && ns < want; j--) {
-    const int b = H->out_bits[j];
-    if (((mmask >> b) & 1) || b == a.h) continue;
-    sidx[ns] = j;
-    sbit[ns] = b;
-    ns++;
-  }
-  if (ns == 0) return SV_OK;
-  if (ns == 2) {  // ascending out-bit index for expand_tile
-    std::swap(sidx[0], sidx[1]);
-    std::swap(sbit[0], sbit[1]);
-  }
-  if (!h->st_x) {
-    int lo = 0, hi = 0;  // the exchange stream at the highest priority: its blocks go first
-    cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    CUDA_TRY(h, cudaStreamCreateWithPriority(&h->st_x, cudaStreamNonBlocking, hi));
-    for (auto& e : h->ev_x) CUDA_TRY(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  }
-  const uint64_t block = 1ull << (h->nL - a.k);
-  h->stats.bytes_sent += (uint64_t)((1ull << a.k) - 1) * block * h->amp;
-  h->stats.exchanges += a.k;
-  h->stats.exchange_batches++;
-  // the exchange stream starts after everything queued so far on the compute stream
-  CUDA_TRY(h, cudaEventRecord(h->ev_x[4], h->st));
-  CUDA_TRY(h, cudaStreamWaitEvent(h->st_x, h->ev_x[4], 0));
-  cudaEvent_t t0 = nullptr, t1 = nullptr;
-  if (h->timing) {
-    t0 = ev_get(h);
-    CUDA_TRY(h, cudaEventRecord(t0, h->st_x));
-  }
-  if (int rc = barrier(h, h->st_x)) return rc;
-  const int P = 1 << ns;
-  for (int p = 0; p < P; p++) {
-    a.nfix = ns;
-    for (int i = 0; i < ns; i++) {
-      a.fix_pos[i] = sbit[i];
-      a.fix_val[i] = (p >> i) & 1;
-    }
-    int launches = 0;
-    CUDA_TRY(h, launch_exchange_peer(h->dbl, h->sv, h->peers.data(), h->rank, h->nL, a, h->st_x, &launches,
-                                     xgrid));
-    h->stats.kernel_launches += launches;
-    if (int rc = barrier(h, h->st_x)) return rc;
-    CUDA_TRY(h, cudaEventRecord(h->ev_x[p], h->st_x));
-  }
-  if (h->timing) {
-    t1 = ev_get(h);
-    CUDA_TRY(h, cudaEventRecord(t1, h->st_x));
-    h->trecs.push_back({t0, t1, 1, 0.0, 0.0});
-  }
-  const double amps = (double)(1ull << h->nL) / P;
-  for (int p = 0; p < P; p++) {
-    CUDA_TRY(h, cudaStreamWaitEvent(h->st, h->ev_x[p], 0));
-    int sp[2] = {0, 0};
-    for (int i = 0; i < ns; i++) sp[i] = (1 << 16) | (((p >> i) & 1) << 8) | sidx[i];
-    cudaEvent_t t = tstart(h);
-    if (int rc = launch_one(h, L0, sp[0], sp[1])) return rc;
-    tend(h, t, 0, 2.0 * amps * (double)h->amp, L0.flops_per_amp * amps);
-  }
-  h->stats.sections++;
-  *done = 1;
-  return SV_OK;
-}
-
 int drain_timing(sv_state* h) {
   if (h->trecs.empty()) return SV_OK;
   CUDA_TRY(h, cudaEventSynchronize(h->trecs.back().b));
@@ -484,11 +346,16 @@ int drain_timing(sv_state* h) {
     float ms = 0.f;
     CUDA_TRY(h, cudaEventElapsedTime(&ms, r.a, r.b));
     if (dbg) std::fprintf(stderr, "[sv] rank %d kind %d %.3f ms\n", h->rank, r.kind, ms);
-    if (r.kind == 0) {
+    if (r.kind == 0 || r.kind == 3) {
       h->stats.timed_sections++;
       h->stats.section_ms += ms;
       h->stats.section_bytes += r.bytes;
       h->stats.section_flops += r.flops;
+      if (r.kind == 3) {
+        h->stats.timed_input_sections++;
+        h->stats.input_section_ms += ms;
+        h->stats.input_section_bytes += r.bytes;
+      }
     } else if (r.kind == 1) {
       h->stats.exchange_ms += ms;
     } else {
@@ -555,14 +422,17 @@ int allreduce(sv_state* h, void* buf, size_t count, CommType type) {
   return SV_OK;
 }
 
-int setup_p2p(sv_state* h, void* base_alloc, size_t base_off) {
-  if (h->comm->local()) {  // one process, one device: the other ranks' shards are plain pointers
-    h->peers.assign(h->world, nullptr);
-    COMM_TRY(h, h->comm->share_pointers(h->sv, h->peers.data()));
-    h->p2p = true;
+// Map every rank's buffer `mine` (allocation base_alloc + base_off) into this process: CUDA IPC
+// handles all-gathered over the communicator (NCCL worlds), plain pointers (local worlds).
+// *ok: every rank mapped every peer (agreed across ranks).
+int share_buffer(sv_state* h, void* mine_ptr, void* base_alloc, size_t base_off, std::vector<void*>& out,
+                 std::vector<void*>& opened, bool* ok_all) {
+  out.assign(h->world, nullptr);
+  if (h->comm->local()) {  // one process, one device: the other ranks' buffers are plain pointers
+    COMM_TRY(h, h->comm->share_pointers(mine_ptr, out.data()));
+    *ok_all = true;
     return SV_OK;
   }
-  // Exchange CUDA IPC handles of every rank's shard allocation (NCCL all-gather).
   struct Rec {
     cudaIpcMemHandle_t hd;
     uint64_t off;
@@ -582,8 +452,7 @@ int setup_p2p(sv_state* h, void* base_alloc, size_t base_off) {
   if (int rc_ = sync_stream(h)) return rc_;
   int ok = 1;
   for (auto& r : all) ok &= r.ok;
-  h->peers.assign(h->world, nullptr);
-  h->peers[h->rank] = h->sv;
+  out[h->rank] = mine_ptr;
   for (int r = 0; ok && r < h->world; r++) {
     if (r == h->rank) continue;
     void* p = nullptr;
@@ -592,8 +461,8 @@ int setup_p2p(sv_state* h, void* base_alloc, size_t base_off) {
       ok = 0;
       break;
     }
-    h->ipc_opened.push_back(p);
-    h->peers[r] = (char*)p + all[r].off;
+    opened.push_back(p);
+    out[r] = (char*)p + all[r].off;
   }
   // agree across ranks
   float f = ok ? 0.f : 1.f;
@@ -601,7 +470,182 @@ int setup_p2p(sv_state* h, void* base_alloc, size_t base_off) {
   if (int rc = allreduce(h, h->d_small.p, 1, kF32)) return rc;
   CUDA_TRY(h, cudaMemcpyAsync(&f, h->d_small.p, sizeof(float), cudaMemcpyDeviceToHost, h->st));
   if (int rc_ = sync_stream(h)) return rc_;
-  h->p2p = (f == 0.f);
+  CUDA_TRY(h, cudaMemsetAsync(h->d_small.p, 0, 16, h->st));
+  *ok_all = (f == 0.f);
+  return SV_OK;
+}
+
+int setup_p2p(sv_state* h, void* base_alloc, size_t base_off) {
+  bool ok = false;
+  if (int rc = share_buffer(h, h->sv, base_alloc, base_off, h->peers, h->ipc_opened, &ok)) return rc;
+  h->p2p = ok;
+  return SV_OK;
+}
+
+// ------------------------------------------------------------------------ cross-GPU exchange
+// The exchange of k local memory bits m_i with rank bits b_i (one grouped step, §8(e); the paper's
+// chunk_swap across processes, pipelined through buffers as in its Fig. 5).
+// In every XOR round t of the subcube, this rank's block mu = mine ^ t (elements whose m-bits equal
+// mu) is replaced by the partner's block `mine`, element j of one block pairing with element j of
+// the other (j: compact index over the remaining local bits).  Blocks are strided whenever an m-bit
+// is low, so they travel packed:
+//   peer path (CUDA IPC / local world): a small-grid push kernel gathers the block piece and stores
+//     it contiguously into the partner's receive slot over NVLink (remote stores only, full
+//     128-byte lines), then an unpack kernel scatters the slot into place;
+//   NCCL path (SV_EXCHANGE_NCCL, the comparator of P:420's send/recv): pack into a local send slot,
+//     grouped ncclSend / ncclRecv, unpack.
+// Pieces alternate between two slots: the transport of piece q (stream st_x) overlaps the unpack of
+// piece q - 1 (stream st_u); two stream-ordered barriers per piece order a push after the partner's
+// unpack of that slot and an unpack after the partner's push.  With the next section's first launch
+// L0 (pipelined exchange + section) the pieces are grouped by up to two of its out-of-tile bits and
+// each quarter of its tiles starts on the compute stream as soon as that quarter has landed, while
+// the next quarter is still on NVLink.
+constexpr unsigned kPushGrid = 132;  // CTAs of the push / unpack kernels: SMs left to the sections
+
+int ensure_exchange_engine(sv_state* h, uint64_t slot_amps, bool nccl_path) {
+  if (!h->st_x) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    CUDA_TRY(h, cudaStreamCreateWithPriority(&h->st_x, cudaStreamNonBlocking, hi));
+    CUDA_TRY(h, cudaStreamCreateWithPriority(&h->st_u, cudaStreamNonBlocking, hi));
+    for (cudaEvent_t* e : {&h->ev_start, &h->ev_done, &h->ev_pushed[0], &h->ev_pushed[1], &h->ev_unpacked[0],
+                           &h->ev_unpacked[1], &h->ev_landed[0], &h->ev_landed[1], &h->ev_landed[2], &h->ev_landed[3]})
+      CUDA_TRY(h, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  }
+  if (h->xslot < slot_amps) {  // collective: every rank grows its slots at the same exchange
+    for (void* p : h->xrecv_opened) cudaIpcCloseMemHandle(p);
+    h->xrecv_opened.clear();
+    h->xrecv_shared = false;
+    if (int rc = ensure_dev(h, h->d_xrecv, 2 * slot_amps * h->amp)) return rc;
+    h->xslot = slot_amps;
+  }
+  if (nccl_path) return ensure_dev(h, h->d_xsend, 2 * h->xslot * h->amp);
+  if (!h->xrecv_shared) {
+    bool ok = false;
+    if (int rc = share_buffer(h, h->d_xrecv.p, h->d_xrecv.p, 0, h->peer_xrecv, h->xrecv_opened, &ok)) return rc;
+    if (!ok) return fail(h, SV_ECUDA, "exchange slots could not be mapped by every peer");
+    h->xrecv_shared = true;
+  }
+  return SV_OK;
+}
+
+int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launch* L0, int* done) {
+  *done = 0;
+  Nvtx r("sv exchange k=%zu%s", pairs.size(), L0 ? " + section" : "");
+  std::sort(pairs.begin(), pairs.end(), [](const ExPair& a, const ExPair& b) { return a.m < b.m; });
+  const int k = (int)pairs.size();
+  if (k < 1 || k > 8) return fail(h, SV_EINVAL, "internal: exchange of 1..8 bits expected");
+  int m[8], bsel[8], mine = 0;
+  uint64_t mmask = 0;
+  for (int i = 0; i < k; i++) {
+    m[i] = pairs[i].m;
+    bsel[i] = pairs[i].b - h->nL;
+    mmask |= 1ull << m[i];
+    mine |= ((h->rank >> bsel[i]) & 1) << i;
+  }
+  const bool nccl_path = (flags & SV_EXCHANGE_NCCL) || !h->p2p;
+  // split bits: the next section's highest out-of-tile bits that are not exchanged
+  int ns = 0, sidx[2] = {0, 0}, sbit[2] = {0, 0};
+  if (L0 && L0->T >= SV_R_BITS) {
+    const SvSecHeader* H = reinterpret_cast<const SvSecHeader*>(h->prog.ints.data() + L0->int_off);
+    for (int j = H->n_out - 1; j >= 0 && ns < 2; j--) {
+      const int b = H->out_bits[j];
+      if ((mmask >> b) & 1) continue;
+      sidx[ns] = j;
+      sbit[ns] = b;
+      ns++;
+    }
+    if (ns == 2) {  // ascending out-bit index for expand_tile
+      std::swap(sidx[0], sidx[1]);
+      std::swap(sbit[0], sbit[1]);
+    }
+  }
+  if (h->nL - k - ns < 0) ns = 0;
+  const int P = 1 << ns;
+  const uint64_t qblock = 1ull << (h->nL - k - ns);  // elements per (quarter, partner)
+  const uint64_t slot = std::min<uint64_t>(qblock, (1ull << 30) / h->amp);  // <= 1 GiB per slot
+  if (int rc = ensure_exchange_engine(h, slot, nccl_path)) return rc;
+  h->stats.bytes_sent += (uint64_t)((1ull << k) - 1) * (1ull << (h->nL - k)) * h->amp;
+  h->stats.exchanges += k;
+  h->stats.exchange_batches++;
+
+  // both exchange streams start after everything queued so far on the compute stream
+  CUDA_TRY(h, cudaEventRecord(h->ev_start, h->st));
+  CUDA_TRY(h, cudaStreamWaitEvent(h->st_x, h->ev_start, 0));
+  CUDA_TRY(h, cudaStreamWaitEvent(h->st_u, h->ev_start, 0));
+  cudaEvent_t t0 = nullptr;
+  if (h->timing) {
+    t0 = ev_get(h);
+    CUDA_TRY(h, cudaEventRecord(t0, h->st_x));
+  }
+  char* recv = (char*)h->d_xrecv.p;
+  char* send = (char*)h->d_xsend.p;
+  int pos[11], val[11];
+  uint64_t q = 0;
+  for (int p = 0; p < P; p++) {
+    for (int t = 1; t < (1 << k); t++) {  // XOR schedule: every round is a perfect matching of ranks
+      const int mu = mine ^ t;
+      int partner = h->rank;
+      for (int i = 0; i < k; i++) partner = (partner & ~(1 << bsel[i])) | (((mu >> i) & 1) << bsel[i]);
+      int nins = 0;
+      for (int i = 0; i < k; i++) {
+        pos[nins] = m[i];
+        val[nins++] = (mu >> i) & 1;
+      }
+      for (int i = 0; i < ns; i++) {
+        pos[nins] = sbit[i];
+        val[nins++] = (p >> i) & 1;
+      }
+      for (uint64_t off = 0; off < qblock; off += slot, q++) {
+        const uint64_t cnt = std::min<uint64_t>(slot, qblock - off);
+        const int b = (int)(q & 1);
+        if (q >= 2) CUDA_TRY(h, cudaStreamWaitEvent(h->st_x, h->ev_unpacked[b], 0));  // my slot b is free
+        if (nccl_path) {
+          char* sb = send + (size_t)b * slot * h->amp;
+          CUDA_TRY(h, launch_pack_bits(h->dbl, true, h->sv, sb, off, cnt, nins, pos, val, h->st_x, kPushGrid));
+          COMM_TRY(h, h->comm->group_start());
+          COMM_TRY(h, h->comm->send(sb, cnt * h->amp, partner, h->st_x));
+          COMM_TRY(h, h->comm->recv(recv + (size_t)b * slot * h->amp, cnt * h->amp, partner, h->st_x));
+          COMM_TRY(h, h->comm->group_end());
+        } else {
+          if (int rc = barrier(h, h->st_x)) return rc;  // the partner's slot b is free too
+          char* dst = (char*)h->peer_xrecv[partner] + (size_t)b * slot * h->amp;
+          CUDA_TRY(h, launch_pack_bits(h->dbl, true, h->sv, dst, off, cnt, nins, pos, val, h->st_x, kPushGrid));
+          if (int rc = barrier(h, h->st_x)) return rc;  // every push of this piece has landed
+        }
+        h->stats.kernel_launches += 2;
+        CUDA_TRY(h, cudaEventRecord(h->ev_pushed[b], h->st_x));
+        CUDA_TRY(h, cudaStreamWaitEvent(h->st_u, h->ev_pushed[b], 0));
+        CUDA_TRY(h, launch_pack_bits(h->dbl, false, h->sv, recv + (size_t)b * slot * h->amp, off, cnt, nins, pos, val,
+                                     h->st_u, kPushGrid));
+        CUDA_TRY(h, cudaEventRecord(h->ev_unpacked[b], h->st_u));
+      }
+    }
+    if (L0) {  // quarter p of the next section: its tiles have every exchanged element now
+      CUDA_TRY(h, cudaEventRecord(h->ev_landed[p], h->st_u));
+      CUDA_TRY(h, cudaStreamWaitEvent(h->st, h->ev_landed[p], 0));
+      int sp[2] = {0, 0};
+      for (int i = 0; i < ns; i++) sp[i] = (1 << 16) | (((p >> i) & 1) << 8) | sidx[i];
+      const double amps = (double)(1ull << h->nL) / P;
+      cudaEvent_t ts = tstart(h);
+      if (int rc = launch_one(h, *L0, sp[0], sp[1])) return rc;
+      tend(h, ts, 0, 2.0 * amps * (double)h->amp, L0->flops_per_amp * amps);
+    }
+  }
+  if (h->timing) {
+    cudaEvent_t t1 = ev_get(h);
+    CUDA_TRY(h, cudaEventRecord(t1, h->st_u));
+    h->trecs.push_back({t0, t1, 1, 0.0, 0.0});
+  }
+  // the compute stream continues after both exchange streams
+  CUDA_TRY(h, cudaEventRecord(h->ev_done, h->st_u));
+  CUDA_TRY(h, cudaStreamWaitEvent(h->st, h->ev_done, 0));
+  CUDA_TRY(h, cudaEventRecord(h->ev_done, h->st_x));
+  CUDA_TRY(h, cudaStreamWaitEvent(h->st, h->ev_done, 0));
+  if (L0) {
+    h->stats.sections++;
+    *done = 1;
+  }
   return SV_OK;
 }
 
@@ -610,7 +654,7 @@ int setup_p2p(sv_state* h, void* base_alloc, size_t base_off) {
 // ====================================================================== ABI
 extern "C" {
 
-int sv_abi_version(void) { return 1; }
+int sv_abi_version(void) { return 2; }
 
 const char* sv_last_error(sv_handle h) { return h ? h->err.c_str() : g_last_error.c_str(); }
 
@@ -760,9 +804,14 @@ int sv_destroy(sv_handle h) {
     cudaEventDestroy(r.b);
   }
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
-  for (cudaEvent_t e : h->ev_x)
+  for (void* p : h->xrecv_opened) cudaIpcCloseMemHandle(p);
+  for (cudaEvent_t e : {h->ev_start, h->ev_done, h->ev_pushed[0], h->ev_pushed[1], h->ev_unpacked[0], h->ev_unpacked[1],
+                        h->ev_landed[0], h->ev_landed[1], h->ev_landed[2], h->ev_landed[3]})
     if (e) cudaEventDestroy(e);
   if (h->st_x) cudaStreamDestroy(h->st_x);
+  if (h->st_u) cudaStreamDestroy(h->st_u);
+  for (DevBuf* b : {&h->d_xrecv, &h->d_xsend})
+    if (b->p) cudaFree(b->p);
   if (h->own_stream && h->st) cudaStreamDestroy(h->st);
   cudaGetLastError();
   delete h;
@@ -790,6 +839,7 @@ int sv_synchronize(sv_handle h) {
 
 int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t flags) {
   if (int rc = check_handle(h)) return rc;
+  Nvtx r("sv_apply_circuit n=%d gates=%zu rank=%d/%d", h->n, n_gates, h->rank, h->world);
   if (n_gates && !gates) return fail(h, SV_EINVAL, "null gate array");
   const double t0 = now_ms();
   std::vector<int> pi = h->pi, sigma = h->sigma;
@@ -848,18 +898,11 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
     const Step& st = steps[i];
     switch (st.type) {
       case Step::EXCHANGE: {
-        if (h->p2p && !(flags & SV_EXCHANGE_NCCL) && i + 1 < steps.size() && steps[i + 1].type == Step::SECTION &&
-            h->nL >= SV_R_BITS && si < launch_end[i + 1]) {
-          int done = 0;
-          if (int rc = exchange_pipelined(h, st.ex, h->prog.launches[si], &done)) return rc;
-          if (done) {
-            si++;  // the next section's first launch already ran, piece by piece
-            break;
-          }
-        }
-        cudaEvent_t t = tstart(h);
-        if (int rc = do_exchange(h, st.ex, flags)) return rc;
-        tend(h, t, 1, 0.0, 0.0);
+        const bool next_section = i + 1 < steps.size() && steps[i + 1].type == Step::SECTION &&
+                                  h->nL >= SV_R_BITS && si < launch_end[i + 1];
+        int done = 0;
+        if (int rc = exchange(h, st.ex, flags, next_section ? &h->prog.launches[si] : nullptr, &done)) return rc;
+        if (done) si++;  // the next section's first launch already ran, quarter by quarter
         break;
       }
       case Step::SECTION: {
@@ -876,7 +919,7 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
           const bool gen_input = si == 0 && vidx != -1;  // the deferred basis state: a write-only pass
           if (int rc = launch_one(h, L, 0, 0, si == 0 ? vidx : -1)) return rc;
           const double amps = (double)(1ull << h->nL);
-          tend(h, t, 0, (gen_input ? 1.0 : 2.0) * amps * (double)h->amp, L.flops_per_amp * amps);
+          tend(h, t, gen_input ? 3 : 0, (gen_input ? 1.0 : 2.0) * amps * (double)h->amp, L.flops_per_amp * amps);
           h->stats.sections++;
         }
         break;
@@ -938,6 +981,7 @@ int sv_set_timing(sv_handle h, int enable) {
 
 int sv_norm(sv_handle h, double* out) {
   if (int rc = ready(h)) return rc;
+  Nvtx r("sv_norm");
   if (!out) return fail(h, SV_EINVAL, "null output");
   if (int rc = ensure_dev(h, h->d_scratch, norm_scratch_doubles() * sizeof(double))) return rc;
   CUDA_TRY(h, launch_norm(h->dbl, h->sv, h->nL, (double*)h->d_scratch.p, (double*)h->d_small.p + 8, h->st));
@@ -950,6 +994,7 @@ int sv_norm(sv_handle h, double* out) {
 
 int sv_probabilities(sv_handle h, const int32_t* qubits, int nq, double* host_out) {
   if (int rc = ready(h)) return rc;
+  Nvtx r("sv_probabilities nq=%d", nq);
   if (nq < 0 || nq > 24 || (nq && (!qubits || !host_out))) return fail(h, SV_EINVAL, "bad qubit list (nq <= 24)");
   uint64_t seen = 0;
   std::vector<int> loc_bits, loc_pos;
@@ -1067,6 +1112,7 @@ static uint64_t splitmix64(uint64_t x) {
 
 int sv_sample(sv_handle h, size_t shots, uint64_t seed, uint64_t* host_out) {
   if (int rc = ready(h)) return rc;
+  Nvtx r("sv_sample shots=%zu", shots);
   if (shots == 0) return SV_OK;
   if (!host_out) return fail(h, SV_EINVAL, "null output");
   const int B = std::min(12, h->nL);

@@ -95,6 +95,15 @@ Mode mode() {
 }
 
 // ------------------------------------------------------------------------------------ source
+// Cache hints on the state's loads / stores (SV_STREAM_HINTS=1, measurement switch)
+bool stream_hints() {
+  static const bool on = [] {
+    const char* e = std::getenv("SV_STREAM_HINTS");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 size_t smem_bytes(const Launch& L, bool dbl) {
   const size_t amp = dbl ? 16 : 8;
   const bool no_smem = L.n_phases == 1 && (L.flags & SV_FLAG_FIRST_DIRECT) && (L.flags & SV_FLAG_LAST_DIRECT);
@@ -188,9 +197,17 @@ struct Gen {
       o << "#pragma unroll\n    for (int k = 0; k < 16; k++) { v[k].x = (long long)(b + RO[k]) == vidx ? 1 : 0; v[k].y = 0; }\n";
       return;
     }
-    o << "#pragma unroll\n    for (int k = 0; k < 16; k++) v[k] = psi[b + RO[k]];\n";
+    if (stream_hints())  // the state streams through once per section: evict it first from L1 / L2
+      o << "#pragma unroll\n    for (int k = 0; k < 16; k++) v[k] = __ldcs(psi + b + RO[k]);\n";
+    else
+      o << "#pragma unroll\n    for (int k = 0; k < 16; k++) v[k] = psi[b + RO[k]];\n";
   }
-  void stg() { o << "#pragma unroll\n    for (int k = 0; k < 16; k++) psi[b + RO[k]] = v[k];\n"; }
+  void stg() {
+    if (stream_hints())
+      o << "#pragma unroll\n    for (int k = 0; k < 16; k++) __stcs(psi + b + RO[k], v[k]);\n";
+    else
+      o << "#pragma unroll\n    for (int k = 0; k < 16; k++) psi[b + RO[k]] = v[k];\n";
+  }
 };
 
 struct TmaPlan;
@@ -232,30 +249,30 @@ std::string gen_source(const int* p, const Launch& L, bool dbl, bool virt = fals
   } else {
     o << "  {\n  const uint64_t tile_off = tile_of(expand_tile(blockIdx.x, split_a, split_b));\n";
   }
+  // The tile's HBM loads are issued first (phase 0's registers, or the load step's), so their
+  // latency overlaps the per-CTA DIAGSET factors computed next.
+  o << "  V v[16];\n";
+  o << "  {  // " << (first ? "phase 0 reads HBM directly" : "load: lanes walk the lowest load memory bits") << "\n";
+  g.hbm(first ? H->din : H->load);
+  g.ldg();
+  o << "  }\n";
   if (H->n_sets > 0) {
     o << "  for (int f = tid; f < " << 5 * H->n_sets << "; f += " << nt << ") {\n"
       << "    const int d = c_prog[kH_SETS + f / 5], i = f % 5;\n"
-      << "    ctaf[f] = cta_factor<V>(c_prog[d + 2 + i], c_prog[d + 3 + i], tile_off, P);\n  }\n"
-      << "  __syncthreads();\n";
+      << "    ctaf[f] = cta_factor<V>(c_prog[d + 2 + i], c_prog[d + 3 + i], tile_off, P);\n  }\n";
   }
-  o << "  V v[16];\n";
   if (!first) {
-    o << "  {  // load: lanes walk the lowest load memory bits, scatter into the swizzled tile\n";
-    g.hbm(H->load);
-    g.ldg();
+    o << "  {  // scatter into the swizzled tile\n";
     g.smem(H->load.tw, H->load.rw);
     g.sts();
-    o << "    __syncthreads();\n  }\n";
+    o << "  }\n";
   }
+  if (!first || H->n_sets > 0) o << "  __syncthreads();\n";
   const SvPhase* ph = reinterpret_cast<const SvPhase*>(p + H->phase_off);
   const SvOp* ops = reinterpret_cast<const SvOp*>(p + H->op_off);
   for (int k = 0; k < nph; k++) {
     const bool din = first && k == 0, dout = last && k == nph - 1;
     o << "  {  // phase " << k << "\n";
-    if (din) {
-      g.hbm(H->din);
-      g.ldg();
-    }
     if (!din || !dout) g.smem(ph[k].tw, ph[k].rw);
     if (!din) g.lds();
     for (int i = 0; i < ph[k].op_count; i++) {
@@ -315,7 +332,7 @@ struct TmaPlan {
 int tma_mode() {
   static const int m = [] {
     const char* e = std::getenv("SV_TMA");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : 0;
   }();
   return m;
 }

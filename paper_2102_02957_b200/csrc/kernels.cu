@@ -281,78 +281,52 @@ __global__ void k_sample_resolve(const V* __restrict__ sv, int B, const int64_t*
   }
 }
 
-// ------------------------------------------------------------------ exchange over peer memory
-struct ExDev {
-  int nins;         // number of inserted bits (k m-bits + the split bit h + fixed piece bits)
-  int pos[11];      // insertion positions, ascending
-  int val_my[11];   // bit values on the local side
-  int val_peer[11]; // bit values on the partner side
-};
-
+// ------------------------------------------------------------------ exchange
 __device__ __forceinline__ uint64_t insert_bit(uint64_t x, int p, int v) {
   const uint64_t lo = x & ((1ull << p) - 1);
   return ((x - lo) << 1) | ((uint64_t)v << p) | lo;
 }
 
-// Swap local[x] <-> remote[x'] for every compact index j (2^(nL - k - 1) of them).
-#ifndef SV_XU
-#define SV_XU 8
-#endif
-// Eight pairs per thread per iteration (j, j + stride, ...): eight remote loads in flight per
-// thread keep more NVLink requests outstanding than one.
-template <typename V>
-__global__ void k_exchange_peer(V* __restrict__ local, V* __restrict__ remote, uint64_t count, ExDev e) {
-  constexpr int U = SV_XU;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  auto idx = [&](uint64_t j, uint64_t& x, uint64_t& y) {
-    x = j;
-    y = j;
-    for (int i = 0; i < e.nins; i++) {
-      x = insert_bit(x, e.pos[i], e.val_my[i]);
-      y = insert_bit(y, e.pos[i], e.val_peer[i]);
-    }
-  };
-  uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  for (; j + (U - 1) * stride < count; j += U * stride) {
-    uint64_t x[U], y[U];
-    V a[U], b[U];
-#pragma unroll
-    for (int u = 0; u < U; u++) idx(j + u * stride, x[u], y[u]);
-#pragma unroll
-    for (int u = 0; u < U; u++) {
-      a[u] = local[x[u]];
-      b[u] = remote[y[u]];
-    }
-#pragma unroll
-    for (int u = 0; u < U; u++) {
-      local[x[u]] = b[u];
-      remote[y[u]] = a[u];
-    }
-  }
-  for (; j < count; j += stride) {
-    uint64_t x, y;
-    idx(j, x, y);
-    const V a = local[x];
-    const V b = remote[y];
-    local[x] = b;
-    remote[y] = a;
-  }
-}
-
-// Pack / unpack for the NCCL send/recv exchange: element j of a block (compact index over the
-// local bits that are not exchanged) lives at the index with the exchanged bits inserted
-// (values fixed per block); consecutive j are consecutive amplitudes below the lowest m-bit.
+// Pack / unpack of an exchanged block: element j of a block (compact index over the local bits that
+// are not exchanged) lives at the index with the exchanged bits inserted (values fixed per block);
+// consecutive j are consecutive amplitudes below the lowest inserted bit.  Pack writes the block
+// contiguously (into a local send slot, or straight into a peer's receive slot over NVLink: remote
+// stores only, full lines); unpack scatters a received slot into place.
 struct InsDev {
   int nins;
   int pos[11];  // ascending
   int val[11];
 };
+// Eight elements per thread per iteration: eight loads in flight per thread before any store, so
+// a small grid (the exchange leaves most SMs to the concurrent section) still keeps enough bytes in
+// flight for NVLink (one element per thread topped out near 0.5 of the link).
 template <typename V, bool PACK>
 __global__ void k_pack_bits(V* __restrict__ sv, V* __restrict__ stage, uint64_t first, uint64_t count, InsDev e) {
+  constexpr int U = 8;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += stride) {
+  auto at = [&](uint64_t i) {
     uint64_t x = first + i;
     for (int k = 0; k < e.nins; k++) x = insert_bit(x, e.pos[k], e.val[k]);
+    return x;
+  };
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  for (; i + (U - 1) * stride < count; i += U * stride) {
+    uint64_t x[U];
+    V t[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) x[u] = at(i + u * stride);
+#pragma unroll
+    for (int u = 0; u < U; u++) t[u] = PACK ? sv[x[u]] : stage[i + u * stride];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      if (PACK)
+        stage[i + u * stride] = t[u];
+      else
+        sv[x[u]] = t[u];
+    }
+  }
+  for (; i < count; i += stride) {
+    const uint64_t x = at(i);
     if (PACK)
       stage[i] = sv[x];
     else
@@ -542,58 +516,8 @@ cudaError_t launch_gather(bool dbl, const void* sv, const uint64_t* offs, size_t
   return cudaGetLastError();
 }
 
-cudaError_t launch_exchange_peer(bool dbl, void* local, void* const* peer_bases, int rank, int nL,
-                                 const ExchangeArgs& a, cudaStream_t st, int* launches, unsigned max_blocks) {
-  // rank bits of this rank at the exchanged positions
-  int mine = 0;
-  for (int i = 0; i < a.k; i++) mine |= ((rank >> a.bsel[i]) & 1) << i;
-  const uint64_t count = 1ull << (nL - a.k - 1 - a.nfix);
-  // round t pairs every rank with the one whose subcube bits differ by t (XOR schedule): each
-  // round is a perfect matching, so no GPU serves two peers at once
-  for (int t = 1; t < (1 << a.k); t++) {
-    const int mu = mine ^ t;
-    int partner = rank;
-    for (int i = 0; i < a.k; i++) partner = (partner & ~(1 << a.bsel[i])) | (((mu >> i) & 1) << a.bsel[i]);
-    // my block mu (local bits m = mu) <-> partner's block `mine`; pairs split by bit h
-    ExDev e{};
-    struct PV {
-      int p, vm, vp;
-    } ins[11];
-    int n = 0;
-    for (int i = 0; i < a.k; i++) ins[n++] = {a.m[i], (mu >> i) & 1, (mine >> i) & 1};
-    const int hv = rank < partner ? 0 : 1;
-    ins[n++] = {a.h, hv, hv};
-    for (int i = 0; i < a.nfix; i++) ins[n++] = {a.fix_pos[i], a.fix_val[i], a.fix_val[i]};
-    for (int i = 1; i < n; i++)  // ascending positions
-      for (int j = i; j > 0 && ins[j].p < ins[j - 1].p; j--) {
-        PV t = ins[j];
-        ins[j] = ins[j - 1];
-        ins[j - 1] = t;
-      }
-    e.nins = n;
-    for (int i = 0; i < n; i++) {
-      e.pos[i] = ins[i].p;
-      e.val_my[i] = ins[i].vm;
-      e.val_peer[i] = ins[i].vp;
-    }
-    const int th = 256;
-    unsigned gx = grid_for(count, th);
-    if (max_blocks && gx > max_blocks) gx = max_blocks;  // leave SMs to a concurrent section
-    if (dbl)
-      k_exchange_peer<double2><<<gx, th, 0, st>>>((double2*)local, (double2*)peer_bases[partner],
-                                                                   count, e);
-    else
-      k_exchange_peer<float2><<<gx, th, 0, st>>>((float2*)local, (float2*)peer_bases[partner], count,
-                                                                  e);
-    if (launches) (*launches)++;
-    cudaError_t err = cudaGetLastError();
-    if (err != cudaSuccess) return err;
-  }
-  return cudaSuccess;
-}
-
 cudaError_t launch_pack_bits(bool dbl, bool pack, void* sv, void* stage, uint64_t first, uint64_t count, int nins,
-                             const int* pos, const int* val, cudaStream_t st) {
+                             const int* pos, const int* val, cudaStream_t st, unsigned max_blocks) {
   if (nins > 11) return cudaErrorInvalidValue;
   InsDev e{};
   e.nins = nins;
@@ -606,7 +530,8 @@ cudaError_t launch_pack_bits(bool dbl, bool pack, void* sv, void* stage, uint64_
       std::swap(e.pos[j], e.pos[j - 1]);
       std::swap(e.val[j], e.val[j - 1]);
     }
-  const unsigned g = grid_for(count, 256);
+  unsigned g = grid_for(count, 256);
+  if (max_blocks && g > max_blocks) g = max_blocks;
   if (dbl) {
     if (pack)
       k_pack_bits<double2, true><<<g, 256, 0, st>>>((double2*)sv, (double2*)stage, first, count, e);

@@ -46,22 +46,10 @@ cudaError_t launch_sample_resolve(bool dbl, const void* sv, int B, const int64_t
 // K7: out[i] = sv[offs[i]] if offs[i] != ~0 else 0.
 cudaError_t launch_gather(bool dbl, const void* sv, const uint64_t* offs, size_t cnt, void* out, cudaStream_t st);
 
-// Cross-GPU exchange of k local bits m[] with rank bits b[] (rank-bit indices), peer-memory swap.
-struct ExchangeArgs {
-  int k;
-  int m[8];       // local memory bits, ascending
-  int bsel[8];    // rank-bit index (0..g-1) paired with m[i]
-  int h;          // local bit (not in m) that splits each pair's work between the two ranks
-  int nfix = 0;   // pipelined exchange: only the pairs whose local bits fix_pos[i] equal fix_val[i]
-  int fix_pos[2] = {0, 0};
-  int fix_val[2] = {0, 0};
-};
-cudaError_t launch_exchange_peer(bool dbl, void* local, void* const* peer_bases /*host array [world]*/, int rank,
-                                 int nL, const ExchangeArgs& a, cudaStream_t st, int* launches,
-                                 unsigned max_blocks = 0);
-// NCCL exchange path: pack (stage[i] = sv[x_i]) or unpack (sv[x_i] = stage[i]) elements
-// first .. first + count - 1 of a block, x_i = (first + i) with bit val[k] inserted at pos[k].
+// Exchange: pack (stage[i] = sv[x_i]) or unpack (sv[x_i] = stage[i]) elements first .. first +
+// count - 1 of a block, x_i = (first + i) with bit val[k] inserted at pos[k]; stage may be a peer's
+// buffer mapped over NVLink.  max_blocks caps the grid (0: a full grid).
 cudaError_t launch_pack_bits(bool dbl, bool pack, void* sv, void* stage, uint64_t first, uint64_t count, int nins,
-                             const int* pos, const int* val, cudaStream_t st);
+                             const int* pos, const int* val, cudaStream_t st, unsigned max_blocks = 0);
 
 }  // namespace sv

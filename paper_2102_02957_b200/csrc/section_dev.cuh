@@ -460,7 +460,7 @@ __device__ __forceinline__ void diagset_c(V (&v)[16], int desc, int cb, int tid,
 #pragma unroll
   for (int i = 0; i < 5; i++) {
     if ((TABM >> i) & 1) {
-      F[i] = tab[i * nthr + tid];
+      F[i] = __ldg(tab + i * nthr + tid);  // small per-thread tables: keep them in L1
       if ((CTAM >> i) & 1) F[i] = cmul(F[i], ctaf[5 * SET + i]);
     } else if ((CTAM >> i) & 1) {
       F[i] = ctaf[5 * SET + i];
