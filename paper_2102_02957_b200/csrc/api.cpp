@@ -500,7 +500,30 @@ int setup_p2p(sv_state* h, void* base_alloc, size_t base_off) {
 // L0 (pipelined exchange + section) the pieces are grouped by up to two of its out-of-tile bits and
 // each quarter of its tiles starts on the compute stream as soon as that quarter has landed, while
 // the next quarter is still on NVLink.
-constexpr unsigned kPushGrid = 132;  // CTAs of the push / unpack kernels: SMs left to the sections
+// Exchange tuning (measurement switches; defaults are the measured best): SV_XGRID CTAs of the push /
+// unpack kernels (SMs left to the overlapped section), SV_XSLOT_MB receive-slot size, SV_XPIPE=0
+// runs the exchange without starting the next section's quarters as they land.
+unsigned x_grid() {
+  static const unsigned g = [] {
+    const char* e = std::getenv("SV_XGRID");
+    return e ? (unsigned)std::atoi(e) : 132u;
+  }();
+  return g;
+}
+uint64_t x_slot_bytes() {
+  static const uint64_t b = [] {
+    const char* e = std::getenv("SV_XSLOT_MB");
+    return (e ? (uint64_t)std::atoll(e) : 1024ull) << 20;
+  }();
+  return b;
+}
+bool x_pipe() {
+  static const bool on = [] {
+    const char* e = std::getenv("SV_XPIPE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 int ensure_exchange_engine(sv_state* h, uint64_t slot_amps, bool nccl_path) {
   if (!h->st_x) {
@@ -546,6 +569,7 @@ int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launc
   const bool nccl_path = (flags & SV_EXCHANGE_NCCL) || !h->p2p;
   // split bits: the next section's highest out-of-tile bits that are not exchanged
   int ns = 0, sidx[2] = {0, 0}, sbit[2] = {0, 0};
+  if (L0 && !x_pipe()) L0 = nullptr;
   if (L0 && L0->T >= SV_R_BITS) {
     const SvSecHeader* H = reinterpret_cast<const SvSecHeader*>(h->prog.ints.data() + L0->int_off);
     for (int j = H->n_out - 1; j >= 0 && ns < 2; j--) {
@@ -563,7 +587,7 @@ int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launc
   if (h->nL - k - ns < 0) ns = 0;
   const int P = 1 << ns;
   const uint64_t qblock = 1ull << (h->nL - k - ns);  // elements per (quarter, partner)
-  const uint64_t slot = std::min<uint64_t>(qblock, (1ull << 30) / h->amp);  // <= 1 GiB per slot
+  const uint64_t slot = std::min<uint64_t>(qblock, std::max<uint64_t>(1, x_slot_bytes() / h->amp));
   if (int rc = ensure_exchange_engine(h, slot, nccl_path)) return rc;
   h->stats.bytes_sent += (uint64_t)((1ull << k) - 1) * (1ull << (h->nL - k)) * h->amp;
   h->stats.exchanges += k;
@@ -602,7 +626,7 @@ int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launc
         if (q >= 2) CUDA_TRY(h, cudaStreamWaitEvent(h->st_x, h->ev_unpacked[b], 0));  // my slot b is free
         if (nccl_path) {
           char* sb = send + (size_t)b * slot * h->amp;
-          CUDA_TRY(h, launch_pack_bits(h->dbl, true, h->sv, sb, off, cnt, nins, pos, val, h->st_x, kPushGrid));
+          CUDA_TRY(h, launch_pack_bits(h->dbl, true, h->sv, sb, off, cnt, nins, pos, val, h->st_x, x_grid()));
           COMM_TRY(h, h->comm->group_start());
           COMM_TRY(h, h->comm->send(sb, cnt * h->amp, partner, h->st_x));
           COMM_TRY(h, h->comm->recv(recv + (size_t)b * slot * h->amp, cnt * h->amp, partner, h->st_x));
@@ -610,14 +634,14 @@ int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launc
         } else {
           if (int rc = barrier(h, h->st_x)) return rc;  // the partner's slot b is free too
           char* dst = (char*)h->peer_xrecv[partner] + (size_t)b * slot * h->amp;
-          CUDA_TRY(h, launch_pack_bits(h->dbl, true, h->sv, dst, off, cnt, nins, pos, val, h->st_x, kPushGrid));
+          CUDA_TRY(h, launch_pack_bits(h->dbl, true, h->sv, dst, off, cnt, nins, pos, val, h->st_x, x_grid()));
           if (int rc = barrier(h, h->st_x)) return rc;  // every push of this piece has landed
         }
         h->stats.kernel_launches += 2;
         CUDA_TRY(h, cudaEventRecord(h->ev_pushed[b], h->st_x));
         CUDA_TRY(h, cudaStreamWaitEvent(h->st_u, h->ev_pushed[b], 0));
         CUDA_TRY(h, launch_pack_bits(h->dbl, false, h->sv, recv + (size_t)b * slot * h->amp, off, cnt, nins, pos, val,
-                                     h->st_u, kPushGrid));
+                                     h->st_u, x_grid()));
         CUDA_TRY(h, cudaEventRecord(h->ev_unpacked[b], h->st_u));
       }
     }

@@ -95,15 +95,6 @@ Mode mode() {
 }
 
 // ------------------------------------------------------------------------------------ source
-// Cache hints on the state's loads / stores (SV_STREAM_HINTS=1, measurement switch)
-bool stream_hints() {
-  static const bool on = [] {
-    const char* e = std::getenv("SV_STREAM_HINTS");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
-
 size_t smem_bytes(const Launch& L, bool dbl) {
   const size_t amp = dbl ? 16 : 8;
   const bool no_smem = L.n_phases == 1 && (L.flags & SV_FLAG_FIRST_DIRECT) && (L.flags & SV_FLAG_LAST_DIRECT);
@@ -197,18 +188,55 @@ struct Gen {
       o << "#pragma unroll\n    for (int k = 0; k < 16; k++) { v[k].x = (long long)(b + RO[k]) == vidx ? 1 : 0; v[k].y = 0; }\n";
       return;
     }
-    if (stream_hints())  // the state streams through once per section: evict it first from L1 / L2
-      o << "#pragma unroll\n    for (int k = 0; k < 16; k++) v[k] = __ldcs(psi + b + RO[k]);\n";
-    else
-      o << "#pragma unroll\n    for (int k = 0; k < 16; k++) v[k] = psi[b + RO[k]];\n";
+    o << "#pragma unroll\n    for (int k = 0; k < 16; k++) v[k] = psi[b + RO[k]];\n";
   }
-  void stg() {
-    if (stream_hints())
-      o << "#pragma unroll\n    for (int k = 0; k < 16; k++) __stcs(psi + b + RO[k], v[k]);\n";
-    else
-      o << "#pragma unroll\n    for (int k = 0; k < 16; k++) psi[b + RO[k]] = v[k];\n";
-  }
+  void stg() { o << "#pragma unroll\n    for (int k = 0; k < 16; k++) psi[b + RO[k]] = v[k];\n"; }
 };
+
+// Per-CTA DIAGSET factors (out-of-tile terms, program.h): the product of each factor's terms is
+// emitted as straight-line code with the masks and coefficient offsets as immediates, a balanced
+// product tree per factor, one factor per warp (lane 0; warp-uniform branches).  The interpreter's
+// loop over the terms (a dependent chain with a constant-bank load per term, 10 threads busy)
+// stalled every warp of a QFT tile at the following barrier (ncu: barrier stalls dominant, ADU 28%).
+void emit_cta_factors(std::ostringstream& o, const int* p, int nt) {
+  const SvSecHeader* H = reinterpret_cast<const SvSecHeader*>(p);
+  const int nf = 5 * H->n_sets, nw = std::max(1, nt / 32);
+  o << "  if ((tid & 31) == 0) {\n    const V one = cone<V>();\n    (void)one;\n";
+  for (int w = 0; w < nw && w < nf; w++) {
+    o << "    if ((tid >> 5) == " << w << ") {\n";
+    for (int f = w; f < nf; f += nw) {
+      const int d = H->set_desc[f / 5], i = f % 5;
+      const int b = p[d + 2 + i], e = p[d + 3 + i];
+      std::vector<std::string> terms;
+      for (int t = b; t < e; t += 3) {
+        const unsigned long long M = (unsigned long long)(uint32_t)p[t] | ((unsigned long long)(uint32_t)p[t + 1] << 32);
+        terms.push_back("((tile_off & " + std::to_string(M) + "ull) == " + std::to_string(M) + "ull ? P(" +
+                        std::to_string(p[t + 2]) + ") : one)");
+      }
+      if (terms.empty()) {
+        o << "      ctaf[" << f << "] = one;\n";
+        continue;
+      }
+      // four interleaved accumulators: short dependency chains, few live registers (the tile's loads
+      // are already in flight in 64 registers)
+      const size_t na = std::min<size_t>(4, terms.size());
+      o << "      {\n";
+      for (size_t k = 0; k < na; k++) o << "        V a" << k << " = " << terms[k] << ";\n";
+      for (size_t k = na; k < terms.size(); k++) {
+        const std::string& t = terms[k];  // "((cond) ? P(i) : one)" -> multiply only where the bits are set
+        const size_t q = t.find(" ? ");
+        o << "        if (" << t.substr(1, q - 1) << ") a" << (k % na) << " = cmul(a" << (k % na) << ", "
+          << t.substr(q + 3, t.find(" : ") - q - 3) << ");\n";
+      }
+      std::string r = "a0";
+      if (na >= 2) r = "cmul(a0, a1)";
+      if (na >= 3) r = "cmul(" + r + ", " + (na == 4 ? std::string("cmul(a2, a3)") : std::string("a2")) + ")";
+      o << "        ctaf[" << f << "] = " << r << ";\n      }\n";
+    }
+    o << "    }\n";
+  }
+  o << "  }\n";
+}
 
 struct TmaPlan;
 void emit_tma_coords(std::ostringstream& o, const TmaPlan& TP, const char* base, const char* call);
@@ -256,11 +284,7 @@ std::string gen_source(const int* p, const Launch& L, bool dbl, bool virt = fals
   g.hbm(first ? H->din : H->load);
   g.ldg();
   o << "  }\n";
-  if (H->n_sets > 0) {
-    o << "  for (int f = tid; f < " << 5 * H->n_sets << "; f += " << nt << ") {\n"
-      << "    const int d = c_prog[kH_SETS + f / 5], i = f % 5;\n"
-      << "    ctaf[f] = cta_factor<V>(c_prog[d + 2 + i], c_prog[d + 3 + i], tile_off, P);\n  }\n";
-  }
+  if (H->n_sets > 0) emit_cta_factors(o, p, nt);
   if (!first) {
     o << "  {  // scatter into the swizzled tile\n";
     g.smem(H->load.tw, H->load.rw);
@@ -513,10 +537,8 @@ std::string gen_source_tma(const int* p, const Launch& L, bool dbl, const TmaPla
     << "    const uint64_t tile_off = tile_of(expand_tile(blk, split_a, split_b));\n"
     << "    V* const sm = slots + s * TILE;\n";
   if (H->n_sets > 0) {
-    o << "    for (int f = tid; f < " << 5 * H->n_sets << "; f += " << nt << ") {\n"
-      << "      const int d = c_prog[kH_SETS + f / 5], i = f % 5;\n"
-      << "      ctaf[f] = cta_factor<V>(c_prog[d + 2 + i], c_prog[d + 3 + i], tile_off, P);\n    }\n"
-      << "    __syncthreads();\n";
+    emit_cta_factors(o, p, nt);
+    o << "    __syncthreads();\n";
   }
   o << "    mbar_wait_parity(&bar[s], (j / S) & 1);\n";
   o << "    V v[16];\n";
