@@ -115,7 +115,7 @@ typedef struct sv_stats {
   uint64_t timed_input_sections;
   double input_section_ms;
   double input_section_bytes;
-} sv_stats;
+} sv_stats_t;
 
 /* ---- lifetime ------------------------------------------------------------------------- */
 /* One GPU (the caller's current CUDA device), state |0..0>, memory allocated by the library. */
@@ -129,8 +129,10 @@ int sv_create(int n_qubits, int chunk_bits, sv_precision prec, sv_handle* out);
 int sv_create_dist(int n_qubits, int chunk_bits, sv_precision prec, int rank, int world,
                    const void* nccl_unique_id, void* ext_dev_buf, size_t ext_bytes,
                    void* cuda_stream, sv_handle* out);
+/* Release the handle: its shard (unless ext_dev_buf), stream (unless the caller's), communicator
+ * and peer mappings; waits for the handle's queued work first.  NULL is a no-op.  Always SV_OK. */
 int sv_destroy(sv_handle h);
-/* Write ncclGetUniqueId() into out (128 bytes). */
+/* Write ncclGetUniqueId() into out (128 bytes): the bootstrap of P:137-143's process grid. */
 int sv_nccl_unique_id(void* out128);
 
 /* ---- in-process virtual world (testing the multi-GPU path on one device) ----------------
@@ -164,11 +166,13 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
 int sv_synchronize(sv_handle h);
 
 /* ---- readout (all collective; results on every rank) --------------------------------- */
-/* host_out[i] = amplitude of LOGICAL index logical_idx[i] (cnt complex values, amp dtype). */
+/* host_out[i] = amplitude of LOGICAL index logical_idx[i] (cnt complex values, amp dtype): the
+ * paper's output state read through the tracked permutation (DESIGN R7).
+ * SV_EINVAL for an index >= 2^n or null pointers. */
 int sv_get_amplitudes(sv_handle h, const uint64_t* logical_idx, size_t cnt, void* host_out);
 /* Full state in LOGICAL order into host_out (2^n complex, amp dtype); written on rank 0 only. */
 int sv_get_state(sv_handle h, void* host_out);
-/* sum |a|^2 */
+/* *out = sum_x |a_x|^2 (unitarity check, north_star).  SV_EINVAL if out is NULL. */
 int sv_norm(sv_handle h, double* out);
 /* Marginal probabilities over LOGICAL qubits Q (qubits[0] -> bit 0 of the output index),
  * host_out has 2^nq doubles, nq <= 24.  p[y] = sum_{x : x|Q = y} |a_x|^2 (DESIGN R17). */
@@ -176,10 +180,17 @@ int sv_probabilities(sv_handle h, const int32_t* qubits, int nq, double* host_ou
 /* shots samples of LOGICAL basis indices from |a|^2 into host_out; u_s = (splitmix64(seed ^ s)
  * >> 11) * 2^-53 is inverted through the CDF in memory order (DESIGN R16). */
 int sv_sample(sv_handle h, size_t shots, uint64_t seed, uint64_t* host_out);
-/* logical_to_physical[q] = paper-physical position of logical qubit q (the pass's pi). */
+/* logical_to_physical[q] = paper-physical position of logical qubit q: the permutation pi the
+ * blocking pass leaves behind ("the order of qubits is changed").  Host only, no sync.
+ * SV_EINVAL if an argument is NULL; the caller's array has n entries. */
 int sv_get_permutation(sv_handle h, int32_t* logical_to_physical);
-/* Cumulative counters since creation / the last sv_stats_reset (synchronizes when timing). */
-int sv_stats_get(sv_handle h, sv_stats* out);
+/* Cumulative counters since creation / the last sv_stats_reset (synchronizes when timing).
+ * sv_stats is SURVEY §8(b)'s name; sv_stats_get the same call.  Counts what the blocking pass and
+ * the executor did (sections = the paper's blocked passes over the chunks, P:383, P:386-394;
+ * chunk_swaps; exchanges / bytes_sent).  Errors: SV_EINVAL (null argument),
+ * SV_ECUDA (reading the timing events). */
+int sv_stats(sv_handle h, struct sv_stats* out);
+int sv_stats_get(sv_handle h, struct sv_stats* out);
 int sv_stats_reset(sv_handle h);
 /* enable != 0: bracket every section / exchange / per-gate launch with CUDA events on the
  * handle's stream and accumulate device times into sv_stats (small overhead per launch). */

@@ -44,7 +44,7 @@ class Stats(ctypes.Structure):
 
 EXPORTS = ["sv_create", "sv_create_dist", "sv_world_create", "sv_world_destroy", "sv_create_local", "sv_destroy", "sv_nccl_unique_id", "sv_reset", "sv_apply_circuit",
            "sv_synchronize", "sv_get_amplitudes", "sv_get_state", "sv_norm", "sv_probabilities", "sv_sample",
-           "sv_get_permutation", "sv_stats_get", "sv_stats_reset", "sv_set_timing", "sv_last_error", "sv_block_circuit", "sv_plan_circuit",
+           "sv_get_permutation", "sv_stats", "sv_stats_get", "sv_stats_reset", "sv_set_timing", "sv_last_error", "sv_block_circuit", "sv_plan_circuit",
            "sv_compile_circuit", "sv_jit_compile_circuit", "sv_jit_mode", "sv_jit_wait", "sv_host_create", "sv_host_destroy", "sv_host_reset",
            "sv_host_apply_circuit", "sv_host_get_state", "sv_host_norm", "sv_host_probabilities",
            "sv_host_last_error", "sv_free",
@@ -82,6 +82,7 @@ def lib():
         "sv_probabilities": ([vp, ip, i32, dp], i32),
         "sv_sample": ([vp, sz, u64, vp], i32),
         "sv_get_permutation": ([vp, ip], i32),
+        "sv_stats": ([vp, ctypes.POINTER(Stats)], i32),
         "sv_stats_get": ([vp, ctypes.POINTER(Stats)], i32),
         "sv_stats_reset": ([vp], i32),
         "sv_set_timing": ([vp, i32], i32),

@@ -116,7 +116,7 @@ struct sv_state {
   cudaEvent_t ev_start = nullptr, ev_pushed[2] = {}, ev_unpacked[2] = {}, ev_landed[4] = {}, ev_done = nullptr;
 
   Program prog;
-  sv_stats stats{};
+  sv_stats_t stats{};
   std::string err;
   bool basis_pending = false;  // state is exactly |basis_index> (set by sv_reset)
   uint64_t basis_index = 0;
@@ -495,8 +495,10 @@ int setup_p2p(sv_state* h, void* base_alloc, size_t base_off) {
 //   NCCL path (SV_EXCHANGE_NCCL, the comparator of P:420's send/recv): pack into a local send slot,
 //     grouped ncclSend / ncclRecv, unpack.
 // Pieces alternate between two slots: the transport of piece q (stream st_x) overlaps the unpack of
-// piece q - 1 (stream st_u); two stream-ordered barriers per piece order a push after the partner's
-// unpack of that slot and an unpack after the partner's push.  With the next section's first launch
+// piece q - 1 (stream st_u); one stream-ordered barrier per piece (peer path) certifies that piece
+// q has landed everywhere and that piece q - 1 is unpacked everywhere, which frees its slot for
+// piece q + 1 (a barrier at the start orders the first push after the previous exchange's
+// unpacks).  With the next section's first launch
 // L0 (pipelined exchange + section) the pieces are grouped by up to two of its out-of-tile bits and
 // each quarter of its tiles starts on the compute stream as soon as that quarter has landed, while
 // the next quarter is still on NVLink.
@@ -604,6 +606,10 @@ int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launc
   }
   char* recv = (char*)h->d_xrecv.p;
   char* send = (char*)h->d_xsend.p;
+  // every rank is done with everything before this exchange — its unpacks of the previous one
+  // included — before any push lands in a peer's slot
+  if (!nccl_path)
+    if (int rc = barrier(h, h->st_x)) return rc;
   int pos[11], val[11];
   uint64_t q = 0;
   for (int p = 0; p < P; p++) {
@@ -623,8 +629,8 @@ int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launc
       for (uint64_t off = 0; off < qblock; off += slot, q++) {
         const uint64_t cnt = std::min<uint64_t>(slot, qblock - off);
         const int b = (int)(q & 1);
-        if (q >= 2) CUDA_TRY(h, cudaStreamWaitEvent(h->st_x, h->ev_unpacked[b], 0));  // my slot b is free
         if (nccl_path) {
+          if (q >= 2) CUDA_TRY(h, cudaStreamWaitEvent(h->st_x, h->ev_unpacked[b], 0));  // my slot b is free
           char* sb = send + (size_t)b * slot * h->amp;
           CUDA_TRY(h, launch_pack_bits(h->dbl, true, h->sv, sb, off, cnt, nins, pos, val, h->st_x, x_grid()));
           COMM_TRY(h, h->comm->group_start());
@@ -632,10 +638,13 @@ int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launc
           COMM_TRY(h, h->comm->recv(recv + (size_t)b * slot * h->amp, cnt * h->amp, partner, h->st_x));
           COMM_TRY(h, h->comm->group_end());
         } else {
-          if (int rc = barrier(h, h->st_x)) return rc;  // the partner's slot b is free too
+          // One barrier per piece: after it every push of piece q has landed AND every rank's
+          // unpack of piece q - 1 is done (each rank's exchange stream waited for its own first),
+          // so piece q + 1 may be pushed into the slot piece q - 1 used.
           char* dst = (char*)h->peer_xrecv[partner] + (size_t)b * slot * h->amp;
           CUDA_TRY(h, launch_pack_bits(h->dbl, true, h->sv, dst, off, cnt, nins, pos, val, h->st_x, x_grid()));
-          if (int rc = barrier(h, h->st_x)) return rc;  // every push of this piece has landed
+          if (q >= 1) CUDA_TRY(h, cudaStreamWaitEvent(h->st_x, h->ev_unpacked[b ^ 1], 0));
+          if (int rc = barrier(h, h->st_x)) return rc;
         }
         h->stats.kernel_launches += 2;
         CUDA_TRY(h, cudaEventRecord(h->ev_pushed[b], h->st_x));
@@ -980,7 +989,7 @@ int sv_get_permutation(sv_handle h, int32_t* out) {
   return SV_OK;
 }
 
-int sv_stats_get(sv_handle h, sv_stats* out) {
+int sv_stats_get(sv_handle h, sv_stats_t* out) {
   if (!h || !out) return fail(h, SV_EINVAL, "null argument");
   if (int rc = drain_timing(h)) return rc;
   *out = h->stats;
@@ -990,10 +999,12 @@ int sv_stats_get(sv_handle h, sv_stats* out) {
   return SV_OK;
 }
 
+int sv_stats(sv_handle h, sv_stats_t* out) { return sv_stats_get(h, out); }
+
 int sv_stats_reset(sv_handle h) {
   if (!h) return fail(h, SV_EINVAL, "null handle");
   if (int rc = drain_timing(h)) return rc;
-  h->stats = sv_stats{};
+  h->stats = sv_stats_t{};
   return SV_OK;
 }
 

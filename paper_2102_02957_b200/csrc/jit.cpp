@@ -238,9 +238,7 @@ void emit_cta_factors(std::ostringstream& o, const int* p, int nt) {
   o << "  }\n";
 }
 
-struct TmaPlan;
-void emit_tma_coords(std::ostringstream& o, const TmaPlan& TP, const char* base, const char* call);
-std::string gen_source(const int* p, const Launch& L, bool dbl, bool virt = false, const TmaPlan* pf = nullptr) {
+std::string gen_source(const int* p, const Launch& L, bool dbl, bool virt = false) {
   const SvSecHeader* H = reinterpret_cast<const SvSecHeader*>(p);
   Gen g;
   g.virt = virt;
@@ -256,8 +254,7 @@ std::string gen_source(const int* p, const Launch& L, bool dbl, bool virt = fals
   o << "\n#include \"section_dev.cuh\"\nusing namespace sv;\ntypedef " << (dbl ? "double2" : "float2") << " V;\n";
   o << "extern \"C\" __global__ void __launch_bounds__(" << nt << ", " << resident_ctas(H->T, nt, has_dense(p))
     << ") sv_sec(V* __restrict__ psi, const V* __restrict__ aux, int split_a, int split_b, long long vidx, "
-    << (pf ? "const __grid_constant__ SvTmap tm, unsigned long long ntiles, " : "") << coef_param_decl_impl(L, dbl)
-    << ") {\n";
+    << coef_param_decl_impl(L, dbl) << ") {\n";
   o << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n"
     << "  V* sm = reinterpret_cast<V*>(smem_raw);\n"
     << "  V* ctaf = reinterpret_cast<V*>(smem_raw + (sizeof(V) << " << H->T << "));\n"
@@ -266,17 +263,7 @@ std::string gen_source(const int* p, const Launch& L, bool dbl, bool virt = fals
   g.arr("int", "OB", H->out_bits, H->n_out);
   o << "  auto tile_of = [&](uint64_t t) {\n    uint64_t r = 0;\n#pragma unroll\n    for (int j = 0; j < "
     << H->n_out << "; j++) r |= ((t >> j) & 1ull) << OB[j];\n    return r;\n  };\n";
-  if (pf) {  // persistent CTAs; the TMA stages each CTA's next tile in L2 during this one
-    o << "  auto prefetch = [&](uint64_t b) {\n";
-    emit_tma_coords(o, *pf, "tile_of(expand_tile(b, split_a, split_b))", "tma_prefetch_l2");
-    o << "  };\n"
-      << "  if (tid == 0) prefetch(blockIdx.x);\n"
-      << "#pragma unroll 1\n  for (uint64_t blk = blockIdx.x; blk < ntiles; blk += gridDim.x) {\n"
-      << "  if (tid == 0 && blk + gridDim.x < ntiles) prefetch(blk + gridDim.x);\n"
-      << "  const uint64_t tile_off = tile_of(expand_tile(blk, split_a, split_b));\n";
-  } else {
-    o << "  {\n  const uint64_t tile_off = tile_of(expand_tile(blockIdx.x, split_a, split_b));\n";
-  }
+  o << "  {\n  const uint64_t tile_off = tile_of(expand_tile(blockIdx.x, split_a, split_b));\n";
   // The tile's HBM loads are issued first (phase 0's registers, or the load step's), so their
   // latency overlaps the per-CTA DIAGSET factors computed next.
   o << "  V v[16];\n";
@@ -324,13 +311,14 @@ std::string gen_source(const int* p, const Launch& L, bool dbl, bool virt = fals
     g.stg();
     o << "  }\n";
   }
-  if (pf) o << "  __syncthreads();  // the next tile reuses shared memory\n";
   o << "  }\n}\n";
   return o.str();
 }
 
 // ------------------------------------------------------------------------------- TMA variant
-// Tile loads by the Tensor Memory Accelerator (cp.async.bulk.tensor, SASS UTMALDG): the shard is
+// Tile loads by the Tensor Memory Accelerator (cp.async.bulk.tensor, SASS UTMALDG) — an opt-in
+// variant (SV_TMA), measured slower than the plain kernel (QFT30 7.39 vs 6.65 ms per
+// section before the DIAGSET prologue fix; only 3 tiles per SM compute at a time).  The shard is
 // described to the TMA as a tensor of up to 5 dimensions cut at the starts of the tile's runs of
 // consecutive memory bits, so one box (2^w0 x ... amplitudes, rows of >= 128 bytes) is a whole
 // tile, or 2^E boxes when more runs than dimensions remain (E "enumerated" tile bits).  A
@@ -351,8 +339,8 @@ struct TmaPlan {
   int boxbits = 0;
 };
 
-// SV_TMA (measurement switch): 0 off; 1 / 2: TMA L2 prefetch of the next tile in the persistent plain
-// kernel for sections without dense gates / every section; 3 / 4: the shared-memory slot ring
+// SV_TMA (opt-in, measured slower — DESIGN §6): 0 off (default); 1 / 2: the TMA-fed slot ring for
+// sections without dense gates / for every section with a tile of <= 11 bits
 int tma_mode() {
   static const int m = [] {
     const char* e = std::getenv("SV_TMA");
@@ -367,9 +355,9 @@ TmaPlan tma_plan(const int* p, const Launch& L, bool dbl) {
   const SvSecHeader* H = reinterpret_cast<const SvSecHeader*>(p);
   const int T = H->T, nL = H->T + H->n_out;
   const int md = tma_mode();
-  if (md == 0 || T < SV_R_BITS || (md >= 3 && T > 11)) return P;
-  if ((md == 1 || md == 3) && has_dense(p)) return P;
-  if (md >= 3 && kTmaSlots * (size_t(dbl ? 16 : 8) << T) + 5 * SV_MAX_SETS * 16 + 64 > 227 * 1024) return P;
+  if (md == 0 || T < SV_R_BITS || T > 11) return P;
+  if (md == 1 && has_dense(p)) return P;
+  if (kTmaSlots * (size_t(dbl ? 16 : 8) << T) + 5 * SV_MAX_SETS * 16 + 64 > 227 * 1024) return P;
   (void)L;
   const int* tb = H->tile_bits;
   const int G = dbl ? 3 : 4;  // rows of >= 128 bytes
@@ -468,10 +456,7 @@ void emit_tma_coords(std::ostringstream& o, const TmaPlan& TP, const char* base,
     else
       o << "      c[" << d << "] = (int)((a >> " << TP.lo[d] << ") & " << mask << "ull);\n";
   }
-  if (std::strcmp(call, "tma_load") == 0)
-    o << "      tma_load<" << TP.D << ">(slots + s * TILE + e * BOX, &tm, c[0], c[1], c[2], c[3], c[4], &bar[s]);\n    }\n";
-  else
-    o << "      " << call << "<" << TP.D << ">(&tm, c[0], c[1], c[2], c[3], c[4]);\n    }\n";
+  o << "      " << call << "<" << TP.D << ">(slots + s * TILE + e * BOX, &tm, c[0], c[1], c[2], c[3], c[4], &bar[s]);\n    }\n";
 }
 
 int tma_ctas_per_sm(const Launch& L, bool dbl) {
@@ -638,7 +623,6 @@ struct Entry {
   cudaKernel_t kern = nullptr;
   std::string err;
   bool tma = false;  // the TMA-fed persistent variant (gen_source_tma), with its tile plan
-  bool pf = false;   // the persistent plain variant with TMA L2 prefetch of the next tile
   TmaPlan tp;
   std::atomic<int> occ{0};  // resident CTAs on the device of the TMA variant (its persistent grid)
 };
@@ -648,11 +632,10 @@ struct Entry {
 std::string source_for(const int* p, const Launch& L, bool dbl, bool virt, Entry& e) {
   if (!virt) {
     e.tp = tma_plan(p, L, dbl);
-    e.tma = e.tp.ok && tma_mode() >= 3;
-    e.pf = e.tp.ok && tma_mode() <= 2;
+    e.tma = e.tp.ok;
   }
   if (e.tma) return gen_source_tma(p, L, dbl, e.tp);
-  return gen_source(p, L, dbl, virt, e.pf ? &e.tp : nullptr);
+  return gen_source(p, L, dbl, virt);
 }
 
 struct Job {
@@ -1037,7 +1020,7 @@ bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const double* 
   }
   const unsigned threads = 1u << (L.T - SV_R_BITS);
   const unsigned long long ntiles = 1ull << (L.n_out - (split_a ? 1 : 0) - (split_b ? 1 : 0));
-  if (e->tma || e->pf) {
+  if (e->tma) {
     alignas(64) unsigned char tmap[128];
     if (!encode_tmap(e->tp, dbl, sv, tmap)) {
       *err = cudaErrorInvalidValue;
@@ -1047,8 +1030,7 @@ bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const double* 
       int nb = 0, sms = 0;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, reinterpret_cast<const void*>(e->kern), (int)threads,
-                                                        e->tma ? tma_smem_bytes(L, dbl) : smem_bytes(L, dbl)) !=
-              cudaSuccess ||
+                                                        tma_smem_bytes(L, dbl)) != cudaSuccess ||
           nb < 1)
         nb = 1;
       cudaGetLastError();
@@ -1058,7 +1040,7 @@ bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const double* 
     void* args[] = {&a0, &a1, &a2, &a3, &av, tmap, &nt, a4};
     const unsigned grid = (unsigned)std::min<unsigned long long>(ntiles, (unsigned long long)e->occ);
     *err = cudaLaunchKernel(reinterpret_cast<const void*>(e->kern), dim3(grid), dim3(threads), args,
-                            e->tma ? tma_smem_bytes(L, dbl) : smem_bytes(L, dbl), st);
+                            tma_smem_bytes(L, dbl), st);
   } else {
     void* args[] = {&a0, &a1, &a2, &a3, &av, a4};
     *err = cudaLaunchKernel(reinterpret_cast<const void*>(e->kern), dim3((unsigned)ntiles), dim3(threads), args,

@@ -71,7 +71,8 @@ __global__ void k_gate_diag(V* __restrict__ sv, uint64_t N, int c0, int c1, V d0
   for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < N; x += stride) {
     const int b0 = c0 < 100 ? (int)((x >> c0) & 1) : c0 - 200;
     const int b1 = c1 < 100 ? (int)((x >> c1) & 1) : c1 - 200;
-    sv[x] = cmul(sv[x], sel4(b0 | (b1 << 1), d0, d1, d2, d3));
+    const V f = sel4(b0 | (b1 << 1), d0, d1, d2, d3);
+    if (f.x != 1 || f.y != 0) sv[x] = cmul(sv[x], f);  // untouched amplitudes are not read (CP: 1/4)
   }
 }
 

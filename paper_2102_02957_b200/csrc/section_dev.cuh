@@ -411,27 +411,6 @@ __device__ __forceinline__ void tma_load(void* dst, const SvTmap* tm, int c0, in
         : "memory");
 }
 
-// L2 prefetch of a tile through the same tensor map (no shared memory, no registers held): the
-// persistent plain kernel asks the TMA to stage its next tile in L2 while it computes this one.
-template <int D>
-__device__ __forceinline__ void tma_prefetch_l2(const SvTmap* tm, int c0, int c1, int c2, int c3, int c4) {
-  const int c[5] = {c0, c1, c2, c3, c4};
-  const unsigned long long t = reinterpret_cast<unsigned long long>(tm);
-  if constexpr (D == 1)
-    asm volatile("cp.async.bulk.prefetch.tensor.1d.L2.global.tile [%0, {%1}];" ::"l"(t), "r"(c[0]) : "memory");
-  else if constexpr (D == 2)
-    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(t), "r"(c[0]), "r"(c[1]) : "memory");
-  else if constexpr (D == 3)
-    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(t), "r"(c[0]), "r"(c[1]),
-                 "r"(c[2]) : "memory");
-  else if constexpr (D == 4)
-    asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(t), "r"(c[0]), "r"(c[1]),
-                 "r"(c[2]), "r"(c[3]) : "memory");
-  else
-    asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(t), "r"(c[0]),
-                 "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]) : "memory");
-}
-
 // Tile index of launch block b when the launch covers only the tiles whose out-bit indices
 // (split & 255) have the value ((split >> 8) & 1); split = 0: all tiles.  Lower index first.
 __device__ __forceinline__ uint64_t expand_tile(uint64_t b, int split_a, int split_b) {

@@ -241,3 +241,13 @@ def test_nccl_exchange_plan_is_the_default_plan():
         b, pb, sb = sv.plan_circuit(circ, n, 9, g, flags=sv.SV_FREE_LAYOUT)
         assert np.array_equal(a, b) and np.array_equal(pa, pb) and np.array_equal(sa, sb)
         assert any(int(r["kind"]) == sv.SV_EXCHANGE for r in a)
+
+
+def test_header_compiles_as_c_and_cpp():
+    # include/sv.h is a plain C ABI: it must compile on its own as C99 and as C++
+    import shutil
+    import subprocess
+    hdr = os.path.join(ROOT, "include", "sv.h")
+    for cc, lang in (("gcc", ["-x", "c", "-std=c99"]), ("g++", ["-x", "c++", "-std=c++17"])):
+        if shutil.which(cc):
+            subprocess.run([cc, "-fsyntax-only", "-Wall", "-Werror", *lang, hdr], check=True)
