@@ -112,8 +112,9 @@ struct sv_state {
   std::vector<void*> xrecv_opened;
   bool xrecv_shared = false;
   uint64_t xslot = 0;             // amplitudes per slot
-  cudaStream_t st_x = nullptr, st_u = nullptr;
+  cudaStream_t st_x = nullptr, st_u = nullptr, st_p = nullptr;
   cudaEvent_t ev_start = nullptr, ev_pushed[2] = {}, ev_unpacked[2] = {}, ev_landed[4] = {}, ev_done = nullptr;
+  cudaEvent_t ev_packed[2] = {};
 
   Program prog;
   sv_stats_t stats{};
@@ -519,6 +520,15 @@ uint64_t x_slot_bytes() {
   }();
   return b;
 }
+// SV_XCE=0: the peer path pushes with a small-grid kernel (remote stores) instead of packing into a
+// local send slot and copying it to the peer with the copy engines (default)
+bool x_ce() {
+  static const bool on = [] {
+    const char* e = std::getenv("SV_XCE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 bool x_pipe() {
   static const bool on = [] {
     const char* e = std::getenv("SV_XPIPE");
@@ -533,8 +543,10 @@ int ensure_exchange_engine(sv_state* h, uint64_t slot_amps, bool nccl_path) {
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
     CUDA_TRY(h, cudaStreamCreateWithPriority(&h->st_x, cudaStreamNonBlocking, hi));
     CUDA_TRY(h, cudaStreamCreateWithPriority(&h->st_u, cudaStreamNonBlocking, hi));
+    CUDA_TRY(h, cudaStreamCreateWithPriority(&h->st_p, cudaStreamNonBlocking, hi));
     for (cudaEvent_t* e : {&h->ev_start, &h->ev_done, &h->ev_pushed[0], &h->ev_pushed[1], &h->ev_unpacked[0],
-                           &h->ev_unpacked[1], &h->ev_landed[0], &h->ev_landed[1], &h->ev_landed[2], &h->ev_landed[3]})
+                           &h->ev_unpacked[1], &h->ev_landed[0], &h->ev_landed[1], &h->ev_landed[2], &h->ev_landed[3],
+                           &h->ev_packed[0], &h->ev_packed[1]})
       CUDA_TRY(h, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   }
   if (h->xslot < slot_amps) {  // collective: every rank grows its slots at the same exchange
@@ -544,7 +556,9 @@ int ensure_exchange_engine(sv_state* h, uint64_t slot_amps, bool nccl_path) {
     if (int rc = ensure_dev(h, h->d_xrecv, 2 * slot_amps * h->amp)) return rc;
     h->xslot = slot_amps;
   }
-  if (nccl_path) return ensure_dev(h, h->d_xsend, 2 * h->xslot * h->amp);
+  if (nccl_path || x_ce())
+    if (int rc = ensure_dev(h, h->d_xsend, 2 * h->xslot * h->amp)) return rc;
+  if (nccl_path) return SV_OK;
   if (!h->xrecv_shared) {
     bool ok = false;
     if (int rc = share_buffer(h, h->d_xrecv.p, h->d_xrecv.p, 0, h->peer_xrecv, h->xrecv_opened, &ok)) return rc;
@@ -599,6 +613,8 @@ int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launc
   CUDA_TRY(h, cudaEventRecord(h->ev_start, h->st));
   CUDA_TRY(h, cudaStreamWaitEvent(h->st_x, h->ev_start, 0));
   CUDA_TRY(h, cudaStreamWaitEvent(h->st_u, h->ev_start, 0));
+  CUDA_TRY(h, cudaStreamWaitEvent(h->st_p, h->ev_start, 0));
+  const bool ce = !nccl_path && x_ce();
   cudaEvent_t t0 = nullptr;
   if (h->timing) {
     t0 = ev_get(h);
@@ -632,7 +648,7 @@ int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launc
         if (nccl_path) {
           if (q >= 2) CUDA_TRY(h, cudaStreamWaitEvent(h->st_x, h->ev_unpacked[b], 0));  // my slot b is free
           char* sb = send + (size_t)b * slot * h->amp;
-          CUDA_TRY(h, launch_pack_bits(h->dbl, true, h->sv, sb, off, cnt, nins, pos, val, h->st_x, x_grid()));
+          CUDA_TRY(h, launch_pack_bits(h->dbl, true, h->sv, sb, off, cnt, nins, pos, val, 1ull << h->nL, h->st_x, x_grid()));
           COMM_TRY(h, h->comm->group_start());
           COMM_TRY(h, h->comm->send(sb, cnt * h->amp, partner, h->st_x));
           COMM_TRY(h, h->comm->recv(recv + (size_t)b * slot * h->amp, cnt * h->amp, partner, h->st_x));
@@ -642,14 +658,23 @@ int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launc
           // unpack of piece q - 1 is done (each rank's exchange stream waited for its own first),
           // so piece q + 1 may be pushed into the slot piece q - 1 used.
           char* dst = (char*)h->peer_xrecv[partner] + (size_t)b * slot * h->amp;
-          CUDA_TRY(h, launch_pack_bits(h->dbl, true, h->sv, dst, off, cnt, nins, pos, val, h->st_x, x_grid()));
+          if (ce) {  // pack on its own stream, copy engine over NVLink: no SM holds the transfer
+            char* sb = send + (size_t)b * slot * h->amp;
+            if (q >= 2) CUDA_TRY(h, cudaStreamWaitEvent(h->st_p, h->ev_pushed[b], 0));  // send slot b copied
+            CUDA_TRY(h, launch_pack_bits(h->dbl, true, h->sv, sb, off, cnt, nins, pos, val, 1ull << h->nL, h->st_p, x_grid()));
+            CUDA_TRY(h, cudaEventRecord(h->ev_packed[b], h->st_p));
+            CUDA_TRY(h, cudaStreamWaitEvent(h->st_x, h->ev_packed[b], 0));
+            CUDA_TRY(h, cudaMemcpyAsync(dst, sb, cnt * h->amp, cudaMemcpyDeviceToDevice, h->st_x));
+          } else {
+            CUDA_TRY(h, launch_pack_bits(h->dbl, true, h->sv, dst, off, cnt, nins, pos, val, 1ull << h->nL, h->st_x, x_grid()));
+          }
           if (q >= 1) CUDA_TRY(h, cudaStreamWaitEvent(h->st_x, h->ev_unpacked[b ^ 1], 0));
           if (int rc = barrier(h, h->st_x)) return rc;
         }
         h->stats.kernel_launches += 2;
         CUDA_TRY(h, cudaEventRecord(h->ev_pushed[b], h->st_x));
         CUDA_TRY(h, cudaStreamWaitEvent(h->st_u, h->ev_pushed[b], 0));
-        CUDA_TRY(h, launch_pack_bits(h->dbl, false, h->sv, recv + (size_t)b * slot * h->amp, off, cnt, nins, pos, val,
+        CUDA_TRY(h, launch_pack_bits(h->dbl, false, h->sv, recv + (size_t)b * slot * h->amp, off, cnt, nins, pos, val, 1ull << h->nL,
                                      h->st_u, x_grid()));
         CUDA_TRY(h, cudaEventRecord(h->ev_unpacked[b], h->st_u));
       }
@@ -839,10 +864,12 @@ int sv_destroy(sv_handle h) {
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   for (void* p : h->xrecv_opened) cudaIpcCloseMemHandle(p);
   for (cudaEvent_t e : {h->ev_start, h->ev_done, h->ev_pushed[0], h->ev_pushed[1], h->ev_unpacked[0], h->ev_unpacked[1],
-                        h->ev_landed[0], h->ev_landed[1], h->ev_landed[2], h->ev_landed[3]})
+                        h->ev_landed[0], h->ev_landed[1], h->ev_landed[2], h->ev_landed[3], h->ev_packed[0],
+                        h->ev_packed[1]})
     if (e) cudaEventDestroy(e);
   if (h->st_x) cudaStreamDestroy(h->st_x);
   if (h->st_u) cudaStreamDestroy(h->st_u);
+  if (h->st_p) cudaStreamDestroy(h->st_p);
   for (DevBuf* b : {&h->d_xrecv, &h->d_xsend})
     if (b->p) cudaFree(b->p);
   if (h->own_stream && h->st) cudaStreamDestroy(h->st);

@@ -95,6 +95,17 @@ Mode mode() {
 }
 
 // ------------------------------------------------------------------------------------ source
+// SV_CHECK=1: generated kernels trap on any HBM index outside the shard or shared-memory index
+// outside the tile (a debugging build of the section kernels; compute-sanitizer is closed on this
+// pool, so the GPU suite is run once with it: DESIGN §12)
+bool checked() {
+  static const bool on = [] {
+    const char* e = std::getenv("SV_CHECK");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 size_t smem_bytes(const Launch& L, bool dbl) {
   const size_t amp = dbl ? 16 : 8;
   const bool no_smem = L.n_phases == 1 && (L.flags & SV_FLAG_FIRST_DIRECT) && (L.flags & SV_FLAG_LAST_DIRECT);
@@ -181,16 +192,35 @@ struct Gen {
       << op.coef << ", tid, " << nthr << ", aux, ctaf, P);\n";
     return true;
   }
-  void lds() { o << "#pragma unroll\n    for (int k = 0; k < 16; k++) v[k] = sm[x ^ W[k]];\n"; }
-  void sts() { o << "#pragma unroll\n    for (int k = 0; k < 16; k++) sm[x ^ W[k]] = v[k];\n"; }
+  long long namps = 0;  // checked builds: amplitudes of the shard
+  void chk_smem() {
+    if (checked())
+      o << "#pragma unroll\n    for (int k = 0; k < 16; k++) if ((unsigned)(x ^ W[k]) >= " << (1u << T) << "u) __trap();\n";
+  }
+  void chk_hbm() {
+    if (checked())
+      o << "#pragma unroll\n    for (int k = 0; k < 16; k++) if ((unsigned long long)(b + RO[k]) >= " << namps << "ull) __trap();\n";
+  }
+  void lds() {
+    chk_smem();
+    o << "#pragma unroll\n    for (int k = 0; k < 16; k++) v[k] = sm[x ^ W[k]];\n";
+  }
+  void sts() {
+    chk_smem();
+    o << "#pragma unroll\n    for (int k = 0; k < 16; k++) sm[x ^ W[k]] = v[k];\n";
+  }
   void ldg() {
     if (virt) {
       o << "#pragma unroll\n    for (int k = 0; k < 16; k++) { v[k].x = (long long)(b + RO[k]) == vidx ? 1 : 0; v[k].y = 0; }\n";
       return;
     }
+    chk_hbm();
     o << "#pragma unroll\n    for (int k = 0; k < 16; k++) v[k] = psi[b + RO[k]];\n";
   }
-  void stg() { o << "#pragma unroll\n    for (int k = 0; k < 16; k++) psi[b + RO[k]] = v[k];\n"; }
+  void stg() {
+    chk_hbm();
+    o << "#pragma unroll\n    for (int k = 0; k < 16; k++) psi[b + RO[k]] = v[k];\n";
+  }
 };
 
 // Per-CTA DIAGSET factors (out-of-tile terms, program.h): the product of each factor's terms is
@@ -243,6 +273,7 @@ std::string gen_source(const int* p, const Launch& L, bool dbl, bool virt = fals
   Gen g;
   g.virt = virt;
   g.T = H->T;
+  g.namps = 1ll << (H->T + H->n_out);
   g.ntl = H->T - SV_R_BITS;
   const int nt = 1 << g.ntl;
   const bool first = H->flags & SV_FLAG_FIRST_DIRECT, last = H->flags & SV_FLAG_LAST_DIRECT;
@@ -471,6 +502,7 @@ std::string gen_source_tma(const int* p, const Launch& L, bool dbl, const TmaPla
   const SvSecHeader* H = reinterpret_cast<const SvSecHeader*>(p);
   Gen g;
   g.T = H->T;
+  g.namps = 1ll << (H->T + H->n_out);
   g.ntl = H->T - SV_R_BITS;
   const int nt = 1 << g.ntl;
   const bool first = H->flags & SV_FLAG_FIRST_DIRECT, last = H->flags & SV_FLAG_LAST_DIRECT;

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <algorithm>
 #include <cstring>
 #include <utility>
 
@@ -297,6 +298,7 @@ struct InsDev {
   int nins;
   int pos[11];  // ascending
   int val[11];
+  uint64_t limit;  // SV_CHECK=1: trap on an index >= limit (0: unchecked)
 };
 // Eight elements per thread per iteration: eight loads in flight per thread before any store, so
 // a small grid (the exchange leaves most SMs to the concurrent section) still keeps enough bytes in
@@ -308,6 +310,7 @@ __global__ void k_pack_bits(V* __restrict__ sv, V* __restrict__ stage, uint64_t 
   auto at = [&](uint64_t i) {
     uint64_t x = first + i;
     for (int k = 0; k < e.nins; k++) x = insert_bit(x, e.pos[k], e.val[k]);
+    if (e.limit && x >= e.limit) __trap();
     return x;
   };
   uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -518,10 +521,15 @@ cudaError_t launch_gather(bool dbl, const void* sv, const uint64_t* offs, size_t
 }
 
 cudaError_t launch_pack_bits(bool dbl, bool pack, void* sv, void* stage, uint64_t first, uint64_t count, int nins,
-                             const int* pos, const int* val, cudaStream_t st, unsigned max_blocks) {
+                             const int* pos, const int* val, uint64_t shard_amps, cudaStream_t st, unsigned max_blocks) {
   if (nins > 11) return cudaErrorInvalidValue;
   InsDev e{};
   e.nins = nins;
+  static const bool check = [] {
+    const char* v = std::getenv("SV_CHECK");
+    return v && v[0] == '1';
+  }();
+  if (check) e.limit = shard_amps;
   for (int i = 0; i < nins; i++) {  // ascending positions (insert_bit order)
     e.pos[i] = pos[i];
     e.val[i] = val[i];

@@ -49,7 +49,9 @@ cudaError_t launch_gather(bool dbl, const void* sv, const uint64_t* offs, size_t
 // Exchange: pack (stage[i] = sv[x_i]) or unpack (sv[x_i] = stage[i]) elements first .. first +
 // count - 1 of a block, x_i = (first + i) with bit val[k] inserted at pos[k]; stage may be a peer's
 // buffer mapped over NVLink.  max_blocks caps the grid (0: a full grid).
+// shard_amps: the shard's amplitude count (a checked build, SV_CHECK=1, traps on indices beyond it).
 cudaError_t launch_pack_bits(bool dbl, bool pack, void* sv, void* stage, uint64_t first, uint64_t count, int nins,
-                             const int* pos, const int* val, cudaStream_t st, unsigned max_blocks = 0);
+                             const int* pos, const int* val, uint64_t shard_amps, cudaStream_t st,
+                             unsigned max_blocks = 0);
 
 }  // namespace sv
