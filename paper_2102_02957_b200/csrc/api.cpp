@@ -114,7 +114,7 @@ struct sv_state {
   uint64_t xslot = 0;             // amplitudes per slot
   cudaStream_t st_x = nullptr, st_u = nullptr, st_p = nullptr;
   cudaEvent_t ev_start = nullptr, ev_pushed[2] = {}, ev_unpacked[2] = {}, ev_landed[4] = {}, ev_done = nullptr;
-  cudaEvent_t ev_packed[2] = {};
+  cudaEvent_t ev_packed[2] = {}, ev_prev[4] = {};
 
   Program prog;
   sv_stats_t stats{};
@@ -219,7 +219,7 @@ int sync_stream(sv_state* h) {
   return SV_OK;
 }
 
-int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launch* L0, int* done);
+int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launch* L0, const Launch* Lp, int* done);
 
 int upload_program(sv_state* h) {
   const size_t ib = h->prog.ints.size() * sizeof(int);
@@ -546,7 +546,8 @@ int ensure_exchange_engine(sv_state* h, uint64_t slot_amps, bool nccl_path) {
     CUDA_TRY(h, cudaStreamCreateWithPriority(&h->st_p, cudaStreamNonBlocking, hi));
     for (cudaEvent_t* e : {&h->ev_start, &h->ev_done, &h->ev_pushed[0], &h->ev_pushed[1], &h->ev_unpacked[0],
                            &h->ev_unpacked[1], &h->ev_landed[0], &h->ev_landed[1], &h->ev_landed[2], &h->ev_landed[3],
-                           &h->ev_packed[0], &h->ev_packed[1]})
+                           &h->ev_packed[0], &h->ev_packed[1], &h->ev_prev[0], &h->ev_prev[1], &h->ev_prev[2],
+                           &h->ev_prev[3]})
       CUDA_TRY(h, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   }
   if (h->xslot < slot_amps) {  // collective: every rank grows its slots at the same exchange
@@ -568,7 +569,7 @@ int ensure_exchange_engine(sv_state* h, uint64_t slot_amps, bool nccl_path) {
   return SV_OK;
 }
 
-int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launch* L0, int* done) {
+int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launch* L0, const Launch* Lp, int* done) {
   *done = 0;
   Nvtx r("sv exchange k=%zu%s", pairs.size(), L0 ? " + section" : "");
   std::sort(pairs.begin(), pairs.end(), [](const ExPair& a, const ExPair& b) { return a.m < b.m; });
@@ -583,24 +584,35 @@ int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launc
     mine |= ((h->rank >> bsel[i]) & 1) << i;
   }
   const bool nccl_path = (flags & SV_EXCHANGE_NCCL) || !h->p2p;
-  // split bits: the next section's highest out-of-tile bits that are not exchanged
-  int ns = 0, sidx[2] = {0, 0}, sbit[2] = {0, 0};
+  // split bits: the next section's highest out-of-tile bits that are not exchanged (and, with the
+  // previous section's last launch Lp to pipeline too, out of its tile as well)
+  int ns = 0, sidx[2] = {0, 0}, sbit[2] = {0, 0}, pidx[2] = {0, 0};
   if (L0 && !x_pipe()) L0 = nullptr;
+  const SvSecHeader* Hp =
+      Lp && Lp->T >= SV_R_BITS ? reinterpret_cast<const SvSecHeader*>(h->prog.ints.data() + Lp->int_off) : nullptr;
   if (L0 && L0->T >= SV_R_BITS) {
     const SvSecHeader* H = reinterpret_cast<const SvSecHeader*>(h->prog.ints.data() + L0->int_off);
     for (int j = H->n_out - 1; j >= 0 && ns < 2; j--) {
       const int b = H->out_bits[j];
       if ((mmask >> b) & 1) continue;
+      int jp = -1;
+      if (Hp)
+        for (int q = 0; q < Hp->n_out; q++)
+          if (Hp->out_bits[q] == b) jp = q;
+      if (Hp && jp < 0) continue;
       sidx[ns] = j;
+      pidx[ns] = jp;
       sbit[ns] = b;
       ns++;
     }
     if (ns == 2) {  // ascending out-bit index for expand_tile
       std::swap(sidx[0], sidx[1]);
+      std::swap(pidx[0], pidx[1]);
       std::swap(sbit[0], sbit[1]);
     }
   }
   if (h->nL - k - ns < 0) ns = 0;
+  if (Hp && (ns == 0 || (ns == 2 && pidx[0] > pidx[1]))) Hp = nullptr;  // quarters of Lp: ascending out bits
   const int P = 1 << ns;
   const uint64_t qblock = 1ull << (h->nL - k - ns);  // elements per (quarter, partner)
   const uint64_t slot = std::min<uint64_t>(qblock, std::max<uint64_t>(1, x_slot_bytes() / h->amp));
@@ -609,11 +621,32 @@ int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launc
   h->stats.exchanges += k;
   h->stats.exchange_batches++;
 
-  // both exchange streams start after everything queued so far on the compute stream
+  // the exchange streams start after everything queued so far on the compute stream; the previous
+  // section's last launch (Lp), if given, runs in quarters there, the exchange of quarter p
+  // starting as soon as quarter p is written
+  if (Lp && !Hp) {  // no common split: run it whole first
+    cudaEvent_t ts = tstart(h);
+    if (int rc = launch_one(h, *Lp)) return rc;
+    const double amps = (double)(1ull << h->nL);
+    tend(h, ts, 0, 2.0 * amps * (double)h->amp, Lp->flops_per_amp * amps);
+    Lp = nullptr;
+  }
   CUDA_TRY(h, cudaEventRecord(h->ev_start, h->st));
   CUDA_TRY(h, cudaStreamWaitEvent(h->st_x, h->ev_start, 0));
   CUDA_TRY(h, cudaStreamWaitEvent(h->st_u, h->ev_start, 0));
   CUDA_TRY(h, cudaStreamWaitEvent(h->st_p, h->ev_start, 0));
+  const int P0 = 1 << ns;
+  if (Lp) {
+    for (int p = 0; p < P0; p++) {
+      int sp[2] = {0, 0};
+      for (int i = 0; i < ns; i++) sp[i] = (1 << 16) | (((p >> i) & 1) << 8) | pidx[i];
+      const double amps = (double)(1ull << h->nL) / P0;
+      cudaEvent_t ts = tstart(h);
+      if (int rc = launch_one(h, *Lp, sp[0], sp[1])) return rc;
+      tend(h, ts, 0, 2.0 * amps * (double)h->amp, Lp->flops_per_amp * amps);
+      CUDA_TRY(h, cudaEventRecord(h->ev_prev[p], h->st));
+    }
+  }
   const bool ce = !nccl_path && x_ce();
   cudaEvent_t t0 = nullptr;
   if (h->timing) {
@@ -629,6 +662,10 @@ int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launc
   int pos[11], val[11];
   uint64_t q = 0;
   for (int p = 0; p < P; p++) {
+    if (Lp) {  // quarter p of the previous section is written before it is packed / sent
+      CUDA_TRY(h, cudaStreamWaitEvent(h->st_p, h->ev_prev[p], 0));
+      CUDA_TRY(h, cudaStreamWaitEvent(h->st_x, h->ev_prev[p], 0));
+    }
     for (int t = 1; t < (1 << k); t++) {  // XOR schedule: every round is a perfect matching of ranks
       const int mu = mine ^ t;
       int partner = h->rank;
@@ -865,7 +902,7 @@ int sv_destroy(sv_handle h) {
   for (void* p : h->xrecv_opened) cudaIpcCloseMemHandle(p);
   for (cudaEvent_t e : {h->ev_start, h->ev_done, h->ev_pushed[0], h->ev_pushed[1], h->ev_unpacked[0], h->ev_unpacked[1],
                         h->ev_landed[0], h->ev_landed[1], h->ev_landed[2], h->ev_landed[3], h->ev_packed[0],
-                        h->ev_packed[1]})
+                        h->ev_packed[1], h->ev_prev[0], h->ev_prev[1], h->ev_prev[2], h->ev_prev[3]})
     if (e) cudaEventDestroy(e);
   if (h->st_x) cudaStreamDestroy(h->st_x);
   if (h->st_u) cudaStreamDestroy(h->st_u);
@@ -954,6 +991,7 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
   jit_prepare(h->prog, h->dbl, vidx != -1);  // run-time specialised kernels (jit.h): compile what is missing
   if (int rc = upload_program(h)) return rc;
   size_t si = 0;
+  const Launch* deferred = nullptr;  // a section's last launch left to the following exchange
   for (size_t i = 0; i < steps.size(); i++) {
     const Step& st = steps[i];
     switch (st.type) {
@@ -961,8 +999,10 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
         const bool next_section = i + 1 < steps.size() && steps[i + 1].type == Step::SECTION &&
                                   h->nL >= SV_R_BITS && si < launch_end[i + 1];
         int done = 0;
-        if (int rc = exchange(h, st.ex, flags, next_section ? &h->prog.launches[si] : nullptr, &done)) return rc;
-        if (done) si++;  // the next section's first launch already ran, quarter by quarter
+        if (int rc = exchange(h, st.ex, flags, next_section ? &h->prog.launches[si] : nullptr, deferred, &done))
+          return rc;
+        deferred = nullptr;  // launched by the exchange, quarter by quarter
+        if (done) si++;      // the next section's first launch already ran, quarter by quarter
         break;
       }
       case Step::SECTION: {
@@ -975,8 +1015,16 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
         }
         for (; si < launch_end[i]; si++) {
           const Launch& L = h->prog.launches[si];
-          cudaEvent_t t = tstart(h);
           const bool gen_input = si == 0 && vidx != -1;  // the deferred basis state: a write-only pass
+          // the last launch of a section followed by an exchange and another section is issued by
+          // the exchange in quarters, so the exchange of quarter p starts as soon as it is written
+          if (si + 1 == launch_end[i] && !gen_input && x_pipe() && i + 2 < steps.size() &&
+              steps[i + 1].type == Step::EXCHANGE && steps[i + 2].type == Step::SECTION) {
+            deferred = &L;
+            h->stats.sections++;
+            continue;
+          }
+          cudaEvent_t t = tstart(h);
           if (int rc = launch_one(h, L, 0, 0, si == 0 ? vidx : -1)) return rc;
           const double amps = (double)(1ull << h->nL);
           tend(h, t, gen_input ? 3 : 0, (gen_input ? 1.0 : 2.0) * amps * (double)h->amp, L.flops_per_amp * amps);
