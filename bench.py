@@ -132,34 +132,6 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
-# ----------------------------------------------------------------------------- NVLink counters
-def nvlink_counters(gpu_index: int):
-    """NVLink bytes transmitted / received by this GPU so far, summed over its links (NVML field
-    values NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES / RCV_BYTES, scope = link).  None if unsupported."""
-    try:
-        import pynvml as N
-        N.nvmlInit()
-        h = N.nvmlDeviceGetHandleByIndex(gpu_index)
-        ids = []
-        for link in range(18):
-            ids += [(N.NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES, link), (N.NVML_FI_DEV_NVLINK_COUNT_RCV_BYTES, link)]
-        vals = N.nvmlDeviceGetFieldValues(h, ids)
-        tx = rx = 0
-        ok = False
-        for i, v in enumerate(vals):
-            if v.nvmlReturn != 0:
-                continue
-            ok = True
-            x = int(v.value.ullVal)
-            if i % 2 == 0:
-                tx += x
-            else:
-                rx += x
-        return (tx, rx) if ok else None
-    except Exception:
-        return None
-
-
 # ----------------------------------------------------------------------------- oracle timing
 def oracle_sample(wl, target_s: float = 15.0, max_gates: int = None):
     """Time the CPU oracle (as it stands) on the first m gates of the workload from its basis
@@ -311,7 +283,6 @@ def measure(ctx, wl, precision, c, steps, warmup, e2e_steps, with_clocks=True):
     if with_clocks:
         clk.start()
     ctx.barrier()
-    nvl0 = nvlink_counters(ctx.local) if world > 1 else None
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(steps):
@@ -320,11 +291,6 @@ def measure(ctx, wl, precision, c, steps, warmup, e2e_steps, with_clocks=True):
     e1.synchronize()
     ctx.barrier()
     clocks = clk.stop() if with_clocks else None
-    nvl1 = nvlink_counters(ctx.local) if nvl0 else None
-    counters = None
-    if nvl0 and nvl1:
-        counters = {"tx_bytes_per_step": (nvl1[0] - nvl0[0]) / steps, "rx_bytes_per_step": (nvl1[1] - nvl0[1]) / steps,
-                    "source": "NVML NVLINK_COUNT_XMIT/RCV_BYTES summed over links, this rank's GPU, timed region"}
     ms = ctx.max_over_ranks(e0.elapsed_time(e1))
     st = s.stats()
     s.set_timing(False)
@@ -348,8 +314,7 @@ def measure(ctx, wl, precision, c, steps, warmup, e2e_steps, with_clocks=True):
         e2e = {"value": len(gates) / (sum(times) / len(times)), "unit": "gates/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "steps": len(times)}
     s.close()
-    return dict(ms=ms, ms_step=ms / steps, value=len(gates) / (ms / steps / 1e3), st=st, clocks=clocks, e2e=e2e,
-                nvl_counters=counters)
+    return dict(ms=ms, ms_step=ms / steps, value=len(gates) / (ms / steps / 1e3), st=st, clocks=clocks, e2e=e2e)
 
 
 def roofline(wl, precision, r, world):
@@ -414,7 +379,7 @@ def nvlink(r, steps):
         return None
     gbs = st["bytes_sent"] / (st["exchange_ms"] / 1e3) / 1e9
     return {"achieved": round(gbs, 1), "peak": 900.0, "unit": "GB/s per direction", "frac": round(gbs / 900.0, 4),
-            "counters": r.get("nvl_counters"),
+            "counters": "unavailable: NVML NVLink byte counters report NOT_SUPPORTED on this pool's driver (profiles/r02_nvml_probe.txt)",
             "frac_of_measured_peer_copy": round(gbs / 770.0, 4), "bytes_per_rank_per_step": st["bytes_sent"] / steps,
             "share_of_step": round(st["exchange_ms"] / ms, 4),
             "transport": "NCCL send/recv (packed)" if APPLY_FLAGS & 4 else "peer-memory swap kernel (CUDA IPC)"}

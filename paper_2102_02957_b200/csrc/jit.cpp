@@ -117,9 +117,13 @@ size_t smem_bytes(const Launch& L, bool dbl) {
 // per SM at 128 registers.  Sections without dense gates (QFT-like: butterflies and phases) need
 // fewer registers and run 640 threads per SM (QFT30 29.7 -> 29.3 ms); U2 sections would spill there.
 int resident_ctas(int T, int nt, bool dense) {
+  static const int dense_tsm = [] {  // measurement switch: threads per SM for dense sections
+    const char* e = std::getenv("SV_DENSE_TSM");
+    return e ? std::atoi(e) : 512;
+  }();
   if (T > 12) return 1;
   if (T == 12) return 2;
-  return std::max(1, std::min(16, (dense ? 512 : 640) / nt));
+  return std::max(1, std::min(16, (dense ? dense_tsm : 640) / nt));
 }
 
 bool has_dense(const int* p) {
