@@ -503,23 +503,13 @@ int setup_p2p(sv_state* h, void* base_alloc, size_t base_off) {
 // L0 (pipelined exchange + section) the pieces are grouped by up to two of its out-of-tile bits and
 // each quarter of its tiles starts on the compute stream as soon as that quarter has landed, while
 // the next quarter is still on NVLink.
-// Exchange tuning (measurement switches; defaults are the measured best): SV_XGRID CTAs of the push /
-// unpack kernels (SMs left to the overlapped section), SV_XSLOT_MB receive-slot size, SV_XPIPE=0
-// runs the exchange without starting the next section's quarters as they land.
-unsigned x_grid() {
-  static const unsigned g = [] {
-    const char* e = std::getenv("SV_XGRID");
-    return e ? (unsigned)std::atoi(e) : 132u;
-  }();
-  return g;
-}
-uint64_t x_slot_bytes() {
-  static const uint64_t b = [] {
-    const char* e = std::getenv("SV_XSLOT_MB");
-    return (e ? (uint64_t)std::atoll(e) : 1024ull) << 20;
-  }();
-  return b;
-}
+// Exchange tuning (measured: docs DESIGN §7): 132 CTAs for the pack / push / unpack kernels (264 or
+// 528 no faster alone, slower overlapped), receive slots of 1 GiB (4 GiB no faster).  SV_XPIPE=0
+// runs the exchange without overlapping its neighbouring sections (a comparator line).
+constexpr unsigned kXGrid = 132;
+constexpr uint64_t kXSlotBytes = 1ull << 30;
+unsigned x_grid() { return kXGrid; }
+uint64_t x_slot_bytes() { return kXSlotBytes; }
 // SV_XCE=0: the peer path pushes with a small-grid kernel (remote stores) instead of packing into a
 // local send slot and copying it to the peer with the copy engines (default)
 bool x_ce() {

@@ -116,14 +116,12 @@ size_t smem_bytes(const Launch& L, bool dbl) {
 // Resident CTAs per SM the generated kernel is register-budgeted for (launch bounds): 512 threads
 // per SM at 128 registers.  Sections without dense gates (QFT-like: butterflies and phases) need
 // fewer registers and run 640 threads per SM (QFT30 29.7 -> 29.3 ms); U2 sections would spill there.
+// (384 threads per SM for dense sections, 168 registers: QV28 52.6 vs 46.8 ms, QV33 2015 vs 1744 ms —
+// fewer warps lose more than the extra registers gain; 640 spills.)
 int resident_ctas(int T, int nt, bool dense) {
-  static const int dense_tsm = [] {  // measurement switch: threads per SM for dense sections
-    const char* e = std::getenv("SV_DENSE_TSM");
-    return e ? std::atoi(e) : 512;
-  }();
   if (T > 12) return 1;
   if (T == 12) return 2;
-  return std::max(1, std::min(16, (dense ? dense_tsm : 640) / nt));
+  return std::max(1, std::min(16, (dense ? 512 : 640) / nt));
 }
 
 bool has_dense(const int* p) {
