@@ -67,6 +67,10 @@ typedef struct {
 #define SV_RESTORE_ORDER (1u << 1) /* append swaps returning the paper-physical order to logical */
 #define SV_EXCHANGE_NCCL (1u << 2) /* cross-GPU exchange by NCCL send/recv through a staging ring */
                                    /* instead of the peer-memory swap kernel                    */
+#define SV_ABSORB_SWAPS  (1u << 5) /* the pass absorbs user SWAP gates as relabels of pi (the  */
+                                   /* paper's bit reordering) instead of   */
+                                   /* treating them as 2-qubit gates; sections that would hold  */
+                                   /* only absorbed swaps are not emitted                       */
 #define SV_FREE_LAYOUT   (1u << 3) /* sv_plan_circuit / sv_compile_circuit: plan as sv_apply_   */
                                    /* circuit does right after sv_reset (the state is a basis   */
                                    /* state, so the planner chooses the initial memory layout; */

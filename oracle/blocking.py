@@ -28,6 +28,7 @@ from typing import List, Optional, Sequence, Tuple
 
 U1, U2, D1, D2, SWAP = 1, 2, 3, 4, 5
 RESTORE_ORDER = 1 << 1
+ABSORB_SWAPS = 1 << 5  # a user SWAP relabels pi instead of being a 2-qubit gate
 
 
 class Infeasible(ValueError):
@@ -58,10 +59,14 @@ def block_circuit(gates: Sequence[Tuple[int, int, int]], n: int, c: int,
     out: List[tuple] = []
     remaining = list(range(len(gates)))
 
+    absorb = bool(flags & ABSORB_SWAPS)
     while remaining:
-        # ---- choose QB_CHUNK (R3: in order, dependency aware, whole-gate admission)
+        # ---- choose QB_CHUNK (R3: in order, dependency aware, whole-gate admission).  With
+        # ABSORB_SWAPS a swap is no gate: later gates on its qubits act on the state that was on
+        # the other qubit at the start of the section (start[q]).
         S: List[int] = []
         blocked = set()
+        start = list(range(n))
         for gi in remaining:
             k, q0, q1 = gates[gi]
             qs = _qubits(k, q0, q1)
@@ -70,7 +75,10 @@ def block_circuit(gates: Sequence[Tuple[int, int, int]], n: int, c: int,
                 continue
             if _diagonal(k):
                 continue
-            need = [q for q in sorted(qs) if q not in S]
+            if absorb and k == SWAP:
+                start[q0], start[q1] = start[q1], start[q0]
+                continue
+            need = [q for q in sorted(start[x] for x in qs) if q not in S]
             if len(S) + len(need) <= c:
                 S.extend(need)
             else:
@@ -89,6 +97,7 @@ def block_circuit(gates: Sequence[Tuple[int, int, int]], n: int, c: int,
             inv[sq1], inv[p] = evicted, q
         # ---- emit the section
         out.append(("BEGIN",))
+        opened = len(out)
         blocked = set()
         nxt: List[int] = []
         for gi in remaining:
@@ -98,12 +107,19 @@ def block_circuit(gates: Sequence[Tuple[int, int, int]], n: int, c: int,
                 blocked.update(qs)
                 nxt.append(gi)
                 continue
+            if absorb and k == SWAP:  # relabel: the states of q0 and q1 trade physical positions
+                pi[q0], pi[q1] = pi[q1], pi[q0]
+                inv[pi[q0]], inv[pi[q1]] = q0, q1
+                continue
             if _diagonal(k) or all(pi[q] < c for q in qs):
                 out.append((k, pi[q0], pi[q1] if len(qs) == 2 else -1, gi))
             else:
                 blocked.update(qs)
                 nxt.append(gi)
-        out.append(("END",))
+        if len(out) == opened:
+            out.pop()  # only absorbed swaps: no section
+        else:
+            out.append(("END",))
         remaining = nxt
 
     if flags & RESTORE_ORDER:

@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libsv.so")
 GATE_DTYPE = np.dtype([("kind", "<i4"), ("q0", "<i4"), ("q1", "<i4"), ("pad", "<i4"), ("m", "<f8", (32,))])
 SV_U1, SV_U2, SV_D1, SV_D2, SV_SWAP, SV_CHUNK_SWAP, SV_BEGIN, SV_END, SV_EXCHANGE = range(1, 10)
 SV_FP32, SV_FP64 = 0, 1
-SV_UNBLOCKED, SV_RESTORE_ORDER, SV_EXCHANGE_NCCL, SV_FREE_LAYOUT = 1, 2, 4, 8
+SV_UNBLOCKED, SV_RESTORE_ORDER, SV_EXCHANGE_NCCL, SV_FREE_LAYOUT, SV_ABSORB_SWAPS = 1, 2, 4, 8, 32
 ERRORS = {-1: "SV_EINVAL", -2: "SV_ECAPACITY", -3: "SV_EINFEASIBLE", -4: "SV_EMALFORMED", -5: "SV_ECUDA", -6: "SV_ENCCL"}
 
 

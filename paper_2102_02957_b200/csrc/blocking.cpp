@@ -11,7 +11,10 @@
 //       blocked qubit (blocking theirs too), skip diagonal gates, admit a gate only whole;
 //   R4  chunk_swaps fill the free slots in DESCENDING slot order;
 //   R5  diagonal gates are always executable inside a chunk and are never selected;
-//   R6  SWAP is an ordinary non-diagonal two-qubit gate.
+//   R6  SWAP is an ordinary non-diagonal two-qubit gate — or, with SV_ABSORB_SWAPS (SURVEY Q6,
+//       the paper's "bit reordering"), a relabel of pi at the point the section reaches
+//       it: selection then sees later gates on the swapped qubits through the same relabel, and
+//       a section left with no gate is not emitted.
 // Bitmasks over qubits (n <= 40) keep the pass O(gates * sections) with small constants.
 #include <algorithm>
 #include <cstring>
@@ -74,10 +77,13 @@ Status block_pass(const sv_gate* g, size_t count, int n, int c, std::vector<int>
   for (size_t i = 0; i < count; i++) queue[i] = (uint32_t)i;
   next.reserve(count);
 
+  const bool absorb = (flags & SV_ABSORB_SWAPS) != 0;
   std::vector<int> chosen;  // QB_CHUNK, in selection order
+  std::vector<int> sel(n);  // absorbed swaps during selection: logical q -> the section-start qubit
   while (!queue.empty()) {
     // --- choose QB_CHUNK (R3)
     chosen.clear();
+    for (int q = 0; q < n; q++) sel[q] = q;
     uint64_t chosen_mask = 0, blocked = 0;
     for (uint32_t gi : queue) {
       const uint64_t qm = masks[gi];
@@ -86,7 +92,12 @@ Status block_pass(const sv_gate* g, size_t count, int n, int c, std::vector<int>
         continue;
       }
       if (is_diag(g[gi].kind)) continue;
-      uint64_t need = qm & ~chosen_mask;
+      if (absorb && g[gi].kind == SV_SWAP) {
+        std::swap(sel[g[gi].q0], sel[g[gi].q1]);
+        continue;
+      }
+      uint64_t need = (1ull << sel[g[gi].q0]) | (is_two(g[gi].kind) ? 1ull << sel[g[gi].q1] : 0ull);
+      need &= ~chosen_mask;
       if ((int)chosen.size() + __builtin_popcountll(need) <= c) {
         while (need) {  // ascending qubit order
           int q = __builtin_ctzll(need);
@@ -116,6 +127,7 @@ Status block_pass(const sv_gate* g, size_t count, int n, int c, std::vector<int>
       where[slot] = q;
     }
     // --- emit the section
+    const size_t begin_at = tokens.size();
     tokens.push_back(marker(SV_BEGIN));
     uint64_t blk = 0;
     next.clear();
@@ -125,6 +137,14 @@ Status block_pass(const sv_gate* g, size_t count, int n, int c, std::vector<int>
       if (qm & blk) {
         blk |= qm;
         next.push_back(gi);
+        continue;
+      }
+      if (absorb && r.kind == SV_SWAP) {  // the state of q0 now lives where q1's was, and vice versa
+        const int a = pi[r.q0], b = pi[r.q1];
+        pi[r.q0] = b;
+        pi[r.q1] = a;
+        where[a] = r.q1;
+        where[b] = r.q0;
         continue;
       }
       bool local = is_diag(r.kind) || (pi[r.q0] < c && (!is_two(r.kind) || pi[r.q1] < c));
@@ -139,7 +159,10 @@ Status block_pass(const sv_gate* g, size_t count, int n, int c, std::vector<int>
         next.push_back(gi);
       }
     }
-    tokens.push_back(marker(SV_END));
+    if (tokens.size() == begin_at + 1)
+      tokens.pop_back();  // nothing but absorbed swaps: no section
+    else
+      tokens.push_back(marker(SV_END));
     queue.swap(next);
   }
 

@@ -37,8 +37,10 @@ def load_golden(path):
         if not line or line.startswith("#"):
             continue
         head, gates, out, pi = (s.strip() for s in line.split("|"))
-        n, c = (int(x) for x in head.split())
-        rows.append((n, c, gates, out, [int(x) for x in pi.split()]))
+        words = head.split()
+        n, c = int(words[0]), int(words[1])
+        flags = 32 if "absorb" in words[2:] else 0  # SV_ABSORB_SWAPS / oracle.blocking.ABSORB_SWAPS
+        rows.append((n, c, gates, out, [int(x) for x in pi.split()], flags))
     return rows
 
 

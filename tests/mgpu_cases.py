@@ -10,7 +10,7 @@ What the cases exercise (SURVEY §8(a) a6 / §8(f) NEXT-1..3
   * qv-restore: SV_RESTORE_ORDER (order restored physically, P:379);
   * qv-unblocked: the paper's unblocked multi-GPU baseline (per-gate exchanges, NEXT-3);
   * qv-twice: a second circuit on the layout the first one left (no free layout);
-  * qft-fp32: the fp32 path.
+  * qft-fp32: the fp32 path; qft-absorb: SV_ABSORB_SWAPS (swaps as relabels of pi).
 G-invariance (SURVEY P-G): a plan on G ranks relabels and exchanges bits differently from the
 one-GPU plan, so sections group gates into different phases, DIAGSETs and slot orders; amplitudes
 then agree to rounding (asserted: max |d| <= 1e-12), and bitwise only where every operation is
@@ -25,7 +25,7 @@ import circuits as C
 
 def cases():
     """(name, records, n, chunk_bits, flags, basis, precision, second circuit or None)."""
-    SV_UNBLOCKED, SV_RESTORE_ORDER, SV_EXCHANGE_NCCL = 1, 2, 4
+    SV_UNBLOCKED, SV_RESTORE_ORDER, SV_EXCHANGE_NCCL, SV_ABSORB_SWAPS = 1, 2, 4, 32
     return [
         ("qv", C.quantum_volume(20, 10, 1), 20, 10, 0, 0, "fp64", None),
         ("qv-nccl", C.quantum_volume(20, 10, 2), 20, 10, SV_EXCHANGE_NCCL, 0, "fp64", None),
@@ -37,6 +37,7 @@ def cases():
         ("qv-twice", C.quantum_volume(18, 6, 6), 18, 7, 0, C.basis_index(3, 18), "fp64", C.qft(18)),
         ("qft-fp32", C.qft(20), 20, 9, 0, C.basis_index(5, 20), "fp32", None),
         ("qft-nccl", C.qft(19), 19, 7, SV_EXCHANGE_NCCL, C.basis_index(2, 19), "fp64", None),
+        ("qft-absorb", C.qft(20), 20, 8, SV_ABSORB_SWAPS, C.basis_index(6, 20), "fp64", None),
     ]
 
 

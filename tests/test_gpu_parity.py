@@ -282,3 +282,18 @@ def test_host_memory_tier(prec):
             back = np.zeros(1 << n, dtype=np.complex128)
             back[:] = O.apply_circuit(C.mirror(circ), n, ref)
             check(s.state(), back, prec)
+
+
+def test_absorb_swaps():
+    # SV_ABSORB_SWAPS: user SWAPs relabel the tracked permutation instead of being gates (the
+    # paper's bit reordering); QFT's terminal swap layer then costs no section
+    for n, c, circ, basis in [(16, 8, C.qft(16), C.basis_index(4, 16)), (14, 6, C.random_circuit(14, 200, 12, kinds=("u3", "cx", "swap", "cp", "su4")), 0)]:
+        with sv.StateVector(n, c) as s:
+            s.reset(basis)
+            s.apply(circ, flags=sv.SV_ABSORB_SWAPS)
+            s.apply(circ[: len(circ) // 2], flags=sv.SV_ABSORB_SWAPS)  # pi carried into the next circuit
+            got = s.state()
+            st = s.stats()
+        ref = O.apply_circuit(circ[: len(circ) // 2], n, O.apply_circuit(circ, n, basis=basis))
+        check(got, ref, "fp64")
+        assert st["sections"] > 0

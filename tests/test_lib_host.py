@@ -52,9 +52,9 @@ def assert_same_pass(recs, n, c, flags=0, pi0=None):
 
 @pytest.mark.parametrize("row", load_golden(os.path.join(ROOT, "tests", "golden", "blocking_traces.txt")))
 def test_pass_golden(row):
-    n, c, gates, expected, pi_expected = row
+    n, c, gates, expected, pi_expected, flags = row
     recs = parse_gates(gates, n)
-    toks, pi = sv.block_circuit(recs, n, c)
+    toks, pi = sv.block_circuit(recs, n, c, flags=flags)
     assert B.format_tokens(lib_tokens(toks)) == expected
     assert list(pi) == pi_expected
 
@@ -251,3 +251,27 @@ def test_header_compiles_as_c_and_cpp():
     for cc, lang in (("gcc", ["-x", "c", "-std=c99"]), ("g++", ["-x", "c++", "-std=c++17"])):
         if shutil.which(cc):
             subprocess.run([cc, "-fsyntax-only", "-Wall", "-Werror", *lang, hdr], check=True)
+
+
+def test_pass_absorb_swaps_bit_exact_and_plans():
+    # SV_ABSORB_SWAPS (the paper's bit reordering P:287-289): the library's pass matches
+    # the oracle's independent pass token for token on random swap-heavy circuits and QFT, and the
+    # executor's plans built on it still compute the original circuit (dense, under pi / sigma).
+    rng = np.random.default_rng(55)
+    for t in range(3000):
+        n = int(rng.integers(2, 14))
+        c = int(rng.integers(2, n + 1))
+        recs = C.random_circuit(n, int(rng.integers(0, 40)), 91000 + t, kinds=("u3", "cx", "swap", "cp", "su4"))
+        flags = sv.SV_ABSORB_SWAPS | (B.RESTORE_ORDER if t % 6 == 0 else 0)
+        assert_same_pass(recs, n, c, flags=flags, pi0=rng.permutation(n) if t % 4 == 0 else None)
+    for n, c in [(10, 6), (16, 8), (30, 8), (36, 12)]:
+        assert_same_pass(C.qft(n), n, c, flags=sv.SV_ABSORB_SWAPS)
+        plain = sum(1 for r in sv.block_circuit(C.qft(n), n, c)[0] if int(r["kind"]) == C.BEGIN)
+        absorbed = sum(1 for r in sv.block_circuit(C.qft(n), n, c, flags=sv.SV_ABSORB_SWAPS)[0] if int(r["kind"]) == C.BEGIN)
+        assert absorbed < plain  # the terminal swap layer costs no section
+    for g in (0, 1, 2):
+        for t in range(40):
+            n = int(rng.integers(g + 3, 11))
+            c = int(rng.integers(2, n - g + 1))
+            recs = C.random_circuit(n, int(rng.integers(0, 50)), 93000 + t, kinds=("u3", "cx", "swap", "cp", "su4"))
+            run_plan_dense(recs, n, c, g, flags=sv.SV_ABSORB_SWAPS, seed=t)

@@ -17,9 +17,9 @@ GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "blocking_traces.txt"
 
 @pytest.mark.parametrize("row", load_golden(GOLDEN))
 def test_golden_traces(row):
-    n, c, gates, expected, pi_expected = row
+    n, c, gates, expected, pi_expected, flags = row
     recs = parse_gates(gates, n)
-    toks, pi = B.block_circuit(triples(recs), n, c)
+    toks, pi = B.block_circuit(triples(recs), n, c, flags=flags)
     assert B.format_tokens(toks) == expected
     assert pi == pi_expected
 
@@ -110,3 +110,21 @@ def test_infeasible():
         B.block_circuit([(C.U2, 0, 1)], 4, 1)
     toks, _ = B.block_circuit([(C.D2, 0, 1), (C.U1, 3, -1)], 4, 1)
     assert B.verify_blocked(toks, 1)
+
+
+def test_absorb_swaps_semantics():
+    # ABSORB_SWAPS: user SWAPs become relabels of pi; the blocked circuit (no SWAP tokens left)
+    # executed densely and un-permuted by the final pi equals the input circuit, and no emitted
+    # section is empty.
+    rng = np.random.default_rng(321)
+    for t in range(300):
+        n = int(rng.integers(3, 11))
+        c = int(rng.integers(2, n + 1))
+        recs = C.random_circuit(n, int(rng.integers(0, 60)), 5000 + t, kinds=("u3", "cx", "swap", "cp", "su4", "d2"))
+        flags = B.ABSORB_SWAPS | (B.RESTORE_ORDER if t % 5 == 0 else 0)
+        toks, pi = check_semantics(recs, n, c, flags=flags, seed=t)
+        body = [tk for tk in toks if tk[0] not in ("BEGIN", "END", "CS")]
+        if not flags & B.RESTORE_ORDER:
+            assert all(tk[0] != B.SWAP for tk in body)
+        for a, b in zip(toks, toks[1:]):
+            assert not (a[0] == "BEGIN" and b[0] == "END")
