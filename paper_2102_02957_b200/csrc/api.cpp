@@ -638,11 +638,7 @@ int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launc
     }
   }
   const bool ce = !nccl_path && x_ce();
-  cudaEvent_t t0 = nullptr;
-  if (h->timing) {
-    t0 = ev_get(h);
-    CUDA_TRY(h, cudaEventRecord(t0, h->st_x));
-  }
+  cudaEvent_t t0 = nullptr;  // recorded where the first piece starts (after quarter 0 of Lp)
   char* recv = (char*)h->d_xrecv.p;
   char* send = (char*)h->d_xsend.p;
   // every rank is done with everything before this exchange — its unpacks of the previous one
@@ -655,6 +651,10 @@ int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launc
     if (Lp) {  // quarter p of the previous section is written before it is packed / sent
       CUDA_TRY(h, cudaStreamWaitEvent(h->st_p, h->ev_prev[p], 0));
       CUDA_TRY(h, cudaStreamWaitEvent(h->st_x, h->ev_prev[p], 0));
+    }
+    if (h->timing && p == 0) {  // the exchange's span: from its first piece to its last unpack
+      t0 = ev_get(h);
+      CUDA_TRY(h, cudaEventRecord(t0, ce ? h->st_p : h->st_x));
     }
     for (int t = 1; t < (1 << k); t++) {  // XOR schedule: every round is a perfect matching of ranks
       const int mu = mine ^ t;

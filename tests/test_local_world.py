@@ -87,9 +87,32 @@ def test_local_world_two_level_volume():
 
 
 def test_local_world_errors():
-    # a world of a non-power-of-two size, a bad rank, and a timeout when one rank never joins
+    # a world of a non-power-of-two size and a rank outside the world are rejected (SV_EINVAL)
     with pytest.raises(sv.SvError):
         sv.LocalWorld(3)
     with sv.LocalWorld(2) as w:
         with pytest.raises(sv.SvError):
             sv.StateVector(12, 4, rank=2, local_world=w)
+
+
+def test_local_world_interpreter_shared_constants():
+    # The interpreter kernel reads its program from the module's one __constant__ bank; four ranks
+    # on four streams copy and launch concurrently, serialised by the per-device event chain
+    # (section.cu launch_section).  Without it a rank's launch could read another's program.
+    import oracle as O
+    prev = sv.jit_mode(0)
+    try:
+        for world, (n, c, circ) in [(4, (14, 6, C.quantum_volume(14, 6, 11))), (2, (13, 5, C.qft(13)))]:
+            with sv.LocalWorld(world) as w:
+                def body(r):
+                    with sv.StateVector(n, c, "fp64", rank=r, local_world=w) as s:
+                        s.reset(3)
+                        s.apply(circ)
+                        st = s.stats()
+                        return s.state(), st
+                res = w.run(body)
+            got, st = res[0]
+            assert st["interp_launches"] > 0 and st["jit_launches"] == 0
+            assert float(np.max(np.abs(got - O.apply_circuit(circ, n, basis=3)))) <= 1e-10
+    finally:
+        sv.jit_mode(prev)
