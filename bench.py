@@ -373,13 +373,22 @@ def roofline(wl, precision, r, world):
     return roof
 
 
-def nvlink(r, steps):
+def nvlink(r, steps, wl_name=None, world=1):
     st, ms = r["st"], r["ms"]
     if not st["exchange_ms"]:
         return None
     gbs = st["bytes_sent"] / (st["exchange_ms"] / 1e3) / 1e9
+    alone = None
+    prof = os.path.join(ROOT, "profiles", "r02_exchange_alone.json")
+    if os.path.exists(prof) and not APPLY_FLAGS:
+        try:
+            alone = json.load(open(prof)).get(f"{wl_name}_n{world}")
+        except Exception:
+            alone = None
     return {"achieved": round(gbs, 1), "peak": 900.0, "unit": "GB/s per direction", "frac": round(gbs / 900.0, 4),
             "counters": "unavailable: NVML NVLink byte counters report NOT_SUPPORTED on this pool's driver (profiles/r02_nvml_probe.txt)",
+            "overlapped": os.environ.get("SV_XPIPE", "1") != "0",
+            "alone_measured": alone,
             "frac_of_measured_peer_copy": round(gbs / 770.0, 4), "bytes_per_rank_per_step": st["bytes_sent"] / steps,
             "share_of_step": round(st["exchange_ms"] / ms, 4),
             "transport": "NCCL send/recv (packed)" if APPLY_FLAGS & 4 else "peer-memory swap kernel (CUDA IPC)"}
@@ -402,7 +411,7 @@ def run_ours(args):
     r = measure(ctx, wl, args.precision, c, args.steps, args.warmup, 0 if args.no_e2e else args.e2e_steps)
     st, ms, clocks = r["st"], r["ms"], r["clocks"]
     roof = roofline(wl, args.precision, r, world)
-    nvl = nvlink(r, args.steps) if world > 1 else None
+    nvl = nvlink(r, args.steps, wl["name"], world) if world > 1 else None
 
     # ---- the HBM-bound workload beside it (BASELINE configs[2], QFT30 fp64 c = 8), same GPUs
     sub = {}
@@ -412,7 +421,7 @@ def run_ours(args):
         sub["qft30"] = {"workload": wq["desc"], "value": rq["value"], "unit": "gates/s", "ms_per_step": rq["ms_step"],
                         "steps": 20, "warmup": 3, "chunk_bits": wq["chunk_bits"],
                         "roofline": roofline(wq, "fp64", rq, world),
-                        "nvlink": nvlink(rq, 20) if world > 1 else None, "clocks": rq["clocks"],
+                        "nvlink": nvlink(rq, 20, "qft30", world) if world > 1 else None, "clocks": rq["clocks"],
                         "gpu_launches": int(rq["st"]["kernel_launches"])}
 
     # ---- CPU oracle baseline (rank 0, N = 1 only)

@@ -1,9 +1,9 @@
-# 1 GPU: the GPU suite under the bounds-checking build (SV_CHECK=1), then dense-section occupancy A/B and fp32 lines
+# 4 GPUs: the whole GPU suite (multi-GPU parity at 2 and 4 ranks included), then the pipelined
+# QV33 / QFT35 lines with the exchange span timed from its first piece
 set -x
-SV_CHECK=1 SV_JIT_CACHE=0 timeout 1700 python -m pytest tests -m gpu -q -x > gpurun_out/r02_gpu_checked.log 2>&1; echo checked=$?
-for t in 384 512; do
-  SV_DENSE_TSM=$t timeout 600 python bench.py --workload qv28 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --no-sub > gpurun_out/r02_ab6_qv28_t$t.json 2>/dev/null; echo qv28 t$t=$?
-  SV_DENSE_TSM=$t timeout 900 python bench.py --workload qv33 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-sub > gpurun_out/r02_ab6_qv33_t$t.json 2>/dev/null; echo qv33 t$t=$?
-done
-timeout 900 python bench.py --workload qft_weak_fp32 --steps 5 --warmup 3 --no-cpu-baseline --no-e2e --no-sub > gpurun_out/r02_ab6_qft34_fp32.json 2>/dev/null; echo qft34fp32=$?
-timeout 900 python bench.py --workload qv28 --precision fp32 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --no-sub > gpurun_out/r02_ab6_qv28_fp32.json 2>/dev/null; echo qv28fp32=$?
+T0=$(date +%s)
+timeout 2400 python -m pytest tests -m gpu -q -x --durations=15 > gpurun_out/r02_final_gpu_suite_4gpu.log 2>&1; echo suite=$? secs=$(( $(date +%s) - T0 ))
+N=4
+R="python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1"
+timeout 900 $R --master-port 29951 bench.py --gpus $N --steps 5 --warmup 3 > gpurun_out/r02_final_qv33_n4.json 2> gpurun_out/r02_final_qv33_n4.err; echo qv33=$?
+timeout 900 $R --master-port 29952 bench.py --gpus $N --steps 5 --warmup 3 --no-sub --no-e2e --workload qft_weak > gpurun_out/r02_final_qftweak_n4.json 2> gpurun_out/r02_final_qftweak_n4.err; echo qftweak=$?
