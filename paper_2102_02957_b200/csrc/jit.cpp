@@ -116,6 +116,8 @@ size_t smem_bytes(const Launch& L, bool dbl) {
 // Resident CTAs per SM the generated kernel is register-budgeted for (launch bounds): 512 threads
 // per SM at 128 registers.  Sections without dense gates (QFT-like: butterflies and phases) need
 // fewer registers and run 640 threads per SM (QFT30 29.7 -> 29.3 ms); U2 sections would spill there.
+// (The four-multiply form of a dense 2-qubit gate — 64 FP64 operations and 32 coefficient loads per
+// 4 amplitudes instead of the Gauss form's 60 and 48 — was measured slower: QV33 1880 vs 1754 ms.)
 // (384 threads per SM for dense sections, 168 registers: QV28 52.6 vs 46.8 ms, QV33 2015 vs 1744 ms —
 // fewer warps lose more than the extra registers gain; 640 spills.)
 int resident_ctas(int T, int nt, bool dense) {
