@@ -106,7 +106,6 @@ __global__ void __launch_bounds__(NT, MINB) k_section(V* __restrict__ sv, const 
                                                      int split_b) {
   using R = decltype(V().x);
   constexpr int RB = SV_R_BITS;  // the host guarantees T >= RB, so every phase has RB register slots
-  constexpr int M0 = FIRST ? kH_DIN : kH_LOAD;  // the map the tile is read with
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V* sm = reinterpret_cast<V*>(smem_raw);
   const int T = c_prog[kH_T], n_out = c_prog[kH_NOUT], nph = c_prog[kH_NPH];
@@ -117,8 +116,7 @@ __global__ void __launch_bounds__(NT, MINB) k_section(V* __restrict__ sv, const 
   V* ctaf = reinterpret_cast<V*>(smem_raw + (sizeof(V) << T));
   const int n_sets = c_prog[kH_NSETS];
 
-  (void)M0;
-  (void)G;
+  (void)G;  // the swizzle width is baked into the host's maps
   // one tile per CTA (a grid-stride loop only if the launch ever exceeds the grid limit)
   for (uint64_t blk = blockIdx.x; blk < n_tiles; blk += gridDim.x) {
     uint64_t tile_off = 0;

@@ -1,7 +1,6 @@
-# 1 GPU: dense 2-qubit gate form A/B (Gauss three-multiply vs four-multiply)
+# randomised parity sweeps on one GPU (logs for profiles/)
 set -x
-for f in 4 3; do
-  SV_U2_FORM=$f timeout 600 python bench.py --workload qv28 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --no-sub > gpurun_out/r02_ab7_qv28_f$f.json 2>/dev/null; echo qv28 f$f=$?
-  SV_U2_FORM=$f timeout 900 python bench.py --workload qv33 --steps 5 --warmup 3 --no-cpu-baseline --no-e2e --no-sub > gpurun_out/r02_ab7_qv33_f$f.json 2>/dev/null; echo qv33 f$f=$?
-done
-SV_U2_FORM=4 timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "random or qv_and_qft" > gpurun_out/r02_ab7_tests.log 2>&1; echo tests=$?
+timeout 1200 python tools/stress.py 7 300 > gpurun_out/r02_stress.log 2>&1; echo stress=$?
+timeout 1500 python tools/stress_local.py 8 150 > gpurun_out/r02_stress_local.log 2>&1; echo local=$?
+SV_XCE=0 timeout 900 python tools/stress_local.py 9 60 > gpurun_out/r02_stress_local_push.log 2>&1; echo push=$?
+SV_TMA=2 timeout 900 python tools/stress.py 10 100 > gpurun_out/r02_stress_tma.log 2>&1; echo tma=$?
