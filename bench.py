@@ -440,7 +440,7 @@ def run_ours(args):
             "config": {"workload": wl["desc"], "n_qubits": n, "gates": int(len(gates)), "chunk_bits": c,
                        "precision": args.precision, "parallelism": f"state sharded over {world} GPU(s)",
                        "l2": "state >= 4 GiB per GPU >> 126 MB L2 (no flush needed)",
-                       "step": "sv_reset(basis; generated inside the first section's load) + sv_apply_circuit (pass+plan+upload+sections+exchanges) + sv_probabilities(10 qubits)",
+                       "step": "sv_reset(basis; deferred: the first section clears the shard and runs only the tile holding the basis amplitude) + sv_apply_circuit (pass+plan+upload+sections+exchanges) + sv_probabilities(10 qubits)",
                        "path": ("unblocked per-gate baseline (SV_UNBLOCKED)" if APPLY_FLAGS & 1 else "cache-blocked") +
                                (", NCCL send/recv exchange" if APPLY_FLAGS & 4 else "")},
             "amp_updates_per_s": r["value"] * (1 << n),

@@ -321,6 +321,24 @@ int launch_one(sv_state* h, const Launch& L, int split_a = 0, int split_b = 0, i
   const char* cdev = (const char*)h->d_coef.p + L.coef_off * h->amp;
   const char* adev = (const char*)h->d_aux.p + L.aux_off * h->amp;
   cudaError_t je = cudaSuccess;
+  if (vidx != -1 && !split_a && !split_b && jit_virtual_input_ok(L, h->dbl)) {
+    // The input is a basis state and a section is a linear map applied tile by tile: every tile but
+    // the one holding the amplitude is zero in and zero out.  Clear the shard and run that tile.
+    CUDA_TRY(h, cudaMemsetAsync(h->sv, 0, h->amp << h->nL, h->st));
+    if (vidx < 0) return SV_OK;  // the amplitude is on another GPU: this shard stays zero
+    const SvSecHeader* H = reinterpret_cast<const SvSecHeader*>(h->prog.ints.data() + L.int_off);
+    int64_t tile = 0;
+    for (int j = 0; j < H->n_out; j++) tile |= (int64_t)((vidx >> H->out_bits[j]) & 1) << j;
+    if (jit_launch_section(h->dbl, h->sv, h->prog.ints.data() + L.int_off, h->prog.coefs.data() + 2 * L.coef_off, L,
+                           cdev, adev, h->st, &je, 0, 0, vidx, tile)) {
+      CUDA_TRY(h, je);
+      h->stats.jit_launches++;
+      h->stats.kernel_launches++;
+      return SV_OK;
+    }
+    if (int rc = materialize_at(h, vidx)) return rc;  // no generated kernel after all
+    return launch_one(h, L, split_a, split_b, -1);
+  }
   if (jit_launch_section(h->dbl, h->sv, h->prog.ints.data() + L.int_off, h->prog.coefs.data() + 2 * L.coef_off, L,
                          cdev, adev, h->st, &je, split_a, split_b, vidx)) {
     CUDA_TRY(h, je);

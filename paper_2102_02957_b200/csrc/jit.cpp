@@ -289,7 +289,7 @@ std::string gen_source(const int* p, const Launch& L, bool dbl, bool virt = fals
   o << "\n#include \"section_dev.cuh\"\nusing namespace sv;\ntypedef " << (dbl ? "double2" : "float2") << " V;\n";
   o << "extern \"C\" __global__ void __launch_bounds__(" << nt << ", " << resident_ctas(H->T, nt, has_dense(p))
     << ") sv_sec(V* __restrict__ psi, const V* __restrict__ aux, int split_a, int split_b, long long vidx, "
-    << coef_param_decl_impl(L, dbl) << ") {\n";
+    << "unsigned long long blk0, " << coef_param_decl_impl(L, dbl) << ") {\n";
   o << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n"
     << "  V* sm = reinterpret_cast<V*>(smem_raw);\n"
     << "  V* ctaf = reinterpret_cast<V*>(smem_raw + (sizeof(V) << " << H->T << "));\n"
@@ -298,7 +298,7 @@ std::string gen_source(const int* p, const Launch& L, bool dbl, bool virt = fals
   g.arr("int", "OB", H->out_bits, H->n_out);
   o << "  auto tile_of = [&](uint64_t t) {\n    uint64_t r = 0;\n#pragma unroll\n    for (int j = 0; j < "
     << H->n_out << "; j++) r |= ((t >> j) & 1ull) << OB[j];\n    return r;\n  };\n";
-  o << "  {\n  const uint64_t tile_off = tile_of(expand_tile(blockIdx.x, split_a, split_b));\n";
+  o << "  {\n  const uint64_t tile_off = tile_of(expand_tile(blockIdx.x + blk0, split_a, split_b));\n";
   // The tile's HBM loads are issued first (phase 0's registers, or the load step's), so their
   // latency overlaps the per-CTA DIAGSET factors computed next.
   o << "  V v[16];\n";
@@ -687,7 +687,7 @@ JitCounters g_ctr;
 
 const char* const kNvrtcOpts[] = {"-arch=sm_100a", "-std=c++17", "-lineinfo", "-DSV_JIT_KERNEL=1"};
 constexpr int kNvrtcNopts = 4;
-constexpr const char* kAbiTag = "sv_sec/abi-3";  // bump when the generated kernel's parameters change
+constexpr const char* kAbiTag = "sv_sec/abi-4";  // bump when the generated kernel's parameters change
 
 // NVRTC: source -> sm_100a cubin
 bool compile_cubin(const std::string& src, std::vector<char>& cubin, std::string& err) {
@@ -997,7 +997,7 @@ void jit_prepare(const Program& prog, bool dbl, bool virt_first) {
 
 bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const double* coef_host, const Launch& L,
                         const void* coef_dev, const void* aux_dev, cudaStream_t st, cudaError_t* err, int split_a,
-                        int split_b, int64_t vidx) {
+                        int split_b, int64_t vidx, int64_t only_tile) {
   *err = cudaSuccess;
   const Mode m = mode();
   if (m == kOff || L.T < SV_R_BITS) return false;
@@ -1078,9 +1078,10 @@ bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const double* 
     *err = cudaLaunchKernel(reinterpret_cast<const void*>(e->kern), dim3(grid), dim3(threads), args,
                             tma_smem_bytes(L, dbl), st);
   } else {
-    void* args[] = {&a0, &a1, &a2, &a3, &av, a4};
-    *err = cudaLaunchKernel(reinterpret_cast<const void*>(e->kern), dim3((unsigned)ntiles), dim3(threads), args,
-                            smem_bytes(L, dbl), st);
+    unsigned long long blk0 = only_tile >= 0 ? (unsigned long long)only_tile : 0ull;
+    void* args[] = {&a0, &a1, &a2, &a3, &av, &blk0, a4};
+    *err = cudaLaunchKernel(reinterpret_cast<const void*>(e->kern), dim3(only_tile >= 0 ? 1u : (unsigned)ntiles),
+                            dim3(threads), args, smem_bytes(L, dbl), st);
   }
   {
     std::lock_guard<std::mutex> lk(g_mu);

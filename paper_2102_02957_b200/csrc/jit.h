@@ -38,9 +38,10 @@ struct JitCounters {
 // the kernel-parameter space).
 bool jit_launch_section(bool dbl, void* sv, const int* prog_host, const double* coef_host, const Launch& L,
                         const void* coef_dev, const void* aux_dev, cudaStream_t st, cudaError_t* err,
-                        int split_a = 0, int split_b = 0, int64_t vidx = -1);
+                        int split_a = 0, int split_b = 0, int64_t vidx = -1, int64_t only_tile = -1);
 // vidx != -1: the launch does not read the state; its input is the basis state whose single
 // amplitude (1) sits at shard offset vidx (-2: on another GPU, all zeros here).
+// only_tile >= 0: launch the one tile with that block index (plain kernels only).
 
 // Make sure every launch of the program has its kernel: mode sync compiles the missing ones in
 // parallel now, mode async queues them.

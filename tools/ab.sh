@@ -1,6 +1,7 @@
-# randomised parity sweeps on one GPU (logs for profiles/)
+# final one-GPU verification as the driver runs it: build, the GPU suite, smoke, the default bench line
 set -x
-timeout 1200 python tools/stress.py 7 300 > gpurun_out/r02_stress.log 2>&1; echo stress=$?
-timeout 1500 python tools/stress_local.py 8 150 > gpurun_out/r02_stress_local.log 2>&1; echo local=$?
-SV_XCE=0 timeout 900 python tools/stress_local.py 9 60 > gpurun_out/r02_stress_local_push.log 2>&1; echo push=$?
-SV_TMA=2 timeout 900 python tools/stress.py 10 100 > gpurun_out/r02_stress_tma.log 2>&1; echo tma=$?
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r02_last_build.log 2>&1; echo build=$?
+T0=$(date +%s)
+timeout 1200 python -m pytest tests/ -x -q -m gpu > gpurun_out/r02_last_gpu_suite.log 2>&1; echo suite=$? secs=$(( $(date +%s) - T0 ))
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r02_last_smoke.log 2>&1; echo smoke=$?
+timeout 1200 python bench.py --gpus 1 --steps 20 --warmup 5 > gpurun_out/r02_last_bench.json 2> gpurun_out/r02_last_bench.err; echo bench=$?
