@@ -1035,7 +1035,9 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
           cudaEvent_t t = tstart(h);
           if (int rc = launch_one(h, L, 0, 0, si == 0 ? vidx : -1)) return rc;
           const double amps = (double)(1ull << h->nL);
-          tend(h, t, gen_input ? 3 : 0, (gen_input ? 1.0 : 2.0) * amps * (double)h->amp, L.flops_per_amp * amps);
+          // a generated input: the shard is cleared (write-only bytes) and one tile computed
+          const double fl = gen_input ? (vidx >= 0 ? L.flops_per_amp * (double)(1ull << L.T) : 0.0) : L.flops_per_amp * amps;
+          tend(h, t, gen_input ? 3 : 0, (gen_input ? 1.0 : 2.0) * amps * (double)h->amp, fl);
           h->stats.sections++;
         }
         break;
