@@ -335,7 +335,8 @@ def roofline(wl, precision, r, world):
     rw = None
     if n_rw > 0 and n_in > 0:
         rw = ((st["section_bytes"] - st["input_section_bytes"]) / n_rw,
-              (st["section_ms"] - st["input_section_ms"]) / n_rw / 1e3)
+              (st["section_ms"] - st["input_section_ms"]) / n_rw / 1e3,
+              (st["section_flops"] - st.get("input_section_flops", 0.0)) / n_rw)
     traffic = None
     prof = os.path.join(ROOT, "profiles", "section_traffic.json")
     if os.path.exists(prof) and world == 1:  # captured on one GPU: the N = 1 launch shape only
@@ -344,15 +345,17 @@ def roofline(wl, precision, r, world):
         except Exception:
             traffic = None
     if bytes_l / (hbm_peak * 1e9) >= flops_l / (fpk * 1e12):
-        b_rw, t_rw = rw if rw else (bytes_l, t_launch)
+        b_rw, t_rw, _ = rw if rw else (bytes_l, t_launch, flops_l)
         ach = b_rw / t_rw / 1e9
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(ach / hbm_peak, 4), "traffic": traffic, "peak_source": hbm_src,
                 "launches_rw": n_rw, "avg_launch_ms_rw": round(t_rw * 1e3, 4), "alg_bytes_per_launch_rw": b_rw}
     else:
-        ach = flops_l / t_launch / 1e12
+        _, t_rw, f_rw = rw if rw else (bytes_l, t_launch, flops_l)
+        ach = f_rw / t_rw / 1e12
         roof = {"bound": "alu", "achieved": round(ach, 3), "peak": round(fpk, 2), "unit": "TFLOP/s",
-                "frac": round(ach / fpk, 4), "traffic": traffic, "peak_source": fsrc}
+                "frac": round(ach / fpk, 4), "traffic": traffic, "peak_source": fsrc,
+                "launches_rw": n_rw, "avg_launch_ms_rw": round(t_rw * 1e3, 4), "alg_flops_per_launch_rw": f_rw}
     roof.update({"kernel": "sv_sec (run-time specialised section kernel; k_section when interpreted)",
                  "launches_timed": st["timed_sections"], "avg_launch_ms": round(t_launch * 1e3, 4),
                  "alg_bytes_per_launch": bytes_l, "alg_flops_per_launch": flops_l,
@@ -361,8 +364,10 @@ def roofline(wl, precision, r, world):
                  "input_sections": ({"launches": n_in, "avg_ms": round(st["input_section_ms"] / n_in, 4),
                                      "write_only_gbs": round(st["input_section_bytes"] / (st["input_section_ms"] / 1e3) / 1e9, 1)}
                                     if n_in else None),
-                 "alg_bytes_note": "2 x shard bytes per section launch (read + write); 1 x for the first section "
-                                   "after sv_reset, whose input is generated in-kernel (write only)"})
+                 "alg_bytes_note": "2 x shard bytes per section launch (read + write); the first section after "
+                                   "sv_reset clears the shard and computes only the tile holding the basis amplitude "
+                                   "(1 x shard bytes, one tile of flops): reported as input_sections, excluded from "
+                                   "frac (the read + write launches, *_rw)"})
     clocks = r.get("clocks") or {}
     if roof["bound"] == "alu" and clocks.get("sm_mhz"):
         # the FP64 peak scales with the SM clock; under FP64 + HBM load the B200 runs below its

@@ -119,6 +119,7 @@ typedef struct sv_stats {
   uint64_t timed_input_sections;
   double input_section_ms;
   double input_section_bytes;
+  double input_section_flops;
 } sv_stats_t;
 
 /* ---- lifetime ------------------------------------------------------------------------- */

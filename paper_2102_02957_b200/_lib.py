@@ -39,7 +39,7 @@ class Stats(ctypes.Structure):
                 ("jit_launches", ctypes.c_uint64), ("interp_launches", ctypes.c_uint64),
                 ("jit_compiled", ctypes.c_uint64), ("jit_compile_ms", ctypes.c_double),
                 ("timed_input_sections", ctypes.c_uint64), ("input_section_ms", ctypes.c_double),
-                ("input_section_bytes", ctypes.c_double)]
+                ("input_section_bytes", ctypes.c_double), ("input_section_flops", ctypes.c_double)]
 
 
 EXPORTS = ["sv_create", "sv_create_dist", "sv_world_create", "sv_world_destroy", "sv_create_local", "sv_destroy", "sv_nccl_unique_id", "sv_reset", "sv_apply_circuit",
@@ -110,7 +110,7 @@ def lib():
         f = getattr(L, name)
         f.argtypes = args
         f.restype = res
-    if L.sv_abi_version() != 2:
+    if L.sv_abi_version() != 3:
         raise RuntimeError("libsv.so ABI version mismatch")
     _lib = L
     return L

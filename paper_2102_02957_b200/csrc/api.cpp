@@ -374,6 +374,7 @@ int drain_timing(sv_state* h) {
         h->stats.timed_input_sections++;
         h->stats.input_section_ms += ms;
         h->stats.input_section_bytes += r.bytes;
+        h->stats.input_section_flops += r.flops;
       }
     } else if (r.kind == 1) {
       h->stats.exchange_ms += ms;
@@ -757,7 +758,7 @@ int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launc
 // ====================================================================== ABI
 extern "C" {
 
-int sv_abi_version(void) { return 2; }
+int sv_abi_version(void) { return 3; }
 
 const char* sv_last_error(sv_handle h) { return h ? h->err.c_str() : g_last_error.c_str(); }
 
