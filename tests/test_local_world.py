@@ -1,7 +1,7 @@
 """Multi-rank parity on ONE GPU: the in-process virtual world (sv_world_create / sv_create_local).
 
 G ranks, each a host thread with its own handle and shard on the same B200, run the multi-GPU path
-end to end — the two-level plan, the peer-memory swap kernel and the pipelined exchange + section,
+end to end — the two-level plan, the packed-piece peer exchange and its pipeline with the sections,
 the NCCL-style send/recv exchange (as device copies), the unblocked per-gate exchanges, every
 collective readout — and rank 0's results are checked against the CPU oracle and against a
 one-GPU run (tests/mgpu_cases.py).  PAPER.md P:137-166 (data distribution, pipelined exchange),
