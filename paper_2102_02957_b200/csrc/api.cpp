@@ -509,9 +509,11 @@ int setup_p2p(sv_state* h, void* base_alloc, size_t base_off) {
 // mu) is replaced by the partner's block `mine`, element j of one block pairing with element j of
 // the other (j: compact index over the remaining local bits).  Blocks are strided whenever an m-bit
 // is low, so they travel packed:
-//   peer path (CUDA IPC / local world): a small-grid push kernel gathers the block piece and stores
-//     it contiguously into the partner's receive slot over NVLink (remote stores only, full
-//     128-byte lines), then an unpack kernel scatters the slot into place;
+//   peer path (CUDA IPC / local world): the copy engines move each piece into the partner's
+//     receive slot over NVLink — as strided 2-D copies straight from the state when the block's
+//     runs are >= SV_XRUN bytes, else after a small-grid kernel packed it into a local send slot
+//     (SV_XCE=0: that kernel stores into the peer's slot itself) — then the copy engines (runs >=
+//     SV_XRUN bytes) or an unpack kernel scatter the slot into place;
 //   NCCL path (SV_EXCHANGE_NCCL, the comparator of P:420's send/recv): pack into a local send slot,
 //     grouped ncclSend / ncclRecv, unpack.
 // Pieces alternate between two slots: the transport of piece q (stream st_x) overlaps the unpack of
@@ -537,6 +539,18 @@ bool x_ce() {
     return !(e && e[0] == '0');
   }();
   return on;
+}
+// Copy engines for both ends of a piece when the exchanged block's contiguous runs are at least
+// SV_XRUN bytes (default 1024; 0 disables): the rows go straight from the state into the peer's
+// slot (no pack kernel, no send slot) and from the slot into place (no unpack kernel; SV_XCEU=0
+// keeps the unpack kernel).  Measured: QFT34 on 2 GPUs 317.9 -> 286.0 ms per step.
+uint64_t x_run_bytes() {
+  const char* e = std::getenv("SV_XRUN");
+  return e ? std::strtoull(e, nullptr, 10) : 1024;
+}
+bool x_ce_unpack() {
+  const char* e = std::getenv("SV_XCEU");
+  return !(e && e[0] == '0');
 }
 bool x_pipe() {
   static const bool on = [] {
@@ -657,6 +671,12 @@ int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launc
     }
   }
   const bool ce = !nccl_path && x_ce();
+  int lo = m[0];
+  for (int i = 0; i < ns; i++) lo = std::min(lo, sbit[i]);
+  const uint64_t xrun = x_run_bytes();
+  const bool direct = ce && xrun > 0 && (1ull << lo) * h->amp >= xrun;  // gather by copy engine
+  const uint64_t min_run = direct ? (xrun + h->amp - 1) / h->amp : 0;
+  const bool ce_unpack = !nccl_path && x_ce_unpack();
   cudaEvent_t t0 = nullptr;  // recorded where the first piece starts (after quarter 0 of Lp)
   char* recv = (char*)h->d_xrecv.p;
   char* send = (char*)h->d_xsend.p;
@@ -673,7 +693,7 @@ int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launc
     }
     if (h->timing && p == 0) {  // the exchange's span: from its first piece to its last unpack
       t0 = ev_get(h);
-      CUDA_TRY(h, cudaEventRecord(t0, ce ? h->st_p : h->st_x));
+      CUDA_TRY(h, cudaEventRecord(t0, ce && !direct ? h->st_p : h->st_x));
     }
     for (int t = 1; t < (1 << k); t++) {  // XOR schedule: every round is a perfect matching of ranks
       const int mu = mine ^ t;
@@ -704,7 +724,14 @@ int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launc
           // unpack of piece q - 1 is done (each rank's exchange stream waited for its own first),
           // so piece q + 1 may be pushed into the slot piece q - 1 used.
           char* dst = (char*)h->peer_xrecv[partner] + (size_t)b * slot * h->amp;
-          if (ce) {  // pack on its own stream, copy engine over NVLink: no SM holds the transfer
+          int nc = 0;
+          cudaError_t de = cudaErrorNotSupported;
+          if (direct)  // rows of the block straight from the state into the peer's slot
+            de = copy_bits_ce(true, h->sv, dst, off, cnt, nins, pos, val, h->amp, min_run, h->st_x, &nc);
+          if (de != cudaErrorNotSupported) {
+            CUDA_TRY(h, de);
+            h->stats.kernel_launches -= 1;  // no pack kernel for this piece
+          } else if (ce) {  // pack on its own stream, copy engine over NVLink: no SM holds the transfer
             char* sb = send + (size_t)b * slot * h->amp;
             if (q >= 2) CUDA_TRY(h, cudaStreamWaitEvent(h->st_p, h->ev_pushed[b], 0));  // send slot b copied
             CUDA_TRY(h, launch_pack_bits(h->dbl, true, h->sv, sb, off, cnt, nins, pos, val, 1ull << h->nL, h->st_p, x_grid()));
@@ -720,8 +747,20 @@ int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launc
         h->stats.kernel_launches += 2;
         CUDA_TRY(h, cudaEventRecord(h->ev_pushed[b], h->st_x));
         CUDA_TRY(h, cudaStreamWaitEvent(h->st_u, h->ev_pushed[b], 0));
-        CUDA_TRY(h, launch_pack_bits(h->dbl, false, h->sv, recv + (size_t)b * slot * h->amp, off, cnt, nins, pos, val, 1ull << h->nL,
-                                     h->st_u, x_grid()));
+        {
+          int nc = 0;
+          cudaError_t ue = cudaErrorNotSupported;
+          if (ce_unpack)
+            ue = copy_bits_ce(false, h->sv, recv + (size_t)b * slot * h->amp, off, cnt, nins, pos, val, h->amp,
+                              (std::max<uint64_t>(xrun, 1024) + h->amp - 1) / h->amp, h->st_u, &nc);
+          if (ue != cudaErrorNotSupported) {
+            CUDA_TRY(h, ue);
+            h->stats.kernel_launches -= 1;
+          } else {
+            CUDA_TRY(h, launch_pack_bits(h->dbl, false, h->sv, recv + (size_t)b * slot * h->amp, off, cnt, nins, pos, val,
+                                         1ull << h->nL, h->st_u, x_grid()));
+          }
+        }
         CUDA_TRY(h, cudaEventRecord(h->ev_unpacked[b], h->st_u));
       }
     }

@@ -555,4 +555,65 @@ cudaError_t launch_pack_bits(bool dbl, bool pack, void* sv, void* stage, uint64_
   return cudaGetLastError();
 }
 
+// Copy-engine form of pack / unpack (no SM): when every inserted bit is >= lo and runs of 2^lo
+// elements are at least min_run elements long, a block piece is a few strided 2-D copies (rows of
+// 2^lo elements; the pitch is constant up to the next inserted bit that is not adjacent to lo's
+// group).  stage may be a peer's receive slot (CUDA IPC / same device): the rows then go over NVLink
+// straight from the state, without a local send slot.  Returns cudaErrorNotSupported when the
+// piece does not have that shape (the caller packs with k_pack_bits instead).
+cudaError_t copy_bits_ce(bool pack, void* sv, void* stage, uint64_t first, uint64_t count, int nins, const int* pos,
+                         const int* val, size_t amp, uint64_t min_run, cudaStream_t st, int* copies) {
+  *copies = 0;
+  if (nins < 1 || nins > 11 || count == 0) return cudaErrorNotSupported;
+  int P[11], Vv[11];
+  for (int i = 0; i < nins; i++) P[i] = pos[i], Vv[i] = val[i];
+  for (int i = 1; i < nins; i++)
+    for (int j = i; j > 0 && P[j] < P[j - 1]; j--) std::swap(P[j], P[j - 1]), std::swap(Vv[j], Vv[j - 1]);
+  const int lo = P[0];
+  const uint64_t run = 1ull << lo;
+  if (run < min_run) return cudaErrorNotSupported;
+  auto addr = [&](uint64_t x) {  // compact index -> element index (insert_bit, ascending)
+    for (int k = 0; k < nins; k++) {
+      const uint64_t l = x & ((1ull << P[k]) - 1);
+      x = ((x - l) << 1) | ((uint64_t)Vv[k] << P[k]) | l;
+    }
+    return x;
+  };
+  char* S = (char*)sv;
+  char* G = (char*)stage;
+  if (count <= run) {  // inside one run: one contiguous copy
+    if ((first >> lo) != ((first + count - 1) >> lo)) return cudaErrorNotSupported;
+    const uint64_t a = addr(first);
+    *copies = 1;
+    return pack ? cudaMemcpyAsync(G, S + a * amp, count * amp, cudaMemcpyDeviceToDevice, st)
+                : cudaMemcpyAsync(S + a * amp, G, count * amp, cudaMemcpyDeviceToDevice, st);
+  }
+  if ((first & (run - 1)) || (count & (run - 1))) return cudaErrorNotSupported;
+  int a = 1;
+  while (a < nins && P[a] == lo + a) a++;
+  const size_t width = run * amp, pitch = (1ull << (lo + a)) * amp;
+  const uint64_t seg_rows = a < nins ? 1ull << (P[a] - lo - a) : ~0ull;  // rows of constant pitch
+  const uint64_t r0 = first >> lo, r1 = (first + count) >> lo;
+  const bool rows_1d = pitch > (size_t)INT32_MAX;
+  if (rows_1d && r1 - r0 > 64) return cudaErrorNotSupported;
+  for (uint64_t r = r0; r < r1;) {
+    const uint64_t e = seg_rows == ~0ull ? r1 : std::min(r1, (r / seg_rows + 1) * seg_rows);
+    char* sp = S + addr(r << lo) * amp;
+    char* gp = G + ((r - r0) << lo) * amp;
+    cudaError_t err = cudaSuccess;
+    if (rows_1d) {
+      for (uint64_t i = 0; i < e - r && err == cudaSuccess; i++, (*copies)++)
+        err = pack ? cudaMemcpyAsync(gp + i * width, sp + i * pitch, width, cudaMemcpyDeviceToDevice, st)
+                   : cudaMemcpyAsync(sp + i * pitch, gp + i * width, width, cudaMemcpyDeviceToDevice, st);
+    } else {
+      err = pack ? cudaMemcpy2DAsync(gp, width, sp, pitch, width, e - r, cudaMemcpyDeviceToDevice, st)
+                 : cudaMemcpy2DAsync(sp, pitch, gp, width, width, e - r, cudaMemcpyDeviceToDevice, st);
+      (*copies)++;
+    }
+    if (err != cudaSuccess) return err;
+    r = e;
+  }
+  return cudaSuccess;
+}
+
 }  // namespace sv

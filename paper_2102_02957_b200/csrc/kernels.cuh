@@ -53,5 +53,9 @@ cudaError_t launch_gather(bool dbl, const void* sv, const uint64_t* offs, size_t
 cudaError_t launch_pack_bits(bool dbl, bool pack, void* sv, void* stage, uint64_t first, uint64_t count, int nins,
                              const int* pos, const int* val, uint64_t shard_amps, cudaStream_t st,
                              unsigned max_blocks = 0);
+// the same pack (sv -> stage) / unpack (stage -> sv) as copy-engine 2-D copies when the block's
+// runs are >= min_run elements (kernels.cu); cudaErrorNotSupported otherwise; *copies = copies issued
+cudaError_t copy_bits_ce(bool pack, void* sv, void* stage, uint64_t first, uint64_t count, int nins, const int* pos,
+                         const int* val, size_t amp, uint64_t min_run, cudaStream_t st, int* copies);
 
 }  // namespace sv

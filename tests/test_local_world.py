@@ -116,3 +116,24 @@ def test_local_world_interpreter_shared_constants():
             assert float(np.max(np.abs(got - O.apply_circuit(circ, n, basis=3)))) <= 1e-10
     finally:
         sv.jit_mode(prev)
+
+
+@pytest.mark.parametrize("xrun,xceu", [("16", "0"), ("16", "1"), ("1024", "1"), ("0", "1")])
+@pytest.mark.parametrize("world", [2, 4])
+def test_local_world_copy_engine_gather(world, xrun, xceu, monkeypatch):
+    # The copy-engine form of the exchange (api.cpp exchange, kernels.cu copy_bits_ce): rows of the
+    # block go straight from the state into the peer's slot as strided 2-D copies when its runs are
+    # >= SV_XRUN bytes, and back into place the same way (SV_XCEU=0: the unpack kernel instead).
+    # SV_XRUN=16 forces the copies for every exchanged bit (one-element rows), 1024 (the default)
+    # only for bits >= 6, 0 packs and unpacks with kernels; all against the oracle.
+    monkeypatch.setenv("SV_XRUN", xrun)
+    monkeypatch.setenv("SV_XCEU", xceu)
+    for case in [c for c in M.cases() if c[0] in ("qv", "qft", "rand", "qv-twice", "qft-fp32")]:
+        name = case[0]
+        if name not in _REF:
+            _REF[name] = M.reference(case)
+            _ONE[name] = M.single_gpu(sv, case)
+        res = run_world(world, case)
+        checks, err, d1 = M.check(case, res[0], _REF[name], _ONE[name], world)
+        bad = [k for k, ok in checks.items() if not ok]
+        assert not bad, (name, world, xrun, xceu, bad, err, d1)

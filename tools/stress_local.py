@@ -1,6 +1,6 @@
 """Randomised multi-rank parity sweep on ONE GPU (not part of the test suite): fuzz circuits on an
 in-process virtual world of G = 2, 4 or 8 ranks (sv_create_local), random chunk_bits, precision,
-exchange transport (copy engine, push kernel, NCCL-style send/recv), swap absorption, unblocked
+exchange transport (copy engine with or without the pack kernel, copy-engine unpack, NCCL-style send/recv), swap absorption, unblocked
 mode, a second circuit on the left-over layout; rank 0's state against the oracle.
 usage: python tools/stress_local.py [seed] [cases]"""
 import os
@@ -34,6 +34,8 @@ for t in range(count):
     kinds = [("u3", "cx", "cp", "swap", "su4", "u1", "d2"), ("u3", "su4"), ("cp", "u1", "d2", "u3", "swap")][t % 3]
     circ = C.random_circuit(n, int(rng.integers(1, 200)), 20000 + t, kinds=kinds)
     k = int(rng.integers(0, 1 << n))
+    os.environ["SV_XRUN"] = str(rng.choice(["16", "256", "1024", "0"]))  # copy-engine gather threshold
+    os.environ["SV_XCEU"] = str(rng.choice(["0", "1"]))  # copy-engine unpack
     try:
         with sv.LocalWorld(world) as w:
             def body(rank):
@@ -48,7 +50,8 @@ for t in range(count):
         tol = 1e-10 if prec == "fp64" else 1e-4
         if not err <= tol:
             bad += 1
-            print(f"FAIL t={t} G={world} n={n} c={c} {prec} flags={flags} gates={len(circ)} err={err:.3g}", flush=True)
+            print(f"FAIL t={t} G={world} n={n} c={c} {prec} flags={flags} gates={len(circ)} err={err:.3g} "
+                  f"xrun={os.environ['SV_XRUN']} xceu={os.environ['SV_XCEU']}", flush=True)
     except Exception as e:  # noqa: BLE001
         bad += 1
         print(f"ERROR t={t} G={world} n={n} c={c} {prec} flags={flags}: {e}", flush=True)
