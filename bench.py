@@ -396,7 +396,9 @@ def nvlink(r, steps, wl_name=None, world=1):
             "alone_measured": alone,
             "frac_of_measured_peer_copy": round(gbs / 770.0, 4), "bytes_per_rank_per_step": st["bytes_sent"] / steps,
             "share_of_step": round(st["exchange_ms"] / ms, 4),
-            "transport": "NCCL send/recv (packed)" if APPLY_FLAGS & 4 else ("packed pieces, copy-engine peer copies (CUDA IPC)" if os.environ.get("SV_XCE", "1") != "0" else "packed pieces, peer-store push kernel (CUDA IPC)")}
+            "transport": "NCCL send/recv (packed)" if APPLY_FLAGS & 4 else ("copy engines over CUDA IPC: strided rows from the state into the peer's slot and back into place "
+                          "(rows >= SV_XRUN bytes, default 1 KiB), else pack kernel + copy + unpack kernel"
+                          if os.environ.get("SV_XCE", "1") != "0" else "peer-store push kernel (CUDA IPC)")}
 
 
 def run_ours(args):

@@ -219,7 +219,13 @@ int sync_stream(sv_state* h) {
   return SV_OK;
 }
 
-int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launch* L0, const Launch* Lp, int* done);
+// Section launches an exchange runs quarter by quarter around itself (the executor's pipeline
+// plan, apply_circuit): the split bits are out of the tile of every one of them.
+struct XPipe {
+  int ns = 0, sbit[2] = {0, 0};
+  std::vector<size_t> pre, post;  // indices into h->prog.launches
+};
+int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const XPipe& xp);
 
 int upload_program(sv_state* h) {
   const size_t ib = h->prog.ints.size() * sizeof(int);
@@ -528,6 +534,13 @@ int setup_p2p(sv_state* h, void* base_alloc, size_t base_off) {
 // 528 no faster alone, slower overlapped), receive slots of 1 GiB (4 GiB no faster).  SV_XPIPE=0
 // runs the exchange without overlapping its neighbouring sections (a comparator line).
 constexpr unsigned kXGrid = 132;
+// most section launches run quarter by quarter on either side of an exchange (SV_XCHAIN overrides).
+// Longer chains measured no faster (QV33 on 2 GPUs 942 / 940 / 940 ms at 1 / 4 / 16;
+// the FP64-bound sections are power-capped, the HBM-bound ones share HBM with the copies).
+size_t x_chain() {
+  const char* e = std::getenv("SV_XCHAIN");
+  return e ? std::strtoull(e, nullptr, 10) : 1;
+}
 constexpr uint64_t kXSlotBytes = 1ull << 30;
 unsigned x_grid() { return kXGrid; }
 uint64_t x_slot_bytes() { return kXSlotBytes; }
@@ -592,50 +605,20 @@ int ensure_exchange_engine(sv_state* h, uint64_t slot_amps, bool nccl_path) {
   return SV_OK;
 }
 
-int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launch* L0, const Launch* Lp, int* done) {
-  *done = 0;
-  Nvtx r("sv exchange k=%zu%s", pairs.size(), L0 ? " + section" : "");
+int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const XPipe& xp) {
+  Nvtx r("sv exchange k=%zu pre=%zu post=%zu", pairs.size(), xp.pre.size(), xp.post.size());
   std::sort(pairs.begin(), pairs.end(), [](const ExPair& a, const ExPair& b) { return a.m < b.m; });
   const int k = (int)pairs.size();
   if (k < 1 || k > 8) return fail(h, SV_EINVAL, "internal: exchange of 1..8 bits expected");
   int m[8], bsel[8], mine = 0;
-  uint64_t mmask = 0;
   for (int i = 0; i < k; i++) {
     m[i] = pairs[i].m;
     bsel[i] = pairs[i].b - h->nL;
-    mmask |= 1ull << m[i];
     mine |= ((h->rank >> bsel[i]) & 1) << i;
   }
   const bool nccl_path = (flags & SV_EXCHANGE_NCCL) || !h->p2p;
-  // split bits: the next section's highest out-of-tile bits that are not exchanged (and, with the
-  // previous section's last launch Lp to pipeline too, out of its tile as well)
-  int ns = 0, sidx[2] = {0, 0}, sbit[2] = {0, 0}, pidx[2] = {0, 0};
-  if (L0 && !x_pipe()) L0 = nullptr;
-  const SvSecHeader* Hp =
-      Lp && Lp->T >= SV_R_BITS ? reinterpret_cast<const SvSecHeader*>(h->prog.ints.data() + Lp->int_off) : nullptr;
-  if (L0 && L0->T >= SV_R_BITS) {
-    const SvSecHeader* H = reinterpret_cast<const SvSecHeader*>(h->prog.ints.data() + L0->int_off);
-    for (int j = H->n_out - 1; j >= 0 && ns < 2; j--) {
-      const int b = H->out_bits[j];
-      if ((mmask >> b) & 1) continue;
-      int jp = -1;
-      if (Hp)
-        for (int q = 0; q < Hp->n_out; q++)
-          if (Hp->out_bits[q] == b) jp = q;
-      if (Hp && jp < 0) continue;
-      sidx[ns] = j;
-      pidx[ns] = jp;
-      sbit[ns] = b;
-      ns++;
-    }
-    if (ns == 2) {  // ascending out-bit index for expand_tile
-      std::swap(sidx[0], sidx[1]);
-      std::swap(pidx[0], pidx[1]);
-      std::swap(sbit[0], sbit[1]);
-    }
-  }
-  if (h->nL - k - ns < 0) ns = 0;
-  if (Hp && (ns == 0 || (ns == 2 && pidx[0] > pidx[1]))) Hp = nullptr;  // quarters of Lp: ascending out bits
+  const int ns = xp.ns;
+  const int* sbit = xp.sbit;
   const int P = 1 << ns;
   const uint64_t qblock = 1ull << (h->nL - k - ns);  // elements per (quarter, partner)
   const uint64_t slot = std::min<uint64_t>(qblock, std::max<uint64_t>(1, x_slot_bytes() / h->amp));
@@ -643,30 +626,38 @@ int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launc
   h->stats.bytes_sent += (uint64_t)((1ull << k) - 1) * (1ull << (h->nL - k)) * h->amp;
   h->stats.exchanges += k;
   h->stats.exchange_batches++;
-
-  // the exchange streams start after everything queued so far on the compute stream; the previous
-  // section's last launch (Lp), if given, runs in quarters there, the exchange of quarter p
-  // starting as soon as quarter p is written
-  if (Lp && !Hp) {  // no common split: run it whole first
+  // quarter p of a chain launch: the split bits fixed to p's bits (tile-expansion specs in the
+  // launch's ascending out-bit order)
+  auto run_quarter = [&](size_t li, int p) -> int {
+    const Launch& L = h->prog.launches[li];
+    const SvSecHeader* H = reinterpret_cast<const SvSecHeader*>(h->prog.ints.data() + L.int_off);
+    int js[2] = {0, 0}, vs[2] = {0, 0}, sp[2] = {0, 0};
+    for (int i = 0; i < ns; i++) {
+      for (int j = 0; j < H->n_out; j++)
+        if (H->out_bits[j] == sbit[i]) js[i] = j;
+      vs[i] = (p >> i) & 1;
+    }
+    if (ns == 2 && js[0] > js[1]) std::swap(js[0], js[1]), std::swap(vs[0], vs[1]);
+    for (int i = 0; i < ns; i++) sp[i] = (1 << 16) | (vs[i] << 8) | js[i];
+    const double amps = (double)(1ull << h->nL) / P;
     cudaEvent_t ts = tstart(h);
-    if (int rc = launch_one(h, *Lp)) return rc;
-    const double amps = (double)(1ull << h->nL);
-    tend(h, ts, 0, 2.0 * amps * (double)h->amp, Lp->flops_per_amp * amps);
-    Lp = nullptr;
-  }
+    if (int rc = launch_one(h, L, sp[0], sp[1])) return rc;
+    tend(h, ts, 0, 2.0 * amps * (double)h->amp, L.flops_per_amp * amps);
+    return SV_OK;
+  };
+
+  // the exchange streams start after everything queued so far on the compute stream; the chain
+  // before it (xp.pre) then runs quarter by quarter there, the exchange of quarter p starting as
+  // soon as the chain has written quarter p
   CUDA_TRY(h, cudaEventRecord(h->ev_start, h->st));
   CUDA_TRY(h, cudaStreamWaitEvent(h->st_x, h->ev_start, 0));
   CUDA_TRY(h, cudaStreamWaitEvent(h->st_u, h->ev_start, 0));
   CUDA_TRY(h, cudaStreamWaitEvent(h->st_p, h->ev_start, 0));
-  const int P0 = 1 << ns;
-  if (Lp) {
-    for (int p = 0; p < P0; p++) {
-      int sp[2] = {0, 0};
-      for (int i = 0; i < ns; i++) sp[i] = (1 << 16) | (((p >> i) & 1) << 8) | pidx[i];
-      const double amps = (double)(1ull << h->nL) / P0;
-      cudaEvent_t ts = tstart(h);
-      if (int rc = launch_one(h, *Lp, sp[0], sp[1])) return rc;
-      tend(h, ts, 0, 2.0 * amps * (double)h->amp, Lp->flops_per_amp * amps);
+  const bool pre = !xp.pre.empty();
+  if (pre) {
+    for (int p = 0; p < P; p++) {
+      for (size_t li : xp.pre)
+        if (int rc = run_quarter(li, p)) return rc;
       CUDA_TRY(h, cudaEventRecord(h->ev_prev[p], h->st));
     }
   }
@@ -687,7 +678,7 @@ int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launc
   int pos[11], val[11];
   uint64_t q = 0;
   for (int p = 0; p < P; p++) {
-    if (Lp) {  // quarter p of the previous section is written before it is packed / sent
+    if (pre) {  // quarter p of the chain before is written before it is packed / sent
       CUDA_TRY(h, cudaStreamWaitEvent(h->st_p, h->ev_prev[p], 0));
       CUDA_TRY(h, cudaStreamWaitEvent(h->st_x, h->ev_prev[p], 0));
     }
@@ -764,15 +755,11 @@ int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launc
         CUDA_TRY(h, cudaEventRecord(h->ev_unpacked[b], h->st_u));
       }
     }
-    if (L0) {  // quarter p of the next section: its tiles have every exchanged element now
+    if (!xp.post.empty()) {  // quarter p of the chain after: its tiles have every exchanged element now
       CUDA_TRY(h, cudaEventRecord(h->ev_landed[p], h->st_u));
       CUDA_TRY(h, cudaStreamWaitEvent(h->st, h->ev_landed[p], 0));
-      int sp[2] = {0, 0};
-      for (int i = 0; i < ns; i++) sp[i] = (1 << 16) | (((p >> i) & 1) << 8) | sidx[i];
-      const double amps = (double)(1ull << h->nL) / P;
-      cudaEvent_t ts = tstart(h);
-      if (int rc = launch_one(h, *L0, sp[0], sp[1])) return rc;
-      tend(h, ts, 0, 2.0 * amps * (double)h->amp, L0->flops_per_amp * amps);
+      for (size_t li : xp.post)
+        if (int rc = run_quarter(li, p)) return rc;
     }
   }
   if (h->timing) {
@@ -785,10 +772,7 @@ int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const Launc
   CUDA_TRY(h, cudaStreamWaitEvent(h->st, h->ev_done, 0));
   CUDA_TRY(h, cudaEventRecord(h->ev_done, h->st_x));
   CUDA_TRY(h, cudaStreamWaitEvent(h->st, h->ev_done, 0));
-  if (L0) {
-    h->stats.sections++;
-    *done = 1;
-  }
+  h->stats.sections += xp.pre.size() + xp.post.size();
   return SV_OK;
 }
 
@@ -1038,19 +1022,80 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
   }
   jit_prepare(h->prog, h->dbl, vidx != -1);  // run-time specialised kernels (jit.h): compile what is missing
   if (int rc = upload_program(h)) return rc;
+  // Pipeline plan (§8(e), the paper's overlap of exchange and computation): each
+  // exchange takes up to two split bits — local memory bits it does not exchange that lie outside
+  // the tile of the section launches next to it — and runs the launches on either side whose tiles
+  // all avoid those bits quarter by quarter around itself: the chain before it writes quarter p,
+  // quarter p travels, the chain after it computes on quarter p while quarter p + 1 travels.
+  std::vector<XPipe> xps(steps.size());
+  std::vector<char> by_exchange(h->prog.launches.size(), 0);
+  if (x_pipe() && h->nL >= SV_R_BITS) {
+    std::vector<size_t> launch_begin(steps.size());
+    for (size_t i = 0; i < steps.size(); i++) launch_begin[i] = i ? launch_end[i - 1] : 0;
+    auto hdr = [&](size_t li) { return reinterpret_cast<const SvSecHeader*>(h->prog.ints.data() + h->prog.launches[li].int_off); };
+    auto out_has = [&](size_t li, int b) {
+      if (h->prog.launches[li].T < SV_R_BITS) return false;
+      const SvSecHeader* H = hdr(li);
+      for (int j = 0; j < H->n_out; j++)
+        if (H->out_bits[j] == b) return true;
+      return false;
+    };
+    size_t claimed = vidx != -1 ? 1 : 0;  // launches before this index are taken (or the generated input)
+    for (size_t i = 0; i < steps.size(); i++) {
+      if (steps[i].type != Step::EXCHANGE || i + 1 >= steps.size() || steps[i + 1].type != Step::SECTION) continue;
+      const size_t l0 = launch_begin[i + 1];
+      if (l0 >= launch_end[i + 1] || h->prog.launches[l0].T < SV_R_BITS) continue;
+      uint64_t mmask = 0;
+      for (const ExPair& e : steps[i].ex) mmask |= 1ull << e.m;
+      // the chain before: launches of the sections right before the exchange, not yet taken
+      std::vector<size_t> cand_pre;
+      for (size_t j = i; j-- > 0 && steps[j].type == Step::SECTION;)
+        for (size_t li = launch_end[j]; li-- > launch_begin[j];) cand_pre.push_back(li);
+      const bool has_lp = !cand_pre.empty() && cand_pre[0] >= claimed;
+      XPipe& xp = xps[i];
+      const SvSecHeader* H0 = hdr(l0);
+      for (int with_lp = has_lp; with_lp >= 0 && xp.ns == 0; with_lp--)  // common bits first, else the chain after only
+        for (int j = H0->n_out - 1; j >= 0 && xp.ns < 2; j--) {  // highest out bits of the first launch
+          const int b = H0->out_bits[j];
+          if ((mmask >> b) & 1) continue;
+          if (with_lp && !out_has(cand_pre[0], b)) continue;
+          xp.sbit[xp.ns++] = b;
+        }
+      if (h->nL - (int)steps[i].ex.size() - xp.ns < 0) xp.ns = 0;
+      auto fits = [&](size_t li) {
+        for (int q = 0; q < xp.ns; q++)
+          if (!out_has(li, xp.sbit[q])) return false;
+        return true;
+      };
+      if (xp.ns > 0) {
+        for (size_t li : cand_pre) {
+          if (li < claimed || xp.pre.size() >= x_chain() || !fits(li)) break;
+          xp.pre.push_back(li);
+        }
+        std::reverse(xp.pre.begin(), xp.pre.end());
+        for (size_t j = i + 1; j < steps.size() && steps[j].type == Step::SECTION && xp.post.size() < x_chain(); j++) {
+          bool all = true;
+          for (size_t li = launch_begin[j]; li < launch_end[j]; li++) {
+            if (!fits(li) || xp.post.size() >= x_chain()) {
+              all = false;
+              break;
+            }
+            xp.post.push_back(li);
+          }
+          if (!all) break;
+        }
+      }
+      for (size_t li : xp.pre) by_exchange[li] = 1;
+      for (size_t li : xp.post) by_exchange[li] = 1;
+      if (!xp.post.empty()) claimed = xp.post.back() + 1;
+    }
+  }
   size_t si = 0;
-  const Launch* deferred = nullptr;  // a section's last launch left to the following exchange
   for (size_t i = 0; i < steps.size(); i++) {
     const Step& st = steps[i];
     switch (st.type) {
       case Step::EXCHANGE: {
-        const bool next_section = i + 1 < steps.size() && steps[i + 1].type == Step::SECTION &&
-                                  h->nL >= SV_R_BITS && si < launch_end[i + 1];
-        int done = 0;
-        if (int rc = exchange(h, st.ex, flags, next_section ? &h->prog.launches[si] : nullptr, deferred, &done))
-          return rc;
-        deferred = nullptr;  // launched by the exchange, quarter by quarter
-        if (done) si++;      // the next section's first launch already ran, quarter by quarter
+        if (int rc = exchange(h, st.ex, flags, xps[i])) return rc;
         break;
       }
       case Step::SECTION: {
@@ -1064,14 +1109,7 @@ int sv_apply_circuit(sv_handle h, const sv_gate* gates, size_t n_gates, uint32_t
         for (; si < launch_end[i]; si++) {
           const Launch& L = h->prog.launches[si];
           const bool gen_input = si == 0 && vidx != -1;  // the deferred basis state: a write-only pass
-          // the last launch of a section followed by an exchange and another section is issued by
-          // the exchange in quarters, so the exchange of quarter p starts as soon as it is written
-          if (si + 1 == launch_end[i] && !gen_input && x_pipe() && i + 2 < steps.size() &&
-              steps[i + 1].type == Step::EXCHANGE && steps[i + 2].type == Step::SECTION) {
-            deferred = &L;
-            h->stats.sections++;
-            continue;
-          }
+          if (by_exchange[si]) continue;  // run by the neighbouring exchange, quarter by quarter
           cudaEvent_t t = tstart(h);
           if (int rc = launch_one(h, L, 0, 0, si == 0 ? vidx : -1)) return rc;
           const double amps = (double)(1ull << h->nL);

@@ -137,3 +137,21 @@ def test_local_world_copy_engine_gather(world, xrun, xceu, monkeypatch):
         checks, err, d1 = M.check(case, res[0], _REF[name], _ONE[name], world)
         bad = [k for k, ok in checks.items() if not ok]
         assert not bad, (name, world, xrun, xceu, bad, err, d1)
+
+
+@pytest.mark.parametrize("xchain", ["0", "1", "16"])
+@pytest.mark.parametrize("world", [2, 4])
+def test_local_world_pipeline_chains(world, xchain, monkeypatch):
+    # The executor's pipeline plan (api.cpp apply_circuit / exchange): up to SV_XCHAIN section
+    # launches on either side of an exchange run quarter by quarter around it (0: none, the pieces
+    # still grouped by the split bits; 1: one launch each side; 16: long chains across sections).
+    monkeypatch.setenv("SV_XCHAIN", xchain)
+    for case in [c for c in M.cases() if c[0] in ("qv", "qft", "rand", "qv-twice", "qft-absorb")]:
+        name = case[0]
+        if name not in _REF:
+            _REF[name] = M.reference(case)
+            _ONE[name] = M.single_gpu(sv, case)
+        res = run_world(world, case)
+        checks, err, d1 = M.check(case, res[0], _REF[name], _ONE[name], world)
+        bad = [k for k, ok in checks.items() if not ok]
+        assert not bad, (name, world, xchain, bad, err, d1)
