@@ -1,6 +1,6 @@
 #!/bin/bash
 # multi-GPU on one box (under gpurun --gpus N): parity tests over NCCL + CUDA IPC, then bench lines —
-# QV33 strong (peer push exchange pipelined with the section / alone / the NCCL send/recv
+# QV33 strong (copy-engine exchange pipelined with the sections / alone / the NCCL send/recv
 # comparator), QFT weak, QV28 strong blocked vs unblocked (NEXT-3).  NVLink data counters
 # (nvidia-smi) around the QV33 run.  Outputs gpurun_out/r02_mgpu_*_n$N.*
 N=${1:-2}
