@@ -324,8 +324,11 @@ std::string gen_source(const int* p, const Launch& L, bool dbl, bool virt = fals
     for (int i = 0; i < ph[k].op_count; i++) {
       const SvOp& op = ops[ph[k].op_begin + i];
       if (!g.diagset_c(p, op, std::to_string(nt)))
-        o << "    op_c<" << op.type << ", " << op.a << ", " << op.b << ", " << op.coef << ", " << op.extra
-          << ">(v, tid, " << nt << ", tile_off, aux, ctaf, P);\n";
+        // dense gates of a phase fed straight from HBM take the split form (u2_slots SPLIT): with
+        // the chained form ptxas interleaves the tile's loads with the first gate and leaves
+        // HBM latency exposed
+        o << "    op_c<" << op.type << ", " << op.a << ", " << op.b << ", " << op.coef << ", "
+          << (op.type == SV_OP_U2 ? (din ? 1 : 0) : op.extra) << ">(v, tid, " << nt << ", tile_off, aux, ctaf, P);\n";
     }
     if (dout) {
       o << "    {\n";

@@ -83,10 +83,11 @@ __device__ __forceinline__ int swz(int i) {
 // 4x4 complex matrix on the register pairs of slots S0 < S1, three real products per complex
 // multiply-add: with s = x + y of each input, out.re = T + R and out.im = T + I where
 // T = sum m.re s, R = sum -(m.re + m.im) y, I = sum (m.im - m.re) x (the host stores the two
-// derived coefficients after the matrix).  The R and I chains start from T, so the sums need no
-// separate adds: 52 instead of 64 FP64 operations per 4 amplitudes (4 adds for s, per output row
-// one multiply and 11 FMAs).
-template <int S0, int S1, typename V, typename CF = CoefBank<V>>
+// derived coefficients after the matrix).  Chained form (default): the R and I chains start from
+// T, so the sums need no separate adds — 52 instead of 64 FP64 operations per 4 amplitudes (4 adds
+// for s, per output row one multiply and 11 FMAs).  SPLIT form (60 operations: R and I on their own,
+// then T added): shorter dependency chains, used where the inputs come straight from HBM.
+template <int S0, int S1, bool SPLIT = false, typename V, typename CF = CoefBank<V>>
 __device__ __forceinline__ void u2_slots(V (&v)[16], int cb, const CF& cf = CF()) {
   using R = decltype(V().x);
 #pragma unroll
@@ -102,11 +103,25 @@ __device__ __forceinline__ void u2_slots(V (&v)[16], int cb, const CF& cf = CF()
       R t = cf(cb + 4 * rr).x * s[0];
 #pragma unroll
       for (int c = 1; c < 4; c++) t = fma(cf(cb + 4 * rr + c).x, s[c], t);
-      R re = t, im = t;
+      R re, im;
+      if constexpr (SPLIT) {
+        re = cf(cb + 16 + 4 * rr).x * a[0].y;
+        im = cf(cb + 16 + 4 * rr).y * a[0].x;
 #pragma unroll
-      for (int c = 0; c < 4; c++) {
-        re = fma(cf(cb + 16 + 4 * rr + c).x, a[c].y, re);
-        im = fma(cf(cb + 16 + 4 * rr + c).y, a[c].x, im);
+        for (int c = 1; c < 4; c++) {
+          re = fma(cf(cb + 16 + 4 * rr + c).x, a[c].y, re);
+          im = fma(cf(cb + 16 + 4 * rr + c).y, a[c].x, im);
+        }
+        re += t;
+        im += t;
+      } else {
+        re = t;
+        im = t;
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+          re = fma(cf(cb + 16 + 4 * rr + c).x, a[c].y, re);
+          im = fma(cf(cb + 16 + 4 * rr + c).y, a[c].x, im);
+        }
       }
       V o;
       o.x = re;
@@ -478,7 +493,7 @@ template <int TYPE, int A, int B, int CB, int X, typename V, typename CF>
 __device__ __forceinline__ void op_c(V (&v)[16], int tid, int nthr, uint64_t tile_off, const V* __restrict__ aux,
                                      const V* ctaf, const CF& cf) {
   if constexpr (TYPE == SV_OP_U2) {
-    u2_slots<A, B>(v, CB, cf);
+    u2_slots<A, B, X == 1>(v, CB, cf);
   } else if constexpr (TYPE == SV_OP_U1) {
     u1_slot<A>(v, CB, cf);
   } else if constexpr (TYPE == SV_OP_H1) {
