@@ -15,3 +15,6 @@ timeout 900 $R --master-port 29604 bench.py --gpus $N --steps 5 --warmup 3 --no-
 SV_XPIPE=0 timeout 900 $R --master-port 29605 bench.py --gpus $N --steps 5 --warmup 3 --no-sub --no-e2e --workload qft_weak > gpurun_out/r02_mgpu_qftweakraw_n$N.json 2> gpurun_out/r02_mgpu_qftweakraw_n$N.err; echo qftweakraw=$?
 timeout 900 $R --master-port 29606 bench.py --gpus $N --steps 5 --warmup 3 --no-sub --no-e2e --workload qv28 > gpurun_out/r02_mgpu_qv28_n$N.json 2> gpurun_out/r02_mgpu_qv28_n$N.err; echo qv28=$?
 timeout 900 $R --master-port 29607 bench.py --gpus $N --steps 3 --warmup 3 --no-sub --no-e2e --workload qv28 --unblocked > gpurun_out/r02_mgpu_qv28unb_n$N.json 2> gpurun_out/r02_mgpu_qv28unb_n$N.err; echo qv28unb=$?
+# peer-transfer ceilings (copy-engine peer copy, NCCL send/recv) on the same box
+timeout 600 python tools/p2p_bench.py ce $N > gpurun_out/r02_p2p_ce_n$N.jsonl 2> gpurun_out/r02_p2p_ce_n$N.err; echo p2pce=$?
+timeout 600 $R --master-port 29608 tools/p2p_bench.py nccl > gpurun_out/r02_p2p_nccl_n$N.jsonl 2> gpurun_out/r02_p2p_nccl_n$N.err; echo p2pnccl=$?
