@@ -119,7 +119,7 @@ def test_local_world_interpreter_shared_constants():
 
 
 @pytest.mark.parametrize("xrun,xceu", [("16", "0"), ("16", "1"), ("1024", "1"), ("0", "1")])
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_local_world_copy_engine_gather(world, xrun, xceu, monkeypatch):
     # The copy-engine form of the exchange (api.cpp exchange, kernels.cu copy_bits_ce): rows of the
     # block go straight from the state into the peer's slot as strided 2-D copies when its runs are
