@@ -113,7 +113,7 @@ struct sv_state {
   bool xrecv_shared = false;
   uint64_t xslot = 0;             // amplitudes per slot
   cudaStream_t st_x = nullptr, st_u = nullptr, st_p = nullptr;
-  cudaEvent_t ev_start = nullptr, ev_pushed[2] = {}, ev_unpacked[2] = {}, ev_landed[4] = {}, ev_done = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_pushed[3] = {}, ev_unpacked[3] = {}, ev_landed[4] = {}, ev_done = nullptr;
   cudaEvent_t ev_packed[2] = {}, ev_prev[4] = {};
 
   Program prog;
@@ -565,6 +565,13 @@ bool x_ce_unpack() {
   const char* e = std::getenv("SV_XCEU");
   return !(e && e[0] == '0');
 }
+// SV_XINPLACE=1: with copy engines at both ends, one rank of each pair receives in place — its
+// partner writes straight into its state once its own piece has left — so only the other rank
+// unpacks (the roles alternate between groups of pieces); three receive slots.
+bool x_inplace() {
+  const char* e = std::getenv("SV_XINPLACE");
+  return e && e[0] == '1';
+}
 bool x_pipe() {
   static const bool on = [] {
     const char* e = std::getenv("SV_XPIPE");
@@ -580,8 +587,8 @@ int ensure_exchange_engine(sv_state* h, uint64_t slot_amps, bool nccl_path) {
     CUDA_TRY(h, cudaStreamCreateWithPriority(&h->st_x, cudaStreamNonBlocking, hi));
     CUDA_TRY(h, cudaStreamCreateWithPriority(&h->st_u, cudaStreamNonBlocking, hi));
     CUDA_TRY(h, cudaStreamCreateWithPriority(&h->st_p, cudaStreamNonBlocking, hi));
-    for (cudaEvent_t* e : {&h->ev_start, &h->ev_done, &h->ev_pushed[0], &h->ev_pushed[1], &h->ev_unpacked[0],
-                           &h->ev_unpacked[1], &h->ev_landed[0], &h->ev_landed[1], &h->ev_landed[2], &h->ev_landed[3],
+    for (cudaEvent_t* e : {&h->ev_start, &h->ev_done, &h->ev_pushed[0], &h->ev_pushed[1], &h->ev_pushed[2],
+                           &h->ev_unpacked[0], &h->ev_unpacked[1], &h->ev_unpacked[2], &h->ev_landed[0], &h->ev_landed[1], &h->ev_landed[2], &h->ev_landed[3],
                            &h->ev_packed[0], &h->ev_packed[1], &h->ev_prev[0], &h->ev_prev[1], &h->ev_prev[2],
                            &h->ev_prev[3]})
       CUDA_TRY(h, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
@@ -590,7 +597,7 @@ int ensure_exchange_engine(sv_state* h, uint64_t slot_amps, bool nccl_path) {
     for (void* p : h->xrecv_opened) cudaIpcCloseMemHandle(p);
     h->xrecv_opened.clear();
     h->xrecv_shared = false;
-    if (int rc = ensure_dev(h, h->d_xrecv, 2 * slot_amps * h->amp)) return rc;
+    if (int rc = ensure_dev(h, h->d_xrecv, 3 * slot_amps * h->amp)) return rc;  // 3 for the in-place form
     h->xslot = slot_amps;
   }
   if (nccl_path || x_ce())
@@ -675,7 +682,17 @@ int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const XPipe
   // included — before any push lands in a peer's slot
   if (!nccl_path)
     if (int rc = barrier(h, h->st_x)) return rc;
-  int pos[11], val[11];
+  int pos[11], val[11], pval[11];
+  bool inplace = direct && ce_unpack && x_inplace();
+  if (inplace) {  // every piece has the row shape the copy engines take (checked on piece 0)
+    int np = 0, zero[11] = {};
+    for (int i = 0; i < k; i++) pos[np++] = m[i];
+    for (int i = 0; i < ns; i++) pos[np++] = sbit[i];
+    int nc = 0;
+    inplace = copy_bits_ce_xx(h->sv, zero, h->sv, zero, 0, std::min(slot, qblock), np, pos, h->amp, min_run, h->st_x,
+                              &nc, true) == cudaSuccess;
+  }
+  const bool single_group = P * ((1 << k) - 1) == 1;
   uint64_t q = 0;
   for (int p = 0; p < P; p++) {
     if (pre) {  // quarter p of the chain before is written before it is packed / sent
@@ -693,15 +710,44 @@ int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const XPipe
       int nins = 0;
       for (int i = 0; i < k; i++) {
         pos[nins] = m[i];
+        pval[nins] = (mine >> i) & 1;  // the partner's block that mine replaces (in-place form)
         val[nins++] = (mu >> i) & 1;
       }
       for (int i = 0; i < ns; i++) {
         pos[nins] = sbit[i];
+        pval[nins] = (p >> i) & 1;
         val[nins++] = (p >> i) & 1;
       }
       for (uint64_t off = 0; off < qblock; off += slot, q++) {
         const uint64_t cnt = std::min<uint64_t>(slot, qblock - off);
         const int b = (int)(q & 1);
+        if (inplace) {
+          // Roles per group of pieces (alternating, so each rank unpacks about half): the stager
+          // copies its rows into the partner's slot before the piece's barrier; after it (the
+          // stager's rows have left) the partner copies its rows straight into the stager's state
+          // and then unpacks its slot.  Slot q % 3 is free: its previous unpack (piece q - 3) was
+          // waited for before the previous barrier.
+          const bool lower = h->rank < partner;
+          const bool stager = lower ^ (single_group ? off >= qblock / 2 : (((p * ((1 << k) - 1)) + t - 1) & 1) != 0);
+          const int b3 = (int)(q % 3);
+          int nc = 0;
+          if (stager) {
+            char* dst = (char*)h->peer_xrecv[partner] + (size_t)b3 * slot * h->amp;
+            CUDA_TRY(h, copy_bits_ce(true, h->sv, dst, off, cnt, nins, pos, val, h->amp, min_run, h->st_x, &nc));
+          }
+          if (q >= 2) CUDA_TRY(h, cudaStreamWaitEvent(h->st_x, h->ev_unpacked[(q - 2) % 3], 0));
+          if (int rc = barrier(h, h->st_x)) return rc;
+          if (!stager) {
+            CUDA_TRY(h, copy_bits_ce_xx(h->sv, val, h->peers[partner], pval, off, cnt, nins, pos, h->amp, min_run,
+                                        h->st_x, &nc, false));
+            CUDA_TRY(h, cudaEventRecord(h->ev_pushed[b3], h->st_x));
+            CUDA_TRY(h, cudaStreamWaitEvent(h->st_u, h->ev_pushed[b3], 0));
+            CUDA_TRY(h, copy_bits_ce(false, h->sv, recv + (size_t)b3 * slot * h->amp, off, cnt, nins, pos, val, h->amp,
+                                     min_run, h->st_u, &nc));
+            CUDA_TRY(h, cudaEventRecord(h->ev_unpacked[b3], h->st_u));
+          }
+          continue;
+        }
         if (nccl_path) {
           if (q >= 2) CUDA_TRY(h, cudaStreamWaitEvent(h->st_x, h->ev_unpacked[b], 0));  // my slot b is free
           char* sb = send + (size_t)b * slot * h->amp;
@@ -754,6 +800,11 @@ int exchange(sv_state* h, std::vector<ExPair> pairs, uint32_t flags, const XPipe
         }
         CUDA_TRY(h, cudaEventRecord(h->ev_unpacked[b], h->st_u));
       }
+    }
+    if (inplace) {  // the partners' in-place copies of quarter p have landed after one more barrier
+      if (int rc = barrier(h, h->st_x)) return rc;
+      CUDA_TRY(h, cudaEventRecord(h->ev_done, h->st_x));
+      CUDA_TRY(h, cudaStreamWaitEvent(h->st_u, h->ev_done, 0));
     }
     if (!xp.post.empty()) {  // quarter p of the chain after: its tiles have every exchanged element now
       CUDA_TRY(h, cudaEventRecord(h->ev_landed[p], h->st_u));
@@ -932,7 +983,8 @@ int sv_destroy(sv_handle h) {
   }
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   for (void* p : h->xrecv_opened) cudaIpcCloseMemHandle(p);
-  for (cudaEvent_t e : {h->ev_start, h->ev_done, h->ev_pushed[0], h->ev_pushed[1], h->ev_unpacked[0], h->ev_unpacked[1],
+  for (cudaEvent_t e : {h->ev_start, h->ev_done, h->ev_pushed[0], h->ev_pushed[1], h->ev_pushed[2], h->ev_unpacked[0],
+                        h->ev_unpacked[1], h->ev_unpacked[2],
                         h->ev_landed[0], h->ev_landed[1], h->ev_landed[2], h->ev_landed[3], h->ev_packed[0],
                         h->ev_packed[1], h->ev_prev[0], h->ev_prev[1], h->ev_prev[2], h->ev_prev[3]})
     if (e) cudaEventDestroy(e);

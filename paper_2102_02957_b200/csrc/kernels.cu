@@ -616,4 +616,62 @@ cudaError_t copy_bits_ce(bool pack, void* sv, void* stage, uint64_t first, uint6
   return cudaSuccess;
 }
 
+// State to state: the rows of a block piece (inserted bits valued vsrc) of src go to the same rows
+// of dst with the inserted bits valued vdst — the in-place form of the exchange, dst a peer's
+// state.  dry: only check the shape.  cudaErrorNotSupported as copy_bits_ce.
+cudaError_t copy_bits_ce_xx(void* src, const int* vsrc, void* dst, const int* vdst, uint64_t first, uint64_t count,
+                            int nins, const int* pos, size_t amp, uint64_t min_run, cudaStream_t st, int* copies,
+                            bool dry) {
+  *copies = 0;
+  if (nins < 1 || nins > 11 || count == 0) return cudaErrorNotSupported;
+  int P[11], Vs[11], Vd[11];
+  for (int i = 0; i < nins; i++) P[i] = pos[i], Vs[i] = vsrc[i], Vd[i] = vdst[i];
+  for (int i = 1; i < nins; i++)
+    for (int j = i; j > 0 && P[j] < P[j - 1]; j--)
+      std::swap(P[j], P[j - 1]), std::swap(Vs[j], Vs[j - 1]), std::swap(Vd[j], Vd[j - 1]);
+  const int lo = P[0];
+  const uint64_t run = 1ull << lo;
+  if (run < min_run) return cudaErrorNotSupported;
+  auto addr = [&](uint64_t x, const int* V) {
+    for (int k = 0; k < nins; k++) {
+      const uint64_t l = x & ((1ull << P[k]) - 1);
+      x = ((x - l) << 1) | ((uint64_t)V[k] << P[k]) | l;
+    }
+    return x;
+  };
+  char* S = (char*)src;
+  char* D = (char*)dst;
+  if (count <= run) {
+    if ((first >> lo) != ((first + count - 1) >> lo)) return cudaErrorNotSupported;
+    if (dry) return cudaSuccess;
+    *copies = 1;
+    return cudaMemcpyAsync(D + addr(first, Vd) * amp, S + addr(first, Vs) * amp, count * amp, cudaMemcpyDeviceToDevice, st);
+  }
+  if ((first & (run - 1)) || (count & (run - 1))) return cudaErrorNotSupported;
+  int a = 1;
+  while (a < nins && P[a] == lo + a) a++;
+  const size_t width = run * amp, pitch = (1ull << (lo + a)) * amp;
+  const uint64_t seg_rows = a < nins ? 1ull << (P[a] - lo - a) : ~0ull;
+  const uint64_t r0 = first >> lo, r1 = (first + count) >> lo;
+  const bool rows_1d = pitch > (size_t)INT32_MAX;
+  if (rows_1d && r1 - r0 > 64) return cudaErrorNotSupported;
+  if (dry) return cudaSuccess;
+  for (uint64_t r = r0; r < r1;) {
+    const uint64_t e = seg_rows == ~0ull ? r1 : std::min(r1, (r / seg_rows + 1) * seg_rows);
+    char* sp = S + addr(r << lo, Vs) * amp;
+    char* dp = D + addr(r << lo, Vd) * amp;
+    cudaError_t err = cudaSuccess;
+    if (rows_1d) {
+      for (uint64_t i = 0; i < e - r && err == cudaSuccess; i++, (*copies)++)
+        err = cudaMemcpyAsync(dp + i * pitch, sp + i * pitch, width, cudaMemcpyDeviceToDevice, st);
+    } else {
+      err = cudaMemcpy2DAsync(dp, pitch, sp, pitch, width, e - r, cudaMemcpyDeviceToDevice, st);
+      (*copies)++;
+    }
+    if (err != cudaSuccess) return err;
+    r = e;
+  }
+  return cudaSuccess;
+}
+
 }  // namespace sv

@@ -57,5 +57,9 @@ cudaError_t launch_pack_bits(bool dbl, bool pack, void* sv, void* stage, uint64_
 // runs are >= min_run elements (kernels.cu); cudaErrorNotSupported otherwise; *copies = copies issued
 cudaError_t copy_bits_ce(bool pack, void* sv, void* stage, uint64_t first, uint64_t count, int nins, const int* pos,
                          const int* val, size_t amp, uint64_t min_run, cudaStream_t st, int* copies);
+// state rows -> the same rows of another (peer) state with other inserted-bit values (kernels.cu)
+cudaError_t copy_bits_ce_xx(void* src, const int* vsrc, void* dst, const int* vdst, uint64_t first, uint64_t count,
+                            int nins, const int* pos, size_t amp, uint64_t min_run, cudaStream_t st, int* copies,
+                            bool dry);
 
 }  // namespace sv

@@ -155,3 +155,22 @@ def test_local_world_pipeline_chains(world, xchain, monkeypatch):
         checks, err, d1 = M.check(case, res[0], _REF[name], _ONE[name], world)
         bad = [k for k, ok in checks.items() if not ok]
         assert not bad, (name, world, xchain, bad, err, d1)
+
+
+@pytest.mark.parametrize("xrun", ["16", "1024"])
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_local_world_inplace_exchange(world, xrun, monkeypatch):
+    # The in-place form of the exchange (SV_XINPLACE=1, api.cpp exchange): per group of pieces one
+    # rank of each pair stages its rows into the partner's slot, the partner writes its rows straight
+    # into the stager's state after the piece's barrier and unpacks its slot; roles alternate.
+    monkeypatch.setenv("SV_XINPLACE", "1")
+    monkeypatch.setenv("SV_XRUN", xrun)
+    for case in [c for c in M.cases() if c[0] in ("qv", "qft", "rand", "qv-twice", "qft-fp32", "qft-absorb")]:
+        name = case[0]
+        if name not in _REF:
+            _REF[name] = M.reference(case)
+            _ONE[name] = M.single_gpu(sv, case)
+        res = run_world(world, case)
+        checks, err, d1 = M.check(case, res[0], _REF[name], _ONE[name], world)
+        bad = [k for k, ok in checks.items() if not ok]
+        assert not bad, (name, world, xrun, bad, err, d1)

@@ -37,6 +37,7 @@ for t in range(count):
     os.environ["SV_XRUN"] = str(rng.choice(["16", "256", "1024", "0"]))  # copy-engine gather threshold
     os.environ["SV_XCEU"] = str(rng.choice(["0", "1"]))  # copy-engine unpack
     os.environ["SV_XCHAIN"] = str(rng.choice(["0", "1", "4", "16"]))  # launches pipelined per exchange side
+    os.environ["SV_XINPLACE"] = str(rng.choice(["0", "1"]))  # in-place exchange form
     try:
         with sv.LocalWorld(world) as w:
             def body(rank):
@@ -52,7 +53,7 @@ for t in range(count):
         if not err <= tol:
             bad += 1
             print(f"FAIL t={t} G={world} n={n} c={c} {prec} flags={flags} gates={len(circ)} err={err:.3g} "
-                  f"xrun={os.environ['SV_XRUN']} xceu={os.environ['SV_XCEU']} xchain={os.environ['SV_XCHAIN']}", flush=True)
+                  f"xrun={os.environ['SV_XRUN']} xceu={os.environ['SV_XCEU']} xchain={os.environ['SV_XCHAIN']} inplace={os.environ['SV_XINPLACE']}", flush=True)
     except Exception as e:  # noqa: BLE001
         bad += 1
         print(f"ERROR t={t} G={world} n={n} c={c} {prec} flags={flags}: {e}", flush=True)
