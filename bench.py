@@ -60,8 +60,10 @@ def workload(name: str, world: int):
                     basis=C.basis_index(1, 30), scaling="strong", chunk_bits=8)
     if name == "qft_weak":
         n = 33 + g
+        # c = 9: one read + write pass fewer than c = 8 at 2^33 local amplitudes (QFT33 188 vs 228 ms,
+        # profiles/r02_qft_chunk_bits.md)
         return dict(name="qft_weak", desc=f"QFT({n}) fp64, 2^33 amplitudes per GPU (weak)", n=n, gates=C.qft(n),
-                    basis=C.basis_index(1, n), scaling="weak", chunk_bits=8)
+                    basis=C.basis_index(1, n), scaling="weak", chunk_bits=9)
     if name == "qft_weak_fp32":  # BASELINE configs[4]'s fp32 variant: 2^34 fp32 amplitudes per GPU (37q at 8)
         n = 34 + g
         return dict(name="qft_weak_fp32", desc=f"QFT({n}) fp32, 2^34 amplitudes per GPU (weak)", n=n, gates=C.qft(n),
