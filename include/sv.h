@@ -66,7 +66,7 @@ typedef struct {
 #define SV_UNBLOCKED     (1u << 0) /* per-gate baseline: one HBM pass per gate, no pass  */
 #define SV_RESTORE_ORDER (1u << 1) /* append swaps returning the paper-physical order to logical */
 #define SV_EXCHANGE_NCCL (1u << 2) /* cross-GPU exchange by NCCL send/recv through a staging ring */
-                                   /* instead of copy-engine peer copies of packed pieces       */
+                                   /* instead of copy-engine peer copies (CUDA IPC)              */
 #define SV_ABSORB_SWAPS  (1u << 5) /* the pass absorbs user SWAP gates as relabels of pi (the  */
                                    /* paper's bit reordering) instead of   */
                                    /* treating them as 2-qubit gates; sections that would hold  */
@@ -147,8 +147,9 @@ int sv_nccl_unique_id(void* out128);
  * world, sv_create_local(..., w, r, ...) creates rank r's handle (its shard on the current device,
  * cuda_stream nullable as in sv_create_dist).  Each rank's handle must be driven by its own host
  * thread, every rank calling the same collective sequence as under NCCL; exchanges run the same
- * plans, pack kernels and peer copies of packed pieces, barriers are CUDA events passed through a host barrier (no
- * device-side waiting), reductions are summed on the host in rank order, send/recv are
+ * plans and peer copies (copy engines, pack kernels for short rows), barriers are CUDA events
+ * passed through a host barrier (no device-side waiting), reductions are summed on the host in
+ * rank order, send/recv are
  * device-to-device copies.  A rank that does not reach a collective within SV_COMM_TIMEOUT_S
  * seconds (default 600) makes the others fail with SV_ENCCL.  The world is reference counted:
  * sv_world_destroy may be called right after the last sv_create_local.  Errors: SV_EINVAL
