@@ -464,10 +464,19 @@ Status compile_section(const std::vector<sv_gate>& gates, int nL, int rank, int 
       P->tpos[j] = po.chosen[j];
       P->tw[j] = swz[po.chosen[j]];
     }
-    // a direct HBM boundary needs lane j of each 2^swizzle_bits group on memory bit j (128 B runs)
+    // a direct HBM boundary needs lane j of each 2^swizzle_bits group on memory bit j (128 B runs);
+    // when the tile holds only memory bits 0..L-1 of them (a section with more active qubits than
+    // the tile leaves room for), lanes 0..L-1 on those bits (runs of 2^L amplitudes, >= 64 B)
     auto lanes_on_low_bits = [&](const int* bits) {
       if ((int)po.chosen.size() < swizzle_bits) return false;
-      for (int j = 0; j < swizzle_bits; j++)
+      int L = 0;
+      for (bool found = true; found && L < swizzle_bits;) {
+        found = false;
+        for (int q = 0; q < T; q++) found = found || bits[q] == L;
+        if (found) L++;
+      }
+      if (L < swizzle_bits - 1) return false;
+      for (int j = 0; j < L; j++)
         if (bits[po.chosen[j]] != j) return false;
       return true;
     };

@@ -69,7 +69,7 @@ def test_diagonal_heavy_emulated():
         emulate(recs, n, c, seed=t)
 
 
-@pytest.mark.parametrize("n,c", [(12, 6), (14, 8), (14, 12), (16, 12)])
+@pytest.mark.parametrize("n,c", [(12, 6), (14, 8), (14, 12), (16, 12), (16, 10), (17, 11)])  # c >= 10: tiles with 2 low bits, direct
 def test_qft_qv_emulated(n, c):
     emulate(C.qft(n), n, c)
     emulate(C.quantum_volume(n, 6, 2), n, c)
